@@ -1,0 +1,267 @@
+"""Parity oracle — TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s cpu_baseline /
+``--impl reference`` legs may import this package, and only as the checker
+or the timed CPU reference arm — never as a product path. Two oracles live
+here:
+
+* ``restated()``: ``oracle/liboracle.so`` built from ``primkit_oracle.c``, a
+  plain-C restatement of the reference CPU algorithms (each function cites
+  the reference file:line it follows);
+* ``reference()``: ``oracle/_ref/libprimkit_ref.so``, the unmodified reference
+  implementation compiled from /root/reference sources by
+  ``oracle/Makefile.ref`` (plus ``ref_shim.cpp`` exposing its C++-only
+  batch-norm / activation entry points). It travels to the GPU box as a
+  prebuilt binary; /root/reference itself is never read at run time.
+
+The restatement is pinned against the reference's golden vectors
+(tests/golden/) and against ``reference()`` (tests/test_oracle.py).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+RESTATED_SO = os.path.join(_HERE, "liboracle.so")
+REF_SO = os.path.join(_HERE, "_ref", "libprimkit_ref.so")
+REF_SOURCES = "/root/reference/proj"
+
+
+def build(force: bool = False) -> None:
+    """Compile the C restatement and (when the reference sources exist here)
+    the reference library. Building the checker is not using it."""
+    src = os.path.join(_HERE, "primkit_oracle.c")
+    if force or not os.path.exists(RESTATED_SO) or os.path.getmtime(src) > os.path.getmtime(RESTATED_SO):
+        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-o", RESTATED_SO, src, "-lm"])
+    if os.path.isdir(REF_SOURCES) and (force or not os.path.exists(REF_SO)):
+        subprocess.check_call(["make", "-s", "-f", os.path.join(_HERE, "Makefile.ref"),
+                               f"-j{os.cpu_count() or 4}"])
+
+
+class _ConvP(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("n", "c", "h", "w", "k", "y", "x", "pad_h", "pad_w",
+                                         "str_h", "str_w", "dil_h", "dil_w", "groups")]
+
+
+_FP = C.POINTER(C.c_float)
+_restated = None
+
+
+def _fp(a):
+    return a.ctypes.data_as(_FP)
+
+
+def restated():
+    """The C restatement (ctypes CDLL with typed entry points)."""
+    global _restated
+    if _restated is None:
+        if not os.path.exists(RESTATED_SO):
+            build()
+        lib = C.CDLL(RESTATED_SO)
+        lib.oc_round_bf16.restype = C.c_float
+        lib.oc_round_bf16.argtypes = [C.c_float]
+        lib.oc_activation.restype = C.c_float
+        lib.oc_activation.argtypes = [C.c_int, C.c_float, C.c_float]
+        lib.oc_activation_grad.restype = C.c_float
+        lib.oc_activation_grad.argtypes = [C.c_int, C.c_float, C.c_float]
+        _restated = lib
+    return _restated
+
+
+def _convp(p) -> _ConvP:
+    cp = _ConvP()
+    for a, b in (("n", "n"), ("c", "c"), ("h", "h"), ("w", "w"), ("k", "k"), ("y", "y"), ("x", "x"),
+                 ("pad_h", "pad_h"), ("pad_w", "pad_w"), ("str_h", "stride_h"),
+                 ("str_w", "stride_w"), ("dil_h", "dilation_h"), ("dil_w", "dilation_w"),
+                 ("groups", "groups")):
+        setattr(cp, a, getattr(p, b))
+    return cp
+
+
+def out_hw(p):
+    def ext(i, pad, d, f, s):
+        span = d * (f - 1) + 1
+        return 0 if i + 2 * pad < span else (i + 2 * pad - span) // s + 1
+    return (ext(p.h, p.pad_h, p.dilation_h, p.y, p.stride_h),
+            ext(p.w, p.pad_w, p.dilation_w, p.x, p.stride_w))
+
+
+def round_bf16(a: np.ndarray) -> np.ndarray:
+    """Vectorised restatement of tensor.cpp:44-54 (RNE, NaN -> quiet NaN)."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    nan = np.isnan(a)
+    r = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    r = np.where(nan, (u.astype(np.uint32) & 0xFFFF0000) | 0x00410000, r).astype(np.uint32)
+    return r.view(np.float32)
+
+
+def conv_forward(p, x, w, bf16=False):
+    oh, ow = out_hw(p)
+    out = np.zeros((p.n, p.k, oh, ow), np.float32)
+    restated().oc_conv_fwd(C.byref(_convp(p)), _fp(np.ascontiguousarray(x, np.float32)),
+                           _fp(np.ascontiguousarray(w, np.float32)), _fp(out), int(bf16))
+    return out
+
+
+def conv_backward_data(p, dy, w, bf16=False):
+    dx = np.zeros((p.n, p.c, p.h, p.w), np.float32)
+    restated().oc_conv_bwd_data(C.byref(_convp(p)), _fp(np.ascontiguousarray(dy, np.float32)),
+                                _fp(np.ascontiguousarray(w, np.float32)), _fp(dx), int(bf16))
+    return dx
+
+
+def conv_backward_weights(p, dy, x, bf16=False):
+    dw = np.zeros((p.k, p.c // p.groups, p.y, p.x), np.float32)
+    restated().oc_conv_bwd_weights(C.byref(_convp(p)), _fp(np.ascontiguousarray(dy, np.float32)),
+                                   _fp(np.ascontiguousarray(x, np.float32)), _fp(dw), int(bf16))
+    return dw
+
+
+def winograd_f23(p, x, w, bf16=False):
+    oh, ow = out_hw(p)
+    out = np.zeros((p.n, p.k, oh, ow), np.float32)
+    restated().oc_winograd_f23(C.byref(_convp(p)), _fp(np.ascontiguousarray(x, np.float32)),
+                               _fp(np.ascontiguousarray(w, np.float32)), _fp(out), int(bf16))
+    return out
+
+
+def _d4(shape):
+    return (C.c_int64 * 4)(*shape)
+
+
+def bn_forward_train(mode, x, gamma, beta, rmean, rvar, eps=1e-5, momentum=0.1, bf16=False):
+    x = np.ascontiguousarray(x, np.float32)
+    rm, rv = np.array(rmean, np.float32).ravel(), np.array(rvar, np.float32).ravel()
+    ns = rm.size
+    y = np.zeros_like(x)
+    sm, si = np.zeros(ns, np.float32), np.zeros(ns, np.float32)
+    restated().oc_bn_forward_train(mode, _d4(x.shape), _fp(x),
+                                   _fp(np.ascontiguousarray(gamma, np.float32).ravel()),
+                                   _fp(np.ascontiguousarray(beta, np.float32).ravel()), _fp(rm),
+                                   _fp(rv), C.c_float(eps), C.c_float(momentum), _fp(y), _fp(sm),
+                                   _fp(si), int(bf16))
+    return y, sm, si, rm, rv
+
+
+def bn_forward_infer(mode, x, gamma, beta, rmean, rvar, eps=1e-5, bf16=False):
+    x = np.ascontiguousarray(x, np.float32)
+    y = np.zeros_like(x)
+    f = lambda a: _fp(np.ascontiguousarray(a, np.float32).ravel())  # noqa: E731
+    args = [np.ascontiguousarray(a, np.float32).ravel() for a in (gamma, beta, rmean, rvar)]
+    restated().oc_bn_forward_infer(mode, _d4(x.shape), _fp(x), *[_fp(a) for a in args],
+                                   C.c_float(eps), _fp(y), int(bf16))
+    del f
+    return y
+
+
+def bn_backward(mode, x, dy, gamma, smean, sinv, bf16=False):
+    x, dy = np.ascontiguousarray(x, np.float32), np.ascontiguousarray(dy, np.float32)
+    g = np.ascontiguousarray(gamma, np.float32).ravel()
+    dx = np.zeros_like(x)
+    dg, db = np.zeros(g.size, np.float32), np.zeros(g.size, np.float32)
+    restated().oc_bn_backward(mode, _d4(x.shape), _fp(x), _fp(dy), _fp(g),
+                              _fp(np.ascontiguousarray(smean, np.float32)),
+                              _fp(np.ascontiguousarray(sinv, np.float32)), _fp(dx), _fp(dg),
+                              _fp(db), int(bf16))
+    return dx, dg, db
+
+
+def activation(kind, alpha, x):
+    f = np.vectorize(lambda v: restated().oc_activation(kind, alpha, float(v)), otypes=[np.float32])
+    return f(np.asarray(x, np.float32))
+
+
+def conv_ref_f64(p, x, w):
+    """Independent f64 scatter-form reference (structure of the reference's
+    tests/test_util.hpp:37-116 conv_ref), vectorised over (n, k) with numpy."""
+    oh, ow = out_hw(p)
+    out = np.zeros((p.n, p.k, oh, ow), np.float64)
+    cg, kg = p.c // p.groups, p.k // p.groups
+    x = x.astype(np.float64)
+    w = w.astype(np.float64)
+    for g in range(p.groups):
+        for yy in range(p.y):
+            for xx in range(p.x):
+                for o_h in range(oh):
+                    ih = o_h * p.stride_h - p.pad_h + yy * p.dilation_h
+                    if ih < 0 or ih >= p.h:
+                        continue
+                    iws = np.arange(ow) * p.stride_w - p.pad_w + xx * p.dilation_w
+                    ok = (iws >= 0) & (iws < p.w)
+                    if not ok.any():
+                        continue
+                    xs = x[:, g * cg:(g + 1) * cg, ih, :][:, :, iws[ok]]          # n, cg, q
+                    ws = w[g * kg:(g + 1) * kg, :, yy, xx]                         # kg, cg
+                    out[:, g * kg:(g + 1) * kg, o_h, ok] += np.einsum("ncq,kc->nkq", xs, ws)
+    return out
+
+
+# ---- the unmodified reference library -------------------------------------
+
+def reference_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+_ref = None
+
+
+def reference():
+    """(Library, shim) for oracle/_ref/libprimkit_ref.so, or None if absent."""
+    global _ref
+    if _ref is None:
+        if not reference_available():
+            return None
+        from paper_1910_00078_b200.primkit import Library
+        lib = Library(REF_SO, extended=False)
+        s = lib.lib
+        I64P = C.POINTER(C.c_int64)
+        s.ref_bn_forward_train.argtypes = [C.c_int, I64P, C.c_int] + [_FP] * 5 + [
+            C.c_float, C.c_float] + [_FP] * 3
+        s.ref_bn_forward_infer.argtypes = [C.c_int, I64P, C.c_int] + [_FP] * 5 + [C.c_float, _FP]
+        s.ref_bn_backward.argtypes = [C.c_int, I64P, C.c_int] + [_FP] * 6 + [C.c_float] + [_FP] * 3
+        s.ref_activation_forward.argtypes = [C.c_int, C.c_float, I64P, C.c_int, _FP, _FP]
+        s.ref_activation_backward.argtypes = [C.c_int, C.c_float, I64P, C.c_int, _FP, _FP, _FP]
+        s.ref_round_bf16.restype = C.c_float
+        s.ref_round_bf16.argtypes = [C.c_float]
+        s.ref_shim_last_error.restype = C.c_char_p
+        _ref = lib
+    return _ref
+
+
+def ref_check(st):
+    if st != 0:
+        raise RuntimeError(f"reference shim status {st}: "
+                           f"{reference().lib.ref_shim_last_error().decode()}")
+
+
+def ref_bn_forward_train(mode, x, gamma, beta, rmean, rvar, eps=1e-5, momentum=0.1, bf16=False):
+    L = reference().lib
+    x = np.ascontiguousarray(x, np.float32)
+    rm, rv = np.array(rmean, np.float32).ravel(), np.array(rvar, np.float32).ravel()
+    y = np.zeros_like(x)
+    sm, si = np.zeros(rm.size, np.float32), np.zeros(rm.size, np.float32)
+    ref_check(L.ref_bn_forward_train(mode, _d4(x.shape), int(bf16), _fp(x),
+                                     _fp(np.ascontiguousarray(gamma, np.float32).ravel()),
+                                     _fp(np.ascontiguousarray(beta, np.float32).ravel()), _fp(rm),
+                                     _fp(rv), C.c_float(eps), C.c_float(momentum), _fp(y), _fp(sm),
+                                     _fp(si)))
+    return y, sm, si, rm, rv
+
+
+def ref_bn_backward(mode, x, dy, gamma, beta, smean, sinv, eps=1e-5, bf16=False):
+    L = reference().lib
+    x, dy = np.ascontiguousarray(x, np.float32), np.ascontiguousarray(dy, np.float32)
+    g = np.ascontiguousarray(gamma, np.float32).ravel()
+    dx = np.zeros_like(x)
+    dg, db = np.zeros(g.size, np.float32), np.zeros(g.size, np.float32)
+    ref_check(L.ref_bn_backward(mode, _d4(x.shape), int(bf16), _fp(x), _fp(dy), _fp(g),
+                                _fp(np.ascontiguousarray(beta, np.float32).ravel()),
+                                _fp(np.ascontiguousarray(smean, np.float32)),
+                                _fp(np.ascontiguousarray(sinv, np.float32)), C.c_float(eps),
+                                _fp(dx), _fp(dg), _fp(db)))
+    return dx, dg, db

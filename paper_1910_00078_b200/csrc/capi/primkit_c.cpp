@@ -1,0 +1,760 @@
+// C ABI of primkit-b200 (include/primkit/primkit.h).
+//
+// Section 1 functions are drop-in replacements for the reference's
+// proj/src/capi/primkit_c.cpp:154-496: same validation order, same status
+// mapping (no exception crosses the boundary; a thread-local message records
+// the last failure), same operand conventions. The compute behind them runs
+// on the GPU: host NCHW buffers are staged into the device layout, the
+// selected sm_100a kernel runs on the handle's stream, results come back.
+#include "primkit/primkit.h"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "../cuda/kernels.h"
+#include "../host/fusion.hpp"
+#include "../host/handle.hpp"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+primkit_status fail(primkit_status st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+template <typename Fn>
+primkit_status guarded(Fn&& fn) {
+    try {
+        fn();
+        return PRIMKIT_STATUS_OK;
+    } catch (const primkit::Error& e) {
+        return fail(static_cast<primkit_status>(e.code()), e.what());
+    } catch (const std::exception& e) {
+        return fail(PRIMKIT_STATUS_INTERNAL, e.what());
+    } catch (...) {
+        return fail(PRIMKIT_STATUS_INTERNAL, "unknown error");
+    }
+}
+
+template <typename T>
+T* need(T* p, const char* what) {
+    if (!p) primkit::throw_error(primkit::ErrorCode::InvalidValue, std::string("null ") + what);
+    return p;
+}
+
+primkit::ConvProblem to_problem(const primkit_conv_problem* pp) {
+    const primkit_conv_problem& p = *need(pp, "problem");
+    primkit::ConvProblem o;
+    o.n = p.n; o.c = p.c; o.h = p.h; o.w = p.w;
+    o.k = p.k; o.y = p.y; o.x = p.x;
+    o.pad_h = p.pad_h; o.pad_w = p.pad_w;
+    o.stride_h = p.stride_h; o.stride_w = p.stride_w;
+    o.dilation_h = p.dilation_h; o.dilation_w = p.dilation_w;
+    o.groups = p.groups;
+    o.direction = static_cast<primkit::ConvDirection>(p.direction);
+    o.mode = static_cast<primkit::ConvMode>(p.mode);
+    o.etype = static_cast<primkit::ElementType>(p.etype);
+    return o;
+}
+
+// Data operands per direction: Forward (input, filter), BackwardData
+// (dOutput, filter), BackwardWeights (dOutput, input).
+std::pair<primkit::TensorDescriptor, primkit::TensorDescriptor> operand_descs(
+    const primkit::ConvProblem& p) {
+    using D = primkit::ConvDirection;
+    if (p.direction == D::Forward) return {p.input_desc(), p.filter_desc()};
+    if (p.direction == D::BackwardData) return {p.output_desc(), p.filter_desc()};
+    return {p.output_desc(), p.input_desc()};
+}
+
+primkit::TensorDescriptor result_desc(const primkit::ConvProblem& p) {
+    using D = primkit::ConvDirection;
+    if (p.direction == D::Forward) return p.output_desc();
+    if (p.direction == D::BackwardData) return p.input_desc();
+    return p.filter_desc();
+}
+
+void copy_name(char* buf, size_t len, const std::string& name) {
+    if (!buf || len == 0) primkit::throw_error(primkit::ErrorCode::InvalidValue, "null output buffer");
+    if (name.size() + 1 > len)
+        primkit::throw_error(primkit::ErrorCode::InvalidValue, "output buffer too small");
+    std::memcpy(buf, name.c_str(), name.size() + 1);
+}
+
+// Host copy quantized to the element type (tensor_from in the reference).
+primkit::HostTensor host_tensor(const primkit::TensorDescriptor& d, const float* data) {
+    primkit::HostTensor t{d, std::vector<float>(data, data + d.elem_count())};
+    if (d.etype == primkit::ElementType::BF16)
+        for (float& v : t.data) v = primkit::round_bf16(v);
+    return t;
+}
+
+}  // namespace
+
+struct primkit_handle {
+    primkit::Handle impl;
+    primkit_handle() = default;
+    primkit_handle(cudaStream_t s, int dev) : impl(s, dev) {}
+};
+
+struct primkit_fusion_plan {
+    primkit::FusionPlan impl;
+};
+
+namespace {
+
+primkit::Handle& H(primkit_handle* h) { return need(h, "handle")->impl; }
+primkit::FusionPlan& P(primkit_fusion_plan* p) { return need(p, "fusion plan")->impl; }
+
+const primkit::Solver& solver_named(primkit_handle* h, const char* name) {
+    const primkit::Solver* s = H(h).find_solver(name ? name : "");
+    if (!s)
+        primkit::throw_error(primkit::ErrorCode::InvalidValue,
+                             std::string("unknown solver '") + (name ? name : "") + "'");
+    return *s;
+}
+
+// Solver selection shared by the host and device run entry points
+// (primkit_c.cpp:296-312 of the reference).
+const primkit::Solver& select_solver(primkit_handle* h, const primkit::ConvProblem& p,
+                                     const char* name) {
+    if (name) {
+        const primkit::Solver& s = solver_named(h, name);
+        if (!s.is_applicable(p))
+            primkit::throw_error(primkit::ErrorCode::AlgoNotApplicable,
+                                 s.name() + " is not applicable to " + p.key());
+        return s;
+    }
+    for (const auto& s : H(h).solvers())
+        if (s->is_applicable(p)) return *s;
+    primkit::throw_error(primkit::ErrorCode::NoApplicableSolver, "no applicable solver for " + p.key());
+}
+
+primkit::TensorDescriptor dims4(const int64_t d[4], primkit_element_type et) {
+    need(d, "dims");
+    return primkit::TensorDescriptor::packed({d[0], d[1], d[2], d[3]},
+                                             static_cast<primkit::ElementType>(et));
+}
+
+std::int64_t bn_stat_count(primkit_batchnorm_mode mode, const int64_t d[4]) {
+    return mode == PRIMKIT_BN_PER_ACTIVATION ? d[1] * d[2] * d[3] : d[1];
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* primkit_last_error(void) { return g_last_error.c_str(); }
+
+primkit_status primkit_handle_create(primkit_handle** out) {
+    return guarded([&] {
+        need(out, "handle output");
+        *out = new primkit_handle();
+    });
+}
+
+void primkit_handle_destroy(primkit_handle* handle) { delete handle; }
+
+primkit_status primkit_handle_use_fake_clock(primkit_handle* h) {
+    return guarded([&] { H(h).use_fake_clock(); });
+}
+
+primkit_status primkit_handle_now_ms(primkit_handle* h, double* out) {
+    return guarded([&] { *need(out, "output") = H(h).now_ms(); });
+}
+
+primkit_status primkit_handle_set_cache_dir(primkit_handle* h, const char* dir) {
+    return guarded([&] { H(h).set_cache_dir(need(dir, "directory")); });
+}
+
+primkit_status primkit_handle_counters(primkit_handle* h, primkit_counters* out) {
+    return guarded([&] {
+        const primkit::OpCounters& c = H(h).counters();
+        need(out, "output");
+        out->gemm_calls = c.gemm_calls;
+        out->scalar_muls = c.scalar_muls;
+        out->buffer_roundtrips = c.buffer_roundtrips;
+    });
+}
+
+primkit_status primkit_handle_reset_counters(primkit_handle* h) {
+    return guarded([&] { H(h).counters().reset(); });
+}
+
+primkit_status primkit_handle_set_seed(primkit_handle* h, uint64_t seed) {
+    return guarded([&] { H(h).rng_seed = seed; });
+}
+
+primkit_status primkit_problem_key(const primkit_conv_problem* p, char* buf, size_t len) {
+    return guarded([&] { copy_name(buf, len, to_problem(p).key()); });
+}
+
+primkit_status primkit_conv_output_dims(const primkit_conv_problem* p, int64_t dims[4]) {
+    return guarded([&] {
+        const primkit::TensorDescriptor d = result_desc(to_problem(p));
+        for (int i = 0; i < 4; ++i) dims[i] = d.dims[static_cast<size_t>(i)];
+    });
+}
+
+primkit_status primkit_solver_count(primkit_handle* h, int* out) {
+    return guarded([&] { *need(out, "output") = static_cast<int>(H(h).solvers().size()); });
+}
+
+primkit_status primkit_solver_name(primkit_handle* h, int index, char* buf, size_t len) {
+    return guarded([&] {
+        const auto& s = H(h).solvers();
+        if (index < 0 || index >= static_cast<int>(s.size()))
+            primkit::throw_error(primkit::ErrorCode::InvalidValue, "solver index out of range");
+        copy_name(buf, len, s[static_cast<size_t>(index)]->name());
+    });
+}
+
+primkit_status primkit_solver_is_applicable(primkit_handle* h, const char* name,
+                                            const primkit_conv_problem* p, int* out) {
+    return guarded([&] { *out = solver_named(h, name).is_applicable(to_problem(p)) ? 1 : 0; });
+}
+
+primkit_status primkit_solver_is_tunable(primkit_handle* h, const char* name, int* out) {
+    return guarded([&] { *out = solver_named(h, name).is_tunable() ? 1 : 0; });
+}
+
+primkit_status primkit_solver_workspace_bytes(primkit_handle* h, const char* name,
+                                              const primkit_conv_problem* pp, uint64_t* out) {
+    return guarded([&] {
+        const primkit::Solver& s = solver_named(h, name);
+        const primkit::ConvProblem p = to_problem(pp);
+        const primkit::PerfConfig cfg = H(h).resolve_config(p, s);
+        *out = s.workspace_bytes(p, &cfg);
+    });
+}
+
+primkit_status primkit_find_convolution(primkit_handle* h, const primkit_conv_problem* pp,
+                                        const float* a, const float* b, size_t ws_bytes,
+                                        primkit_algo_perf* results, int capacity, int* out_count) {
+    return guarded([&] {
+        const primkit::ConvProblem p = to_problem(pp);
+        const auto [da, db] = operand_descs(p);
+        primkit::Handle& hd = H(h);
+        void* dva = hd.scratch(1, primkit::device_bytes(da));
+        void* dvb = hd.scratch(2, primkit::device_bytes(db));
+        primkit::upload_nchw(hd, da, need(a, "operand a"), dva);
+        primkit::upload_nchw(hd, db, need(b, "operand b"), dvb);
+        const auto perf = hd.find_convolution(p, dva, dvb, ws_bytes);
+        *out_count = static_cast<int>(perf.size());
+        const int n = std::min(capacity, *out_count);
+        for (int i = 0; i < n; ++i) {
+            const auto& src = perf[static_cast<size_t>(i)];
+            copy_name(results[i].solver_name, sizeof(results[i].solver_name), src.solver_name);
+            results[i].algo = static_cast<primkit_conv_algo>(src.algo);
+            results[i].time_ms = src.time_ms;
+            results[i].workspace_bytes = src.workspace_bytes;
+        }
+    });
+}
+
+primkit_status primkit_conv_run(primkit_handle* h, const primkit_conv_problem* pp,
+                                const char* solver_name, const float* a, const float* b,
+                                float* output, size_t ws_bytes) {
+    return guarded([&] {
+        const primkit::ConvProblem p = to_problem(pp);
+        const primkit::Solver& solver = select_solver(h, p, solver_name);
+        primkit::Handle& hd = H(h);
+        const primkit::PerfConfig cfg = hd.resolve_config(p, solver);
+        if (solver.workspace_bytes(p, &cfg) > ws_bytes)
+            primkit::throw_error(primkit::ErrorCode::WorkspaceTooSmall,
+                                 "workspace too small for " + solver.name());
+        const auto [da, db] = operand_descs(p);
+        const primkit::TensorDescriptor dr = result_desc(p);
+        void* dva = hd.scratch(1, primkit::device_bytes(da));
+        void* dvb = hd.scratch(2, primkit::device_bytes(db));
+        void* dvo = hd.scratch(3, primkit::device_bytes(dr));
+        primkit::upload_nchw(hd, da, need(a, "operand a"), dva);
+        primkit::upload_nchw(hd, db, need(b, "operand b"), dvb);
+        auto plan = hd.cached_build(p, solver, &cfg);
+        const size_t dws = plan->device_workspace_bytes();
+        void* ws = hd.scratch(0, dws);
+        if (hd.device_timing())
+            hd.record_device_ms(hd.time_ms([&] { plan->run(hd, dva, dvb, dvo, ws, dws); }));
+        else
+            plan->run(hd, dva, dvb, dvo, ws, dws);
+        primkit::download_nchw(hd, dr, dvo, need(output, "output"));
+    });
+}
+
+primkit_status primkit_tune(primkit_handle* h, const primkit_conv_problem* pp,
+                            const char* solver_name, int64_t budget, int exhaustive,
+                            int64_t* evals) {
+    return guarded([&] {
+        const primkit::ConvProblem p = to_problem(pp);
+        const primkit::Solver& s = solver_named(h, solver_name);
+        if (budget <= 0) budget = primkit::default_tune_budget(s, p);
+        const primkit::TuneResult r = primkit::tune(H(h), s, p, budget, exhaustive != 0);
+        if (evals) *evals = r.evaluations;
+    });
+}
+
+primkit_status primkit_perfdb_save(primkit_handle* h, const char* path) {
+    return guarded([&] { H(h).perfdb().save(need(path, "path")); });
+}
+
+primkit_status primkit_perfdb_load(primkit_handle* h, const char* path) {
+    return guarded([&] { H(h).perfdb() = primkit::PerfDb::load(need(path, "path")); });
+}
+
+primkit_status primkit_fusion_plan_create(const int64_t dims[4], primkit_element_type et,
+                                          primkit_fusion_plan** out) {
+    return guarded([&] {
+        need(out, "plan output");
+        *out = new primkit_fusion_plan{primkit::FusionPlan(dims4(dims, et))};
+    });
+}
+
+void primkit_fusion_plan_destroy(primkit_fusion_plan* plan) { delete plan; }
+
+primkit_status primkit_fusion_add_conv(primkit_fusion_plan* plan, const int64_t fd[4],
+                                       int64_t pad_h, int64_t pad_w, int64_t stride_h,
+                                       int64_t stride_w, int64_t groups, primkit_conv_algo algo) {
+    return guarded([&] {
+        primkit::ConvDescriptor cv;
+        cv.pad_h = pad_h;
+        cv.pad_w = pad_w;
+        cv.stride_h = stride_h;
+        cv.stride_w = stride_w;
+        cv.group_count = groups;
+        primkit::FusionPlan& pl = P(plan);
+        pl.add_op(primkit::FusionOp::conv_forward(
+            cv, dims4(fd, static_cast<primkit_element_type>(pl.input_desc().etype)),
+            static_cast<primkit::ConvAlgo>(algo)));
+    });
+}
+
+primkit_status primkit_fusion_add_bias(primkit_fusion_plan* plan, int64_t channels) {
+    return guarded([&] { P(plan).add_op(primkit::FusionOp::bias(channels)); });
+}
+
+primkit_status primkit_fusion_add_batchnorm(primkit_fusion_plan* plan, primkit_batchnorm_mode m) {
+    return guarded([&] {
+        P(plan).add_op(primkit::FusionOp::batchnorm_inference(
+            m == PRIMKIT_BN_PER_ACTIVATION ? primkit::BatchNormMode::PerActivation
+                                           : primkit::BatchNormMode::Spatial));
+    });
+}
+
+primkit_status primkit_fusion_add_activation(primkit_fusion_plan* plan, primkit_activation kind,
+                                             float alpha) {
+    return guarded([&] {
+        primkit::ActivationKind act;
+        switch (kind) {
+            case PRIMKIT_ACT_RELU: act = {primkit::ActivationKind::Tag::ReLU, 0.0f}; break;
+            case PRIMKIT_ACT_LEAKY_RELU: act = {primkit::ActivationKind::Tag::LeakyReLU, alpha}; break;
+            case PRIMKIT_ACT_SIGMOID: act = {primkit::ActivationKind::Tag::Sigmoid, 0.0f}; break;
+            case PRIMKIT_ACT_TANH: act = {primkit::ActivationKind::Tag::Tanh, 0.0f}; break;
+            default: primkit::throw_error(primkit::ErrorCode::InvalidValue, "unknown activation kind");
+        }
+        P(plan).add_op(primkit::FusionOp::activation(act));
+    });
+}
+
+primkit_status primkit_fusion_compile(primkit_handle* h, primkit_fusion_plan* plan) {
+    return guarded([&] { primkit::fusion_compile(H(h), P(plan)); });
+}
+
+primkit_status primkit_fusion_output_dims(primkit_fusion_plan* plan, int64_t dims[4]) {
+    return guarded([&] {
+        const auto& d = P(plan).output_desc().dims;
+        for (int i = 0; i < 4; ++i) dims[i] = d[static_cast<size_t>(i)];
+    });
+}
+
+primkit_status primkit_fusion_set_args(primkit_fusion_plan* plan, const float* filter,
+                                       const float* bias, const float* g, const float* b,
+                                       const float* mean, const float* var, float eps,
+                                       const float* act_alpha) {
+    return guarded([&] {
+        primkit::FusionPlan& pl = P(plan);
+        primkit::FusionArgs args;
+        primkit::TensorDescriptor cur = pl.input_desc();
+        using K = primkit::FusionOp::Kind;
+        for (const primkit::FusionOp& op : pl.ops()) {
+            switch (op.kind) {
+                case K::ConvForward:
+                    if (filter) args.filter = host_tensor(op.filter_desc, filter);
+                    cur = primkit::output_dims(cur, op.filter_desc, op.conv);
+                    break;
+                case K::Bias:
+                    if (bias) args.bias = host_tensor(primkit::TensorDescriptor::packed({op.bias_channels}), bias);
+                    break;
+                case K::BatchNormInference: {
+                    const primkit::TensorDescriptor shape =
+                        op.bn_mode == primkit::BatchNormMode::Spatial
+                            ? primkit::TensorDescriptor::packed({1, cur.dims[1], 1, 1})
+                            : primkit::TensorDescriptor::packed({1, cur.dims[1], cur.dims[2], cur.dims[3]});
+                    // flat f32 parameter vectors
+                    const auto flat = primkit::TensorDescriptor::packed({shape.elem_count()});
+                    if (g) args.bn_gamma = host_tensor(flat, g);
+                    if (b) args.bn_beta = host_tensor(flat, b);
+                    if (mean) args.bn_mean = host_tensor(flat, mean);
+                    if (var) args.bn_var = host_tensor(flat, var);
+                    args.bn_epsilon = eps;
+                    break;
+                }
+                case K::Activation: break;
+            }
+        }
+        if (act_alpha) args.act_alpha = *act_alpha;
+        pl.set_args(std::move(args));
+    });
+}
+
+primkit_status primkit_fusion_execute(primkit_handle* h, primkit_fusion_plan* plan,
+                                      const float* input, float* output, int unfused) {
+    return guarded([&] {
+        primkit::FusionPlan& pl = P(plan);
+        primkit::Handle& hd = H(h);
+        if (!pl.compiled())
+            primkit::throw_error(primkit::ErrorCode::NotCompiled, "fusion plan is not compiled");
+        // bindings are validated before any device work (MissingArgs is a
+        // host-side error in the reference too)
+        {
+            const auto& a = pl.args();
+            for (const auto& op : pl.ops()) {
+                using K = primkit::FusionOp::Kind;
+                if (op.kind == K::ConvForward && !a.filter)
+                    primkit::throw_error(primkit::ErrorCode::MissingArgs, "filter not bound");
+                if (op.kind == K::Bias && !a.bias)
+                    primkit::throw_error(primkit::ErrorCode::MissingArgs, "bias not bound");
+                if (op.kind == K::BatchNormInference &&
+                    (!a.bn_gamma || !a.bn_beta || !a.bn_mean || !a.bn_var))
+                    primkit::throw_error(primkit::ErrorCode::MissingArgs,
+                                         "batchnorm parameters not bound");
+            }
+        }
+        const primkit::TensorDescriptor& din = pl.input_desc();
+        const primkit::TensorDescriptor dout = primkit::TensorDescriptor::packed(
+            pl.output_desc().dims, din.etype);
+        void* dvi = hd.scratch(1, primkit::device_bytes(din));
+        void* dvo = hd.scratch(2, primkit::device_bytes(dout));
+        primkit::upload_nchw(hd, din, need(input, "input"), dvi);
+        auto run = [&] {
+            if (unfused)
+                primkit::fusion_execute_unfused(hd, pl, dvi, dvo);
+            else
+                primkit::fusion_execute(hd, pl, dvi, dvo);
+        };
+        if (hd.device_timing())
+            hd.record_device_ms(hd.time_ms(run));
+        else
+            run();
+        primkit::download_nchw(hd, dout, dvo, need(output, "output"));
+    });
+}
+
+// ---- section 2 --------------------------------------------------------------
+
+primkit_status primkit_handle_create_with_stream(void* stream, int device, primkit_handle** out) {
+    return guarded([&] {
+        need(out, "handle output");
+        *out = new primkit_handle(static_cast<cudaStream_t>(stream), device);
+    });
+}
+
+primkit_status primkit_handle_set_stream(primkit_handle* h, void* stream) {
+    return guarded([&] { H(h).set_stream(static_cast<cudaStream_t>(stream)); });
+}
+
+int64_t primkit_channel_pitch(int64_t c) { return (c + 7) / 8 * 8; }
+
+primkit_status primkit_conv_device_workspace(primkit_handle* h, const primkit_conv_problem* pp,
+                                             const char* solver_name, uint64_t* out) {
+    return guarded([&] {
+        const primkit::ConvProblem p = to_problem(pp);
+        const primkit::Solver& s = select_solver(h, p, solver_name);
+        auto plan = H(h).cached_build(p, s, nullptr);
+        *need(out, "output") = plan->device_workspace_bytes();
+    });
+}
+
+primkit_status primkit_conv_run_device(primkit_handle* h, const primkit_conv_problem* pp,
+                                       const char* solver_name, const void* a, const void* b,
+                                       void* output, void* workspace, size_t ws_bytes) {
+    return guarded([&] {
+        const primkit::ConvProblem p = to_problem(pp);
+        const primkit::Solver& s = select_solver(h, p, solver_name);
+        auto plan = H(h).cached_build(p, s, nullptr);
+        plan->run(H(h), need(a, "operand a"), need(b, "operand b"), need(output, "output"),
+                  workspace, ws_bytes);
+    });
+}
+
+primkit_status primkit_fusion_execute_device(primkit_handle* h, primkit_fusion_plan* plan,
+                                             const void* input, void* output, int unfused) {
+    return guarded([&] {
+        if (unfused)
+            primkit::fusion_execute_unfused(H(h), P(plan), need(input, "input"), need(output, "output"));
+        else
+            primkit::fusion_execute(H(h), P(plan), need(input, "input"), need(output, "output"));
+    });
+}
+
+primkit_status primkit_batchnorm_forward_train(primkit_handle* h, primkit_batchnorm_mode mode,
+                                               const int64_t dims[4], primkit_element_type et,
+                                               const float* x, const float* gamma,
+                                               const float* beta, float* running_mean,
+                                               float* running_var, float eps, float momentum,
+                                               float* y, float* saved_mean, float* saved_invstd) {
+    return guarded([&] {
+        if (eps <= 0.0f)
+            primkit::throw_error(primkit::ErrorCode::InvalidEpsilon, "epsilon must be positive");
+        const primkit::TensorDescriptor d = dims4(dims, et);
+        primkit::Handle& hd = H(h);
+        const std::int64_t ns = bn_stat_count(mode, dims);
+        const int per_act = mode == PRIMKIT_BN_PER_ACTIVATION;
+        const int n = (int)dims[0], c = (int)dims[1], hw = (int)(dims[2] * dims[3]);
+        void* dx = hd.scratch(1, primkit::device_bytes(d));
+        void* dy = hd.scratch(2, primkit::device_bytes(d));
+        float* par = static_cast<float*>(hd.scratch(6, (size_t)ns * 6 * 4));
+        void* scratch = hd.scratch(7, pk_bn_scratch_bytes(n, c, hw, per_act));
+        primkit::upload_nchw(hd, d, need(x, "x"), dx);
+        const size_t vb = (size_t)ns * 4;
+        auto up = [&](float* dst, const float* src) {
+            primkit::check_cuda(cudaMemcpyAsync(dst, need(src, "parameter"), vb,
+                                                cudaMemcpyHostToDevice, hd.stream()),
+                                "cudaMemcpyAsync");
+        };
+        up(par, gamma);
+        up(par + ns, beta);
+        up(par + 2 * ns, running_mean);
+        up(par + 3 * ns, running_var);
+        primkit::check_cuda(
+            pk_cuda_bn_fwd_train(dx, dy, n, c, hw, pk_pitch(c),
+                                 et == PRIMKIT_BF16 ? PK_BF16 : PK_F32, per_act, par, par + ns,
+                                 par + 2 * ns, par + 3 * ns, eps, momentum, par + 4 * ns,
+                                 par + 5 * ns, 0, scratch, hd.stream()),
+            "bn_fwd_train");
+        primkit::download_nchw(hd, d, dy, need(y, "y"));
+        auto down = [&](float* dst, const float* src) {
+            primkit::check_cuda(cudaMemcpyAsync(need(dst, "output"), src, vb,
+                                                cudaMemcpyDeviceToHost, hd.stream()),
+                                "cudaMemcpyAsync");
+        };
+        down(running_mean, par + 2 * ns);
+        down(running_var, par + 3 * ns);
+        down(saved_mean, par + 4 * ns);
+        down(saved_invstd, par + 5 * ns);
+        hd.sync();
+    });
+}
+
+primkit_status primkit_batchnorm_forward_infer(primkit_handle* h, primkit_batchnorm_mode mode,
+                                               const int64_t dims[4], primkit_element_type et,
+                                               const float* x, const float* gamma,
+                                               const float* beta, const float* running_mean,
+                                               const float* running_var, float eps, float* y) {
+    return guarded([&] {
+        if (eps <= 0.0f)
+            primkit::throw_error(primkit::ErrorCode::InvalidEpsilon, "epsilon must be positive");
+        const primkit::TensorDescriptor d = dims4(dims, et);
+        primkit::Handle& hd = H(h);
+        const std::int64_t ns = bn_stat_count(mode, dims);
+        const int n = (int)dims[0], c = (int)dims[1], hw = (int)(dims[2] * dims[3]);
+        void* dx = hd.scratch(1, primkit::device_bytes(d));
+        void* dy = hd.scratch(2, primkit::device_bytes(d));
+        float* par = static_cast<float*>(hd.scratch(6, (size_t)ns * 4 * 4));
+        primkit::upload_nchw(hd, d, need(x, "x"), dx);
+        const float* src[4] = {gamma, beta, running_mean, running_var};
+        for (int i = 0; i < 4; ++i)
+            primkit::check_cuda(cudaMemcpyAsync(par + i * ns, need(src[i], "parameter"),
+                                                (size_t)ns * 4, cudaMemcpyHostToDevice,
+                                                hd.stream()),
+                                "cudaMemcpyAsync");
+        pk_epilogue e{};
+        e.act = -1;
+        e.bn_gamma = par;
+        e.bn_beta = par + ns;
+        e.bn_mean = par + 2 * ns;
+        e.bn_var = par + 3 * ns;
+        e.bn_per_activation = mode == PRIMKIT_BN_PER_ACTIVATION;
+        e.bn_standalone = 1;
+        e.bn_eps = eps;
+        primkit::check_cuda(pk_cuda_pointwise(dx, dy, n, c, hw, pk_pitch(c),
+                                              et == PRIMKIT_BF16 ? PK_BF16 : PK_F32, &e,
+                                              hd.stream()),
+                            "pointwise");
+        primkit::download_nchw(hd, d, dy, need(y, "y"));
+    });
+}
+
+primkit_status primkit_batchnorm_backward(primkit_handle* h, primkit_batchnorm_mode mode,
+                                          const int64_t dims[4], primkit_element_type et,
+                                          const float* x, const float* dy, const float* gamma,
+                                          const float* saved_mean, const float* saved_invstd,
+                                          float* dx, float* dgamma, float* dbeta) {
+    return guarded([&] {
+        const primkit::TensorDescriptor d = dims4(dims, et);
+        primkit::Handle& hd = H(h);
+        const std::int64_t ns = bn_stat_count(mode, dims);
+        const int per_act = mode == PRIMKIT_BN_PER_ACTIVATION;
+        const int n = (int)dims[0], c = (int)dims[1], hw = (int)(dims[2] * dims[3]);
+        void* dvx = hd.scratch(1, primkit::device_bytes(d));
+        void* dvdy = hd.scratch(2, primkit::device_bytes(d));
+        void* dvdx = hd.scratch(3, primkit::device_bytes(d));
+        float* par = static_cast<float*>(hd.scratch(6, (size_t)ns * 5 * 4));
+        void* scratch = hd.scratch(7, pk_bn_scratch_bytes(n, c, hw, per_act));
+        primkit::upload_nchw(hd, d, need(x, "x"), dvx);
+        primkit::upload_nchw(hd, d, need(dy, "dy"), dvdy);
+        const float* src[3] = {gamma, saved_mean, saved_invstd};
+        for (int i = 0; i < 3; ++i)
+            primkit::check_cuda(cudaMemcpyAsync(par + i * ns, need(src[i], "parameter"),
+                                                (size_t)ns * 4, cudaMemcpyHostToDevice,
+                                                hd.stream()),
+                                "cudaMemcpyAsync");
+        primkit::check_cuda(
+            pk_cuda_bn_bwd(dvx, nullptr, dvdy, dvdx, n, c, hw, pk_pitch(c),
+                           et == PRIMKIT_BF16 ? PK_BF16 : PK_F32, per_act, par, par + ns,
+                           par + 2 * ns, par + 3 * ns, par + 4 * ns, 0, et == PRIMKIT_BF16,
+                           scratch, hd.stream()),
+            "bn_bwd");
+        primkit::download_nchw(hd, d, dvdx, need(dx, "dx"));
+        primkit::check_cuda(cudaMemcpyAsync(need(dgamma, "dgamma"), par + 3 * ns, (size_t)ns * 4,
+                                            cudaMemcpyDeviceToHost, hd.stream()),
+                            "cudaMemcpyAsync");
+        primkit::check_cuda(cudaMemcpyAsync(need(dbeta, "dbeta"), par + 4 * ns, (size_t)ns * 4,
+                                            cudaMemcpyDeviceToHost, hd.stream()),
+                            "cudaMemcpyAsync");
+        hd.sync();
+    });
+}
+
+primkit_status primkit_batchnorm_forward_train_device(
+    primkit_handle* h, const int64_t dims[4], primkit_element_type et, const void* x,
+    const float* gamma, const float* beta, float* running_mean, float* running_var, float eps,
+    float momentum, void* y, float* saved_mean, float* saved_invstd, int relu) {
+    return guarded([&] {
+        if (eps <= 0.0f)
+            primkit::throw_error(primkit::ErrorCode::InvalidEpsilon, "epsilon must be positive");
+        primkit::Handle& hd = H(h);
+        hd.activate();
+        const int n = (int)dims[0], c = (int)dims[1], hw = (int)(dims[2] * dims[3]);
+        void* scratch = hd.scratch(7, pk_bn_scratch_bytes(n, c, hw, 0));
+        primkit::check_cuda(pk_cuda_bn_fwd_train(x, y, n, c, hw, pk_pitch(c),
+                                                 et == PRIMKIT_BF16 ? PK_BF16 : PK_F32, 0, gamma,
+                                                 beta, running_mean, running_var, eps, momentum,
+                                                 saved_mean, saved_invstd, relu, scratch,
+                                                 hd.stream()),
+                            "bn_fwd_train");
+    });
+}
+
+primkit_status primkit_batchnorm_backward_device(
+    primkit_handle* h, const int64_t dims[4], primkit_element_type et, const void* x,
+    const void* y, const void* dy, const float* gamma, const float* beta,
+    const float* saved_mean, const float* saved_invstd, void* dx, float* dgamma, float* dbeta,
+    int relu) {
+    (void)beta;
+    return guarded([&] {
+        primkit::Handle& hd = H(h);
+        hd.activate();
+        const int n = (int)dims[0], c = (int)dims[1], hw = (int)(dims[2] * dims[3]);
+        void* scratch = hd.scratch(7, pk_bn_scratch_bytes(n, c, hw, 0));
+        primkit::check_cuda(pk_cuda_bn_bwd(x, y, dy, dx, n, c, hw, pk_pitch(c),
+                                           et == PRIMKIT_BF16 ? PK_BF16 : PK_F32, 0, gamma,
+                                           saved_mean, saved_invstd, dgamma, dbeta, relu, 0,
+                                           scratch, hd.stream()),
+                            "bn_bwd");
+    });
+}
+
+primkit_status primkit_activation_forward(primkit_handle* h, primkit_activation kind, float alpha,
+                                          const int64_t dims[4], primkit_element_type et,
+                                          const float* x, float* y) {
+    return guarded([&] {
+        if (kind == PRIMKIT_ACT_LEAKY_RELU && alpha < 0.0f)
+            primkit::throw_error(primkit::ErrorCode::InvalidValue, "LeakyReLU alpha must be >= 0");
+        const primkit::TensorDescriptor d = dims4(dims, et);
+        primkit::Handle& hd = H(h);
+        void* dx = hd.scratch(1, primkit::device_bytes(d));
+        void* dy = hd.scratch(2, primkit::device_bytes(d));
+        primkit::upload_nchw(hd, d, need(x, "x"), dx);
+        pk_epilogue e{};
+        e.act = static_cast<int>(kind);
+        e.act_alpha = alpha;
+        const int c = (int)dims[1];
+        primkit::check_cuda(pk_cuda_pointwise(dx, dy, (int)dims[0], c, (int)(dims[2] * dims[3]),
+                                              pk_pitch(c), et == PRIMKIT_BF16 ? PK_BF16 : PK_F32,
+                                              &e, hd.stream()),
+                            "pointwise");
+        primkit::download_nchw(hd, d, dy, need(y, "y"));
+    });
+}
+
+primkit_status primkit_activation_backward(primkit_handle* h, primkit_activation kind,
+                                           float alpha, const int64_t dims[4],
+                                           primkit_element_type et, const float* x,
+                                           const float* dy, float* dx) {
+    return guarded([&] {
+        const primkit::TensorDescriptor d = dims4(dims, et);
+        primkit::Handle& hd = H(h);
+        void* dvx = hd.scratch(1, primkit::device_bytes(d));
+        void* dvdy = hd.scratch(2, primkit::device_bytes(d));
+        void* dvdx = hd.scratch(3, primkit::device_bytes(d));
+        primkit::upload_nchw(hd, d, need(x, "x"), dvx);
+        primkit::upload_nchw(hd, d, need(dy, "dy"), dvdy);
+        const int c = (int)dims[1];
+        primkit::check_cuda(pk_cuda_activation_bwd(dvx, dvdy, dvdx, (int)dims[0], c,
+                                                   (int)(dims[2] * dims[3]), pk_pitch(c),
+                                                   et == PRIMKIT_BF16 ? PK_BF16 : PK_F32,
+                                                   static_cast<int>(kind), alpha, hd.stream()),
+                            "activation_bwd");
+        primkit::download_nchw(hd, d, dvdx, need(dx, "dx"));
+    });
+}
+
+primkit_status primkit_nchw_to_device(primkit_handle* h, const int64_t dims[4],
+                                      primkit_element_type et, const float* src, void* dst) {
+    return guarded([&] {
+        primkit::Handle& hd = H(h);
+        hd.activate();
+        const int c = (int)dims[1];
+        primkit::check_cuda(pk_cuda_nchw_to_nhwc(src, dst, (int)dims[0], c,
+                                                 (int)(dims[2] * dims[3]), pk_pitch(c),
+                                                 et == PRIMKIT_BF16 ? PK_BF16 : PK_F32,
+                                                 hd.stream()),
+                            "nchw_to_nhwc");
+    });
+}
+
+primkit_status primkit_device_to_nchw(primkit_handle* h, const int64_t dims[4],
+                                      primkit_element_type et, const void* src, float* dst) {
+    return guarded([&] {
+        primkit::Handle& hd = H(h);
+        hd.activate();
+        const int c = (int)dims[1];
+        primkit::check_cuda(pk_cuda_nhwc_to_nchw(src, dst, (int)dims[0], c,
+                                                 (int)(dims[2] * dims[3]), pk_pitch(c),
+                                                 et == PRIMKIT_BF16 ? PK_BF16 : PK_F32,
+                                                 hd.stream()),
+                            "nhwc_to_nchw");
+    });
+}
+
+primkit_status primkit_handle_kernel_launches(primkit_handle* h, uint64_t* out) {
+    return guarded([&] {
+        (void)H(h);
+        *need(out, "output") = pk_cuda_launch_count();
+    });
+}
+
+primkit_status primkit_handle_last_device_ms(primkit_handle* h, double* out) {
+    return guarded([&] { *need(out, "output") = H(h).last_device_ms(); });
+}
+
+primkit_status primkit_handle_last_kernel(primkit_handle* h, char* buf, size_t len) {
+    return guarded([&] { copy_name(buf, len, H(h).last_kernel); });
+}
+
+}  // extern "C"

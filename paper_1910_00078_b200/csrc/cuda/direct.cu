@@ -1,0 +1,227 @@
+// Direct convolution on CUDA cores (fp32 FMA), NHWC.
+//
+// Device counterpart of the reference's Direct algorithm
+// (proj/src/core/conv.cpp:99-173 forward / transpose, :716-756 backward data,
+// :816-850 backward weights). Same arithmetic (fp32 accumulate of x*w over
+// (c, y, x) with zero padding, groups, dilation), different schedule: lanes of
+// a warp own consecutive output pixels and share the filter taps, which are
+// warp-uniform loads served from L1.
+#include "common.cuh"
+
+namespace pk {
+
+// Forward / transpose-forward: thread = (output pixel, KT consecutive output
+// channels of one group).
+template <typename T, int KT>
+__global__ void __launch_bounds__(128) direct_fwd_kernel(pk_conv_geom g, const T* __restrict__ x,
+                                                         const T* __restrict__ f,
+                                                         T* __restrict__ y, pk_epilogue e) {
+    const long long pix = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long npix = (long long)g.n * g.p * g.q;
+    const int k0 = blockIdx.y * KT;
+    if (pix >= npix || k0 >= g.k) return;
+    const int ow = (int)(pix % g.q);
+    const int oh = (int)((pix / g.q) % g.p);
+    const int n = (int)(pix / ((long long)g.q * g.p));
+    const int grp = k0 / g.kg;
+    float acc[KT];
+#pragma unroll
+    for (int j = 0; j < KT; ++j) acc[j] = 0.0f;
+    const T* xn = x + (size_t)n * g.h * g.w * g.x_pitch + grp * g.cg;
+    for (int r = 0; r < g.r; ++r) {
+        int ih;
+        if (!g.transpose) {
+            ih = oh * g.str_h - g.pad_h + r * g.dil_h;
+            if (ih < 0 || ih >= g.h) continue;
+        } else {
+            const int num = oh + g.pad_h - r;
+            if (num < 0 || num % g.str_h) continue;
+            ih = num / g.str_h;
+            if (ih >= g.h) continue;
+        }
+        for (int s = 0; s < g.s; ++s) {
+            int iw;
+            if (!g.transpose) {
+                iw = ow * g.str_w - g.pad_w + s * g.dil_w;
+                if (iw < 0 || iw >= g.w) continue;
+            } else {
+                const int num = ow + g.pad_w - s;
+                if (num < 0 || num % g.str_w) continue;
+                iw = num / g.str_w;
+                if (iw >= g.w) continue;
+            }
+            const T* xp = xn + ((size_t)ih * g.w + iw) * g.x_pitch;
+            for (int c = 0; c < g.cg; ++c) {
+                const float xv = ld(xp + c);
+#pragma unroll
+                for (int j = 0; j < KT; ++j) {
+                    const int k = k0 + j;
+                    if (k >= g.k) break;
+                    size_t fi;
+                    if (!g.transpose)
+                        fi = (((size_t)k * g.r + r) * g.s + s) * g.f_pitch + c;
+                    else  // transpose filter [C][R][S][pitch(kg)]
+                        fi = ((((size_t)grp * g.cg + c) * g.r + r) * g.s + s) * g.f_pitch +
+                             (k - grp * g.kg);
+                    acc[j] += xv * ld(f + fi);
+                }
+            }
+        }
+    }
+    T* yp = y + (size_t)pix * g.y_pitch;
+    const bool epi = epilogue_active(&e);
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+        const int k = k0 + j;
+        if (k >= g.k) break;
+        st(yp + k, epi ? apply_epilogue(e, acc[j], k, oh, ow, g.p, g.q) : acc[j]);
+    }
+}
+
+// Backward data: thread = (input pixel, CT consecutive input channels of one
+// group), gathering over the output positions that read it.
+template <typename T, int CT>
+__global__ void __launch_bounds__(128) direct_bwd_data_kernel(pk_conv_geom g,
+                                                              const T* __restrict__ dy,
+                                                              const T* __restrict__ f,
+                                                              T* __restrict__ dx) {
+    const long long pix = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long npix = (long long)g.n * g.h * g.w;
+    const int c0 = blockIdx.y * CT;
+    if (pix >= npix || c0 >= g.c) return;
+    const int iw = (int)(pix % g.w);
+    const int ih = (int)((pix / g.w) % g.h);
+    const int n = (int)(pix / ((long long)g.w * g.h));
+    const int grp = c0 / g.cg;
+    const int cl0 = c0 - grp * g.cg;
+    float acc[CT];
+#pragma unroll
+    for (int j = 0; j < CT; ++j) acc[j] = 0.0f;
+    for (int r = 0; r < g.r; ++r) {
+        const int nh = ih + g.pad_h - r * g.dil_h;
+        if (nh < 0 || nh % g.str_h) continue;
+        const int oh = nh / g.str_h;
+        if (oh >= g.p) continue;
+        for (int s = 0; s < g.s; ++s) {
+            const int nw = iw + g.pad_w - s * g.dil_w;
+            if (nw < 0 || nw % g.str_w) continue;
+            const int ow = nw / g.str_w;
+            if (ow >= g.q) continue;
+            const T* dyp = dy + (((size_t)n * g.p + oh) * g.q + ow) * g.y_pitch + grp * g.kg;
+            for (int kk = 0; kk < g.kg; ++kk) {
+                const float dv = ld(dyp + kk);
+                const T* fp = f + (((size_t)(grp * g.kg + kk) * g.r + r) * g.s + s) * g.f_pitch;
+#pragma unroll
+                for (int j = 0; j < CT; ++j)
+                    if (cl0 + j < g.cg) acc[j] += dv * ld(fp + cl0 + j);
+            }
+        }
+    }
+    T* dxp = dx + (size_t)pix * g.x_pitch;
+#pragma unroll
+    for (int j = 0; j < CT; ++j)
+        if (cl0 + j < g.cg) st(dxp + c0 + j, acc[j]);
+}
+
+// Backward weights: block = (k, r, s, 32-channel slice); 8 warps split the
+// (n, p, q) reduction, lane = channel; fixed-order smem combine, so the result
+// is deterministic.
+template <typename T>
+__global__ void __launch_bounds__(256) direct_bwd_weights_kernel(pk_conv_geom g,
+                                                                 const T* __restrict__ dy,
+                                                                 const T* __restrict__ x,
+                                                                 T* __restrict__ dw) {
+    __shared__ float part[8][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cslices = (g.cg + 31) / 32;
+    int b = blockIdx.x;
+    const int cs = b % cslices;
+    b /= cslices;
+    const int s = b % g.s;
+    b /= g.s;
+    const int r = b % g.r;
+    const int k = b / g.r;
+    const int grp = k / g.kg;
+    const int c = cs * 32 + lane;
+    float acc = 0.0f;
+    const long long npq = (long long)g.n * g.p * g.q;
+    if (c < g.cg) {
+        for (long long i = warp; i < npq; i += 8) {
+            const int ow = (int)(i % g.q);
+            const int oh = (int)((i / g.q) % g.p);
+            const int n = (int)(i / ((long long)g.q * g.p));
+            const int ih = oh * g.str_h - g.pad_h + r * g.dil_h;
+            const int iw = ow * g.str_w - g.pad_w + s * g.dil_w;
+            if (ih < 0 || ih >= g.h || iw < 0 || iw >= g.w) continue;
+            acc += ld(dy + (size_t)i * g.y_pitch + k) *
+                   ld(x + (((size_t)n * g.h + ih) * g.w + iw) * g.x_pitch + grp * g.cg + c);
+        }
+    }
+    part[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0) {
+        float t = 0.0f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += part[w][lane];
+        T* out = dw + (((size_t)k * g.r + r) * g.s + s) * g.f_pitch;
+        if (c < g.cg)
+            st(out + c, t);
+        else if (c < g.f_pitch)
+            st(out + c, 0.0f);  // keep the zero pad lanes defined
+    }
+}
+
+}  // namespace pk
+
+using namespace pk;
+
+extern "C" {
+
+cudaError_t pk_cuda_direct_fwd(const pk_conv_geom* g, int dtype, const void* x, const void* f,
+                               void* y, const pk_epilogue* epi, cudaStream_t st) {
+    pk_epilogue none{};
+    none.act = -1;
+    const pk_epilogue e = epi ? *epi : none;
+    const long long npix = (long long)g->n * g->p * g->q;
+    const bool wide = (g->kg % 8) == 0;
+    const int kt = wide ? 8 : 1;
+    dim3 grid(ceil_div(npix, 128), ceil_div(g->k, kt));
+    PK_DISPATCH_DTYPE(dtype, T, {
+        if (wide)
+            direct_fwd_kernel<T, 8><<<grid, 128, 0, st>>>(*g, (const T*)x, (const T*)f, (T*)y, e);
+        else
+            direct_fwd_kernel<T, 1><<<grid, 128, 0, st>>>(*g, (const T*)x, (const T*)f, (T*)y, e);
+    });
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t pk_cuda_direct_bwd_data(const pk_conv_geom* g, int dtype, const void* dy,
+                                    const void* f, void* dx, cudaStream_t st) {
+    const long long npix = (long long)g->n * g->h * g->w;
+    const bool wide = (g->cg % 8) == 0;
+    const int ct = wide ? 8 : 1;
+    dim3 grid(ceil_div(npix, 128), ceil_div(g->c, ct));
+    PK_DISPATCH_DTYPE(dtype, T, {
+        if (wide)
+            direct_bwd_data_kernel<T, 8>
+                <<<grid, 128, 0, st>>>(*g, (const T*)dy, (const T*)f, (T*)dx);
+        else
+            direct_bwd_data_kernel<T, 1>
+                <<<grid, 128, 0, st>>>(*g, (const T*)dy, (const T*)f, (T*)dx);
+    });
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t pk_cuda_direct_bwd_weights(const pk_conv_geom* g, int dtype, const void* dy,
+                                       const void* x, void* dw, cudaStream_t st) {
+    const long long blocks = (long long)g->k * g->r * g->s * ((g->cg + 31) / 32);
+    PK_DISPATCH_DTYPE(dtype, T,
+                      direct_bwd_weights_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(
+                          *g, (const T*)dy, (const T*)x, (T*)dw));
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // extern "C"

@@ -1,0 +1,160 @@
+// Internal host -> device boundary of primkit-b200.
+//
+// The C++ host layer only ever calls the extern "C" pk_cuda_* launchers
+// declared here: POD argument structs, raw device pointers and a
+// cudaStream_t, returning cudaError_t. No C++ or torch types cross this line.
+//
+// Device layout:
+//   activations  NHWC, channel pitch = pk_pitch(C) (zero padded lanes)
+//   filters      [K][R][S][pitch(C/groups)]   (transpose: [C][R][S][pitch(K/groups)])
+//   element type f32 or bf16 storage; arithmetic is always fp32 (SIMT FMA or
+//                tcgen05 with an fp32 TMEM accumulator).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum pk_dtype { PK_F32 = 0, PK_BF16 = 1 };
+
+static inline int pk_pitch(int c) { return (c + 7) / 8 * 8; }
+
+// One convolution instance in device terms (shapes are those of the forward
+// convolution even for the backward passes).
+typedef struct pk_conv_geom {
+    int n, c, h, w;          // input image
+    int k, r, s;             // filter: output channels, rows (y), cols (x)
+    int p, q;                // output image
+    int pad_h, pad_w, str_h, str_w, dil_h, dil_w;
+    int groups, cg, kg;      // channels per group
+    int x_pitch;             // channel pitch of the input activations
+    int y_pitch;             // channel pitch of the output activations
+    int f_pitch;             // innermost filter pitch
+    int transpose;           // 1 = transpose-mode forward
+} pk_conv_geom;
+
+// Epilogue applied to the fp32 accumulator before the single store:
+// bias -> batch-norm inference -> activation (reference order,
+// proj/src/core/fusion.cpp:384-398). Null pointers / act < 0 disable a stage.
+typedef struct pk_epilogue {
+    const float* bias;       // [K]
+    const float* bn_mean;    // [K] (spatial) or [K*P*Q] (per activation)
+    const float* bn_var;
+    const float* bn_gamma;
+    const float* bn_beta;
+    int bn_per_activation;
+    int bn_standalone;       // 1: gamma*(x-mu)*(1/sqrt(var+eps))+beta (primitives.cpp:105-108)
+                             // 0: (x-mu)/sqrt(var+eps)*gamma+beta    (fusion.cpp:390-394)
+    float bn_eps;
+    int act;                 // -1 none, 0 ReLU, 1 LeakyReLU, 2 Sigmoid, 3 Tanh
+    float act_alpha;
+} pk_epilogue;
+
+// ---- layout conversion ------------------------------------------------------
+// NCHW f32 [n][c][hw] <-> NHWC [n][hw][pitch] of dtype (RNE on bf16 stores).
+cudaError_t pk_cuda_nchw_to_nhwc(const float* src, void* dst, int n, int c, int hw, int pitch,
+                                 int dtype, cudaStream_t st);
+cudaError_t pk_cuda_nhwc_to_nchw(const void* src, float* dst, int n, int c, int hw, int pitch,
+                                 int dtype, cudaStream_t st);
+// Filter [K][R][S][f_pitch] -> dgrad operand [C][R][S][pitch(K)] (same dtype).
+cudaError_t pk_cuda_filter_to_dgrad(const pk_conv_geom* g, int dtype, const void* f, void* dst,
+                                    cudaStream_t st);
+
+// ---- Direct (SIMT fp32) -------------------------------------------------------
+cudaError_t pk_cuda_direct_fwd(const pk_conv_geom* g, int dtype, const void* x, const void* f,
+                               void* y, const pk_epilogue* epi, cudaStream_t st);
+cudaError_t pk_cuda_direct_bwd_data(const pk_conv_geom* g, int dtype, const void* dy,
+                                    const void* f, void* dx, cudaStream_t st);
+cudaError_t pk_cuda_direct_bwd_weights(const pk_conv_geom* g, int dtype, const void* dy,
+                                       const void* x, void* dw, cudaStream_t st);
+
+// ---- im2col / col2im + GEMM (Im2colGemm solver) ------------------------------
+// col[(p,q)][(r,s,c)] for one (image, group); row pitch = r*s*f_pitch
+// (zero in padded lanes), element type dtype.
+cudaError_t pk_cuda_im2col(const pk_conv_geom* g, int dtype, const void* x, int image, int group,
+                           void* col, cudaStream_t st);
+// dx[image][:, group channels] = col2im(col), col fp32 [(p,q)][(r,s,c)] with
+// row pitch r*s*f_pitch (gather formulation: no atomics, overwrites dx).
+cudaError_t pk_cuda_col2im(const pk_conv_geom* g, int dtype, const float* col, int image,
+                           int group, void* dx, cudaStream_t st);
+// Transpose mode: out[image][oh][ow][group*kg + kk] = sum over taps of
+// col[((r*S + s)*f_pitch + kk) * (H*W) + h*W + w] with oh = h*str - pad + r.
+cudaError_t pk_cuda_col2im_transpose(const pk_conv_geom* g, int dtype, const float* col,
+                                     int image, int group, void* out, cudaStream_t st);
+// Strided SIMT GEMM, fp32 arithmetic:
+//   C[i*ldc + j] (+)= sum_l A[i*sam + l*sak] * B[l*sbk + j*sbn]
+// A/B element type dtype_ab; C is fp32 (accumulate != 0 adds to C).
+cudaError_t pk_cuda_gemm_simt(int m, int n, int k, int dtype_ab, const void* a, long long sam,
+                              long long sak, const void* b, long long sbk, long long sbn,
+                              float* c, long long ldc, int accumulate, cudaStream_t st);
+// dst[i*dst_pitch + j] = (dtype) src[i*ld + j] for i<rows, j<cols, with the
+// epilogue applied per column (column = output channel).
+cudaError_t pk_cuda_store_rows(const float* src, int rows, int cols, long long ld, void* dst,
+                               long long dst_pitch, int dtype, const pk_epilogue* epi,
+                               int chan_offset, cudaStream_t st);
+
+// ---- SIMT implicit GEMM forward (fp32 arithmetic, any shape/groups/dilation)
+cudaError_t pk_cuda_igemm_simt_fwd(const pk_conv_geom* g, int dtype, const void* x, const void* f,
+                                   void* y, const pk_epilogue* epi, cudaStream_t st);
+
+// ---- Winograd F(2x2,3x3) (SIMT, zero workspace) -------------------------------
+cudaError_t pk_cuda_winograd_f23(const pk_conv_geom* g, int dtype, const void* x, const void* f,
+                                 void* y, const pk_epilogue* epi, cudaStream_t st);
+
+// ---- FFT convolution (complex<double>, radix-2, pow2 planes) -----------------
+size_t pk_cuda_fft_scratch_bytes(const pk_conv_geom* g);
+cudaError_t pk_cuda_fft_fwd(const pk_conv_geom* g, int dtype, const void* x, const void* f,
+                            void* y, void* scratch, cudaStream_t st);
+
+// ---- tcgen05 implicit GEMM (bf16 in, fp32 TMEM accumulate) -------------------
+typedef struct pk_tc_config {
+    int block_n;     // output-channel tile: 32..256 (multiple of 16)
+    int stages;      // smem pipeline depth
+    int raster;      // M-tile group width for L2-friendly rasterisation
+} pk_tc_config;
+// 1 if the tensor-core path supports this geometry (groups == 1, bf16, ...).
+int pk_tc_fwd_supported(const pk_conv_geom* g);
+int pk_tc_dgrad_supported(const pk_conv_geom* g);
+int pk_tc_wgrad_supported(const pk_conv_geom* g);
+size_t pk_tc_dgrad_workspace(const pk_conv_geom* g);
+size_t pk_tc_wgrad_workspace(const pk_conv_geom* g, int num_sms);
+cudaError_t pk_cuda_igemm_tc_fwd(const pk_conv_geom* g, const void* x, const void* f, void* y,
+                                 const pk_epilogue* epi, const pk_tc_config* cfg,
+                                 cudaStream_t st);
+cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const void* f, void* dx,
+                                   void* workspace, const pk_tc_config* cfg, cudaStream_t st);
+cudaError_t pk_cuda_igemm_tc_wgrad(const pk_conv_geom* g, const void* dy, const void* x, void* dw,
+                                   void* workspace, int num_sms, const pk_tc_config* cfg,
+                                   cudaStream_t st);
+
+// ---- pointwise / batch-norm ----------------------------------------------------
+// y = epilogue(x + 0) elementwise over NHWC (bias/bn/act all optional).
+cudaError_t pk_cuda_pointwise(const void* x, void* y, int n, int c, int hw, int pitch, int dtype,
+                              const pk_epilogue* epi, cudaStream_t st);
+cudaError_t pk_cuda_activation_bwd(const void* x, const void* dy, void* dx, int n, int c, int hw,
+                                   int pitch, int dtype, int act, float alpha, cudaStream_t st);
+// Training-mode batch-norm over NHWC. Spatial mode reduces over n*hw per
+// channel; per-activation mode (per_act=1) reduces over n per (c, hw).
+// scratch: pk_bn_scratch_bytes(); stats are reduced deterministically.
+size_t pk_bn_scratch_bytes(int n, int c, int hw, int per_act);
+cudaError_t pk_cuda_bn_fwd_train(const void* x, void* y, int n, int c, int hw, int pitch,
+                                 int dtype, int per_act, const float* gamma, const float* beta,
+                                 float* running_mean, float* running_var, float eps,
+                                 float momentum, float* saved_mean, float* saved_invstd,
+                                 int relu, void* scratch, cudaStream_t st);
+cudaError_t pk_cuda_bn_bwd(const void* x, const void* y, const void* dy, void* dx, int n, int c,
+                           int hw, int pitch, int dtype, int per_act, const float* gamma,
+                           const float* saved_mean, const float* saved_invstd, float* dgamma,
+                           float* dbeta, int relu, int round_params_bf16, void* scratch,
+                           cudaStream_t st);
+
+// Launch accounting: number of kernels this library launched (process-wide).
+uint64_t pk_cuda_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif

@@ -1,0 +1,208 @@
+// Layout conversion and pointwise kernels (HBM-bound; coalesced through a
+// shared-memory transpose tile, one pass over the data).
+#include <atomic>
+
+#include "common.cuh"
+
+namespace pk {
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+// [n][c][hw] f32 -> [n][hw][pitch] T. Tile: 32 channels x 32 pixels.
+template <typename T>
+__global__ void __launch_bounds__(256) nchw_to_nhwc_kernel(const float* __restrict__ src,
+                                                           T* __restrict__ dst, int c, int hw,
+                                                           int pitch) {
+    __shared__ float tile[32][33];
+    const int n = blockIdx.z;
+    const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    const float* s = src + (size_t)n * c * hw;
+    T* d = dst + (size_t)n * hw * pitch;
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int ch = c0 + i, px = p0 + threadIdx.x;
+        tile[i][threadIdx.x] = (ch < c && px < hw) ? s[(size_t)ch * hw + px] : 0.0f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int px = p0 + i, ch = c0 + threadIdx.x;
+        if (px < hw && ch < pitch) st(d + (size_t)px * pitch + ch, tile[threadIdx.x][i]);
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) nhwc_to_nchw_kernel(const T* __restrict__ src,
+                                                           float* __restrict__ dst, int c, int hw,
+                                                           int pitch) {
+    __shared__ float tile[32][33];
+    const int n = blockIdx.z;
+    const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+    const T* s = src + (size_t)n * hw * pitch;
+    float* d = dst + (size_t)n * c * hw;
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int px = p0 + i, ch = c0 + threadIdx.x;
+        tile[i][threadIdx.x] = (px < hw && ch < c) ? ld(s + (size_t)px * pitch + ch) : 0.0f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int ch = c0 + i, px = p0 + threadIdx.x;
+        if (ch < c && px < hw) d[(size_t)ch * hw + px] = tile[threadIdx.x][i];
+    }
+}
+
+template <typename T>
+__global__ void filter_to_dgrad_kernel(pk_conv_geom g, const T* __restrict__ f, T* __restrict__ d,
+                                       int kp) {
+    const long long total = (long long)g.c * g.r * g.s * kp;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int k = (int)(i % kp);
+        long long t = i / kp;
+        const int s = (int)(t % g.s);
+        t /= g.s;
+        const int r = (int)(t % g.r);
+        const int c = (int)(t / g.r);
+        float v = 0.0f;
+        if (k < g.k) v = ld(f + (((size_t)k * g.r + r) * g.s + s) * g.f_pitch + c);
+        st(d + i, v);
+    }
+}
+
+template <typename T>
+__global__ void pointwise_kernel(const T* __restrict__ x, T* __restrict__ y, long long rows,
+                                 int c, int hw, int pitch, pk_epilogue e) {
+    const long long total = rows * pitch;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int ch = (int)(i % pitch);
+        const long long row = i / pitch;
+        float v = 0.0f;
+        if (ch < c) v = apply_epilogue(e, ld(x + i), ch, 0, (int)(row % hw), 1, hw);
+        st(y + i, v);
+    }
+}
+
+template <typename T>
+__global__ void activation_bwd_kernel(const T* __restrict__ x, const T* __restrict__ dy,
+                                      T* __restrict__ dx, long long total, int c, int pitch,
+                                      int act, float alpha) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int ch = (int)(i % pitch);
+        float out = 0.0f;
+        if (ch < c) {
+            const float v = ld(x + i);
+            float d = 0.0f;
+            switch (act) {  // primitives.cpp:181-198 (ReLU'(0) = 0)
+                case 0: d = v > 0.0f ? 1.0f : 0.0f; break;
+                case 1: d = v > 0.0f ? 1.0f : alpha; break;
+                case 2: {
+                    const float s = 1.0f / (1.0f + expf(-v));
+                    d = s * (1.0f - s);
+                    break;
+                }
+                default: {
+                    const float t = tanhf(v);
+                    d = 1.0f - t * t;
+                }
+            }
+            out = d * ld(dy + i);
+        }
+        st(dx + i, out);
+    }
+}
+
+template <typename T>
+__global__ void store_rows_kernel(const float* __restrict__ src, int rows, int cols, long long ld_,
+                                  T* __restrict__ dst, long long dpitch, pk_epilogue e,
+                                  int chan_offset, int P, int Q) {
+    const long long total = (long long)rows * cols;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int j = (int)(i % cols);
+        const int r = (int)(i / cols);
+        float v = src[(long long)r * ld_ + j];
+        if (epilogue_active(&e)) v = apply_epilogue(e, v, chan_offset + j, r / Q, r % Q, P, Q);
+        st(dst + (long long)r * dpitch + j, v);
+    }
+}
+
+inline unsigned grid_for(long long total, int threads = 256) {
+    long long b = (total + threads - 1) / threads;
+    if (b > 148LL * 64) b = 148LL * 64;
+    if (b < 1) b = 1;
+    return (unsigned)b;
+}
+
+}  // namespace pk
+
+using namespace pk;
+
+extern "C" {
+
+uint64_t pk_cuda_launch_count(void) { return g_launches.load(); }
+
+cudaError_t pk_cuda_nchw_to_nhwc(const float* src, void* dst, int n, int c, int hw, int pitch,
+                                 int dtype, cudaStream_t st) {
+    dim3 grid(ceil_div(hw, 32), ceil_div(pitch, 32), n), block(32, 8);
+    PK_DISPATCH_DTYPE(dtype, T,
+                      nchw_to_nhwc_kernel<T><<<grid, block, 0, st>>>(src, (T*)dst, c, hw, pitch));
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t pk_cuda_nhwc_to_nchw(const void* src, float* dst, int n, int c, int hw, int pitch,
+                                 int dtype, cudaStream_t st) {
+    dim3 grid(ceil_div(hw, 32), ceil_div(c, 32), n), block(32, 8);
+    PK_DISPATCH_DTYPE(dtype, T,
+                      nhwc_to_nchw_kernel<T><<<grid, block, 0, st>>>((const T*)src, dst, c, hw,
+                                                                      pitch));
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t pk_cuda_filter_to_dgrad(const pk_conv_geom* g, int dtype, const void* f, void* dst,
+                                    cudaStream_t st) {
+    const int kp = pk_pitch(g->k);
+    const long long total = (long long)g->c * g->r * g->s * kp;
+    PK_DISPATCH_DTYPE(dtype, T,
+                      filter_to_dgrad_kernel<T><<<grid_for(total), 256, 0, st>>>(
+                          *g, (const T*)f, (T*)dst, kp));
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t pk_cuda_pointwise(const void* x, void* y, int n, int c, int hw, int pitch, int dtype,
+                              const pk_epilogue* epi, cudaStream_t st) {
+    const long long rows = (long long)n * hw;
+    PK_DISPATCH_DTYPE(dtype, T,
+                      pointwise_kernel<T><<<grid_for(rows * pitch), 256, 0, st>>>(
+                          (const T*)x, (T*)y, rows, c, hw, pitch, *epi));
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t pk_cuda_activation_bwd(const void* x, const void* dy, void* dx, int n, int c, int hw,
+                                   int pitch, int dtype, int act, float alpha, cudaStream_t st) {
+    const long long total = (long long)n * hw * pitch;
+    PK_DISPATCH_DTYPE(dtype, T,
+                      activation_bwd_kernel<T><<<grid_for(total), 256, 0, st>>>(
+                          (const T*)x, (const T*)dy, (T*)dx, total, c, pitch, act, alpha));
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t pk_cuda_store_rows(const float* src, int rows, int cols, long long ld, void* dst,
+                               long long dst_pitch, int dtype, const pk_epilogue* epi,
+                               int chan_offset, cudaStream_t st) {
+    pk_epilogue none{};
+    none.act = -1;
+    const pk_epilogue e = epi ? *epi : none;
+    PK_DISPATCH_DTYPE(dtype, T,
+                      store_rows_kernel<T><<<grid_for((long long)rows * cols), 256, 0, st>>>(
+                          src, rows, cols, ld, (T*)dst, dst_pitch, e, chan_offset, 1, rows));
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // extern "C"

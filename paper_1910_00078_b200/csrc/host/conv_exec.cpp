@@ -1,0 +1,321 @@
+// ConvPlan execution: maps (direction, algorithm, element type, shape) onto
+// the sm_100a kernel families and advances the op counters exactly as the
+// reference's CPU kernels do (proj/src/core/conv.cpp and tensor.cpp:169-170).
+//
+//   direction  algo         f32 (SIMT fp32)              bf16 (tcgen05 when supported)
+//   Forward    Direct       direct_fwd                   direct_fwd
+//              Im2colGemm   im2col + SIMT GEMM / image   im2col + tcgen05 GEMM / image
+//              Winograd     winograd_f23                 winograd_f23
+//              FFT          fft (complex<double>)        fft
+//              ImplicitGemm igemm_simt_fwd               igemm_tc_fwd
+//   BwdData    Direct       direct_bwd_data              direct_bwd_data
+//              Im2colGemm   SIMT GEMM + col2im / image   igemm_tc_dgrad
+//   BwdWeights Direct       direct_bwd_weights           direct_bwd_weights
+//              Im2colGemm   im2col + SIMT GEMM / image   igemm_tc_wgrad (split-K)
+#include <cstring>
+
+#include "../cuda/kernels.h"
+#include "handle.hpp"
+#include "solver.hpp"
+
+namespace primkit {
+
+namespace {
+
+int dtype_of(ElementType t) { return t == ElementType::BF16 ? PK_BF16 : PK_F32; }
+
+pk_conv_geom make_geom(const ConvProblem& p) {
+    const ConvShapes s = resolve_shapes(p.input_desc(), p.filter_desc(), p.conv_desc());
+    pk_conv_geom g{};
+    g.n = (int)s.n;
+    g.c = (int)s.c;
+    g.h = (int)s.h;
+    g.w = (int)s.w;
+    g.k = (int)s.k;
+    g.r = (int)s.y;
+    g.s = (int)s.x;
+    g.p = (int)s.oh;
+    g.q = (int)s.ow;
+    g.pad_h = (int)p.pad_h;
+    g.pad_w = (int)p.pad_w;
+    g.str_h = (int)p.stride_h;
+    g.str_w = (int)p.stride_w;
+    g.dil_h = (int)p.dilation_h;
+    g.dil_w = (int)p.dilation_w;
+    g.groups = (int)s.groups;
+    g.cg = (int)s.cg;
+    g.kg = (int)s.kg;
+    g.x_pitch = pk_pitch(g.c);
+    g.y_pitch = pk_pitch(g.k);
+    g.transpose = p.mode == ConvMode::Transpose ? 1 : 0;
+    g.f_pitch = g.transpose ? pk_pitch(g.kg) : pk_pitch(g.cg);
+    return g;
+}
+
+// Reference counter semantics per (direction, algorithm).
+OpCounters counters_for(const ConvProblem& p, ConvAlgo algo) {
+    const ConvShapes s = resolve_shapes(p.input_desc(), p.filter_desc(), p.conv_desc());
+    using u64 = std::uint64_t;
+    OpCounters c;
+    c.buffer_roundtrips = 1;
+    const u64 n = s.n, k = s.k, oh = s.oh, ow = s.ow, cg = s.cg, kg = s.kg, y = s.y, x = s.x,
+              grp = s.groups, h = s.h, w = s.w, ch = s.c;
+    switch (p.direction) {
+        case ConvDirection::Forward:
+            switch (algo) {
+                case ConvAlgo::Direct:
+                case ConvAlgo::ImplicitGemm: c.scalar_muls = n * k * oh * ow * cg * y * x; break;
+                case ConvAlgo::Im2colGemm:
+                    c.gemm_calls = n * grp;
+                    if (p.mode == ConvMode::Transpose)
+                        c.scalar_muls = n * grp * (kg * y * x) * (h * w) * cg;
+                    else
+                        c.scalar_muls = n * grp * kg * (oh * ow) * (cg * y * x);
+                    break;
+                case ConvAlgo::Winograd:
+                    c.scalar_muls = n * k * ((oh + 1) / 2) * ((ow + 1) / 2) * cg * 16;
+                    break;
+                case ConvAlgo::FFT: break;
+            }
+            break;
+        case ConvDirection::BackwardData:
+            if (algo == ConvAlgo::Direct) {
+                c.scalar_muls = n * ch * h * w * kg * y * x;
+            } else {
+                c.gemm_calls = n * grp;
+                c.scalar_muls = n * grp * (cg * y * x) * (oh * ow) * kg;
+            }
+            break;
+        case ConvDirection::BackwardWeights:
+            if (algo == ConvAlgo::Direct) {
+                c.scalar_muls = k * cg * y * x * n * oh * ow;
+            } else {
+                c.gemm_calls = n * grp;
+                c.scalar_muls = n * grp * kg * (cg * y * x) * (oh * ow);
+            }
+            break;
+    }
+    return c;
+}
+
+// tcgen05 tiling selected by the ImplicitGemm perf config (solver.cpp).
+pk_tc_config tc_config(const ImplicitGemmTiles& t) {
+    pk_tc_config cfg{};
+    cfg.block_n = static_cast<int>(256 / std::max<std::int64_t>(1, t.tile_m));
+    cfg.raster = static_cast<int>(t.tile_n);
+    cfg.stages = t.tile_k == 1 ? 4 : t.tile_k == 2 ? 3 : 2;
+    return cfg;
+}
+
+const pk_tc_config kDefaultTc{256, 4, 1};
+
+std::size_t col_bytes(const pk_conv_geom& g, int dtype) {
+    return (std::size_t)g.p * g.q * g.r * g.s * g.f_pitch * (dtype == PK_BF16 ? 2 : 4);
+}
+
+std::size_t align256(std::size_t v) { return (v + 255) / 256 * 256; }
+
+// The per-image GEMM of the forward Im2colGemm path as a 1x1 "convolution"
+// over the column matrix: pixels = P*Q, reduction = R*S*f_pitch.
+pk_conv_geom gemm_as_1x1(const pk_conv_geom& g) {
+    pk_conv_geom m{};
+    m.n = 1;
+    m.h = 1;
+    m.w = g.p * g.q;
+    m.p = 1;
+    m.q = g.p * g.q;
+    m.c = g.r * g.s * g.f_pitch;
+    m.cg = m.c;
+    m.k = g.kg;
+    m.kg = g.kg;
+    m.r = m.s = 1;
+    m.str_h = m.str_w = m.dil_h = m.dil_w = 1;
+    m.groups = 1;
+    m.x_pitch = m.c;
+    m.f_pitch = m.c;
+    m.y_pitch = g.y_pitch;
+    return m;
+}
+
+}  // namespace
+
+std::size_t ConvPlan::device_workspace_bytes() const {
+    const pk_conv_geom g = make_geom(problem_);
+    const int dt = dtype_of(problem_.etype);
+    const std::size_t acc_rows = (std::size_t)g.p * g.q;
+    switch (problem_.direction) {
+        case ConvDirection::Forward:
+            if (algo_ == ConvAlgo::FFT) return pk_cuda_fft_scratch_bytes(&g);
+            if (algo_ == ConvAlgo::Im2colGemm) {
+                if (g.transpose)  // fp32 column matrix [(r,s,kk)][h*w]
+                    return (std::size_t)g.r * g.s * g.f_pitch * g.h * g.w * 4;
+                return align256(col_bytes(g, dt)) + acc_rows * g.kg * 4;
+            }
+            return 0;
+        case ConvDirection::BackwardData:
+            if (algo_ == ConvAlgo::Im2colGemm) {
+                if (dt == PK_BF16 && pk_tc_dgrad_supported(&g)) return pk_tc_dgrad_workspace(&g);
+                return (std::size_t)g.p * g.q * g.r * g.s * g.f_pitch * 4;
+            }
+            return 0;
+        case ConvDirection::BackwardWeights:
+            if (algo_ == ConvAlgo::Im2colGemm) {
+                if (dt == PK_BF16 && pk_tc_wgrad_supported(&g)) return pk_tc_wgrad_workspace(&g, 148);
+                return align256(col_bytes(g, dt)) + (std::size_t)g.k * g.r * g.s * g.f_pitch * 4;
+            }
+            return 0;
+    }
+    return 0;
+}
+
+void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
+                   std::size_t ws_bytes, const pk_epilogue* epi) const {
+    h.activate();
+    const pk_conv_geom g = make_geom(problem_);
+    const int dt = dtype_of(problem_.etype);
+    const std::size_t esz = dt == PK_BF16 ? 2 : 4;
+    cudaStream_t st = h.stream();
+    if (ws_bytes < device_workspace_bytes())
+        throw_error(ErrorCode::WorkspaceTooSmall, "workspace below requested size");
+    auto ck = [](cudaError_t e, const char* what) { check_cuda(e, what); };
+
+    const ConvDirection dir = problem_.direction;
+    // Output channels beyond K (pitch padding) must hold zeros for the next
+    // consumer; only non-multiple-of-8 channel counts have such lanes.
+    if (dir == ConvDirection::Forward && g.y_pitch != g.k)
+        ck(cudaMemsetAsync(out, 0, (std::size_t)g.n * g.p * g.q * g.y_pitch * esz, st), "memset");
+    if (dir == ConvDirection::BackwardData && g.x_pitch != g.c)
+        ck(cudaMemsetAsync(out, 0, (std::size_t)g.n * g.h * g.w * g.x_pitch * esz, st), "memset");
+
+    const char* kernel = "?";
+    if (dir == ConvDirection::Forward) {
+        switch (algo_) {
+            case ConvAlgo::Direct:
+                kernel = "direct_simt";
+                ck(pk_cuda_direct_fwd(&g, dt, a, b, out, epi, st), "direct_fwd");
+                break;
+            case ConvAlgo::Winograd:
+                kernel = "winograd_f23";
+                ck(pk_cuda_winograd_f23(&g, dt, a, b, out, epi, st), "winograd_f23");
+                break;
+            case ConvAlgo::FFT:
+                kernel = "fft";
+                ck(pk_cuda_fft_fwd(&g, dt, a, b, out, ws, st), "fft_fwd");
+                break;
+            case ConvAlgo::ImplicitGemm: {
+                if (dt == PK_BF16 && pk_tc_fwd_supported(&g)) {
+                    kernel = "igemm_tc_fwd";
+                    const pk_tc_config cfg = tc_config(tiles_);
+                    ck(pk_cuda_igemm_tc_fwd(&g, a, b, out, epi, &cfg, st), "igemm_tc_fwd");
+                } else {
+                    kernel = "igemm_simt_fwd";
+                    ck(pk_cuda_igemm_simt_fwd(&g, dt, a, b, out, epi, st), "igemm_simt_fwd");
+                }
+                break;
+            }
+            case ConvAlgo::Im2colGemm: {
+                if (g.transpose) {
+                    // col[(r,s,kk)][hw] = W_g^T X_g ; then gather into the output
+                    kernel = "im2col_gemm_transpose";
+                    float* col = static_cast<float*>(ws);
+                    const long long rows = (long long)g.r * g.s * g.f_pitch, hw = (long long)g.h * g.w;
+                    for (int n = 0; n < g.n; ++n)
+                        for (int grp = 0; grp < g.groups; ++grp) {
+                            const char* wg = (const char*)b + (size_t)grp * g.cg * rows * esz;
+                            const char* xg = (const char*)a +
+                                             ((size_t)n * hw * g.x_pitch + (size_t)grp * g.cg) * esz;
+                            ck(pk_cuda_gemm_simt((int)rows, (int)hw, g.cg, dt, wg, 1, rows, xg, 1,
+                                                 g.x_pitch, col, hw, 0, st),
+                               "gemm_simt");
+                            ck(pk_cuda_col2im_transpose(&g, dt, col, n, grp, out, st), "col2im_t");
+                        }
+                    break;
+                }
+                const bool tc = dt == PK_BF16 && pk_tc_fwd_supported(&g);
+                kernel = tc ? "im2col+gemm_tc" : "im2col+gemm_simt";
+                void* col = ws;
+                float* acc = reinterpret_cast<float*>(static_cast<char*>(ws) + align256(col_bytes(g, dt)));
+                const pk_conv_geom m = gemm_as_1x1(g);
+                const long long kred = (long long)g.r * g.s * g.f_pitch;
+                for (int n = 0; n < g.n; ++n)
+                    for (int grp = 0; grp < g.groups; ++grp) {
+                        ck(pk_cuda_im2col(&g, dt, a, n, grp, col, st), "im2col");
+                        char* yg = (char*)out + ((size_t)n * g.p * g.q * g.y_pitch + (size_t)grp * g.kg) * esz;
+                        const char* wg = (const char*)b + (size_t)grp * g.kg * kred * esz;
+                        if (tc) {
+                            pk_epilogue e{};
+                            e.act = -1;
+                            if (epi) {
+                                e = *epi;
+                                if (e.bias) e.bias += grp * g.kg;
+                            }
+                            ck(pk_cuda_igemm_tc_fwd(&m, col, wg, yg, epi ? &e : nullptr, &kDefaultTc, st),
+                               "gemm_tc");
+                        } else {
+                            ck(pk_cuda_gemm_simt(g.p * g.q, g.kg, (int)kred, dt, col, kred, 1, wg, 1,
+                                                 kred, acc, g.kg, 0, st),
+                               "gemm_simt");
+                            pk_epilogue e{};
+                            e.act = -1;
+                            if (epi) e = *epi;
+                            ck(pk_cuda_store_rows(acc, g.p * g.q, g.kg, g.kg, yg, g.y_pitch, dt,
+                                                  epi ? &e : nullptr, grp * g.kg, st),
+                               "store_rows");
+                        }
+                    }
+                break;
+            }
+        }
+    } else if (dir == ConvDirection::BackwardData) {
+        if (algo_ == ConvAlgo::Direct) {
+            kernel = "direct_simt_bwd_data";
+            ck(pk_cuda_direct_bwd_data(&g, dt, a, b, out, st), "direct_bwd_data");
+        } else if (dt == PK_BF16 && pk_tc_dgrad_supported(&g)) {
+            kernel = "igemm_tc_dgrad";
+            ck(pk_cuda_igemm_tc_dgrad(&g, a, b, out, ws, &kDefaultTc, st), "igemm_tc_dgrad");
+        } else {
+            kernel = "gemm_simt+col2im";
+            float* col = static_cast<float*>(ws);
+            const long long rowp = (long long)g.r * g.s * g.f_pitch;
+            for (int n = 0; n < g.n; ++n)
+                for (int grp = 0; grp < g.groups; ++grp) {
+                    const char* dyg = (const char*)a +
+                                      ((size_t)n * g.p * g.q * g.y_pitch + (size_t)grp * g.kg) * esz;
+                    const char* wg = (const char*)b + (size_t)grp * g.kg * rowp * esz;
+                    ck(pk_cuda_gemm_simt(g.p * g.q, (int)rowp, g.kg, dt, dyg, g.y_pitch, 1, wg,
+                                         rowp, 1, col, rowp, 0, st),
+                       "gemm_simt");
+                    ck(pk_cuda_col2im(&g, dt, col, n, grp, out, st), "col2im");
+                }
+        }
+    } else {
+        if (algo_ == ConvAlgo::Direct) {
+            kernel = "direct_simt_bwd_weights";
+            ck(pk_cuda_direct_bwd_weights(&g, dt, a, b, out, st), "direct_bwd_weights");
+        } else if (dt == PK_BF16 && pk_tc_wgrad_supported(&g)) {
+            kernel = "igemm_tc_wgrad";
+            ck(pk_cuda_igemm_tc_wgrad(&g, a, b, out, ws, h.num_sms(), &kDefaultTc, st),
+               "igemm_tc_wgrad");
+        } else {
+            kernel = "im2col+gemm_simt_wgrad";
+            void* col = ws;
+            float* acc = reinterpret_cast<float*>(static_cast<char*>(ws) + align256(col_bytes(g, dt)));
+            const long long rowp = (long long)g.r * g.s * g.f_pitch;
+            for (int n = 0; n < g.n; ++n)
+                for (int grp = 0; grp < g.groups; ++grp) {
+                    ck(pk_cuda_im2col(&g, dt, b, n, grp, col, st), "im2col");
+                    const char* dyg = (const char*)a +
+                                      ((size_t)n * g.p * g.q * g.y_pitch + (size_t)grp * g.kg) * esz;
+                    ck(pk_cuda_gemm_simt(g.kg, (int)rowp, g.p * g.q, dt, dyg, 1, g.y_pitch, col,
+                                         rowp, 1, acc + (size_t)grp * g.kg * rowp, rowp, n > 0, st),
+                       "gemm_simt");
+                }
+            ck(pk_cuda_store_rows(acc, g.k, (int)rowp, rowp, out, rowp, dt, nullptr, 0, st),
+               "store_rows");
+        }
+    }
+    h.last_kernel = kernel;
+    h.counters() += counters_for(problem_, algo_);
+}
+
+}  // namespace primkit

@@ -1,0 +1,355 @@
+#include "handle.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <random>
+#include <tuple>
+
+#include "../cuda/kernels.h"
+
+namespace primkit {
+
+namespace {
+
+double steady_ms() {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+std::filesystem::path default_cache_dir() {
+    if (const char* env = std::getenv("PRIMKIT_CACHE_DIR"); env && *env) return env;
+    return std::filesystem::temp_directory_path() / "primkit-cache";
+}
+
+FindEnforce env_find_enforce() {
+    const char* env = std::getenv("PRIMKIT_FIND_ENFORCE");
+    return env && std::string(env) == "SEARCH" ? FindEnforce::Search : FindEnforce::None;
+}
+
+double median_of(std::vector<double> v) {
+    std::sort(v.begin(), v.end());
+    return v[v.size() / 2];
+}
+
+std::string plan_descriptor(const ConvProblem& p, const Solver& s, const PerfConfig& c) {
+    return p.key() + '\n' + s.name() + '\n' + c.serialize_values() + '\n';
+}
+
+TensorDescriptor result_desc(const ConvProblem& p) {
+    switch (p.direction) {
+        case ConvDirection::Forward: return p.output_desc();
+        case ConvDirection::BackwardData: return p.input_desc();
+        default: return p.filter_desc();
+    }
+}
+
+}  // namespace
+
+DeviceBuffer::~DeviceBuffer() {
+    if (ptr_) cudaFree(ptr_);
+}
+
+void* DeviceBuffer::ensure(std::size_t bytes) {
+    if (bytes <= bytes_ && ptr_) return ptr_;
+    if (ptr_) {
+        cudaFree(ptr_);
+        ptr_ = nullptr;
+        bytes_ = 0;
+    }
+    const std::size_t want = std::max<std::size_t>(bytes, 256);
+    check_cuda(cudaMalloc(&ptr_, want), "cudaMalloc");
+    bytes_ = want;
+    return ptr_;
+}
+
+Handle::Handle()
+    : plan_cache_(std::make_shared<PlanCache>(default_cache_dir())),
+      solvers_(builtin_solvers()),
+      clock_(steady_ms),
+      find_enforce_(env_find_enforce()) {
+    device_ = -1;  // resolved lazily: host-only queries never touch the GPU
+}
+
+Handle::Handle(cudaStream_t stream, int device) : Handle() {
+    init_device(device);
+    stream_ = stream;
+}
+
+Handle::~Handle() {
+    if (device_ >= 0) {
+        cudaSetDevice(device_);
+        if (ev0_) cudaEventDestroy(ev0_);
+        if (ev1_) cudaEventDestroy(ev1_);
+    }
+    scratch_.clear();
+}
+
+void Handle::init_device(int device) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        throw std::runtime_error("primkit: no CUDA device available (the library has no CPU path)");
+    }
+    if (device < 0) check_cuda(cudaGetDevice(&device), "cudaGetDevice");
+    device_ = device;
+    check_cuda(cudaSetDevice(device_), "cudaSetDevice");
+    cudaDeviceProp prop{};
+    check_cuda(cudaGetDeviceProperties(&prop, device_), "cudaGetDeviceProperties");
+    if (prop.major < 10)
+        throw std::runtime_error("primkit: device " + std::string(prop.name) +
+                                 " is not sm_100 (Blackwell); this build targets sm_100a only");
+    num_sms_ = prop.multiProcessorCount;
+    check_cuda(cudaEventCreate(&ev0_), "cudaEventCreate");
+    check_cuda(cudaEventCreate(&ev1_), "cudaEventCreate");
+}
+
+void Handle::activate() const {
+    if (device_ < 0) const_cast<Handle*>(this)->init_device(-1);
+    check_cuda(cudaSetDevice(device_), "cudaSetDevice");
+}
+
+void* Handle::scratch(int slot, std::size_t bytes) {
+    activate();
+    return scratch_[slot].ensure(bytes);
+}
+
+void Handle::sync() const {
+    activate();
+    check_cuda(cudaStreamSynchronize(stream_), "cudaStreamSynchronize");
+}
+
+void Handle::use_fake_clock() {
+    auto tick = std::make_shared<double>(0.0);
+    clock_ = [tick]() { return (*tick)++; };
+    device_timing_ = false;
+}
+
+void Handle::set_cache_dir(const std::filesystem::path& dir) {
+    plan_cache_ = std::make_shared<PlanCache>(dir);
+}
+
+void Handle::register_solver(std::shared_ptr<const Solver> solver) {
+    for (const auto& s : solvers_)
+        if (s->name() == solver->name())
+            throw_error(ErrorCode::DuplicateSolver,
+                        "solver '" + solver->name() + "' already registered");
+    solvers_.push_back(std::move(solver));
+}
+
+const Solver* Handle::find_solver(const std::string& name) const {
+    for (const auto& s : solvers_)
+        if (s->name() == name) return s.get();
+    return nullptr;
+}
+
+PerfConfig Handle::resolve_config(const ConvProblem& problem, const Solver& solver) const {
+    if (auto values = perfdb_.get(problem.key(), solver.name())) {
+        try {
+            PerfConfig c = solver.config_from_values(problem, *values);
+            if (solver.config_valid(problem, c)) return c;
+        } catch (const Error&) {
+            // stale / foreign record -> default
+        }
+    }
+    return solver.default_config(problem);
+}
+
+std::shared_ptr<const ConvPlan> Handle::cached_build(const ConvProblem& problem,
+                                                     const Solver& solver,
+                                                     const PerfConfig* config) {
+    const PerfConfig resolved = config ? *config : resolve_config(problem, solver);
+    const std::string key =
+        PlanCache::hash_key(problem.key(), solver.name(), resolved.serialize_values());
+    auto make = [&]() -> std::shared_ptr<void> {
+        return std::make_shared<ConvPlan>(solver.build_plan(problem, &resolved));
+    };
+    auto plan = plan_cache_->get_or_build(key, plan_descriptor(problem, solver, resolved), make,
+                                          [&](const std::string&) { return make(); });
+    return std::static_pointer_cast<const ConvPlan>(plan);
+}
+
+double Handle::time_ms(const std::function<void()>& fn) {
+    activate();
+    if (device_timing_) {
+        check_cuda(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
+        fn();
+        check_cuda(cudaEventRecord(ev1_, stream_), "cudaEventRecord");
+        check_cuda(cudaEventSynchronize(ev1_), "cudaEventSynchronize");
+        float ms = 0.0f;
+        check_cuda(cudaEventElapsedTime(&ms, ev0_, ev1_), "cudaEventElapsedTime");
+        return ms;
+    }
+    const double t0 = now_ms();
+    fn();
+    sync();
+    const double t1 = now_ms();
+    return t1 - t0;
+}
+
+std::vector<ConvAlgoPerf> Handle::find_convolution(const ConvProblem& problem, const void* a,
+                                                   const void* b, std::size_t workspace_bytes) {
+    const std::string memo_key = problem.key() + "#ws" + std::to_string(workspace_bytes);
+    if (auto it = find_memo_.find(memo_key); it != find_memo_.end()) return it->second;
+
+    std::vector<ConvAlgoPerf> results;
+    for (const auto& solver : solvers_) {
+        if (!solver->is_applicable(problem)) continue;
+        if (find_enforce_ == FindEnforce::Search && solver->is_tunable() &&
+            !perfdb_.get(problem.key(), solver->name()))
+            tune(*this, *solver, problem, default_tune_budget(*solver, problem));
+        const PerfConfig config = resolve_config(problem, *solver);
+        const std::size_t need = solver->workspace_bytes(problem, &config);
+        if (need > workspace_bytes) continue;
+
+        auto plan = cached_build(problem, *solver, &config);
+        const std::size_t dws = plan->device_workspace_bytes();
+        void* ws = scratch(0, dws);
+        void* out = scratch(3, device_bytes(result_desc(problem)));
+        std::vector<double> times;
+        for (int run = 0; run < kWarmupRuns + kTimedRuns; ++run) {
+            const double t = time_ms([&] { plan->run(*this, a, b, out, ws, dws); });
+            if (run >= kWarmupRuns) times.push_back(t);
+        }
+        results.push_back({solver->algo(), solver->name(), median_of(std::move(times)), need});
+    }
+    if (results.empty())
+        throw_error(ErrorCode::NoApplicableSolver, "no applicable solver for " + problem.key());
+    std::sort(results.begin(), results.end(), [](const ConvAlgoPerf& l, const ConvAlgoPerf& r) {
+        return std::tie(l.time_ms, l.solver_name) < std::tie(r.time_ms, r.solver_name);
+    });
+    find_memo_[memo_key] = results;
+    return results;
+}
+
+std::int64_t default_tune_budget(const Solver& solver, const ConvProblem& problem) {
+    return std::min<std::int64_t>(static_cast<std::int64_t>(solver.tuning_space(problem).size()),
+                                  256);
+}
+
+namespace {
+// U(-1, 1) host draws from std::mt19937_64 (handle.cpp:32-38 of the
+// reference), rounded on store for bf16, then staged to the device layout.
+void random_device_tensor(Handle& h, const TensorDescriptor& desc, std::uint64_t seed,
+                          void* dev) {
+    std::vector<float> host(static_cast<std::size_t>(desc.elem_count()));
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<float> dist(-1.0f, 1.0f);
+    for (auto& v : host) {
+        v = dist(rng);
+        if (desc.etype == ElementType::BF16) v = round_bf16(v);
+    }
+    upload_nchw(h, desc, host.data(), dev);
+}
+}  // namespace
+
+TuneResult tune(Handle& handle, const Solver& solver, const ConvProblem& problem,
+                std::int64_t budget, bool exhaustive) {
+    if (!solver.is_tunable()) throw_error(ErrorCode::NotTunable, solver.name() + " is not tunable");
+    if (budget < 1) throw_error(ErrorCode::InvalidValue, "tuning budget must be >= 1");
+    auto grid = solver.tuning_space(problem);
+    if (grid.empty()) throw_error(ErrorCode::NoValidConfig, "empty tuning space for " + solver.name());
+    if (static_cast<std::int64_t>(grid.size()) > budget) grid.resize(static_cast<std::size_t>(budget));
+
+    const TensorDescriptor da =
+        problem.direction == ConvDirection::Forward ? problem.input_desc() : problem.output_desc();
+    const TensorDescriptor db = problem.direction == ConvDirection::BackwardWeights
+                                    ? problem.input_desc()
+                                    : problem.filter_desc();
+    void* a = handle.scratch(4, device_bytes(da));
+    void* b = handle.scratch(5, device_bytes(db));
+    random_device_tensor(handle, da, handle.rng_seed, a);
+    random_device_tensor(handle, db, handle.rng_seed + 1, b);
+    void* out = handle.scratch(3, device_bytes(result_desc(problem)));
+
+    TuneResult result;
+    double best = -1.0;
+    for (const auto& config : grid) {
+        const ConvPlan plan = solver.build_plan(problem, &config);
+        const std::size_t dws = plan.device_workspace_bytes();
+        void* ws = handle.scratch(0, dws);
+        result.evaluations += 1;
+        std::vector<double> times;
+        bool pruned = false;
+        for (int run = 0; run < Handle::kWarmupRuns + Handle::kTimedRuns; ++run) {
+            const double t = handle.time_ms([&] { plan.run(handle, a, b, out, ws, dws); });
+            if (run < Handle::kWarmupRuns) continue;
+            times.push_back(t);
+            // pruned search: abandon a config whose first timed run is more
+            // than twice the best median so far
+            if (!exhaustive && times.size() == 1 && best >= 0.0 && t > 2.0 * best) {
+                pruned = true;
+                break;
+            }
+        }
+        if (pruned) continue;
+        const double med = median_of(std::move(times));
+        if (best < 0.0 || med < best) {
+            best = med;
+            result.best = config;
+        }
+    }
+    if (best < 0.0) throw_error(ErrorCode::NoValidConfig, "all configs pruned");
+    handle.perfdb().set(problem.key(), solver.name(), result.best.serialize_values());
+    return result;
+}
+
+// ---- staging --------------------------------------------------------------
+
+std::size_t etype_bytes(ElementType t) { return t == ElementType::BF16 ? 2 : 4; }
+
+std::size_t device_act_bytes(std::int64_t n, std::int64_t c, std::int64_t h, std::int64_t w,
+                             ElementType t) {
+    return static_cast<std::size_t>(n * h * w * pk_pitch(static_cast<int>(c))) * etype_bytes(t);
+}
+
+std::size_t device_bytes(const TensorDescriptor& d) {
+    if (d.rank() == 4) return device_act_bytes(d.dims[0], d.dims[1], d.dims[2], d.dims[3], d.etype);
+    return static_cast<std::size_t>(d.elem_count()) * 4;
+}
+
+void upload_nchw(Handle& h, const TensorDescriptor& d, const float* host, void* dev) {
+    h.activate();
+    if (d.rank() != 4) {
+        check_cuda(cudaMemcpyAsync(dev, host, static_cast<std::size_t>(d.elem_count()) * 4,
+                                   cudaMemcpyHostToDevice, h.stream()),
+                   "cudaMemcpyAsync");
+        return;
+    }
+    const std::size_t bytes = static_cast<std::size_t>(d.elem_count()) * 4;
+    void* stage = h.scratch(10, bytes);
+    check_cuda(cudaMemcpyAsync(stage, host, bytes, cudaMemcpyHostToDevice, h.stream()),
+               "cudaMemcpyAsync");
+    const int c = static_cast<int>(d.dims[1]);
+    check_cuda(pk_cuda_nchw_to_nhwc(static_cast<const float*>(stage), dev,
+                                    static_cast<int>(d.dims[0]), c,
+                                    static_cast<int>(d.dims[2] * d.dims[3]), pk_pitch(c),
+                                    d.etype == ElementType::BF16 ? PK_BF16 : PK_F32, h.stream()),
+               "nchw_to_nhwc");
+    // staging reuse is stream-ordered; regrowing it goes through cudaFree,
+    // which waits for pending work, so no host synchronisation is needed
+}
+
+void download_nchw(Handle& h, const TensorDescriptor& d, const void* dev, float* host) {
+    h.activate();
+    if (d.rank() != 4) {
+        check_cuda(cudaMemcpyAsync(host, dev, static_cast<std::size_t>(d.elem_count()) * 4,
+                                   cudaMemcpyDeviceToHost, h.stream()),
+                   "cudaMemcpyAsync");
+        h.sync();
+        return;
+    }
+    const std::size_t bytes = static_cast<std::size_t>(d.elem_count()) * 4;
+    void* stage = h.scratch(11, bytes);
+    const int c = static_cast<int>(d.dims[1]);
+    check_cuda(pk_cuda_nhwc_to_nchw(dev, static_cast<float*>(stage), static_cast<int>(d.dims[0]),
+                                    c, static_cast<int>(d.dims[2] * d.dims[3]), pk_pitch(c),
+                                    d.etype == ElementType::BF16 ? PK_BF16 : PK_F32, h.stream()),
+               "nhwc_to_nchw");
+    check_cuda(cudaMemcpyAsync(host, stage, bytes, cudaMemcpyDeviceToHost, h.stream()),
+               "cudaMemcpyAsync");
+    h.sync();
+}
+
+}  // namespace primkit
