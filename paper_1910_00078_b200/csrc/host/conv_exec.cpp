@@ -139,6 +139,8 @@ pk_conv_geom gemm_as_1x1(const pk_conv_geom& g) {
 
 }  // namespace
 
+OpCounters conv_counters(const ConvProblem& p, ConvAlgo algo) { return counters_for(p, algo); }
+
 std::size_t ConvPlan::device_workspace_bytes() const {
     const pk_conv_geom g = make_geom(problem_);
     const int dt = dtype_of(problem_.etype);

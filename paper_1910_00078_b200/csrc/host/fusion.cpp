@@ -426,9 +426,20 @@ void fusion_execute_unfused(Handle& h, FusionPlan& plan, const void* input, void
                 p.dilation_h = op.conv.dilation_h; p.dilation_w = op.conv.dilation_w;
                 p.groups = op.conv.group_count;
                 p.etype = et;
-                const ConvPlan cp(p, algo, {});
-                const std::size_t dws = cp.device_workspace_bytes();
-                cp.run(h, src, d.filter.get(), dst, h.scratch(0, dws), dws);
+                const pk_conv_geom g = fused_geom(plan, op);
+                if (dt == PK_BF16 && pk_tc_fwd_supported(&g)) {
+                    // Same tensor-core convolution as the fused path, without
+                    // the epilogue: the two executors differ only in where
+                    // bias/BN/activation run (and the extra round trips).
+                    const pk_tc_config cfg{256, 4, 1};
+                    check_cuda(pk_cuda_igemm_tc_fwd(&g, src, d.filter.get(), dst, nullptr, &cfg, st),
+                               "igemm_tc_fwd");
+                    h.counters() += conv_counters(p, algo);
+                } else {
+                    const ConvPlan cp(p, algo, {});
+                    const std::size_t dws = cp.device_workspace_bytes();
+                    cp.run(h, src, d.filter.get(), dst, h.scratch(0, dws), dws);
+                }
                 break;
             }
             case FusionOp::Kind::Bias:

@@ -208,8 +208,14 @@ class Handle:
                 for r in res[:min(capacity, cnt.value)]]
         return rows, cnt.value
 
-    def conv_run(self, p, solver: str | None, a, b, workspace_bytes: int = 1 << 40):
+    def conv_run(self, p, solver: str | None, a, b, workspace_bytes: int | None = None):
         a, b = _f32(a), _f32(b)
+        if workspace_bytes is None:
+            # exactly what the solver asks for (the reference allocates the
+            # caller's workspace size, so never pass a huge default)
+            names = [solver] if solver else [s for s in self.solver_names()
+                                             if self.is_applicable(s, p)][:1]
+            workspace_bytes = max([self.workspace_bytes(s, p) for s in names] + [0])
         out = np.zeros(operand_shapes(self.L, p)[2], dtype=np.float32)
         self._c("primkit_conv_run", C.byref(p), None if solver is None else solver.encode(),
                 _fp(a), _fp(b), _fp(out), C.c_size_t(workspace_bytes))

@@ -208,7 +208,8 @@ def test_tune_writes_perfdb(lib, tmp_path):
     assert text.startswith("1-4-6-6-4-3-3-1-1-1-1-1-1-1-F-C-f32=ImplicitGemm:")
     # full device-timed tune over the whole grid
     h2 = lib.handle()
-    assert h2.tune(p, "ImplicitGemm", 0, exhaustive=True) == 36
+    # grid {1,2,4,8}^2 x {1,2,4} filtered by k=4, 36 pixels, c=4 divisibility: 3*3*3
+    assert h2.tune(p, "ImplicitGemm", 0, exhaustive=True) == 27
 
 
 def test_bf16_large_tensor_core_paths(lib):
