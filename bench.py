@@ -359,8 +359,37 @@ def roofline(torch, lib, handle, net, peaks):
     return res
 
 
+def layer_report(torch, lib, handle, net, peaks, path):
+    """Per (layer, direction) device time and roofline position."""
+    rows = []
+    hbm = peaks["hbm_gbs"] * 1e9
+    tc = peaks["bf16_tflops"] * 1e12
+    for (L, x, w, y, dy, dx, dw, probs) in net.items:
+        for d, (a, b, o) in ((0, (x, w, y)), (1, (dy, w, dx)), (2, (dy, x, dw))):
+            p, s = probs[d]
+            run_conv(lib, handle, p, s, a, b, o, net.ws)
+            ms = time_region(torch, lambda: run_conv(lib, handle, p, s, a, b, o, net.ws), 5) / 5
+            fl = L.flops(net.n)
+            byts = 2 * (a.numel() + b.numel() + o.numel())
+            bound_ms = max(fl / tc, byts / hbm) * 1e3
+            kname = C.create_string_buffer(64)
+            lib.lib.primkit_handle_last_kernel(handle.ptr, kname, 64)
+            rows.append({"layer": L.name, "dir": ["fwd", "bwd_data", "bwd_weights"][d],
+                         "c": L.c, "k": L.k, "h": L.h, "r": L.r, "stride": L.stride,
+                         "kernel": kname.value.decode(), "ms": ms, "tflops": fl / ms / 1e9,
+                         "roofline_ms": bound_ms, "frac_of_roofline": bound_ms / ms,
+                         "bound": "tensor" if fl / tc > byts / hbm else "hbm"})
+    with open(path, "w") as f:
+        json.dump(rows, f, indent=1)
+    for r in sorted(rows, key=lambda r: -r["ms"])[:25]:
+        print(f"{r['layer']:>10} {r['dir']:>11} {r['kernel']:>16} {r['ms']:8.3f} ms "
+              f"{r['tflops']:7.1f} TF/s  roofline {r['frac_of_roofline']:.2f} ({r['bound']})",
+              file=sys.stderr)
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--layer-report", default=None, help="write per-layer timings (JSON)")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
@@ -401,6 +430,9 @@ def main():
 
     layers = resnet50_layers()
     net = Net(torch, lib, handle, layers, args.batch, device)
+    if args.layer_report:
+        layer_report(torch, lib, handle, net, load_peaks()[0], args.layer_report)
+        return 0
     for _ in range(args.warmup):
         step(lib, handle, net, dist=dist)
     torch.cuda.synchronize()

@@ -1,0 +1,640 @@
+// tcgen05 implicit-GEMM convolution, forward and backward-data (sm_100a).
+//
+//   D[pixel][out_ch] = sum_{(r,s,ch)} A[pixel][(r,s,ch)] * B[out_ch][(r,s,ch)]
+//
+// This is the ImplicitGemm solver for bf16 ("composable
+// kernels": blockwise tiles -> LDS -> threadwise MMA, re-designed for
+// Blackwell) and the bf16 engine of the Im2colGemm backward-data path.
+//
+// Persistent, warp-specialised CTA (one per SM, 288 threads):
+//   warps 0-3  producers: A tiles gathered from NHWC activations with 16-byte
+//              cp.async (zero-fill = padding / stride holes) into the canonical
+//              K-major SWIZZLE_128B layout, or loaded by TMA when the
+//              convolution is a plain GEMM (1x1, stride 1, no padding); B
+//              (filter [out][R][S][pitch]) is a 2-D TMA tile (OOB zero fill
+//              covers the K tail and out-of-range output channels);
+//   warp 4     TMEM allocator + MMA issuer: one elected lane issues
+//              tcgen05.mma (M=128, N=BN, K=16) into a double-buffered TMEM
+//              accumulator; tcgen05.commit recycles smem stages;
+//   warps 5-8  epilogue: tcgen05.ld (32x32b) -> fused bias/BN/activation ->
+//              bf16 -> swizzled smem staging -> fully coalesced 16-byte global
+//              stores, overlapping the next tile's main loop.
+// Backward data with stride > 1 uses sub-pixel (phase) decomposition: output
+// pixels are grouped by (h mod s, w mod s) and each phase only iterates the
+// filter taps that reach it, so no tensor-core work is spent on stride holes.
+#include "common.cuh"
+#include "tc_host.cuh"
+#include "tc_internal.h"
+#include "tc_ptx.cuh"
+
+namespace pk {
+namespace {
+
+using namespace pk::tc;
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 416;  // 4 producer + 1 MMA + 8 epilogue warps
+constexpr int kMaxPhases = 16;
+constexpr int kMaxTaps = 1024;
+
+enum Mode { GATHER_FWD = 0, GATHER_DGRAD = 1, PHASE_DGRAD = 2, PLAIN = 3 };
+
+struct ConvTcArgs {
+    int M;                 // output rows (non-phase modes)
+    int Ho, Wo;            // output image extent
+    int Hs, Ws;            // gathered source extent
+    int src_pitch;         // channel pitch of the source
+    int red_ch;            // reduction channels per tap (multiple of 8)
+    int R, S, pad_h, pad_w, str_h, str_w, dil_h, dil_w;
+    int kred, num_kb;      // non-phase modes
+    int n_out, out_pitch;
+    int n_tiles_n, total_tiles;
+    // phase decomposition (PHASE_DGRAD)
+    int num_phases, cpt;   // cpt = red_ch / 64
+    int ph_tile_start[kMaxPhases + 1];
+    int ph_rows[kMaxPhases], ph_hp[kMaxPhases], ph_wp[kMaxPhases];
+    int ph_h0[kMaxPhases], ph_w0[kMaxPhases];
+    int ph_tap_start[kMaxPhases + 1];
+    unsigned short taps[kMaxTaps];  // (r << 8) | s
+};
+
+template <int BN, int STAGES>
+struct Smem {
+    static constexpr int kA = BM * BK * 2;
+    static constexpr int kB = BN * BK * 2;
+    static constexpr int kStage = kA + kB;
+    static constexpr int kStaging = 8 * 2 * 32 * 128;  // 8 epilogue warps x 2 buffers x 32 x 128 B
+    static constexpr int kStagingOff = STAGES * kStage;
+    static constexpr int kBarOff = kStagingOff + kStaging;
+    static constexpr int kBytes = kBarOff + (2 * STAGES + 4) * 8 + 16 + 1024;
+};
+
+struct TileInfo {
+    int phase, m0, rows, n0, nkb;
+};
+
+template <int MODE>
+__device__ __forceinline__ TileInfo tile_info(const ConvTcArgs& g, int t) {
+    TileInfo ti;
+    const int nt = t % g.n_tiles_n;
+    int mt = t / g.n_tiles_n;
+    ti.n0 = nt;  // N-tile index; callers scale by BN
+    if (MODE == PHASE_DGRAD) {
+        int ph = 0;
+        while (ph + 1 < g.num_phases && mt >= g.ph_tile_start[ph + 1]) ++ph;
+        ti.phase = ph;
+        ti.m0 = (mt - g.ph_tile_start[ph]) * BM;
+        ti.rows = g.ph_rows[ph];
+        ti.nkb = (g.ph_tap_start[ph + 1] - g.ph_tap_start[ph]) * g.cpt;
+    } else {
+        ti.phase = 0;
+        ti.m0 = mt * BM;
+        ti.rows = g.M;
+        ti.nkb = g.num_kb;
+    }
+    return ti;
+}
+
+// Output coordinates (n, oy, ox) of row m of a tile's phase.
+template <int MODE>
+__device__ __forceinline__ void row_coords(const ConvTcArgs& g, int phase, int m, int& n, int& oy,
+                                           int& ox) {
+    if (MODE == PHASE_DGRAD) {
+        const int hp = g.ph_hp[phase], wp = g.ph_wp[phase];
+        const int per = hp * wp;
+        n = m / per;
+        const int rem = m - n * per;
+        const int hy = rem / wp;
+        oy = hy * g.str_h + g.ph_h0[phase];
+        ox = (rem - hy * wp) * g.str_w + g.ph_w0[phase];
+    } else {
+        const int per = g.Ho * g.Wo;
+        n = m / per;
+        const int rem = m - n * per;
+        oy = rem / g.Wo;
+        ox = rem - oy * g.Wo;
+    }
+}
+
+template <int BN, int STAGES, int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_tc_kernel(const __grid_constant__ CUtensorMap amap,
+                   const __grid_constant__ CUtensorMap bmap,
+                   const __grid_constant__ CUtensorMap ymap,
+                   const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ out,
+                   const __grid_constant__ ConvTcArgs g, const pk_epilogue epi) {
+    using L = Smem<BN, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tmem_full = empty + STAGES;   // [2]
+    uint64_t* tmem_empty = tmem_full + 2;   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int kAccCols = 2 * BN;  // double-buffered accumulator
+    constexpr uint32_t kTmemCols = kAccCols <= 32 ? 32 : kAccCols <= 64 ? 64 : kAccCols <= 128 ? 128
+                                   : kAccCols <= 256 ? 256 : 512;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&full[i], MODE == PLAIN ? 1 : 128 + 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tmem_full[i], 1);
+            mbar_init(&tmem_empty[i], 8);
+        }
+        fence_barrier_init();
+        tma_prefetch(&bmap);
+        if (MODE == PLAIN) tma_prefetch(&amap);
+        if (MODE != PHASE_DGRAD) tma_prefetch(&ymap);
+    }
+    if (warp == 4) tmem_alloc(tmem_slot, kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp < 4) {
+        // ======================= producers ==================================
+        int stage = 0;
+        uint32_t phase = 0;
+        const int j = lane & 7;
+        const int rbase = warp * 32 + (lane >> 3);
+        const int chunks_per_tap = g.red_ch >> 3;
+        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
+            const TileInfo ti = tile_info<MODE>(g, t);
+            if (ti.nkb == 0) continue;
+            const int n0 = ti.n0 * BN;
+            int row_img[8], row_h[8], row_w[8];
+            if (MODE != PLAIN) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int m = ti.m0 + rbase + 4 * i;
+                    if (m < ti.rows) {
+                        int n, oy, ox;
+                        row_coords<MODE>(g, ti.phase, m, n, oy, ox);
+                        row_img[i] = n * g.Hs;
+                        if (MODE == GATHER_FWD) {
+                            row_h[i] = oy * g.str_h - g.pad_h;
+                            row_w[i] = ox * g.str_w - g.pad_w;
+                        } else {
+                            row_h[i] = oy + g.pad_h;
+                            row_w[i] = ox + g.pad_w;
+                        }
+                    } else {
+                        row_img[i] = -1;
+                        row_h[i] = row_w[i] = 0;
+                    }
+                }
+            }
+            const int tap0 = MODE == PHASE_DGRAD ? g.ph_tap_start[ti.phase] : 0;
+            for (int kb = 0; kb < ti.nkb; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* sa = smem + stage * L::kStage;
+                int r = 0, s = 0, c8 = 0, bcol = kb * BK;
+                bool kvalid = true;
+                if (MODE == PHASE_DGRAD) {
+                    const int tap = kb / g.cpt, chunk = kb - tap * g.cpt;
+                    const unsigned short rs = g.taps[tap0 + tap];
+                    r = rs >> 8;
+                    s = rs & 0xff;
+                    c8 = chunk * 8 + j;
+                    bcol = (r * g.S + s) * g.red_ch + chunk * BK;
+                } else if (MODE != PLAIN) {
+                    const int k8 = kb * (BK / 8) + j;
+                    kvalid = k8 * 8 < g.kred;
+                    if (kvalid) {
+                        const int rs = k8 / chunks_per_tap;
+                        c8 = k8 - rs * chunks_per_tap;
+                        r = rs / g.S;
+                        s = rs - r * g.S;
+                    }
+                }
+                if (threadIdx.x == 0) {
+                    mbar_arrive_expect_tx(&full[stage], MODE == PLAIN ? L::kA + L::kB : L::kB);
+                    tma_load_2d(smem_u32(sa + L::kA), &bmap, &full[stage], bcol, n0);
+                    if (MODE == PLAIN) tma_load_2d(smem_u32(sa), &amap, &full[stage], kb * BK, ti.m0);
+                }
+                if (MODE != PLAIN) {
+                    const uint32_t sa_u = smem_u32(sa);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int row = rbase + 4 * i;
+                        const uint32_t dst = sa_u + row * 128 + ((j ^ (row & 7)) << 4);
+                        const __nv_bfloat16* p = src;
+                        uint32_t bytes = 0;
+                        if (kvalid && row_img[i] >= 0) {
+                            int ih, iw;
+                            bool ok;
+                            if (MODE == GATHER_FWD) {
+                                ih = row_h[i] + r * g.dil_h;
+                                iw = row_w[i] + s * g.dil_w;
+                                ok = ih >= 0 && ih < g.Hs && iw >= 0 && iw < g.Ws;
+                            } else {
+                                const int nh = row_h[i] - r * g.dil_h, nw = row_w[i] - s * g.dil_w;
+                                ok = nh >= 0 && nw >= 0;
+                                if (MODE == GATHER_DGRAD) {
+                                    if (g.str_h > 1) ok = ok && (nh % g.str_h) == 0;
+                                    if (g.str_w > 1) ok = ok && (nw % g.str_w) == 0;
+                                }
+                                ih = nh / g.str_h;
+                                iw = nw / g.str_w;
+                                ok = ok && ih < g.Hs && iw < g.Ws;
+                            }
+                            if (ok) {
+                                p = src + ((size_t)(row_img[i] + ih) * g.Ws + iw) * g.src_pitch +
+                                    c8 * 8;
+                                bytes = 16;
+                            }
+                        }
+                        cp_async_16(dst, p, bytes);
+                    }
+                    cp_async_arrive_noinc(&full[stage]);
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 4) {
+        // ======================= MMA issuer ==================================
+        constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, false, false);
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
+            const TileInfo ti = tile_info<MODE>(g, t);
+            if (ti.nkb == 0) continue;
+            const int a = it & 1;
+            const uint32_t aphase = (it >> 1) & 1;
+            ++it;
+            mbar_wait(&tmem_empty[a], aphase ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + a * BN;
+            for (int kb = 0; kb < ti.nkb; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    fence_proxy_async_smem();
+                    const uint32_t a_base = smem_u32(smem + stage * L::kStage);
+                    const uint32_t b_base = a_base + L::kA;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t ad = umma_desc_sw128(a_base + k * 32, 16, 1024);
+                        const uint64_t bd = umma_desc_sw128(b_base + k * 32, 16, 1024);
+                        mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    mma_commit(&empty[stage]);
+                    if (kb == ti.nkb - 1) mma_commit(&tmem_full[a]);
+                }
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else {
+        // ======================= epilogue ====================================
+        // 8 warps: two per TMEM lane quarter (warp % 4), splitting the 64-column
+        // chunks between them; each stages a 32 x 64 bf16 tile in swizzled smem
+        // and hands it to a TMA store (double-buffered staging per warp).
+        constexpr bool kTmaStore = MODE != PHASE_DGRAD;
+        const int ew = warp - 5;
+        const int q = warp & 3;
+        const int half = ew >> 2;
+        uint8_t* stg_base = smem + L::kStagingOff + ew * 2 * 4096;
+        int sbuf = 0;
+        const bool has_epi = epilogue_active(&epi);
+        int it = 0;
+        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
+            const TileInfo ti = tile_info<MODE>(g, t);
+            const int n0 = ti.n0 * BN;
+            const int my_m = ti.m0 + q * 32 + lane;
+            int my_n = 0, my_oy = 0, my_ox = 0;  // (n unused: epilogue indexes by oy, ox)
+            if (my_m < ti.rows) row_coords<MODE>(g, ti.phase, my_m, my_n, my_oy, my_ox);
+            int a = 0;
+            const bool live = ti.nkb > 0;
+            if (live) {
+                a = it & 1;
+                const uint32_t aphase = (it >> 1) & 1;
+                ++it;
+                mbar_wait(&tmem_full[a], aphase);
+                tc_fence_after();
+            }
+            // 64-column chunks that reach the output (warp-uniform)
+            const int span = min(BN, g.out_pitch - n0);
+            const int nchunks = (span + 63) / 64;
+            int my_last = -1;
+            for (int ci = half; ci < nchunks; ci += 2) my_last = ci;
+            if (live && my_last < 0) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tmem_empty[a]);
+            }
+            const int srow0 = lane >> 3, sj = lane & 7;
+#pragma unroll 1
+            for (int ci = half; ci < nchunks; ci += 2) {
+                const int c0 = ci * 64;
+                uint32_t v[64];
+                if (live) {
+                    const uint32_t ta = tmem_base + a * BN + c0 + (static_cast<uint32_t>(q * 32) << 16);
+                    tmem_ld16(ta + 0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+                    if (BN >= 32) tmem_ld16(ta + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+                    if (BN >= 64) {
+                        tmem_ld16(ta + 32, *reinterpret_cast<uint32_t(*)[16]>(&v[32]));
+                        tmem_ld16(ta + 48, *reinterpret_cast<uint32_t(*)[16]>(&v[48]));
+                    }
+                    tmem_ld_wait();
+                    if (ci == my_last) {
+                        // this warp's share of the accumulator is read: release
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tmem_empty[a]);
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 64; ++e) v[e] = 0u;
+                }
+                uint8_t* stg = stg_base + sbuf * 4096;
+                const uint32_t stg_u = smem_u32(stg);
+                if (kTmaStore) {
+                    // the store issued from this buffer two chunks ago must have
+                    // finished reading it
+                    if (lane == 0) bulk_wait_read<1>();
+                    __syncwarp();
+                }
+                // math + pack into the swizzled staging row of this lane
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    uint32_t packed[4];
+#pragma unroll
+                    for (int e = 0; e < 8; e += 2) {
+                        const int ch = n0 + c0 + jj * 8 + e;
+                        float x0 = __uint_as_float(v[jj * 8 + e]);
+                        float x1 = __uint_as_float(v[jj * 8 + e + 1]);
+                        if (has_epi) {
+                            if (ch < g.n_out) x0 = apply_epilogue(epi, x0, ch, my_oy, my_ox, g.Ho, g.Wo);
+                            if (ch + 1 < g.n_out)
+                                x1 = apply_epilogue(epi, x1, ch + 1, my_oy, my_ox, g.Ho, g.Wo);
+                        }
+                        if (ch >= g.n_out || c0 + jj * 8 + e >= BN) x0 = 0.0f;
+                        if (ch + 1 >= g.n_out || c0 + jj * 8 + e + 1 >= BN) x1 = 0.0f;
+                        __nv_bfloat162 b2 = __floats2bfloat162_rn(x0, x1);
+                        packed[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
+                    }
+                    const uint32_t dst = stg_u + lane * 128 + ((jj ^ (lane & 7)) << 4);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst),
+                                 "r"(packed[0]), "r"(packed[1]), "r"(packed[2]), "r"(packed[3])
+                                 : "memory");
+                }
+                if (kTmaStore) {
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&ymap, stg_u, n0 + c0, ti.m0 + q * 32);
+                        bulk_commit();
+                    }
+                    sbuf ^= 1;
+                } else {
+                    __syncwarp();
+                    // coalesced stores: 4 rows x 128 B per instruction
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int row = srow0 + 4 * i;
+                        const int m = ti.m0 + q * 32 + row;
+                        uint4 val;
+                        const uint32_t srcs = stg_u + row * 128 + ((sj ^ (row & 7)) << 4);
+                        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(val.x), "=r"(val.y), "=r"(val.z), "=r"(val.w)
+                                     : "r"(srcs));
+                        const int ch = n0 + c0 + sj * 8;
+                        if (m < ti.rows && ch < g.out_pitch && c0 + sj * 8 < BN) {
+                            int n, oy, ox;
+                            row_coords<MODE>(g, ti.phase, m, n, oy, ox);
+                            const size_t pix = ((size_t)n * g.Ho + oy) * g.Wo + ox;
+                            *reinterpret_cast<uint4*>(out + pix * g.out_pitch + ch) = val;
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        if (kTmaStore && lane == 0) bulk_wait_all();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 4) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, kTmemCols);
+    }
+}
+
+template <int BN, int STAGES, int MODE>
+cudaError_t launch(const CUtensorMap& amap, const CUtensorMap& bmap, const CUtensorMap& ymap,
+                   const void* src, void* out, const ConvTcArgs& g, const pk_epilogue& e,
+                   cudaStream_t st) {
+    using L = Smem<BN, STAGES>;
+    auto kern = conv_tc_kernel<BN, STAGES, MODE>;
+    static int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+        cudaError_t err =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+        if (err != cudaSuccess) return err;
+        attr_dev = dev;
+    }
+    int grid = num_sms_of_current_device();
+    if (g.total_tiles < grid) grid = g.total_tiles;
+    if (grid < 1) grid = 1;
+    kern<<<grid, kThreads, L::kBytes, st>>>(amap, bmap, ymap, (const __nv_bfloat16*)src,
+                                            (__nv_bfloat16*)out, g, e);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t dispatch_bn(int bn, const CUtensorMap& amap, const CUtensorMap& bmap, const void* src,
+                        void* out, const ConvTcArgs& g, const pk_epilogue& e, cudaStream_t st) {
+    CUtensorMap ymap{};
+    if (MODE != PHASE_DGRAD &&
+        !tc::make_map_2d(&ymap, out, g.M, g.out_pitch, g.out_pitch, 32))
+        return cudaErrorInvalidValue;
+    if (bn == 32) return launch<32, 8, MODE>(amap, bmap, ymap, src, out, g, e, st);
+    if (bn == 64) return launch<64, 6, MODE>(amap, bmap, ymap, src, out, g, e, st);
+    if (bn == 128) return launch<128, 5, MODE>(amap, bmap, ymap, src, out, g, e, st);
+    return launch<256, 3, MODE>(amap, bmap, ymap, src, out, g, e, st);
+}
+
+int pick_bn(int want, int out_pitch) {
+    int bn = want <= 64 ? 64 : want <= 128 ? 128 : 256;
+    const int need = out_pitch <= 32 ? 32 : out_pitch <= 64 ? 64 : out_pitch <= 128 ? 128 : 256;
+    return bn < need ? bn : need;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+void base_args(ConvTcArgs& t, int bn) {
+    t.n_tiles_n = (t.out_pitch + bn - 1) / bn;
+}
+
+// Sub-pixel phase tables for backward data with stride > 1.
+bool build_phases(ConvTcArgs& t, int n_img, int H, int W) {
+    const int sh = t.str_h, sw = t.str_w;
+    if (sh * sw > kMaxPhases || t.R * t.S > kMaxTaps || t.red_ch % BK != 0) return false;
+    t.num_phases = sh * sw;
+    t.cpt = t.red_ch / BK;
+    int tiles = 0, taps = 0;
+    for (int ph = 0; ph < sh; ++ph)
+        for (int pw = 0; pw < sw; ++pw) {
+            const int i = ph * sw + pw;
+            const int hp = H > ph ? (H - ph + sh - 1) / sh : 0;
+            const int wp = W > pw ? (W - pw + sw - 1) / sw : 0;
+            t.ph_hp[i] = hp;
+            t.ph_wp[i] = wp;
+            t.ph_h0[i] = ph;
+            t.ph_w0[i] = pw;
+            t.ph_rows[i] = n_img * hp * wp;
+            t.ph_tile_start[i] = tiles;
+            tiles += (t.ph_rows[i] + BM - 1) / BM;
+            t.ph_tap_start[i] = taps;
+            for (int r = 0; r < t.R; ++r) {
+                const int vh = ph + t.pad_h - r * t.dil_h;
+                if (((vh % sh) + sh) % sh) continue;
+                for (int s = 0; s < t.S; ++s) {
+                    const int vw = pw + t.pad_w - s * t.dil_w;
+                    if (((vw % sw) + sw) % sw) continue;
+                    t.taps[taps++] = static_cast<unsigned short>((r << 8) | s);
+                }
+            }
+        }
+    t.ph_tile_start[t.num_phases] = tiles;
+    t.ph_tap_start[t.num_phases] = taps;
+    t.total_tiles = tiles * t.n_tiles_n;
+    return true;
+}
+
+}  // namespace
+}  // namespace pk
+
+using namespace pk;
+
+extern "C" {
+
+int pk_tc_fwd_supported(const pk_conv_geom* g) {
+    return g->groups == 1 && !g->transpose && g->x_pitch % 8 == 0 && g->f_pitch % 8 == 0 &&
+           g->y_pitch % 8 == 0 && g->r < 256 && g->s < 256 && tc::encode_fn() != nullptr;
+}
+
+int pk_tc_dgrad_supported(const pk_conv_geom* g) {
+    // outputs with very few channels waste most of a 64-wide MMA tile; the
+    // CUDA-core path is faster there
+    return g->groups == 1 && !g->transpose && g->r < 256 && g->s < 256 &&
+           tc::encode_fn() != nullptr;
+}
+
+size_t pk_tc_dgrad_workspace(const pk_conv_geom* g) {
+    return (size_t)g->c * g->r * g->s * pk_pitch(g->k) * 2;  // [C][R][S][pitch(K)] bf16
+}
+
+cudaError_t pk_cuda_igemm_tc_fwd(const pk_conv_geom* g, const void* x, const void* f, void* y,
+                                 const pk_epilogue* epi, const pk_tc_config* cfg,
+                                 cudaStream_t st) {
+    if (!pk_tc_fwd_supported(g) || !aligned16(x) || !aligned16(f) || !aligned16(y))
+        return cudaErrorNotSupported;
+    ConvTcArgs t{};
+    t.M = g->n * g->p * g->q;
+    t.Ho = g->p;
+    t.Wo = g->q;
+    t.Hs = g->h;
+    t.Ws = g->w;
+    t.src_pitch = g->x_pitch;
+    t.red_ch = g->f_pitch;
+    t.R = g->r;
+    t.S = g->s;
+    t.pad_h = g->pad_h;
+    t.pad_w = g->pad_w;
+    t.str_h = g->str_h;
+    t.str_w = g->str_w;
+    t.dil_h = g->dil_h;
+    t.dil_w = g->dil_w;
+    t.kred = g->r * g->s * g->f_pitch;
+    t.num_kb = (t.kred + BK - 1) / BK;
+    t.n_out = g->k;
+    t.out_pitch = g->y_pitch;
+    const int bn = pick_bn(cfg ? cfg->block_n : 256, g->y_pitch);
+    base_args(t, bn);
+    t.total_tiles = ((t.M + BM - 1) / BM) * t.n_tiles_n;
+    pk_epilogue e{};
+    e.act = -1;
+    if (epi) e = *epi;
+    CUtensorMap amap{}, bmap{};
+    if (!tc::make_map_2d(&bmap, f, g->k, t.kred, t.kred, bn)) return cudaErrorInvalidValue;
+    const bool plain = g->r == 1 && g->s == 1 && g->str_h == 1 && g->str_w == 1 &&
+                       g->pad_h == 0 && g->pad_w == 0 && g->x_pitch == g->f_pitch;
+    if (plain) {
+        if (!tc::make_map_2d(&amap, x, t.M, g->x_pitch, g->x_pitch, BM)) return cudaErrorInvalidValue;
+        return dispatch_bn<PLAIN>(bn, amap, bmap, x, y, t, e, st);
+    }
+    // TMA rectangle tiles when the channel pitch is a multiple of 64
+    const cudaError_t te = pk_tma_conv(g, false, x, f, y, &e, cfg ? cfg->block_n : 256, st);
+    if (te != cudaErrorNotSupported) return te;
+    return dispatch_bn<GATHER_FWD>(bn, amap, bmap, x, y, t, e, st);
+}
+
+cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const void* f, void* dx,
+                                   void* workspace, const pk_tc_config* cfg, cudaStream_t st) {
+    if (!pk_tc_dgrad_supported(g) || !aligned16(dy) || !aligned16(dx)) return cudaErrorNotSupported;
+    // B operand: Wt[c][r][s][k] = W[k][r][s][c]
+    cudaError_t err = pk_cuda_filter_to_dgrad(g, PK_BF16, f, workspace, st);
+    if (err != cudaSuccess) return err;
+    const int kp = pk_pitch(g->k);
+    ConvTcArgs t{};
+    t.M = g->n * g->h * g->w;
+    t.Ho = g->h;
+    t.Wo = g->w;
+    t.Hs = g->p;
+    t.Ws = g->q;
+    t.src_pitch = g->y_pitch;
+    t.red_ch = kp;
+    t.R = g->r;
+    t.S = g->s;
+    t.pad_h = g->pad_h;
+    t.pad_w = g->pad_w;
+    t.str_h = g->str_h;
+    t.str_w = g->str_w;
+    t.dil_h = g->dil_h;
+    t.dil_w = g->dil_w;
+    t.kred = g->r * g->s * kp;
+    t.num_kb = (t.kred + BK - 1) / BK;
+    t.n_out = g->c;
+    t.out_pitch = g->x_pitch;
+    const int bn = pick_bn(cfg ? cfg->block_n : 256, g->x_pitch);
+    base_args(t, bn);
+    t.total_tiles = ((t.M + BM - 1) / BM) * t.n_tiles_n;
+    pk_epilogue e{};
+    e.act = -1;
+    CUtensorMap amap{}, bmap{};
+    if (!tc::make_map_2d(&bmap, workspace, g->c, t.kred, t.kred, bn)) return cudaErrorInvalidValue;
+    const bool plain = g->r == 1 && g->s == 1 && g->str_h == 1 && g->str_w == 1 &&
+                       g->pad_h == 0 && g->pad_w == 0;
+    if (plain) {
+        if (!tc::make_map_2d(&amap, dy, t.M, g->y_pitch, g->y_pitch, BM)) return cudaErrorInvalidValue;
+        return dispatch_bn<PLAIN>(bn, amap, bmap, dy, dx, t, e, st);
+    }
+    const cudaError_t te = pk_tma_conv(g, true, dy, workspace, dx, nullptr,
+                                       cfg ? cfg->block_n : 256, st);
+    if (te != cudaErrorNotSupported) return te;
+    if ((g->str_h > 1 || g->str_w > 1) && build_phases(t, g->n, g->h, g->w))
+        return dispatch_bn<PHASE_DGRAD>(bn, amap, bmap, dy, dx, t, e, st);
+    return dispatch_bn<GATHER_DGRAD>(bn, amap, bmap, dy, dx, t, e, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,743 @@
+// TMA-fed tcgen05 convolution kernels (sm_100a) — the fast path for layers
+// whose channel pitches are multiples of 64 (every ResNet-50 / VGG-16 layer
+// except the 3-channel stem).
+//
+// Idea: tile the output as RECTANGLES of pixels (bw x bh x bn = 128) instead
+// of linear pixel ranges. For a filter tap (r, s) the A operand of a
+// rectangle is then itself a rectangle of the NHWC source, shifted by the tap
+// (and traversed with the convolution stride), so one 4-D TMA box load with
+// out-of-bounds zero fill performs the whole im2col gather — padding
+// included — with no producer threads. A single elected thread streams A and
+// B (filter, 2-D box) into a multi-stage SWIZZLE_128B ring; one thread issues
+// tcgen05.mma into a double-buffered TMEM accumulator; 8 epilogue warps drain
+// it (fused bias/BN/activation), stage bf16 tiles in swizzled smem and write
+// them with 4-D TMA stores (hardware clips partial rectangles).
+//
+// Backward data reuses the kernel: stride 1 is a convolution of dY with the
+// transposed filter (tap offsets pad - r*dil); stride > 1 is split into
+// sub-pixel phases (h mod s, w mod s), each a dense convolution over only the
+// taps that reach it, written back with strided global stores.
+//
+// Backward weights: rectangles of 64 pixels form the reduction blocks; dY and
+// the tap-shifted X rectangles arrive by TMA as MN-major operands; split-K
+// over rectangles with a fixed-order fp32 reduction.
+#include "common.cuh"
+#include "tc_host.cuh"
+#include "tc_internal.h"
+#include "tc_ptx.cuh"
+
+namespace pk {
+namespace {
+
+using namespace pk::tc;
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kMaxPhases = 16;
+constexpr int kMaxTaps = 1024;
+constexpr int kFpropThreads = 320;  // producer, MMA, 8 epilogue warps
+
+struct TmaConvArgs {
+    int N;
+    int red_ch, cpt;          // reduction channels per tap (pitch) and 64-chunks per tap
+    int S;                    // filter width (B column = (r*S + s)*red_ch)
+    int mult_h, mult_w;       // source coordinate multiplier (stride for fprop, 1 for dgrad)
+    int n_out, out_pitch;
+    int Ho, Wo;               // full output extent
+    int str_h, str_w;         // output phase strides (dgrad) / 1
+    int bw, bh, bn;           // rectangle tile
+    int qbw, qbh, qbn;        // per-epilogue-warp quarter sub-box
+    int n_tiles_n, total_tiles;
+    int num_phases;
+    int ph_tw[kMaxPhases], ph_th[kMaxPhases], ph_tn[kMaxPhases];
+    int ph_tile_start[kMaxPhases + 1];
+    int ph_hp[kMaxPhases], ph_wp[kMaxPhases], ph_h0[kMaxPhases], ph_w0[kMaxPhases];
+    int ph_tap_start[kMaxPhases + 1];
+    unsigned short taps[kMaxTaps];   // (r << 8) | s
+    short off_h[kMaxTaps], off_w[kMaxTaps];
+};
+
+template <int BN, int STAGES>
+struct FSmem {
+    static constexpr int kA = BM * BK * 2;
+    static constexpr int kB = BN * BK * 2;
+    static constexpr int kStage = kA + kB;
+    static constexpr int kStaging = 8 * 2 * 4096;
+    static constexpr int kStagingOff = STAGES * kStage;
+    static constexpr int kBarOff = kStagingOff + kStaging;
+    static constexpr int kBytes = kBarOff + (2 * STAGES + 4) * 8 + 16 + 1024;
+};
+
+struct RectInfo {
+    int phase, n0, h0, w0, nt, ntaps, tap0;
+};
+
+__device__ __forceinline__ RectInfo rect_info(const TmaConvArgs& g, int t) {
+    RectInfo ri;
+    ri.nt = t % g.n_tiles_n;
+    const int mt = t / g.n_tiles_n;
+    int ph = 0;
+    while (ph + 1 < g.num_phases && mt >= g.ph_tile_start[ph + 1]) ++ph;
+    ri.phase = ph;
+    int loc = mt - g.ph_tile_start[ph];
+    const int tw = g.ph_tw[ph], th = g.ph_th[ph];
+    const int wi = loc % tw;
+    loc /= tw;
+    const int hi = loc % th;
+    const int ni = loc / th;
+    ri.w0 = wi * g.bw;
+    ri.h0 = hi * g.bh;
+    ri.n0 = ni * g.bn;
+    ri.tap0 = g.ph_tap_start[ph];
+    ri.ntaps = g.ph_tap_start[ph + 1] - ri.tap0;
+    return ri;
+}
+
+template <int BN, int STAGES, bool PHASED>
+__global__ void __launch_bounds__(kFpropThreads, 1)
+    conv_tma_fprop_kernel(const __grid_constant__ CUtensorMap amap,
+                          const __grid_constant__ CUtensorMap bmap,
+                          const __grid_constant__ CUtensorMap ymap, __nv_bfloat16* __restrict__ out,
+                          const __grid_constant__ TmaConvArgs g, const pk_epilogue epi) {
+    using L = FSmem<BN, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tmem_full = empty + STAGES;
+    uint64_t* tmem_empty = tmem_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr uint32_t kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
+                                   : 2 * BN <= 256 ? 256 : 512;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tmem_full[i], 1);
+            mbar_init(&tmem_empty[i], 8);
+        }
+        fence_barrier_init();
+        tma_prefetch(&amap);
+        tma_prefetch(&bmap);
+        if (!PHASED) tma_prefetch(&ymap);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer (one elected lane) -------------------
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
+                const RectInfo ri = rect_info(g, t);
+                const int nkb = ri.ntaps * g.cpt;
+                const int ys = ri.h0 * g.mult_h, xs = ri.w0 * g.mult_w;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    const int tap = kb / g.cpt, chunk = kb - tap * g.cpt;
+                    const int ti = ri.tap0 + tap;
+                    const unsigned short rs = g.taps[ti];
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* sa = smem + stage * L::kStage;
+                    mbar_arrive_expect_tx(&full[stage], L::kA + L::kB);
+                    tma_load_4d(smem_u32(sa), &amap, &full[stage], chunk * BK, xs + g.off_w[ti],
+                                ys + g.off_h[ti], ri.n0);
+                    tma_load_2d(smem_u32(sa + L::kA), &bmap, &full[stage],
+                                ((rs >> 8) * g.S + (rs & 0xff)) * g.red_ch + chunk * BK,
+                                ri.nt * BN);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------------------------------
+        constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, false, false);
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
+            const RectInfo ri = rect_info(g, t);
+            const int nkb = ri.ntaps * g.cpt;
+            if (nkb == 0) continue;
+            const int a = it & 1;
+            const uint32_t aphase = (it >> 1) & 1;
+            ++it;
+            mbar_wait(&tmem_empty[a], aphase ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + a * BN;
+            for (int kb = 0; kb < nkb; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t a_base = smem_u32(smem + stage * L::kStage);
+                    const uint32_t b_base = a_base + L::kA;
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t ad = umma_desc_sw128(a_base + k * 32, 16, 1024);
+                        const uint64_t bd = umma_desc_sw128(b_base + k * 32, 16, 1024);
+                        mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    mma_commit(&empty[stage]);
+                    if (kb == nkb - 1) mma_commit(&tmem_full[a]);
+                }
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else {
+        // ---------------- epilogue (8 warps) ---------------------------------
+        const int ew = warp - 2;
+        const int q = warp & 3;       // TMEM lane quarter accessible to this warp
+        const int half = ew >> 2;     // column-chunk parity handled by this warp
+        uint8_t* stg_base = smem + L::kStagingOff + ew * 2 * 4096;
+        int sbuf = 0;
+        const bool has_epi = epilogue_active(&epi);
+        // this lane's row inside the rectangle, and the quarter's sub-box origin
+        const int row = q * 32 + lane;
+        const int rw = row % g.bw, rh = (row / g.bw) % g.bh, rn = row / (g.bw * g.bh);
+        const int q0 = q * 32;
+        const int qw = q0 % g.bw, qh = (q0 / g.bw) % g.bh, qn = q0 / (g.bw * g.bh);
+        int it = 0;
+        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
+            const RectInfo ri = rect_info(g, t);
+            const int n0c = ri.nt * BN;
+            const bool live = ri.ntaps > 0;
+            // output coordinates of this lane's row
+            const int pn = ri.n0 + rn, ph_ = ri.h0 + rh, pw_ = ri.w0 + rw;
+            int oy = ph_, ox = pw_;
+            bool row_ok = pn < g.N && ph_ < g.ph_hp[ri.phase] && pw_ < g.ph_wp[ri.phase];
+            if (PHASED) {
+                oy = ph_ * g.str_h + g.ph_h0[ri.phase];
+                ox = pw_ * g.str_w + g.ph_w0[ri.phase];
+            }
+            int a = 0;
+            if (live) {
+                a = it & 1;
+                const uint32_t aphase = (it >> 1) & 1;
+                ++it;
+                mbar_wait(&tmem_full[a], aphase);
+                tc_fence_after();
+            }
+            const int span = min(BN, g.out_pitch - n0c);
+            const int nchunks = (span + 63) / 64;
+            int my_last = -1;
+            for (int ci = half; ci < nchunks; ci += 2) my_last = ci;
+            if (live && my_last < 0) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tmem_empty[a]);
+            }
+#pragma unroll 1
+            for (int ci = half; ci < nchunks; ci += 2) {
+                const int c0 = ci * 64;
+                uint32_t v[64];
+                if (live) {
+                    const uint32_t ta = tmem_base + a * BN + c0 + (static_cast<uint32_t>(q * 32) << 16);
+                    tmem_ld16(ta + 0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+                    if (BN >= 32) tmem_ld16(ta + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+                    if (BN >= 64) {
+                        tmem_ld16(ta + 32, *reinterpret_cast<uint32_t(*)[16]>(&v[32]));
+                        tmem_ld16(ta + 48, *reinterpret_cast<uint32_t(*)[16]>(&v[48]));
+                    }
+                    tmem_ld_wait();
+                    if (ci == my_last) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tmem_empty[a]);
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 64; ++e) v[e] = 0u;
+                }
+                const uint32_t stg_u = smem_u32(stg_base + sbuf * 4096);
+                if (!PHASED) {
+                    if (lane == 0) bulk_wait_read<1>();
+                    __syncwarp();
+                }
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    uint32_t packed[4];
+#pragma unroll
+                    for (int e = 0; e < 8; e += 2) {
+                        const int ch = n0c + c0 + jj * 8 + e;
+                        float x0 = __uint_as_float(v[jj * 8 + e]);
+                        float x1 = __uint_as_float(v[jj * 8 + e + 1]);
+                        if (has_epi) {
+                            if (ch < g.n_out) x0 = apply_epilogue(epi, x0, ch, oy, ox, g.Ho, g.Wo);
+                            if (ch + 1 < g.n_out)
+                                x1 = apply_epilogue(epi, x1, ch + 1, oy, ox, g.Ho, g.Wo);
+                        }
+                        if (ch >= g.n_out || c0 + jj * 8 + e >= BN) x0 = 0.0f;
+                        if (ch + 1 >= g.n_out || c0 + jj * 8 + e + 1 >= BN) x1 = 0.0f;
+                        __nv_bfloat162 b2 = __floats2bfloat162_rn(x0, x1);
+                        packed[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
+                    }
+                    const uint32_t dst = stg_u + lane * 128 + ((jj ^ (lane & 7)) << 4);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst),
+                                 "r"(packed[0]), "r"(packed[1]), "r"(packed[2]), "r"(packed[3])
+                                 : "memory");
+                }
+                if (!PHASED) {
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_4d(&ymap, stg_u, n0c + c0, ri.w0 + qw, ri.h0 + qh, ri.n0 + qn);
+                        bulk_commit();
+                    }
+                    sbuf ^= 1;
+                } else {
+                    __syncwarp();
+                    // each lane owns its row: write the 128-byte chunk back from
+                    // staging as 8 x 16 B (rows are strided in the output)
+                    if (row_ok) {
+                        __nv_bfloat16* dst = out + (((size_t)pn * g.Ho + oy) * g.Wo + ox) * g.out_pitch +
+                                             n0c + c0;
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) {
+                            if (n0c + c0 + jj * 8 >= g.out_pitch || c0 + jj * 8 >= BN) break;
+                            uint4 val;
+                            const uint32_t srcs = stg_u + lane * 128 + ((jj ^ (lane & 7)) << 4);
+                            asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                         : "=r"(val.x), "=r"(val.y), "=r"(val.z), "=r"(val.w)
+                                         : "r"(srcs));
+                            reinterpret_cast<uint4*>(dst)[jj] = val;
+                        }
+                    }
+                    __syncwarp();
+                }
+            }
+        }
+        if (!PHASED && lane == 0) bulk_wait_all();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, kTmemCols);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// wgrad: D[k][n], n = (r, s, c); reduction over 64-pixel rectangles.
+constexpr int WBN = 128;
+constexpr int kWgThreads = 192;  // producer, MMA, 4 epilogue warps
+
+struct TmaWgArgs {
+    int K, Nn;                 // GEMM M (out channels) and N (R*S*Cp)
+    int Cp, S;
+    int pad_h, pad_w, str_h, str_w, dil_h, dil_w;
+    int rw, rh, rn;            // reduction rectangle (product 64)
+    int tw, th;                // rectangles per row / column
+    int num_kb, kb_per_split;
+};
+
+template <int STAGES>
+struct WSmem {
+    static constexpr int kA = BM * BK * 2;
+    static constexpr int kB = WBN * BK * 2;
+    static constexpr int kStage = kA + kB;
+    static constexpr int kBarOff = STAGES * kStage;
+    static constexpr int kBytes = kBarOff + (2 * STAGES + 1) * 8 + 16 + 1024;
+};
+
+template <int STAGES>
+__global__ void __launch_bounds__(kWgThreads, 1)
+    conv_tma_wgrad_kernel(const __grid_constant__ CUtensorMap dymap,
+                          const __grid_constant__ CUtensorMap xmap, float* __restrict__ partial,
+                          const __grid_constant__ TmaWgArgs g) {
+    using L = WSmem<STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tmem_full = empty + STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.x * BM;
+    const int n0 = blockIdx.y * WBN;
+    const int split = blockIdx.z;
+    const int kb_begin = split * g.kb_per_split;
+    const int kb_end = min(g.num_kb, kb_begin + g.kb_per_split);
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(tmem_full, 1);
+        fence_barrier_init();
+        tma_prefetch(&dymap);
+        tma_prefetch(&xmap);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, WBN);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // the two 64-wide column blocks of B: (tap, channel chunk) each
+            int bc[2], bs[2], br[2];
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+                const int nidx = n0 + a * 64;
+                const int tap = nidx / g.Cp;
+                bc[a] = nidx - tap * g.Cp;
+                br[a] = tap / g.S;
+                bs[a] = tap - br[a] * g.S;
+            }
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int kb = kb_begin; kb < kb_end; ++kb) {
+                int loc = kb;
+                const int wi = loc % g.tw;
+                loc /= g.tw;
+                const int hi = loc % g.th;
+                const int ni = loc / g.th;
+                const int q0 = wi * g.rw, p0 = hi * g.rh, img0 = ni * g.rn;
+                mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* sa = smem + stage * L::kStage;
+                mbar_arrive_expect_tx(&full[stage], L::kA + L::kB);
+                tma_load_4d(smem_u32(sa), &dymap, &full[stage], m0, q0, p0, img0);
+                tma_load_4d(smem_u32(sa + L::kA / 2), &dymap, &full[stage], m0 + 64, q0, p0, img0);
+#pragma unroll
+                for (int a = 0; a < 2; ++a)
+                    tma_load_4d(smem_u32(sa + L::kA + a * (L::kB / 2)), &xmap, &full[stage], bc[a],
+                                q0 * g.str_w - g.pad_w + bs[a] * g.dil_w,
+                                p0 * g.str_h - g.pad_h + br[a] * g.dil_h, img0);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = idesc_bf16_f32(BM, WBN, true, true);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int kb = kb_begin; kb < kb_end; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t a_base = smem_u32(smem + stage * L::kStage);
+                const uint32_t b_base = a_base + L::kA;
+#pragma unroll
+                for (int k = 0; k < BK / 16; ++k) {
+                    const uint64_t ad = umma_desc_sw128(a_base + k * 2048, L::kA / 2, 1024);
+                    const uint64_t bd = umma_desc_sw128(b_base + k * 2048, L::kB / 2, 1024);
+                    mma_bf16(tmem_base, ad, bd, idesc, (kb != kb_begin) || (k != 0));
+                }
+                mma_commit(&empty[stage]);
+                if (kb == kb_end - 1) mma_commit(tmem_full);
+            }
+            __syncwarp();
+            if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+    } else {
+        const int q = warp & 3;
+        const bool live = kb_end > kb_begin;
+        if (live) {
+            mbar_wait(tmem_full, 0);
+            tc_fence_after();
+        }
+        const int k = m0 + q * 32 + lane;
+#pragma unroll 1
+        for (int c0 = 0; c0 < WBN; c0 += 16) {
+            uint32_t v[16];
+            if (live) {
+                tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c0, v);
+                tmem_ld_wait();
+            } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] = 0u;
+            }
+            const int nn = n0 + c0;
+            if (k >= g.K || nn >= g.Nn) continue;
+            float* dst = partial + ((size_t)split * g.K + k) * g.Nn + nn;
+            if (nn + 16 <= g.Nn) {
+#pragma unroll
+                for (int e = 0; e < 16; e += 4)
+                    *reinterpret_cast<float4*>(dst + e) =
+                        make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]),
+                                    __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
+            } else {
+                for (int e = 0; e < 16 && nn + e < g.Nn; ++e) dst[e] = __uint_as_float(v[e]);
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, WBN);
+    }
+}
+
+__global__ void wgrad_sum_kernel(const float* __restrict__ partial, int splits, long long total,
+                                 __nv_bfloat16* __restrict__ dw) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        float acc = 0.0f;
+        for (int s = 0; s < splits; ++s) acc += partial[(size_t)s * total + i];
+        dw[i] = __float2bfloat16_rn(acc);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host
+
+template <int BN, int STAGES, bool PHASED>
+cudaError_t launch_fprop(const CUtensorMap& amap, const CUtensorMap& bmap, const CUtensorMap& ymap,
+                         void* out, const TmaConvArgs& g, const pk_epilogue& e, cudaStream_t st) {
+    using L = FSmem<BN, STAGES>;
+    auto kern = conv_tma_fprop_kernel<BN, STAGES, PHASED>;
+    static int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+        cudaError_t err =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+        if (err != cudaSuccess) return err;
+        attr_dev = dev;
+    }
+    int grid = num_sms_of_current_device();
+    if (g.total_tiles < grid) grid = g.total_tiles;
+    if (grid < 1) grid = 1;
+    kern<<<grid, kFpropThreads, L::kBytes, st>>>(amap, bmap, ymap, (__nv_bfloat16*)out, g, e);
+    count_launch();
+    return cudaGetLastError();
+}
+
+template <bool PHASED>
+cudaError_t dispatch_fprop(int bn, const CUtensorMap& amap, const CUtensorMap& bmap,
+                           const CUtensorMap& ymap, void* out, const TmaConvArgs& g,
+                           const pk_epilogue& e, cudaStream_t st) {
+    if (bn == 64) return launch_fprop<64, 6, PHASED>(amap, bmap, ymap, out, g, e, st);
+    if (bn == 128) return launch_fprop<128, 5, PHASED>(amap, bmap, ymap, out, g, e, st);
+    return launch_fprop<256, 3, PHASED>(amap, bmap, ymap, out, g, e, st);
+}
+
+int choose_bn(int want, int out_pitch) {
+    int bn = want <= 64 ? 64 : want <= 128 ? 128 : 256;
+    const int need = out_pitch <= 64 ? 64 : out_pitch <= 128 ? 128 : 256;
+    return bn < need ? bn : need;
+}
+
+// Fill tile grid / tap tables. Phases: ph in [0, sh) x [0, sw) (1 x 1 for fprop).
+bool fill_phases(TmaConvArgs& t, int n_img, int Ho, int Wo, int sh, int sw, int R, int S,
+                 int pad_h, int pad_w, int dil_h, int dil_w, bool dgrad) {
+    if (sh * sw > kMaxPhases || R * S > kMaxTaps) return false;
+    t.num_phases = sh * sw;
+    int tiles = 0, taps = 0;
+    for (int ph = 0; ph < sh; ++ph)
+        for (int pw = 0; pw < sw; ++pw) {
+            const int i = ph * sw + pw;
+            const int hp = Ho > ph ? (Ho - ph + sh - 1) / sh : 0;
+            const int wp = Wo > pw ? (Wo - pw + sw - 1) / sw : 0;
+            t.ph_hp[i] = hp;
+            t.ph_wp[i] = wp;
+            t.ph_h0[i] = ph;
+            t.ph_w0[i] = pw;
+            t.ph_tw[i] = (wp + t.bw - 1) / t.bw;
+            t.ph_th[i] = (hp + t.bh - 1) / t.bh;
+            t.ph_tn[i] = (n_img + t.bn - 1) / t.bn;
+            t.ph_tile_start[i] = tiles;
+            if (hp > 0 && wp > 0) tiles += t.ph_tw[i] * t.ph_th[i] * t.ph_tn[i];
+            t.ph_tap_start[i] = taps;
+            for (int r = 0; r < R; ++r) {
+                int oh;
+                if (dgrad) {
+                    const int vh = ph + pad_h - r * dil_h;
+                    if (((vh % sh) + sh) % sh) continue;
+                    oh = (vh - (((vh % sh) + sh) % sh)) / sh;  // exact division
+                } else {
+                    oh = r * dil_h - pad_h;
+                }
+                for (int s = 0; s < S; ++s) {
+                    int ow;
+                    if (dgrad) {
+                        const int vw = pw + pad_w - s * dil_w;
+                        if (((vw % sw) + sw) % sw) continue;
+                        ow = (vw - (((vw % sw) + sw) % sw)) / sw;
+                    } else {
+                        ow = s * dil_w - pad_w;
+                    }
+                    t.taps[taps] = static_cast<unsigned short>((r << 8) | s);
+                    t.off_h[taps] = static_cast<short>(oh);
+                    t.off_w[taps] = static_cast<short>(ow);
+                    ++taps;
+                }
+            }
+        }
+    t.ph_tile_start[t.num_phases] = tiles;
+    t.ph_tap_start[t.num_phases] = taps;
+    t.total_tiles = tiles * t.n_tiles_n;
+    return true;
+}
+
+void quarter_box(TmaConvArgs& t) {
+    t.qbw = t.bw >= 32 ? 32 : t.bw;
+    const int rem = 32 / t.qbw;
+    t.qbh = t.bh >= rem ? rem : t.bh;
+    t.qbn = 32 / (t.qbw * t.qbh);
+}
+
+}  // namespace
+}  // namespace pk
+
+using namespace pk;
+
+// Forward / backward-data through the TMA rectangle path. Returns
+// cudaErrorNotSupported (without launching) when the geometry does not fit.
+cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, const void* filt,
+                        void* out, const pk_epilogue* epi, int bn_want, cudaStream_t st) {
+    if (g->groups != 1 || g->transpose || g->r > 255 || g->s > 255) return cudaErrorNotSupported;
+    const int src_pitch = dgrad ? g->y_pitch : g->x_pitch;
+    const int out_pitch = dgrad ? g->x_pitch : g->y_pitch;
+    if (src_pitch % 64 != 0) return cudaErrorNotSupported;
+    if (!dgrad && g->f_pitch != g->x_pitch) return cudaErrorNotSupported;
+    TmaConvArgs t{};
+    t.N = g->n;
+    t.red_ch = src_pitch;
+    t.cpt = src_pitch / 64;
+    t.S = g->s;
+    t.n_out = dgrad ? g->c : g->k;
+    t.out_pitch = out_pitch;
+    t.Ho = dgrad ? g->h : g->p;
+    t.Wo = dgrad ? g->w : g->q;
+    const int sh = dgrad ? g->str_h : 1, sw = dgrad ? g->str_w : 1;
+    t.str_h = sh;
+    t.str_w = sw;
+    t.mult_h = dgrad ? 1 : g->str_h;
+    t.mult_w = dgrad ? 1 : g->str_w;
+    const int hp0 = (t.Ho + sh - 1) / sh, wp0 = (t.Wo + sw - 1) / sw;
+    const RectTile rt = tc::best_rect(g->n, hp0, wp0, BM);
+    t.bw = rt.bw;
+    t.bh = rt.bh;
+    t.bn = rt.bn;
+    quarter_box(t);
+    const int bn = choose_bn(bn_want, out_pitch);
+    t.n_tiles_n = (out_pitch + bn - 1) / bn;
+    if (!fill_phases(t, g->n, t.Ho, t.Wo, sh, sw, g->r, g->s, g->pad_h, g->pad_w, g->dil_h,
+                     g->dil_w, dgrad))
+        return cudaErrorNotSupported;
+    CUtensorMap amap{}, bmap{}, ymap{};
+    const int Hs = dgrad ? g->p : g->h, Ws = dgrad ? g->q : g->w;
+    if (!tc::make_map_nhwc(&amap, src, g->n, Hs, Ws, src_pitch, t.bw, t.bh, t.bn, t.mult_w,
+                           t.mult_h))
+        return cudaErrorNotSupported;
+    const long long kred = (long long)g->r * g->s * src_pitch;
+    if (!tc::make_map_2d(&bmap, filt, t.n_out, kred, kred, bn)) return cudaErrorInvalidValue;
+    const bool phased = sh > 1 || sw > 1;
+    if (!phased &&
+        !tc::make_map_nhwc(&ymap, out, g->n, t.Ho, t.Wo, out_pitch, t.qbw, t.qbh, t.qbn))
+        return cudaErrorInvalidValue;
+    pk_epilogue e{};
+    e.act = -1;
+    if (epi) e = *epi;
+    return phased ? dispatch_fprop<true>(bn, amap, bmap, ymap, out, t, e, st)
+                  : dispatch_fprop<false>(bn, amap, bmap, ymap, out, t, e, st);
+}
+
+static int tma_wgrad_splits(int tiles_mn, int num_kb, int num_sms) {
+    int splits = (2 * num_sms + tiles_mn - 1) / tiles_mn;
+    const int max_splits = num_kb / 4 > 1 ? num_kb / 4 : 1;
+    if (splits > max_splits) splits = max_splits;
+    return splits < 1 ? 1 : splits;
+}
+
+static void wgrad_geometry(const pk_conv_geom* g, int* tiles_mn, int* num_kb, RectTile* rt) {
+    *rt = tc::best_rect(g->n, g->p, g->q, BK);
+    const int tw = (g->q + rt->bw - 1) / rt->bw, th = (g->p + rt->bh - 1) / rt->bh;
+    const int tn = (g->n + rt->bn - 1) / rt->bn;
+    *num_kb = tw * th * tn;
+    const int nn = g->r * g->s * g->x_pitch;
+    *tiles_mn = ((g->k + BM - 1) / BM) * ((nn + WBN - 1) / WBN);
+}
+
+size_t pk_tma_wgrad_workspace(const pk_conv_geom* g, int num_sms) {
+    int tiles_mn, num_kb;
+    RectTile rt;
+    wgrad_geometry(g, &tiles_mn, &num_kb, &rt);
+    return (size_t)tma_wgrad_splits(tiles_mn, num_kb, num_sms) * g->k * g->r * g->s * g->x_pitch * 4;
+}
+
+bool pk_tma_wgrad_supported(const pk_conv_geom* g) {
+    return g->groups == 1 && !g->transpose && g->x_pitch % 64 == 0 && g->y_pitch % 64 == 0 &&
+           g->f_pitch == g->x_pitch && g->str_h * 1 <= 8 && g->str_w <= 8 &&
+           tc::encode_fn() != nullptr;
+}
+
+cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, void* dw,
+                         void* workspace, int num_sms, cudaStream_t st) {
+    if (!pk_tma_wgrad_supported(g)) return cudaErrorNotSupported;
+    int tiles_mn, num_kb;
+    RectTile rt;
+    wgrad_geometry(g, &tiles_mn, &num_kb, &rt);
+    TmaWgArgs w{};
+    w.K = g->k;
+    w.Cp = g->x_pitch;
+    w.S = g->s;
+    w.Nn = g->r * g->s * g->x_pitch;
+    w.pad_h = g->pad_h;
+    w.pad_w = g->pad_w;
+    w.str_h = g->str_h;
+    w.str_w = g->str_w;
+    w.dil_h = g->dil_h;
+    w.dil_w = g->dil_w;
+    w.rw = rt.bw;
+    w.rh = rt.bh;
+    w.rn = rt.bn;
+    w.tw = (g->q + rt.bw - 1) / rt.bw;
+    w.th = (g->p + rt.bh - 1) / rt.bh;
+    w.num_kb = num_kb;
+    const int splits = tma_wgrad_splits(tiles_mn, num_kb, num_sms);
+    w.kb_per_split = (num_kb + splits - 1) / splits;
+    CUtensorMap dymap{}, xmap{};
+    if (!tc::make_map_nhwc(&dymap, dy, g->n, g->p, g->q, g->y_pitch, rt.bw, rt.bh, rt.bn))
+        return cudaErrorNotSupported;
+    if (!tc::make_map_nhwc(&xmap, x, g->n, g->h, g->w, g->x_pitch, rt.bw, rt.bh, rt.bn, g->str_w,
+                           g->str_h))
+        return cudaErrorNotSupported;
+    constexpr int STAGES = 6;
+    using L = WSmem<STAGES>;
+    static int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+        cudaError_t err = cudaFuncSetAttribute(conv_tma_wgrad_kernel<STAGES>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               L::kBytes);
+        if (err != cudaSuccess) return err;
+        attr_dev = dev;
+    }
+    dim3 grid((w.K + BM - 1) / BM, (w.Nn + WBN - 1) / WBN, splits);
+    conv_tma_wgrad_kernel<STAGES><<<grid, kWgThreads, L::kBytes, st>>>(dymap, xmap,
+                                                                       (float*)workspace, w);
+    const long long total = (long long)w.K * w.Nn;
+    long long blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    wgrad_sum_kernel<<<(unsigned)blocks, 256, 0, st>>>((const float*)workspace, splits, total,
+                                                       (__nv_bfloat16*)dw);
+    count_launch(2);
+    return cudaGetLastError();
+}

@@ -1,0 +1,17 @@
+// Internal entry points shared between the tcgen05 kernel translation units
+// (not part of the pk_cuda_* host boundary).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include "kernels.h"
+
+// TMA rectangle-tile path (conv_tma.cu). cudaErrorNotSupported = geometry
+// not eligible (nothing launched); callers then use the cp.async gather path.
+cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, const void* filt,
+                        void* out, const pk_epilogue* epi, int bn_want, cudaStream_t st);
+bool pk_tma_wgrad_supported(const pk_conv_geom* g);
+size_t pk_tma_wgrad_workspace(const pk_conv_geom* g, int num_sms);
+cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, void* dw,
+                         void* workspace, int num_sms, cudaStream_t st);
