@@ -682,7 +682,10 @@ size_t pk_tma_wgrad_workspace(const pk_conv_geom* g, int num_sms) {
 }
 
 bool pk_tma_wgrad_supported(const pk_conv_geom* g) {
-    return g->groups == 1 && !g->transpose && g->x_pitch % 64 == 0 && g->y_pitch % 64 == 0 &&
+    // B column blocks must stay inside one tap unless the filter is 1x1; the
+    // dY (M) and channel boxes tolerate ragged tails through OOB zero fill
+    return g->groups == 1 && !g->transpose &&
+           (g->x_pitch % 64 == 0 || (g->r == 1 && g->s == 1)) && g->y_pitch % 8 == 0 &&
            g->f_pitch == g->x_pitch && g->str_h * 1 <= 8 && g->str_w <= 8 &&
            tc::encode_fn() != nullptr;
 }

@@ -131,6 +131,15 @@ cudaError_t pk_cuda_igemm_tc_wgrad(const pk_conv_geom* g, const void* dy, const 
                                    void* workspace, int num_sms, const pk_tc_config* cfg,
                                    cudaStream_t st);
 
+// ---- dense-reduction packing for narrow-channel (stem) layers, bf16 ---------
+int pk_stem_kc_pitch(const pk_conv_geom* g);  // roundup(R*S*C, 8)
+cudaError_t pk_cuda_im2col_pack(const pk_conv_geom* g, const void* x, void* col, cudaStream_t st);
+// transposed = 0: [K][kc_pitch]; 1: [kc_pitch][pitch(K)]
+cudaError_t pk_cuda_filter_pack(const pk_conv_geom* g, const void* f, void* dst, int transposed,
+                                cudaStream_t st);
+cudaError_t pk_cuda_col2im_pack(const pk_conv_geom* g, const void* colg, void* dx, cudaStream_t st);
+cudaError_t pk_cuda_wgrad_unpack(const pk_conv_geom* g, const void* dwp, void* dw, cudaStream_t st);
+
 // ---- pointwise / batch-norm ----------------------------------------------------
 // y = epilogue(x + 0) elementwise over NHWC (bias/bn/act all optional).
 cudaError_t pk_cuda_pointwise(const void* x, void* y, int n, int c, int hw, int pitch, int dtype,

@@ -137,6 +137,73 @@ pk_conv_geom gemm_as_1x1(const pk_conv_geom& g) {
     return m;
 }
 
+// ---- narrow-channel (stem) layers: dense (r,s,c) packing + plain TMA GEMMs --
+
+bool stem_eligible(const pk_conv_geom& g, int dt, const pk_epilogue* epi) {
+    return dt == PK_BF16 && g.groups == 1 && !g.transpose && g.x_pitch % 64 != 0 &&
+           pk_tc_fwd_supported(&g) && !(epi && epi->bn_mean && epi->bn_per_activation);
+}
+
+// A plain GEMM [rows][kred] x [kout][kred]^T as a 1x1 convolution geometry.
+pk_conv_geom gemm_geom(long long rows, int kred, int kout) {
+    pk_conv_geom m{};
+    m.n = 1;
+    m.h = m.p = 1;
+    m.w = m.q = static_cast<int>(rows);
+    m.c = m.cg = kred;
+    m.k = m.kg = kout;
+    m.r = m.s = 1;
+    m.str_h = m.str_w = m.dil_h = m.dil_w = 1;
+    m.groups = 1;
+    m.x_pitch = m.f_pitch = kred;
+    m.y_pitch = pk_pitch(kout);
+    return m;
+}
+
+std::size_t stem_workspace(const pk_conv_geom& g, ConvDirection dir) {
+    const std::size_t kcp = pk_stem_kc_pitch(&g);
+    const std::size_t rows = (std::size_t)g.n * g.p * g.q;
+    const std::size_t col = align256(rows * kcp * 2);
+    switch (dir) {
+        case ConvDirection::Forward: return col + align256((std::size_t)g.k * kcp * 2);
+        case ConvDirection::BackwardData: return col + align256(kcp * pk_pitch(g.k) * 2);
+        default: {
+            const pk_conv_geom wg = gemm_geom((long long)rows, (int)kcp, g.k);
+            return col + align256((std::size_t)g.k * kcp * 2) + pk_tc_wgrad_workspace(&wg, 148);
+        }
+    }
+}
+
+void run_stem(const pk_conv_geom& g, ConvDirection dir, const void* a, const void* b, void* out,
+              void* ws, const pk_epilogue* epi, int num_sms, cudaStream_t st) {
+    auto ck = [](cudaError_t e, const char* what) { check_cuda(e, what); };
+    const int kcp = pk_stem_kc_pitch(&g);
+    const long long rows = (long long)g.n * g.p * g.q;
+    char* col = static_cast<char*>(ws);
+    char* aux = col + align256((std::size_t)rows * kcp * 2);
+    if (dir == ConvDirection::Forward) {
+        // y = col . Wp^T
+        ck(pk_cuda_im2col_pack(&g, a, col, st), "im2col_pack");
+        ck(pk_cuda_filter_pack(&g, b, aux, 0, st), "filter_pack");
+        pk_conv_geom m = gemm_geom(rows, kcp, g.k);
+        ck(pk_cuda_igemm_tc_fwd(&m, col, aux, out, epi, &kDefaultTc, st), "stem_gemm");
+    } else if (dir == ConvDirection::BackwardData) {
+        // colg = dY . Wp (B = Wp^T as [kcp][pitch K]); dX = col2im(colg)
+        ck(pk_cuda_filter_pack(&g, b, aux, 1, st), "filter_pack_t");
+        pk_conv_geom m = gemm_geom(rows, pk_pitch(g.k), kcp);
+        ck(pk_cuda_igemm_tc_fwd(&m, a, aux, col, nullptr, &kDefaultTc, st), "stem_dgrad_gemm");
+        ck(pk_cuda_col2im_pack(&g, col, out, st), "col2im_pack");
+    } else {
+        // dWp = dY^T . col, then unpack to the filter layout
+        ck(pk_cuda_im2col_pack(&g, b, col, st), "im2col_pack");
+        pk_conv_geom wg = gemm_geom(rows, kcp, g.k);
+        wg.y_pitch = g.y_pitch;
+        char* wtmp = aux + align256((std::size_t)g.k * kcp * 2);
+        ck(pk_cuda_igemm_tc_wgrad(&wg, a, col, aux, wtmp, num_sms, &kDefaultTc, st), "stem_wgrad");
+        ck(pk_cuda_wgrad_unpack(&g, aux, out, st), "wgrad_unpack");
+    }
+}
+
 }  // namespace
 
 OpCounters conv_counters(const ConvProblem& p, ConvAlgo algo) { return counters_for(p, algo); }
@@ -145,6 +212,10 @@ std::size_t ConvPlan::device_workspace_bytes() const {
     const pk_conv_geom g = make_geom(problem_);
     const int dt = dtype_of(problem_.etype);
     const std::size_t acc_rows = (std::size_t)g.p * g.q;
+    const bool tc_algo = problem_.direction == ConvDirection::Forward
+                             ? algo_ == ConvAlgo::ImplicitGemm
+                             : algo_ == ConvAlgo::Im2colGemm;
+    if (tc_algo && stem_eligible(g, dt, nullptr)) return stem_workspace(g, problem_.direction);
     switch (problem_.direction) {
         case ConvDirection::Forward:
             if (algo_ == ConvAlgo::FFT) return pk_cuda_fft_scratch_bytes(&g);
@@ -205,7 +276,10 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                 ck(pk_cuda_fft_fwd(&g, dt, a, b, out, ws, st), "fft_fwd");
                 break;
             case ConvAlgo::ImplicitGemm: {
-                if (dt == PK_BF16 && pk_tc_fwd_supported(&g)) {
+                if (stem_eligible(g, dt, epi)) {
+                    kernel = "stem_pack+gemm_tc";
+                    run_stem(g, dir, a, b, out, ws, epi, h.num_sms(), st);
+                } else if (dt == PK_BF16 && pk_tc_fwd_supported(&g)) {
                     kernel = "igemm_tc_fwd";
                     const pk_tc_config cfg = tc_config(tiles_);
                     ck(pk_cuda_igemm_tc_fwd(&g, a, b, out, epi, &cfg, st), "igemm_tc_fwd");
@@ -272,6 +346,9 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
         if (algo_ == ConvAlgo::Direct) {
             kernel = "direct_simt_bwd_data";
             ck(pk_cuda_direct_bwd_data(&g, dt, a, b, out, st), "direct_bwd_data");
+        } else if (stem_eligible(g, dt, nullptr)) {
+            kernel = "stem_gemm_tc+col2im";
+            run_stem(g, dir, a, b, out, ws, nullptr, h.num_sms(), st);
         } else if (dt == PK_BF16 && pk_tc_dgrad_supported(&g)) {
             kernel = "igemm_tc_dgrad";
             ck(pk_cuda_igemm_tc_dgrad(&g, a, b, out, ws, &kDefaultTc, st), "igemm_tc_dgrad");
@@ -294,6 +371,9 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
         if (algo_ == ConvAlgo::Direct) {
             kernel = "direct_simt_bwd_weights";
             ck(pk_cuda_direct_bwd_weights(&g, dt, a, b, out, st), "direct_bwd_weights");
+        } else if (stem_eligible(g, dt, nullptr)) {
+            kernel = "stem_pack+wgrad_tc";
+            run_stem(g, dir, a, b, out, ws, nullptr, h.num_sms(), st);
         } else if (dt == PK_BF16 && pk_tc_wgrad_supported(&g)) {
             kernel = "igemm_tc_wgrad";
             ck(pk_cuda_igemm_tc_wgrad(&g, a, b, out, ws, h.num_sms(), &kDefaultTc, st),

@@ -229,6 +229,7 @@ def test_bf16_large_tensor_core_paths(lib):
             p = problem(**shp, direction=d, etype=abi.BF16)
             a, b = _inputs(p, rng, True)
             got = h.conv_run(p, s, a, b)
-            assert h.last_kernel() == kern
+            # narrow-channel stems pack (r,s,c) densely before the tcgen05 GEMMs
+            assert h.last_kernel() == kern or (shp["c"] % 64 and h.last_kernel().startswith("stem"))
             err = rel_l2(got, _oracle(p, a, b))
             assert err <= 1e-2, (shp, d, err)
