@@ -371,19 +371,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                 }
                 // math + pack into the swizzled staging row of this lane
+                float xf[64];
+#pragma unroll
+                for (int e = 0; e < 64; ++e) xf[e] = __uint_as_float(v[e]);
+                if (has_epi) epilogue_chunk64(epi, xf, n0 + c0, g.n_out, my_oy, my_ox, g.Ho, g.Wo);
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
                     uint32_t packed[4];
 #pragma unroll
                     for (int e = 0; e < 8; e += 2) {
                         const int ch = n0 + c0 + jj * 8 + e;
-                        float x0 = __uint_as_float(v[jj * 8 + e]);
-                        float x1 = __uint_as_float(v[jj * 8 + e + 1]);
-                        if (has_epi) {
-                            if (ch < g.n_out) x0 = apply_epilogue(epi, x0, ch, my_oy, my_ox, g.Ho, g.Wo);
-                            if (ch + 1 < g.n_out)
-                                x1 = apply_epilogue(epi, x1, ch + 1, my_oy, my_ox, g.Ho, g.Wo);
-                        }
+                        float x0 = xf[jj * 8 + e];
+                        float x1 = xf[jj * 8 + e + 1];
                         if (ch >= g.n_out || c0 + jj * 8 + e >= BN) x0 = 0.0f;
                         if (ch + 1 >= g.n_out || c0 + jj * 8 + e + 1 >= BN) x1 = 0.0f;
                         __nv_bfloat162 b2 = __floats2bfloat162_rn(x0, x1);

@@ -52,6 +52,11 @@ typedef struct pk_epilogue {
     float bn_eps;
     int act;                 // -1 none, 0 ReLU, 1 LeakyReLU, 2 Sigmoid, 3 Tanh
     float act_alpha;
+    // Optional folded per-channel affine (bias and spatial BN folded on the
+    // host): acc * ch_scale[k] + ch_shift[k], then the activation. Used by the
+    // tensor-core epilogues (bf16 outputs) in place of bias/bn_* when set.
+    const float* ch_scale;
+    const float* ch_shift;
 } pk_epilogue;
 
 // ---- layout conversion ------------------------------------------------------

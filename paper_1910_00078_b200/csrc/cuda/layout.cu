@@ -1,6 +1,7 @@
 // Layout conversion and pointwise kernels (HBM-bound; coalesced through a
 // shared-memory transpose tile, one pass over the data).
 #include <atomic>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -68,17 +69,36 @@ __global__ void filter_to_dgrad_kernel(pk_conv_geom g, const T* __restrict__ f, 
     }
 }
 
+// 8 channels per thread (one 16-byte bf16 / two 16-byte f32 vectors).
 template <typename T>
 __global__ void pointwise_kernel(const T* __restrict__ x, T* __restrict__ y, long long rows,
                                  int c, int hw, int pitch, pk_epilogue e) {
-    const long long total = rows * pitch;
+    const int chunks = pitch / 8;
+    const long long total = rows * chunks;
+    using V = typename std::conditional<sizeof(T) == 2, uint4, float4>::type;
+    constexpr int kVecs = sizeof(T) == 2 ? 1 : 2;
+    // element index math in 32 bits (the chunk index of a row-major [rows][pitch]
+    // tensor is simply i: chunk base = i * 8 elements)
+    const bool per_act = e.bn_mean && e.bn_per_activation;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
-        const int ch = (int)(i % pitch);
-        const long long row = i / pitch;
-        float v = 0.0f;
-        if (ch < c) v = apply_epilogue(e, ld(x + i), ch, 0, (int)(row % hw), 1, hw);
-        st(y + i, v);
+        const int ch0 = (total < (1LL << 31) ? (int)((unsigned)i % (unsigned)chunks)
+                                             : (int)(i % chunks)) * 8;
+        const int px = per_act ? (int)((i / chunks) % hw) : 0;
+        __align__(16) T buf[8];
+        const V* src = reinterpret_cast<const V*>(x + i * 8);
+#pragma unroll
+        for (int v = 0; v < kVecs; ++v) reinterpret_cast<V*>(buf)[v] = src[v];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int ch = ch0 + j;
+            float v = 0.0f;
+            if (ch < c) v = apply_epilogue(e, ld(buf + j), ch, 0, px, 1, hw);
+            st(buf + j, v);
+        }
+        V* dst = reinterpret_cast<V*>(y + i * 8);
+#pragma unroll
+        for (int v = 0; v < kVecs; ++v) dst[v] = reinterpret_cast<const V*>(buf)[v];
     }
 }
 
@@ -176,7 +196,7 @@ cudaError_t pk_cuda_pointwise(const void* x, void* y, int n, int c, int hw, int 
                               const pk_epilogue* epi, cudaStream_t st) {
     const long long rows = (long long)n * hw;
     PK_DISPATCH_DTYPE(dtype, T,
-                      pointwise_kernel<T><<<grid_for(rows * pitch), 256, 0, st>>>(
+                      pointwise_kernel<T><<<grid_for(rows * (pitch / 8)), 256, 0, st>>>(
                           (const T*)x, (T*)y, rows, c, hw, pitch, *epi));
     count_launch();
     return cudaGetLastError();

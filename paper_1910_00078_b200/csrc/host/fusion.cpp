@@ -1,5 +1,7 @@
 #include "fusion.hpp"
 
+#include <cmath>
+
 #include "../cuda/kernels.h"
 
 namespace primkit {
@@ -38,6 +40,10 @@ struct FusionPlan::DeviceArgs {
     const Handle* owner = nullptr;
     bool valid = false;
     DeviceBuffer filter, bias, gamma, beta, mean, var;
+    // bias and spatial BN folded into a per-channel affine for the tensor-core
+    // epilogue: acc * scale[k] + shift[k] (padded to a multiple of 64 + 64)
+    DeviceBuffer scale, shift;
+    bool folded = false;
 };
 
 FusionPlan::FusionPlan(TensorDescriptor input_desc)
@@ -331,6 +337,42 @@ FusionPlan::DeviceArgs& FusionPlan::device_args(Handle& h) {
     upload_vec(h, dev_->beta, args_.bn_beta);
     upload_vec(h, dev_->mean, args_.bn_mean);
     upload_vec(h, dev_->var, args_.bn_var);
+    // Folded affine for the bf16 tensor-core epilogue (no per-activation BN):
+    //   ((acc + b) - mu) / sqrt(var + eps) * g + beta = acc * s + t,
+    //   s = g / sqrt(var + eps), t = (b - mu) * s + beta
+    dev_->folded = false;
+    const FusionOp* conv = conv_op(*this);
+    bool per_act = false;
+    for (const FusionOp& op : ops_)
+        if (op.kind == FusionOp::Kind::BatchNormInference && op.bn_mode == BatchNormMode::PerActivation)
+            per_act = true;
+    if (conv && input_desc_.etype == ElementType::BF16 && !per_act) {
+        const std::int64_t k = cur_desc_.dims[1];
+        const std::size_t padded = static_cast<std::size_t>((k + 63) / 64 * 64 + 64);
+        std::vector<float> s(padded, 0.0f), t(padded, 0.0f);
+        for (std::int64_t i = 0; i < k; ++i) {
+            double sc = 1.0, sh = args_.bias ? args_.bias->data[i] : 0.0;
+            if (args_.bn_gamma && args_.bn_var && args_.bn_mean && args_.bn_beta) {
+                const double inv = args_.bn_gamma->data[i] /
+                                   std::sqrt(static_cast<double>(args_.bn_var->data[i]) +
+                                             static_cast<double>(args_.bn_epsilon));
+                sh = (sh - args_.bn_mean->data[i]) * inv + args_.bn_beta->data[i];
+                sc = inv;
+            }
+            s[i] = static_cast<float>(sc);
+            t[i] = static_cast<float>(sh);
+        }
+        dev_->scale.ensure(padded * 4);
+        dev_->shift.ensure(padded * 4);
+        check_cuda(cudaMemcpyAsync(dev_->scale.get(), s.data(), padded * 4, cudaMemcpyHostToDevice,
+                                   h.stream()),
+                   "cudaMemcpyAsync");
+        check_cuda(cudaMemcpyAsync(dev_->shift.get(), t.data(), padded * 4, cudaMemcpyHostToDevice,
+                                   h.stream()),
+                   "cudaMemcpyAsync");
+        h.sync();  // host staging vectors go out of scope
+        dev_->folded = true;
+    }
     dev_->owner = &h;
     dev_->valid = true;
     return *dev_;
@@ -370,7 +412,14 @@ void fusion_execute(Handle& h, FusionPlan& plan, const void* input, void* output
         if (dt == PK_BF16 && pk_tc_fwd_supported(&g)) {
             const pk_tc_config cfg{256, 4, 1};
             h.last_kernel = "igemm_tc_fwd+epilogue";
-            check_cuda(pk_cuda_igemm_tc_fwd(&g, input, d.filter.get(), output, &e, &cfg, st),
+            pk_epilogue tce = e;
+            if (d.folded) {
+                tce.bias = nullptr;
+                tce.bn_mean = tce.bn_var = tce.bn_gamma = tce.bn_beta = nullptr;
+                tce.ch_scale = static_cast<const float*>(d.scale.get());
+                tce.ch_shift = static_cast<const float*>(d.shift.get());
+            }
+            check_cuda(pk_cuda_igemm_tc_fwd(&g, input, d.filter.get(), output, &tce, &cfg, st),
                        "igemm_tc_fwd");
         } else if (wino) {
             h.last_kernel = "winograd_f23+epilogue";
