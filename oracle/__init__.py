@@ -68,6 +68,10 @@ def restated():
         lib.oc_activation.argtypes = [C.c_int, C.c_float, C.c_float]
         lib.oc_activation_grad.restype = C.c_float
         lib.oc_activation_grad.argtypes = [C.c_int, C.c_float, C.c_float]
+        lib.oc_fused_epilogue.restype = C.c_float
+        lib.oc_fused_epilogue.argtypes = [C.c_float, C.c_int, C.c_float, C.c_int, C.c_float,
+                                          C.c_float, C.c_float, C.c_float, C.c_float, C.c_int,
+                                          C.c_float]
         _restated = lib
     return _restated
 

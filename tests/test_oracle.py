@@ -1,0 +1,172 @@
+"""Pin the oracle before trusting it (CPU suite).
+
+1. The reference's own known-answer tests (test_tensor.cpp:12-48,
+   test_conv.cpp:127-136, acceptance.cpp:162-186).
+2. The golden vectors produced by the unmodified reference
+   (tests/golden/reference_vectors.npz, made by tests/golden/make_golden.py).
+3. Live call-by-call comparison with the reference library (oracle/_ref) on
+   seeded random problems, when it is built here.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1910_00078_b200 import abi
+from paper_1910_00078_b200.primkit import operand_shapes, problem
+
+from conftest import max_rel
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "reference_vectors.npz")
+
+
+def test_round_bf16_known_answers():
+    r = oracle.restated()
+    f = r.oc_round_bf16
+    assert f(1.0) == 1.0 and f(2.0) == 2.0 and f(-3.5) == -3.5
+    assert f(1.00390625) == 1.0            # tie to even (kept lsb 0)
+    assert f(1.01171875) == 1.015625       # tie rounds up (kept lsb 1)
+    assert np.isinf(f(float("inf"))) and f(float("-inf")) < 0 and np.isnan(f(float("nan")))
+    assert np.signbit(f(-0.0))
+
+
+def test_round_bf16_vectorised_idempotent():
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1e6, 1e6, 10000).astype(np.float32)
+    r = oracle.round_bf16(x)
+    assert np.array_equal(oracle.round_bf16(r), r)
+    assert np.all((r.view(np.uint32) & 0xFFFF) == 0)
+    lib = oracle.restated()
+    assert all(lib.oc_round_bf16(float(v)) == float(w) for v, w in zip(x[:500], r[:500]))
+
+
+def test_direct_hand_example():
+    x = np.arange(9, dtype=np.float32).reshape(1, 1, 3, 3)
+    w = np.ones((1, 1, 2, 2), np.float32)
+    y = oracle.conv_forward(problem(n=1, c=1, h=3, w=3, k=1, y=2, x=2), x, w)
+    assert y.ravel().tolist() == [8.0, 12.0, 20.0, 24.0]
+
+
+def test_winograd_matches_direct():
+    rng = np.random.default_rng(23)
+    p = problem(n=2, c=8, h=16, w=16, k=4, y=3, x=3, pad=1)
+    x = rng.uniform(-1, 1, (2, 8, 16, 16)).astype(np.float32)
+    w = rng.uniform(-1, 1, (4, 8, 3, 3)).astype(np.float32)
+    assert max_rel(oracle.winograd_f23(p, x, w), oracle.conv_forward(p, x, w)) <= 1e-4
+
+
+def test_direct_matches_independent_f64():
+    rng = np.random.default_rng(5)
+    for shp in (dict(n=2, c=6, h=9, w=7, k=4, y=3, x=2, pad_h=1, pad_w=0, stride=2, dilation=1,
+                     groups=2),
+                dict(n=1, c=3, h=11, w=11, k=5, y=3, x=3, pad=2, dilation=2)):
+        p = problem(**shp)
+        sa, sb, _ = operand_shapes(_lib(), p)
+        x = rng.uniform(-1, 1, sa).astype(np.float32)
+        w = rng.uniform(-1, 1, sb).astype(np.float32)
+        assert max_rel(oracle.conv_forward(p, x, w), oracle.conv_ref_f64(p, x, w)) <= 1e-5
+
+
+def test_backward_is_adjoint_of_forward():
+    # <conv(x, w), dy> == <x, conv_bd(dy, w)> == <w, conv_bw(dy, x)> (test_conv.cpp:387-413)
+    rng = np.random.default_rng(11)
+    p = problem(n=2, c=4, h=8, w=7, k=3, y=3, x=3, pad=1, stride=2)
+    x = rng.uniform(-1, 1, (2, 4, 8, 7))
+    w = rng.uniform(-1, 1, (3, 4, 3, 3))
+    y = oracle.conv_forward(p, x, w)
+    dy = rng.uniform(-1, 1, y.shape)
+    lhs = float(np.sum(y.astype(np.float64) * dy))
+    assert abs(lhs - float(np.sum(oracle.conv_backward_data(p, dy, w) * x))) <= 1e-4 * abs(lhs) + 1e-4
+    assert abs(lhs - float(np.sum(oracle.conv_backward_weights(p, dy, x) * w))) <= 1e-4 * abs(lhs) + 1e-4
+
+
+def _lib():
+    from paper_1910_00078_b200.primkit import library
+    return library()
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return np.load(GOLDEN)
+
+
+def _golden_cases():
+    # the case table lives next to the fixtures, in the generator script
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "make_golden", os.path.join(os.path.dirname(GOLDEN), "make_golden.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod.CONV_CASES
+
+
+@pytest.mark.parametrize("case", [c[0] for c in _golden_cases()])
+@pytest.mark.parametrize("et", [abi.F32, abi.BF16])
+def test_oracle_matches_reference_golden(golden, case, et):
+    name, shp, d = next(c for c in _golden_cases() if c[0] == case)
+    p = problem(**shp, direction=d, etype=et)
+    tag = f"{name}_{'bf16' if et else 'f32'}"
+    a, b = golden[tag + "_a"], golden[tag + "_b"]
+    bf = et == abi.BF16
+    got = {abi.FORWARD: oracle.conv_forward, abi.BACKWARD_DATA: oracle.conv_backward_data,
+           abi.BACKWARD_WEIGHTS: oracle.conv_backward_weights}[d](p, a, b, bf16=bf)
+    # same loop order and f32 arithmetic as the reference: bit-identical
+    assert np.array_equal(got, golden[tag + "_direct"])
+    if tag + "_winograd" in golden.files:
+        assert np.array_equal(oracle.winograd_f23(p, a, b, bf16=bf), golden[tag + "_winograd"])
+
+
+@pytest.mark.parametrize("mode", [abi.BN_SPATIAL, abi.BN_PER_ACTIVATION])
+def test_oracle_bn_matches_reference_golden(golden, mode):
+    t = f"bn{mode}"
+    G = {k: golden[f"{t}_{k}"] for k in ("x", "dy", "g", "b", "rm", "rv", "y", "sm", "si", "rm2",
+                                          "rv2", "dx", "dg", "db")}
+    y, sm, si, rm, rv = oracle.bn_forward_train(mode, G["x"], G["g"], G["b"], G["rm"], G["rv"])
+    for got, want in ((y, "y"), (sm, "sm"), (si, "si"), (rm, "rm2"), (rv, "rv2")):
+        assert np.array_equal(got, G[want]), want
+    dx, dg, db = oracle.bn_backward(mode, G["x"], G["dy"], G["g"], G["sm"], G["si"])
+    assert max_rel(dx, G["dx"]) <= 1e-6 and max_rel(dg, G["dg"]) <= 1e-6
+    assert max_rel(db, G["db"]) <= 1e-6
+
+
+def test_oracle_fused_epilogue_matches_reference_golden(golden):
+    r = oracle.restated()
+    for t, pad, act, has_bn in (("cba", 0, abi.LEAKY_RELU, False), ("cbna", 1, abi.TANH, True)):
+        x, w = golden[f"{t}_x"], golden[f"{t}_filter"]
+        p = problem(n=x.shape[0], c=x.shape[1], h=x.shape[2], w=x.shape[3], k=w.shape[0],
+                    y=w.shape[2], x=w.shape[3], pad=pad)
+        conv = oracle.conv_forward(p, x, w)
+        out = np.empty_like(conv)
+        for k in range(conv.shape[1]):
+            for idx in np.ndindex(conv.shape[0], conv.shape[2], conv.shape[3]):
+                n, i, j = idx
+                out[n, k, i, j] = r.oc_fused_epilogue(
+                    float(conv[n, k, i, j]), 1, float(golden[f"{t}_bias"][k]), int(has_bn),
+                    float(golden[f"{t}_mean"][k]), float(golden[f"{t}_var"][k]),
+                    float(golden[f"{t}_gamma"][k]), float(golden[f"{t}_beta"][k]), 1e-5, act, 0.1)
+        assert max_rel(out, golden[f"{t}_fused"]) <= 1e-6
+        assert max_rel(golden[f"{t}_fused"], golden[f"{t}_unfused"]) <= 1e-5
+
+
+def test_oracle_matches_live_reference(ref):
+    """Random problems, every direction, through the reference's C ABI."""
+    h = ref.handle()
+    rng = np.random.default_rng(99)
+    for _ in range(40):
+        shp = dict(n=int(rng.integers(1, 3)), c=int(rng.integers(1, 6)), h=int(rng.integers(3, 9)),
+                   w=int(rng.integers(3, 9)), k=int(rng.integers(1, 6)), y=int(rng.integers(1, 4)),
+                   x=int(rng.integers(1, 4)), pad=int(rng.integers(0, 2)),
+                   stride=int(rng.integers(1, 3)), dilation=int(rng.integers(1, 3)))
+        for d in (abi.FORWARD, abi.BACKWARD_DATA, abi.BACKWARD_WEIGHTS):
+            p = problem(**shp, direction=d)
+            try:
+                sa, sb, _ = operand_shapes(ref, p)
+            except Exception:
+                break  # invalid geometry
+            a = rng.uniform(-1, 1, sa).astype(np.float32)
+            b = rng.uniform(-1, 1, sb).astype(np.float32)
+            want = h.conv_run(p, "Direct", a, b)
+            got = {abi.FORWARD: oracle.conv_forward, abi.BACKWARD_DATA: oracle.conv_backward_data,
+                   abi.BACKWARD_WEIGHTS: oracle.conv_backward_weights}[d](p, a, b)
+            assert np.array_equal(got, want), (shp, d)
