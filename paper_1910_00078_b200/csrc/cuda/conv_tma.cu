@@ -93,7 +93,14 @@ __device__ __forceinline__ RectInfo rect_info(const TmaConvArgs& g, int t) {
     return ri;
 }
 
-template <int BN, int STAGES, bool PHASED>
+// k-blocks of a tile: (tap, 64-channel chunk) pairs, or for NARROW sources
+// (channel pitch < 64) groups of eight (tap, 8-channel) slots.
+template <bool NARROW>
+__device__ __forceinline__ int tile_kblocks(const TmaConvArgs& g, const RectInfo& ri) {
+    return NARROW ? (ri.ntaps * g.cpt + 7) / 8 : ri.ntaps * g.cpt;
+}
+
+template <int BN, int STAGES, bool PHASED, bool NARROW>
 __global__ void __launch_bounds__(kFpropThreads, 1)
     conv_tma_fprop_kernel(const __grid_constant__ CUtensorMap amap,
                           const __grid_constant__ CUtensorMap bmap,
@@ -139,20 +146,42 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
             uint32_t phase = 0;
             for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
                 const RectInfo ri = rect_info(g, t);
-                const int nkb = ri.ntaps * g.cpt;
+                const int nkb = tile_kblocks<NARROW>(g, ri);
                 const int ys = ri.h0 * g.mult_h, xs = ri.w0 * g.mult_w;
                 for (int kb = 0; kb < nkb; ++kb) {
-                    const int tap = kb / g.cpt, chunk = kb - tap * g.cpt;
-                    const int ti = ri.tap0 + tap;
-                    const unsigned short rs = g.taps[ti];
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * L::kStage;
                     mbar_arrive_expect_tx(&full[stage], L::kA + L::kB);
-                    tma_load_4d(smem_u32(sa), &amap, &full[stage], chunk * BK, xs + g.off_w[ti],
-                                ys + g.off_h[ti], ri.n0);
-                    tma_load_2d(smem_u32(sa + L::kA), &bmap, &full[stage],
-                                ((rs >> 8) * g.S + (rs & 0xff)) * g.red_ch + chunk * BK,
-                                ri.nt * BN);
+                    if (NARROW) {
+                        // eight 16-byte-row boxes, one per (tap, 8-channel group);
+                        // the K order (tap, c8) is exactly the dense filter order
+                        const int slots = ri.ntaps * g.cpt;
+#pragma unroll 1
+                        for (int j = 0; j < 8; ++j) {
+                            const int slot = kb * 8 + j;
+                            int cx = 0, wx = -(1 << 20), hy = 0;  // far OOB -> zeros
+                            if (slot < slots) {
+                                const int tap = slot / g.cpt, c8 = slot - tap * g.cpt;
+                                const int ti = ri.tap0 + tap;
+                                cx = c8 * 8;
+                                wx = xs + g.off_w[ti];
+                                hy = ys + g.off_h[ti];
+                            }
+                            tma_load_4d(smem_u32(sa + j * (L::kA / 8)), &amap, &full[stage], cx,
+                                        wx, hy, ri.n0);
+                        }
+                        tma_load_2d(smem_u32(sa + L::kA), &bmap, &full[stage], kb * BK,
+                                    ri.nt * BN);
+                    } else {
+                        const int tap = kb / g.cpt, chunk = kb - tap * g.cpt;
+                        const int ti = ri.tap0 + tap;
+                        const unsigned short rs = g.taps[ti];
+                        tma_load_4d(smem_u32(sa), &amap, &full[stage], chunk * BK,
+                                    xs + g.off_w[ti], ys + g.off_h[ti], ri.n0);
+                        tma_load_2d(smem_u32(sa + L::kA), &bmap, &full[stage],
+                                    ((rs >> 8) * g.S + (rs & 0xff)) * g.red_ch + chunk * BK,
+                                    ri.nt * BN);
+                    }
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -168,7 +197,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
         int it = 0;
         for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
             const RectInfo ri = rect_info(g, t);
-            const int nkb = ri.ntaps * g.cpt;
+            const int nkb = tile_kblocks<NARROW>(g, ri);
             if (nkb == 0) continue;
             const int a = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
@@ -184,7 +213,11 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                     const uint32_t b_base = a_base + L::kA;
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k) {
-                        const uint64_t ad = umma_desc_sw128(a_base + k * 32, 16, 1024);
+                        // NARROW: K step k covers boxes 2k, 2k+1 (2 KB apart, LBO),
+                        // 16-row core-matrix groups are 128 B apart (SBO)
+                        const uint64_t ad =
+                            NARROW ? umma_desc_noswz(a_base + k * 2 * (L::kA / 8), L::kA / 8, 128)
+                                   : umma_desc_sw128(a_base + k * 32, 16, 1024);
                         const uint64_t bd = umma_desc_sw128(b_base + k * 32, 16, 1024);
                         mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
                     }
@@ -504,11 +537,11 @@ __global__ void wgrad_sum_kernel(const float* __restrict__ partial, int splits, 
 // ---------------------------------------------------------------------------
 // host
 
-template <int BN, int STAGES, bool PHASED>
+template <int BN, int STAGES, bool PHASED, bool NARROW>
 cudaError_t launch_fprop(const CUtensorMap& amap, const CUtensorMap& bmap, const CUtensorMap& ymap,
                          void* out, const TmaConvArgs& g, const pk_epilogue& e, cudaStream_t st) {
     using L = FSmem<BN, STAGES>;
-    auto kern = conv_tma_fprop_kernel<BN, STAGES, PHASED>;
+    auto kern = conv_tma_fprop_kernel<BN, STAGES, PHASED, NARROW>;
     static int attr_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -526,13 +559,13 @@ cudaError_t launch_fprop(const CUtensorMap& amap, const CUtensorMap& bmap, const
     return cudaGetLastError();
 }
 
-template <bool PHASED>
+template <bool PHASED, bool NARROW>
 cudaError_t dispatch_fprop(int bn, const CUtensorMap& amap, const CUtensorMap& bmap,
                            const CUtensorMap& ymap, void* out, const TmaConvArgs& g,
                            const pk_epilogue& e, cudaStream_t st) {
-    if (bn == 64) return launch_fprop<64, 6, PHASED>(amap, bmap, ymap, out, g, e, st);
-    if (bn == 128) return launch_fprop<128, 5, PHASED>(amap, bmap, ymap, out, g, e, st);
-    return launch_fprop<256, 3, PHASED>(amap, bmap, ymap, out, g, e, st);
+    if (bn == 64) return launch_fprop<64, 6, PHASED, NARROW>(amap, bmap, ymap, out, g, e, st);
+    if (bn == 128) return launch_fprop<128, 5, PHASED, NARROW>(amap, bmap, ymap, out, g, e, st);
+    return launch_fprop<256, 3, PHASED, NARROW>(amap, bmap, ymap, out, g, e, st);
 }
 
 int choose_bn(int want, int out_pitch) {
@@ -612,12 +645,16 @@ cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, cons
     if (g->groups != 1 || g->transpose || g->r > 255 || g->s > 255) return cudaErrorNotSupported;
     const int src_pitch = dgrad ? g->y_pitch : g->x_pitch;
     const int out_pitch = dgrad ? g->x_pitch : g->y_pitch;
-    if (src_pitch % 64 != 0) return cudaErrorNotSupported;
+    // narrow sources (pitch < 64, e.g. the 3-channel stem) use 16-byte-row boxes
+    const bool narrow = src_pitch % 64 != 0;
+    if (narrow && (src_pitch > 56 || src_pitch % 8 != 0)) return cudaErrorNotSupported;
+    // narrow k-blocks assume the dense tap order (all taps): not for dgrad phases
+    if (narrow && dgrad && (g->str_h > 1 || g->str_w > 1)) return cudaErrorNotSupported;
     if (!dgrad && g->f_pitch != g->x_pitch) return cudaErrorNotSupported;
     TmaConvArgs t{};
     t.N = g->n;
     t.red_ch = src_pitch;
-    t.cpt = src_pitch / 64;
+    t.cpt = narrow ? src_pitch / 8 : src_pitch / 64;
     t.S = g->s;
     t.n_out = dgrad ? g->c : g->k;
     t.out_pitch = out_pitch;
@@ -642,7 +679,7 @@ cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, cons
     CUtensorMap amap{}, bmap{}, ymap{};
     const int Hs = dgrad ? g->p : g->h, Ws = dgrad ? g->q : g->w;
     if (!tc::make_map_nhwc(&amap, src, g->n, Hs, Ws, src_pitch, t.bw, t.bh, t.bn, t.mult_w,
-                           t.mult_h))
+                           t.mult_h, narrow ? 8 : 64))
         return cudaErrorNotSupported;
     const long long kred = (long long)g->r * g->s * src_pitch;
     if (!tc::make_map_2d(&bmap, filt, t.n_out, kred, kred, bn)) return cudaErrorInvalidValue;
@@ -653,8 +690,11 @@ cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, cons
     pk_epilogue e{};
     e.act = -1;
     if (epi) e = *epi;
-    return phased ? dispatch_fprop<true>(bn, amap, bmap, ymap, out, t, e, st)
-                  : dispatch_fprop<false>(bn, amap, bmap, ymap, out, t, e, st);
+    if (narrow)
+        return phased ? dispatch_fprop<true, true>(bn, amap, bmap, ymap, out, t, e, st)
+                      : dispatch_fprop<false, true>(bn, amap, bmap, ymap, out, t, e, st);
+    return phased ? dispatch_fprop<true, false>(bn, amap, bmap, ymap, out, t, e, st)
+                  : dispatch_fprop<false, false>(bn, amap, bmap, ymap, out, t, e, st);
 }
 
 static int tma_wgrad_splits(int tiles_mn, int num_kb, int num_sms) {

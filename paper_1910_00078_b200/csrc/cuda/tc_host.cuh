@@ -51,17 +51,21 @@ inline bool make_map_2d(CUtensorMap* map, const void* base, long long rows, long
 // passed to the driver is the number of elements traversed (bw*sw), so a
 // strided box still delivers bw x bh x bn rows of 128 bytes.
 inline bool make_map_nhwc(CUtensorMap* map, const void* base, int n, int h, int w, int pitch,
-                          int bw, int bh, int bn, int sw = 1, int sh = 1) {
+                          int bw, int bh, int bn, int sw = 1, int sh = 1, int box_c = 64) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     if (bw * sw > 256 || bh * sh > 256 || bn > 256) return false;
     cuuint64_t dims[4] = {(cuuint64_t)pitch, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
     cuuint64_t strides[3] = {(cuuint64_t)pitch * 2, (cuuint64_t)w * pitch * 2,
                              (cuuint64_t)h * w * pitch * 2};
-    cuuint32_t box[4] = {64, (cuuint32_t)(bw * sw), (cuuint32_t)(bh * sh), (cuuint32_t)bn};
+    cuuint32_t box[4] = {(cuuint32_t)box_c, (cuuint32_t)(bw * sw), (cuuint32_t)(bh * sh),
+                         (cuuint32_t)bn};
     cuuint32_t estr[4] = {1, (cuuint32_t)sw, (cuuint32_t)sh, 1};
+    // 64-channel (128-byte) boxes use the 128B swizzle; 8-channel (16-byte)
+    // boxes land as plain 16-byte rows (UMMA "interleaved" core matrices)
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
-              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              box_c == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }

@@ -144,6 +144,19 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr, uint32_t lbo
     d |= 2ull << 61;  // SWIZZLE_128B
     return d;
 }
+// K-major SWIZZLE_NONE ("interleaved") descriptor: 8 x 16-byte core matrices,
+// SBO = distance between 8-row groups along M/N, LBO = distance between the
+// two core matrices along K of one MMA (K = 16 bf16 = 2 x 8).
+__device__ __forceinline__ uint64_t umma_desc_noswz(uint32_t saddr, uint32_t lbo_bytes,
+                                                    uint32_t sbo_bytes) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+    d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
+    d |= 1ull << 46;  // descriptor version (Blackwell); layout type 0 = no swizzle
+    return d;
+}
+
 // Instruction descriptor: kind::f16, A/B = bf16, D = f32.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int m, int n, bool a_mn_major,
                                                       bool b_mn_major) {

@@ -276,6 +276,9 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                 ck(pk_cuda_fft_fwd(&g, dt, a, b, out, ws, st), "fft_fwd");
                 break;
             case ConvAlgo::ImplicitGemm: {
+                // Narrow-channel stems: dense (r,s,c) packing + plain GEMM
+                // measured faster (1.28 ms) than 16-byte-row TMA boxes
+                // (1.69 ms) for ResNet conv1 at N=256.
                 if (stem_eligible(g, dt, epi)) {
                     kernel = "stem_pack+gemm_tc";
                     run_stem(g, dir, a, b, out, ws, epi, h.num_sms(), st);
