@@ -21,6 +21,8 @@
 // Backward weights: rectangles of 64 pixels form the reduction blocks; dY and
 // the tap-shifted X rectangles arrive by TMA as MN-major operands; split-K
 // over rectangles with a fixed-order fp32 reduction.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tc_host.cuh"
 #include "tc_internal.h"
@@ -62,7 +64,10 @@ struct FSmem {
     static constexpr int kA = BM * BK * 2;
     static constexpr int kB = BN * BK * 2;
     static constexpr int kStage = kA + kB;
-    static constexpr int kStaging = 8 * 2 * 4096;
+    // epilogue staging per warp: double-buffered, except BN=256 where the
+    // smem goes to a 4th pipeline stage instead
+    static constexpr int kStgBufs = BN >= 256 ? 1 : 2;
+    static constexpr int kStaging = 8 * kStgBufs * 4096;
     static constexpr int kStagingOff = STAGES * kStage;
     static constexpr int kBarOff = kStagingOff + kStaging;
     static constexpr int kBytes = kBarOff + (2 * STAGES + 4) * 8 + 16 + 1024;
@@ -236,7 +241,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
         const int ew = warp - 2;
         const int q = warp & 3;       // TMEM lane quarter accessible to this warp
         const int half = ew >> 2;     // column-chunk parity handled by this warp
-        uint8_t* stg_base = smem + L::kStagingOff + ew * 2 * 4096;
+        uint8_t* stg_base = smem + L::kStagingOff + ew * L::kStgBufs * 4096;
         int sbuf = 0;
         const bool has_epi = epilogue_active(&epi);
         // this lane's row inside the rectangle, and the quarter's sub-box origin
@@ -298,7 +303,12 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                 }
                 const uint32_t stg_u = smem_u32(stg_base + sbuf * 4096);
                 if (!PHASED) {
-                    if (lane == 0) bulk_wait_read<1>();
+                    if (lane == 0) {
+                        if (L::kStgBufs == 2)
+                            bulk_wait_read<1>();
+                        else
+                            bulk_wait_read<0>();
+                    }
                     __syncwarp();
                 }
                 float xf[64];
@@ -330,7 +340,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                         tma_store_4d(&ymap, stg_u, n0c + c0, ri.w0 + qw, ri.h0 + qh, ri.n0 + qn);
                         bulk_commit();
                     }
-                    sbuf ^= 1;
+                    if (L::kStgBufs == 2) sbuf ^= 1;
                 } else {
                     __syncwarp();
                     // each lane owns its row: write the 128-byte chunk back from
@@ -565,7 +575,7 @@ cudaError_t dispatch_fprop(int bn, const CUtensorMap& amap, const CUtensorMap& b
                            const pk_epilogue& e, cudaStream_t st) {
     if (bn == 64) return launch_fprop<64, 6, PHASED, NARROW>(amap, bmap, ymap, out, g, e, st);
     if (bn == 128) return launch_fprop<128, 5, PHASED, NARROW>(amap, bmap, ymap, out, g, e, st);
-    return launch_fprop<256, 3, PHASED, NARROW>(amap, bmap, ymap, out, g, e, st);
+    return launch_fprop<256, 4, PHASED, NARROW>(amap, bmap, ymap, out, g, e, st);
 }
 
 int choose_bn(int want, int out_pitch) {
@@ -671,7 +681,12 @@ cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, cons
     t.bh = rt.bh;
     t.bn = rt.bn;
     quarter_box(t);
-    const int bn = choose_bn(bn_want, out_pitch);
+    // PK_TMA_BN (64/128/256) overrides the tile width for tuning experiments
+    static const int env_bn = [] {
+        const char* v = std::getenv("PK_TMA_BN");
+        return v ? std::atoi(v) : 0;
+    }();
+    const int bn = choose_bn(env_bn ? env_bn : bn_want, out_pitch);
     t.n_tiles_n = (out_pitch + bn - 1) / bn;
     if (!fill_phases(t, g->n, t.Ho, t.Wo, sh, sw, g->r, g->s, g->pad_h, g->pad_w, g->dil_h,
                      g->dil_w, dgrad))

@@ -170,47 +170,7 @@ __global__ void col2im_pack_kernel(pk_conv_geom g, const __nv_bfloat16* __restri
         const int r_first = unit_dil ? (ih + g.pad_h) % g.str_h : 0;
         const int s_first = unit_dil ? (iw + g.pad_w) % g.str_w : 0;
         const int r_step = unit_dil ? g.str_h : 1, s_step = unit_dil ? g.str_w : 1;
-        if (cn > 0 && cs == 4) {
-            // gather the contributing column entries in batches of 8 so the
-            // loads are in flight together (latency-bound otherwise)
-            const __nv_bfloat16* base = colg + (size_t)n * g.p * g.q * kcp + c0;
-            int r = r_first, s = s_first;
-            bool done = r >= g.r;
-            while (!done) {
-                uint2 v[8];
-#pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    v[b] = make_uint2(0u, 0u);
-                    // advance (r, s) to the next contributing tap
-                    while (!done) {
-                        const int nh = ih + g.pad_h - r * g.dil_h;
-                        const int nw = iw + g.pad_w - s * g.dil_w;
-                        const int rr = r, ss = s;
-                        s += s_step;
-                        if (s >= g.s) {
-                            s = s_first;
-                            r += r_step;
-                            if (r >= g.r) done = true;
-                        }
-                        if (nh < 0 || nw < 0 || nh % g.str_h || nw % g.str_w) continue;
-                        const int oh = nh / g.str_h, ow = nw / g.str_w;
-                        if (oh >= g.p || ow >= g.q) continue;
-                        v[b] = __ldg(reinterpret_cast<const uint2*>(
-                            base + ((size_t)oh * g.q + ow) * kcp + (rr * g.s + ss) * 4));
-                        break;
-                    }
-                }
-#pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&v[b]);
-                    const float2 f0 = __bfloat1622float2(h2[0]), f1 = __bfloat1622float2(h2[1]);
-                    acc[0] += f0.x;
-                    acc[1] += f0.y;
-                    acc[2] += f1.x;
-                    acc[3] += f1.y;
-                }
-            }
-        } else if (cn > 0) {
+        if (cn > 0) {
             for (int r = r_first; r < g.r; r += r_step) {
                 const int nh = ih + g.pad_h - r * g.dil_h;
                 if (nh < 0) break;
