@@ -375,7 +375,6 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
 
 // ---------------------------------------------------------------------------
 // wgrad: D[k][n], n = (r, s, c); reduction over 64-pixel rectangles.
-constexpr int WBN = 128;
 constexpr int kWgThreads = 192;  // producer, MMA, 4 epilogue warps
 
 struct TmaWgArgs {
@@ -387,21 +386,22 @@ struct TmaWgArgs {
     int num_kb, kb_per_split;
 };
 
-template <int STAGES>
+template <int NB, int STAGES>
 struct WSmem {
-    static constexpr int kA = BM * BK * 2;
-    static constexpr int kB = WBN * BK * 2;
+    static constexpr int kA = BM * BK * 2;   // two 64-channel MN atoms of dY
+    static constexpr int kB = NB * BK * 2;   // NB/64 MN atoms of tap-shifted X
+    static constexpr int kAtom = 64 * BK * 2;
     static constexpr int kStage = kA + kB;
     static constexpr int kBarOff = STAGES * kStage;
     static constexpr int kBytes = kBarOff + (2 * STAGES + 1) * 8 + 16 + 1024;
 };
 
-template <int STAGES>
+template <int NB, int STAGES>
 __global__ void __launch_bounds__(kWgThreads, 1)
     conv_tma_wgrad_kernel(const __grid_constant__ CUtensorMap dymap,
                           const __grid_constant__ CUtensorMap xmap, float* __restrict__ partial,
                           const __grid_constant__ TmaWgArgs g) {
-    using L = WSmem<STAGES>;
+    using L = WSmem<NB, STAGES>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -411,7 +411,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.x * BM;
-    const int n0 = blockIdx.y * WBN;
+    const int n0 = blockIdx.y * NB;
     const int split = blockIdx.z;
     const int kb_begin = split * g.kb_per_split;
     const int kb_end = min(g.num_kb, kb_begin + g.kb_per_split);
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         tma_prefetch(&dymap);
         tma_prefetch(&xmap);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, WBN);
+    if (warp == 1) tmem_alloc(tmem_slot, NB);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -434,10 +434,11 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            // the two 64-wide column blocks of B: (tap, channel chunk) each
-            int bc[2], bs[2], br[2];
+            // the NB/64 column blocks of B: (tap, channel chunk) each
+            constexpr int kAtoms = NB / 64;
+            int bc[kAtoms], bs[kAtoms], br[kAtoms];
 #pragma unroll
-            for (int a = 0; a < 2; ++a) {
+            for (int a = 0; a < kAtoms; ++a) {
                 const int nidx = n0 + a * 64;
                 const int tap = nidx / g.Cp;
                 bc[a] = nidx - tap * g.Cp;
@@ -459,8 +460,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 tma_load_4d(smem_u32(sa), &dymap, &full[stage], m0, q0, p0, img0);
                 tma_load_4d(smem_u32(sa + L::kA / 2), &dymap, &full[stage], m0 + 64, q0, p0, img0);
 #pragma unroll
-                for (int a = 0; a < 2; ++a)
-                    tma_load_4d(smem_u32(sa + L::kA + a * (L::kB / 2)), &xmap, &full[stage], bc[a],
+                for (int a = 0; a < kAtoms; ++a)
+                    tma_load_4d(smem_u32(sa + L::kA + a * L::kAtom), &xmap, &full[stage], bc[a],
                                 q0 * g.str_w - g.pad_w + bs[a] * g.dil_w,
                                 p0 * g.str_h - g.pad_h + br[a] * g.dil_h, img0);
                 if (++stage == STAGES) {
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             }
         }
     } else if (warp == 1) {
-        constexpr uint32_t idesc = idesc_bf16_f32(BM, WBN, true, true);
+        constexpr uint32_t idesc = idesc_bf16_f32(BM, NB, true, true);
         int stage = 0;
         uint32_t phase = 0;
         for (int kb = kb_begin; kb < kb_end; ++kb) {
@@ -481,8 +482,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 const uint32_t b_base = a_base + L::kA;
 #pragma unroll
                 for (int k = 0; k < BK / 16; ++k) {
-                    const uint64_t ad = umma_desc_sw128(a_base + k * 2048, L::kA / 2, 1024);
-                    const uint64_t bd = umma_desc_sw128(b_base + k * 2048, L::kB / 2, 1024);
+                    const uint64_t ad = umma_desc_sw128(a_base + k * 2048, L::kAtom, 1024);
+                    const uint64_t bd = umma_desc_sw128(b_base + k * 2048, L::kAtom, 1024);
                     mma_bf16(tmem_base, ad, bd, idesc, (kb != kb_begin) || (k != 0));
                 }
                 mma_commit(&empty[stage]);
@@ -503,7 +504,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         }
         const int k = m0 + q * 32 + lane;
 #pragma unroll 1
-        for (int c0 = 0; c0 < WBN; c0 += 16) {
+        for (int c0 = 0; c0 < NB; c0 += 16) {
             uint32_t v[16];
             if (live) {
                 tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c0, v);
@@ -530,7 +531,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, WBN);
+        tmem_dealloc(tmem_base, NB);
     }
 }
 
@@ -719,13 +720,40 @@ static int tma_wgrad_splits(int tiles_mn, int num_kb, int num_sms) {
     return splits < 1 ? 1 : splits;
 }
 
+// Filter-position tile width: 256 for spatial filters (more MMA work per byte
+// of X/dY pulled through L2; measured 0.236 -> 0.182 ms on conv2_x 3x3), 128
+// for 1x1 filters (HBM-bound; the wider tile only halves the CTA count there).
+static int wgrad_nb(const pk_conv_geom* g) {
+    return (g->r * g->s > 1 && g->r * g->s * g->x_pitch >= 256) ? 256 : 128;
+}
+
 static void wgrad_geometry(const pk_conv_geom* g, int* tiles_mn, int* num_kb, RectTile* rt) {
     *rt = tc::best_rect(g->n, g->p, g->q, BK);
     const int tw = (g->q + rt->bw - 1) / rt->bw, th = (g->p + rt->bh - 1) / rt->bh;
     const int tn = (g->n + rt->bn - 1) / rt->bn;
     *num_kb = tw * th * tn;
     const int nn = g->r * g->s * g->x_pitch;
-    *tiles_mn = ((g->k + BM - 1) / BM) * ((nn + WBN - 1) / WBN);
+    const int nb = wgrad_nb(g);
+    *tiles_mn = ((g->k + BM - 1) / BM) * ((nn + nb - 1) / nb);
+}
+
+template <int NB, int STAGES>
+cudaError_t launch_wgrad(const CUtensorMap& dymap, const CUtensorMap& xmap, float* partial,
+                         const TmaWgArgs& w, int splits, cudaStream_t st) {
+    using L = WSmem<NB, STAGES>;
+    static int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+        cudaError_t err = cudaFuncSetAttribute(conv_tma_wgrad_kernel<NB, STAGES>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               L::kBytes);
+        if (err != cudaSuccess) return err;
+        attr_dev = dev;
+    }
+    dim3 grid((w.K + BM - 1) / BM, (w.Nn + NB - 1) / NB, splits);
+    conv_tma_wgrad_kernel<NB, STAGES><<<grid, kWgThreads, L::kBytes, st>>>(dymap, xmap, partial, w);
+    return cudaGetLastError();
 }
 
 size_t pk_tma_wgrad_workspace(const pk_conv_geom* g, int num_sms) {
@@ -775,21 +803,10 @@ cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, v
     if (!tc::make_map_nhwc(&xmap, x, g->n, g->h, g->w, g->x_pitch, rt.bw, rt.bh, rt.bn, g->str_w,
                            g->str_h))
         return cudaErrorNotSupported;
-    constexpr int STAGES = 6;
-    using L = WSmem<STAGES>;
-    static int attr_dev = -1;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (attr_dev != dev) {
-        cudaError_t err = cudaFuncSetAttribute(conv_tma_wgrad_kernel<STAGES>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               L::kBytes);
-        if (err != cudaSuccess) return err;
-        attr_dev = dev;
-    }
-    dim3 grid((w.K + BM - 1) / BM, (w.Nn + WBN - 1) / WBN, splits);
-    conv_tma_wgrad_kernel<STAGES><<<grid, kWgThreads, L::kBytes, st>>>(dymap, xmap,
-                                                                       (float*)workspace, w);
+    const cudaError_t le =
+        wgrad_nb(g) == 256 ? launch_wgrad<256, 4>(dymap, xmap, (float*)workspace, w, splits, st)
+                           : launch_wgrad<128, 6>(dymap, xmap, (float*)workspace, w, splits, st);
+    if (le != cudaSuccess) return le;
     const long long total = (long long)w.K * w.Nn;
     long long blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
