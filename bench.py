@@ -359,11 +359,14 @@ def layer_report(torch, lib, handle, net, peaks, path):
     rows = []
     hbm = peaks["hbm_gbs"] * 1e9
     tc = peaks["bf16_tflops"] * 1e12
+    only = set(os.environ.get("PK_LAYERS", "").split(",")) - {""}
     for (L, x, w, y, dy, dx, dw, probs) in net.items:
+        if only and L.name not in only:
+            continue
         for d, (a, b, o) in ((0, (x, w, y)), (1, (dy, w, dx)), (2, (dy, x, dw))):
             p, s = probs[d]
             run_conv(lib, handle, p, s, a, b, o, net.ws)
-            ms = time_region(torch, lambda: run_conv(lib, handle, p, s, a, b, o, net.ws), 5) / 5
+            ms = time_region(torch, lambda: run_conv(lib, handle, p, s, a, b, o, net.ws), 10) / 10
             fl = L.flops(net.n)
             byts = 2 * (a.numel() + b.numel() + o.numel())
             bound_ms = max(fl / tc, byts / hbm) * 1e3

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // tcgen05 implicit-GEMM convolution, forward and backward-data (sm_100a).
 //
 //   D[pixel][out_ch] = sum_{(r,s,ch)} A[pixel][(r,s,ch)] * B[out_ch][(r,s,ch)]
@@ -548,6 +549,12 @@ cudaError_t pk_cuda_igemm_tc_fwd(const pk_conv_geom* g, const void* x, const voi
                                  cudaStream_t st) {
     if (!pk_tc_fwd_supported(g) || !aligned16(x) || !aligned16(f) || !aligned16(y))
         return cudaErrorNotSupported;
+    // narrow-channel stems: halo-staged fused kernel (stem_fused.cu)
+    static const bool stem_on = [] {
+        const char* v = std::getenv("PK_STEM_FUSED");
+        return !(v && v[0] == '0');
+    }();
+    if (stem_on && pk_cuda_stem_fused_supported(g)) return pk_cuda_stem_fused_fprop(g, x, f, y, epi, st);
     ConvTcArgs t{};
     t.M = g->n * g->p * g->q;
     t.Ho = g->p;

@@ -145,6 +145,16 @@ cudaError_t pk_cuda_filter_pack(const pk_conv_geom* g, const void* f, void* dst,
 cudaError_t pk_cuda_col2im_pack(const pk_conv_geom* g, const void* colg, void* dx, cudaStream_t st);
 cudaError_t pk_cuda_wgrad_unpack(const pk_conv_geom* g, const void* dwp, void* dw, cudaStream_t st);
 
+// ---- fused narrow-channel (stem, C <= 4) tcgen05 convolutions, bf16 ---------
+// Input halo staged in smem and expanded into the tap-packed operand on chip
+// (no column matrix in HBM). K (output channels) in {64, 128}, y pitch == K.
+int pk_cuda_stem_fused_supported(const pk_conv_geom* g);
+cudaError_t pk_cuda_stem_fused_fprop(const pk_conv_geom* g, const void* x, const void* w, void* y,
+                                     const pk_epilogue* epi, cudaStream_t st);
+size_t pk_cuda_stem_fused_wgrad_workspace(const pk_conv_geom* g, int num_sms);
+cudaError_t pk_cuda_stem_fused_wgrad(const pk_conv_geom* g, const void* dy, const void* x,
+                                     void* dw, void* workspace, int num_sms, cudaStream_t st);
+
 // ---- pointwise / batch-norm ----------------------------------------------------
 // y = epilogue(x + 0) elementwise over NHWC (bias/bn/act all optional).
 cudaError_t pk_cuda_pointwise(const void* x, void* y, int n, int c, int hw, int pitch, int dtype,

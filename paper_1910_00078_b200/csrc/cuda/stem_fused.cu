@@ -1,0 +1,1048 @@
+#include <cstdio>
+#include <cstdlib>
+// Fused narrow-channel ("stem") convolutions on tcgen05 — ResNet conv1
+// (3 -> 64, 7x7 stride 2) and VGG conv1_1 (3 -> 64, 3x3) — without the
+// column matrix round trip through HBM.
+//
+// A 4-channel input has too little data per pixel for TMA boxes (16-byte
+// rows re-read once per filter tap) and too much redundancy for an explicit
+// im2col (49 taps x 8 bytes per output pixel written and re-read: 1.3 GB for
+// conv1 at N=256). Instead each CTA stages the input HALO of its output
+// rectangle (8 x 16 pixels) in shared memory once, split by column phase
+// (c mod stride) so lanes reading neighbouring output pixels hit consecutive
+// 8-byte words, and 8 builder warps expand it in shared memory into the
+// tap-packed operand the tensor core reads:
+//
+//   kc = tap*4 + c (tap = r*S + s, c < 4), 16-byte unit = (2 taps x 4 ch)
+//
+//   forward   D[pixel][k]  = A[pixel][kc] . B[k][kc]      A K-major (built),
+//             B = packed filter, resident in smem; fused epilogue + TMA store
+//   backward  D[kc][k]    += A[kc][pixel] . dY[k][pixel]  A MN-major SW128
+//   weights   (built), dY by TMA; every CTA accumulates its tiles in TMEM,
+//             writes one fp32 partial; a fixed-order sum finishes (deterministic)
+//
+// Roofline: HBM (x read once, y / dY read or written once); the tensor work
+// (2 * 128 * K * 208 FLOP per tile) is a few percent of the MMA peak.
+#include "common.cuh"
+#include "tc_host.cuh"
+#include "tc_internal.h"
+#include "tc_ptx.cuh"
+
+namespace pk {
+namespace {
+
+using namespace pk::tc;
+
+constexpr int kTile = 128;          // output pixels per tile (8 x 16 rectangle)
+constexpr int kBw = 16, kBh = 8;
+constexpr int kBuilders = 256;      // 8 builder warps
+constexpr int kHaloPer = 4;         // halo pixels per builder thread (<= 1024)
+constexpr int kMaxTaps = 64;
+
+struct StemArgs {
+    int N, H, W, x_pitch;
+    int P, Q;
+    int K, n_pad;             // output channels, MMA N (fprop) / dY channel pitch (wgrad)
+    int R, S, sh, sw, dh, dw, ph, pw;
+    int C;                    // real input channels (<= 4)
+    int tiles_w, tiles_h, total_tiles;
+    int HH, HW, HWp;          // halo rows, cols, cols per column phase
+    int nchunks;              // 16-byte (2-tap) units per pixel, even
+    int taps;
+    int kcm;                  // wgrad: padded kc rows (multiple of 128)
+    unsigned long long* trace;  // PK_STEM_TRACE: per-role clock64 stamps of CTA 0 (profiling only)
+    int debug;                // PK_STEM_DEBUG bits (profiling only): 1 no MMA, 2 no build, 4 no store, 8 no TMEM drain, 16 no halo
+    int box_px, nbox;         // halo TMA: boxes of box_px pixels per halo row
+    int tap_off[kMaxTaps];    // halo word offset of tap t
+};
+
+__device__ __forceinline__ void tile_origin(const StemArgs& g, int t, int& n, int& oy0, int& ox0) {
+    const int tx = t % g.tiles_w;
+    const int rest = t / g.tiles_w;
+    const int ty = rest % g.tiles_h;
+    n = rest / g.tiles_h;
+    oy0 = ty * kBh;
+    ox0 = tx * kBw;
+}
+
+// trace slot: [tile < 32][event < 16]
+__device__ __forceinline__ void stamp(const StemArgs& g, int it, int ev) {
+    if (g.trace && blockIdx.x == 0 && it < 32 && (threadIdx.x & 31) == 0)
+        g.trace[it * 32 + ev] = clock64();
+}
+
+__device__ __forceinline__ void named_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// Per builder thread: the halo pixels it loads (fixed across tiles).
+struct HaloSlots {
+    int hr[kHaloPer], hc[kHaloPer], word[kHaloPer];
+};
+
+__device__ __forceinline__ void halo_slots(const StemArgs& g, int b, HaloSlots& hs) {
+#pragma unroll
+    for (int u = 0; u < kHaloPer; ++u) {
+        const int i = b + u * kBuilders;
+        if (i < g.HH * g.HW) {
+            hs.hr[u] = i / g.HW;
+            hs.hc[u] = i - hs.hr[u] * g.HW;
+            hs.word[u] = (hs.hc[u] % g.sw) * g.HH * g.HWp + hs.hr[u] * g.HWp + hs.hc[u] / g.sw;
+        } else {
+            hs.hr[u] = -1;
+            hs.hc[u] = 0;
+            hs.word[u] = 0;
+        }
+    }
+}
+
+// Halo ring: kHaloStages buffers of the compact (4-channel, column-phase
+// split) input halo, filled by 8-byte cp.async copies (zero fill outside x)
+// kHaloStages - 1 tiles ahead of the build, so ~3 tiles of input are in
+// flight per SM (the stem is HBM-latency bound otherwise).
+constexpr int kHaloStages = 4;
+constexpr int kHaloStageBytes = 8192;
+
+__device__ __forceinline__ void cp_async_8(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// Issue this thread's halo copies of tile t (none past the last tile) into
+// the stage at dst_u and close one cp.async group (always, to keep counts).
+__device__ __forceinline__ void halo_issue(const StemArgs& g, const __nv_bfloat16* __restrict__ x,
+                                           int t, const HaloSlots& hs, uint32_t dst_u) {
+    if (t < g.total_tiles && !(g.debug & 16)) {
+        int n, oy0, ox0;
+        tile_origin(g, t, n, oy0, ox0);
+        const int iy0 = oy0 * g.sh - g.ph, ix0 = ox0 * g.sw - g.pw;
+#pragma unroll
+        for (int u = 0; u < kHaloPer; ++u) {
+            if (hs.hr[u] < 0) continue;
+            const int iy = iy0 + hs.hr[u], ix = ix0 + hs.hc[u];
+            const bool in = iy >= 0 && iy < g.H && ix >= 0 && ix < g.W;
+            const __nv_bfloat16* src = in ? x + (((size_t)n * g.H + iy) * g.W + ix) * g.x_pitch : x;
+            cp_async_8(dst_u + hs.word[u] * 8, src, in ? 8u : 0u);
+        }
+    }
+    cp_async_commit();
+}
+
+__device__ __forceinline__ void st_shared_v2(uint32_t addr, uint2 v) {
+    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ uint2 ld_shared_v2(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// Operand expansion plan of one builder warp: warp w owns the 16-byte units
+// (2 taps x 4 channels) j = w, w + 8, w + 16, w + 24 of all 128 tile pixels;
+// lanes walk 32 consecutive pixels (row groups g = 0..3), so halo reads are
+// consecutive 8-byte words and operand stores consecutive 16-byte units.
+constexpr int kUnitsPerWarp = 4;  // nchunks <= 32
+struct BuildPlan {
+    int count;                                   // units owned by this warp
+    int src0[kUnitsPerWarp], src1[kUnitsPerWarp];  // halo byte offset of tap 2j / 2j+1 (-1: none)
+    uint32_t dst[kUnitsPerWarp];                 // operand byte offset of unit j (+ lane term)
+    uint32_t row[4];                             // halo byte offset of pixel g*32 + lane
+    uint32_t rowdst[4];                          // operand byte offset of pixel g*32 + lane
+};
+
+// MN_MAJOR = false: forward A[pixel][kc] no-swizzle K-major, [j][128 px][16 B]
+// MN_MAJOR = true : wgrad  A[kc][pixel] SWIZZLE_128B MN-major, 64-kc atoms of
+//                   128 px x 128 B (unit j = 16-byte chunk j%8 of atom j/8)
+template <bool MN_MAJOR>
+__device__ __forceinline__ void build_plan(const StemArgs& g, int wib, int lane, BuildPlan& bp) {
+    bp.count = 0;
+#pragma unroll
+    for (int c = 0; c < kUnitsPerWarp; ++c) {
+        const int j = wib + 8 * c;
+        const int t0 = 2 * j, t1 = t0 + 1;
+        bp.src0[c] = (j < g.nchunks && t0 < g.taps) ? g.tap_off[t0] * 8 : -1;
+        bp.src1[c] = (j < g.nchunks && t1 < g.taps) ? g.tap_off[t1] * 8 : -1;
+        if (MN_MAJOR)
+            bp.dst[c] = (j >> 3) * (kTile * 128) + (((j & 7) ^ (lane & 7)) << 4);
+        else
+            bp.dst[c] = j * (kTile * 16);
+        if (j < g.nchunks) bp.count = c + 1;
+    }
+#pragma unroll
+    for (int gi = 0; gi < 4; ++gi) {
+        const int m = gi * 32 + lane;
+        bp.row[gi] = ((m / kBw) * g.sh * g.HWp + (m % kBw)) * 8;
+        bp.rowdst[gi] = MN_MAJOR ? m * 128 : m * 16;
+    }
+}
+
+// Branch-free expansion: taps past R*S read the zero word at the end of
+// the halo stage, so each unit is 8 independent loads then 4 stores.
+constexpr uint32_t kHaloZero = kHaloStageBytes - 8;
+
+__device__ __forceinline__ void build_tile(const BuildPlan& bp, uint32_t a_base, uint32_t halo_u) {
+#pragma unroll
+    for (int c = 0; c < kUnitsPerWarp; ++c) {
+        if (c >= bp.count) break;
+        const int s0 = bp.src0[c], s1 = bp.src1[c];
+        const uint32_t d = a_base + bp.dst[c];
+        uint2 v[8];
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi) {
+            const uint32_t a0 = halo_u + (s0 >= 0 ? bp.row[gi] + s0 : kHaloZero);
+            const uint32_t a1 = halo_u + (s1 >= 0 ? bp.row[gi] + s1 : kHaloZero);
+            v[2 * gi] = ld_shared_v2(a0);
+            v[2 * gi + 1] = ld_shared_v2(a1);
+        }
+#pragma unroll
+        for (int gi = 0; gi < 4; ++gi)
+            st_shared_v4(d + bp.rowdst[gi],
+                         make_uint4(v[2 * gi].x, v[2 * gi].y, v[2 * gi + 1].x, v[2 * gi + 1].y));
+    }
+}
+
+// Zero the reserved last word of every halo stage (never written by cp.async).
+__device__ __forceinline__ void halo_zero_words(uint32_t halo0, int b) {
+    if (b < kHaloStages) st_shared_v2(halo0 + b * kHaloStageBytes + kHaloZero, make_uint2(0u, 0u));
+}
+
+// ---------------------------------------------------------------------------
+// TMA-fed halo: one elected thread loads the input halo of a tile as sw
+// column-phase boxes (traversal stride sw, out-of-bounds zero fill = the
+// convolution padding) into a raw ring of 16-byte pixels; the builders then
+// compact it to 8-byte (4-channel) pixels so operand gathers hit consecutive
+// 8-byte words.
+constexpr int kRawStages = 4;
+constexpr int kRawStageBytes = 16384;
+constexpr int kCompactBytes = kHaloStageBytes;  // 2 compact buffers
+
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ void halo_tma(const StemArgs& g, const CUtensorMap* xmap, int t,
+                                         uint32_t raw_u, uint64_t* bar) {
+    int n, oy0, ox0;
+    tile_origin(g, t, n, oy0, ox0);
+    const int iy0 = oy0 * g.sh - g.ph, ix0 = ox0 * g.sw - g.pw;
+    // raw [box][row][box_px pixels x 16 B]; box destinations 128-byte aligned
+    const int bstride = (g.HH * g.box_px * 16 + 127) / 128 * 128;
+    mbar_arrive_expect_tx(bar, g.nbox * g.HH * g.box_px * 16);
+    for (int bx = 0; bx < g.nbox; ++bx)
+        tma_load_3d(raw_u + bx * bstride, xmap, bar, (ix0 + bx * g.box_px) * g.x_pitch, iy0, n);
+}
+
+// raw halo pixel (row, col) 16 B -> compact [col % sw][row][col / sw] 8 B
+// (channels 0-3, column-phase split)
+__device__ __forceinline__ void halo_compact(const StemArgs& g, uint32_t raw_u, uint32_t cmp_u, int b) {
+    const int per_box = g.HH * g.box_px, total = g.nbox * per_box;
+    const int bstride = (per_box * 16 + 127) / 128 * 128;
+    for (int i = b; i < total; i += kBuilders) {
+        const int bx = i / per_box, rem = i - bx * per_box;
+        const int row = rem / g.box_px, col = bx * g.box_px + (rem - row * g.box_px);
+        if (col >= g.HW) continue;
+        const uint4 v = ld_shared_v4(raw_u + bx * bstride + rem * 16);
+        const int ph = col % g.sw, idx = col / g.sw;
+        st_shared_v2(cmp_u + ((ph * g.HH + row) * g.HWp + idx) * 8, make_uint2(v.x, v.y));
+    }
+}
+
+// Halo byte offsets (relative to the pixel's row base) of the two taps of each
+// unit this warp expands: units [u0, u0 + 16); invalid taps -> the zero word.
+struct UnitOffsets {
+    uint32_t o0[16], o1[16];
+};
+__device__ __forceinline__ void unit_offsets(const StemArgs& g, int u0, int u1, uint32_t rowoff,
+                                             UnitOffsets& uo) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+        const int j = u0 + e, t0 = 2 * j, t1 = t0 + 1;
+        uo.o0[e] = (j < u1 && t0 < g.taps) ? g.tap_off[t0] * 8 : kHaloZero - rowoff;
+        uo.o1[e] = (j < u1 && t1 < g.taps) ? g.tap_off[t1] * 8 : kHaloZero - rowoff;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// forward: A built straight into TENSOR MEMORY (tcgen05.st), MMA with A from
+// TMEM and the resident packed filter from smem. Keeping the 53 KB/tile
+// operand out of shared memory halves the smem traffic per tile (it was the
+// bound: build writes + MMA reads of A competed with everything else).
+//   warp 0: MMA issuer (+ TMEM owner), warps 1-4: epilogue, warps 5-12: builders
+//   (builder warp w writes TMEM lane quarter w % 4; the two warps of a quarter
+//   split the 16-byte units of their 32 pixels)
+constexpr int kFwdThreads = 32 * 13;
+constexpr int kMaxAStages = 4;
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() {
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// Issued by the whole (converged) warp; elect.sync picks the one issuing lane,
+// so the compiler emits no per-instruction divergence loop around UTCHMMA.
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Four back-to-back MMAs (operands computed up front, one elect): keeps the
+// per-instruction issue cost (descriptor math + R2UR moves) out of the chain.
+__device__ __forceinline__ void mma4_bf16_ts(uint32_t tmem_d, uint32_t a0, uint32_t a1, uint32_t a2,
+                                             uint32_t a3, uint64_t b0, uint64_t b1, uint64_t b2,
+                                             uint64_t b3, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %10, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %5, %9, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %6, %9, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %7, %9, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %8, %9, 1;\n\t}" ::"r"(tmem_d),
+        "r"(a0), "r"(a1), "r"(a2), "r"(a3), "l"(b0), "l"(b1), "l"(b2), "l"(b3), "r"(idesc),
+        "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+// Two builder groups (4 warps each, one per TMEM lane quarter) alternate
+// tiles, so two independent halo -> operand chains are in flight; each group
+// streams its halos with 8-byte cp.async copies (zero fill = padding) into its
+// own ring of compact, column-phase-split halo stages.
+constexpr int kGroupThreads = 128;
+constexpr int kGroupHaloStages = 3;
+constexpr int kSlots = 8;  // halo pixels per group thread (<= 1024 per tile)
+
+struct GroupHalo {
+    int goff[kSlots];   // element offset of the slot's pixel from the halo origin
+    int hrc[kSlots];    // (row << 16) | col, -1 = unused slot
+    int word[kSlots];   // compact word index
+};
+
+__device__ __forceinline__ void group_halo_slots(const StemArgs& g, int b, GroupHalo& gh) {
+#pragma unroll
+    for (int u = 0; u < kSlots; ++u) {
+        const int i = b + u * kGroupThreads;
+        if (i < g.HH * g.HW) {
+            const int hr = i / g.HW, hc = i - hr * g.HW;
+            gh.goff[u] = (hr * g.W + hc) * g.x_pitch;
+            gh.hrc[u] = (hr << 16) | hc;
+            gh.word[u] = ((hc % g.sw) * g.HH + hr) * g.HWp + hc / g.sw;
+        } else {
+            gh.goff[u] = 0;
+            gh.hrc[u] = -1;
+            gh.word[u] = 0;
+        }
+    }
+}
+
+// Tile walker: (n, ty, tx) of tile t, advanced by a fixed tile stride without
+// divisions.
+struct TileWalk {
+    int t, n, ty, tx, dn, dty, dtx, step;
+    __device__ __forceinline__ void init(const StemArgs& g, int t0, int stride) {
+        t = t0;
+        step = stride;
+        tx = t0 % g.tiles_w;
+        ty = (t0 / g.tiles_w) % g.tiles_h;
+        n = t0 / (g.tiles_w * g.tiles_h);
+        dtx = stride % g.tiles_w;
+        dty = (stride / g.tiles_w) % g.tiles_h;
+        dn = stride / (g.tiles_w * g.tiles_h);
+    }
+    __device__ __forceinline__ void next(const StemArgs& g) {
+        t += step;
+        tx += dtx;
+        if (tx >= g.tiles_w) {
+            tx -= g.tiles_w;
+            ++ty;
+        }
+        ty += dty;
+        if (ty >= g.tiles_h) {
+            ty -= g.tiles_h;
+            ++n;
+        }
+        n += dn;
+    }
+};
+
+__device__ __forceinline__ void group_halo_issue(const StemArgs& g, const __nv_bfloat16* __restrict__ x,
+                                                 const TileWalk& tw, const GroupHalo& gh,
+                                                 uint32_t dst_u) {
+    if (tw.t < g.total_tiles) {
+        const int iy0 = tw.ty * kBh * g.sh - g.ph, ix0 = tw.tx * kBw * g.sw - g.pw;
+        const __nv_bfloat16* base = x + (((size_t)tw.n * g.H + iy0) * g.W + ix0) * g.x_pitch;
+#pragma unroll
+        for (int u = 0; u < kSlots; ++u) {
+            if (gh.hrc[u] < 0) continue;
+            const int iy = iy0 + (gh.hrc[u] >> 16), ix = ix0 + (gh.hrc[u] & 0xffff);
+            const bool in = (unsigned)iy < (unsigned)g.H && (unsigned)ix < (unsigned)g.W;
+            cp_async_8(dst_u + gh.word[u] * 8, in ? base + gh.goff[u] : x, in ? 8u : 0u);
+        }
+    }
+    cp_async_commit();
+}
+
+// smem: resident filter (SW128 K-major), halo ring, epilogue staging, barriers
+struct FwdLayout {
+    int raw_off, halo_off, stg_off, bar_off, bytes;
+    __host__ __device__ FwdLayout(int nchunks, int np) {
+        const int atoms = (nchunks + 7) / 8;
+        raw_off = atoms * np * 128;  // (unused)
+        halo_off = raw_off;
+        stg_off = halo_off + 2 * kGroupHaloStages * kHaloStageBytes;
+        bar_off = stg_off + 4 * 2 * 4096;  // 4 epilogue warps x 2 staging buffers
+        bytes = bar_off + 256 + 1024;
+    }
+};
+
+template <int NP>
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    stem_fprop_kernel(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap xmap,
+                      const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                      const __nv_bfloat16* __restrict__ w, const __grid_constant__ StemArgs g,
+                      const pk_epilogue epi) {
+    const FwdLayout L(g.nchunks, NP);
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+    uint64_t* empty = full + kMaxAStages;
+    uint64_t* tmem_full = empty + kMaxAStages;
+    uint64_t* tmem_empty = tmem_full + 2;
+    uint64_t* raw_full = tmem_empty + 2;
+    uint64_t* raw_empty = raw_full + kRawStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + kRawStages);
+    const uint32_t halo0 = smem_u32(smem + L.halo_off);
+    const uint32_t raw0 = smem_u32(smem + L.raw_off);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // TMEM columns: [0, 2*NP) accumulators, then A stages of 4 columns per unit
+    const int a_cols = (g.nchunks + 3) / 4 * 16;  // whole 4-unit (16-column) store groups
+    int a_stages = (512 - 2 * NP) / a_cols;
+    if (a_stages > kMaxAStages) a_stages = kMaxAStages;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kMaxAStages; ++i) {
+            mbar_init(&full[i], 4);  // the 4 warps of one builder group
+            mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tmem_full[i], 1);
+            mbar_init(&tmem_empty[i], 4);
+        }
+        for (int i = 0; i < kRawStages; ++i) {
+            mbar_init(&raw_full[i], 1);
+            mbar_init(&raw_empty[i], kBuilders / 32);
+        }
+        fence_barrier_init();
+        tma_prefetch(&ymap);
+        tma_prefetch(&xmap);
+    }
+    if (warp == 0) tmem_alloc(tmem_slot, 512);
+    if (warp >= 5) {
+        // packed filter B[n][kc] (unit j = taps 2j, 2j+1 x 4 channels), K-major
+        // SWIZZLE_128B, resident for the whole kernel
+        const int b = threadIdx.x - 5 * 32;
+        const uint32_t bbase = smem_u32(smem);
+        for (int i = b; i < g.nchunks * NP; i += kBuilders) {
+            const int j = i / NP, n = i - j * NP;
+            __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int t = 2 * j + (e >> 2), c = e & 3;
+                v[e] = (n < g.K && t < g.taps && c < g.C)
+                           ? w[((size_t)n * g.taps + t) * g.x_pitch + c]
+                           : __float2bfloat16_rn(0.0f);
+            }
+            st_shared_v4(bbase + (uint32_t)((j >> 3) * NP * 128 + n * 128 + (((j & 7) ^ (n & 7)) << 4)),
+                         *reinterpret_cast<const uint4*>(v));
+        }
+        if (b < 2 * kGroupHaloStages)
+            st_shared_v2(halo0 + b * kHaloStageBytes + kHaloZero, make_uint2(0u, 0u));
+        fence_proxy_async_smem();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- MMA issuer: D[pix][k] += A_tmem[pix][kc] . B[k][kc] ----
+        constexpr uint32_t idesc = idesc_bf16_f32(kTile, NP, false, false);
+        const uint64_t bd0 = umma_desc_sw128(smem_u32(smem), 16, 1024);
+        const int nk = (g.debug & 1) ? 0 : g.nchunks / 2;
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++it) {
+            const int a = it & 1;
+            stamp(g, it, 0);
+            mbar_wait(&tmem_empty[a], ((it >> 1) & 1) ^ 1);
+            stamp(g, it, 1);
+            mbar_wait(&full[stage], phase);
+            stamp(g, it, 2);
+            tc_fence_after();
+            {
+                const uint32_t ta = tmem_base + 2 * NP + stage * a_cols;
+                const uint32_t td = tmem_base + a * NP;
+                int k = 0;
+                for (; k + 4 <= nk; k += 4) {  // K16 steps k..k+3 share one 64-wide B atom
+                    const uint64_t bk = bd0 + (uint64_t)((k >> 2) * (NP * 128 / 16));
+                    mma4_bf16_ts(td, ta + k * 8, ta + k * 8 + 8, ta + k * 8 + 16, ta + k * 8 + 24, bk,
+                                 bk + 2, bk + 4, bk + 6, idesc, k != 0);
+                }
+                for (; k < nk; ++k)
+                    mma_bf16_ts(td, ta + k * 8,
+                                bd0 + (uint64_t)((k >> 2) * (NP * 128 / 16) + (k & 3) * 2), idesc,
+                                k != 0);
+                if (g.trace && blockIdx.x == 0 && it < 32 && lane == 0)
+                    g.trace[it * 32 + 16] = clock64();
+                mma_commit_elect(&empty[stage]);
+                mma_commit_elect(&tmem_full[a]);
+            }
+            stamp(g, it, 3);
+            __syncwarp();
+            if (++stage == a_stages) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+    } else if (warp <= 4) {
+        // ---------------- epilogue (4 warps, one TMEM lane quarter each) ---------
+        const int q = warp & 3;
+        uint8_t* stg_base = smem + L.stg_off + (warp - 1) * 2 * 4096;
+        int sbuf = 0;
+        const bool has_epi = epilogue_active(&epi);
+        const int row = q * 32 + lane;
+        const int rw = row % kBw, rh = row / kBw;
+        int it = 0;
+        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++it) {
+            int n, oy0, ox0;
+            tile_origin(g, t, n, oy0, ox0);
+            const int a = it & 1;
+            if (warp == 1) stamp(g, it, 4);
+            mbar_wait(&tmem_full[a], (it >> 1) & 1);
+            if (warp == 1) stamp(g, it, 5);
+            tc_fence_after();
+#pragma unroll 1
+            for (int c0 = 0; c0 < NP; c0 += 64) {
+                uint32_t v[64];
+                const uint32_t ta = tmem_base + a * NP + c0 + (static_cast<uint32_t>(q * 32) << 16);
+                tmem_ld16(ta + 0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+                tmem_ld16(ta + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+                tmem_ld16(ta + 32, *reinterpret_cast<uint32_t(*)[16]>(&v[32]));
+                tmem_ld16(ta + 48, *reinterpret_cast<uint32_t(*)[16]>(&v[48]));
+                tmem_ld_wait();
+                if (warp == 1) stamp(g, it, 6);
+                if (c0 + 64 >= NP) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tmem_empty[a]);
+                }
+                const uint32_t stg_u = smem_u32(stg_base + sbuf * 4096);
+                if (lane == 0) bulk_wait_read<1>();
+                __syncwarp();
+                float xf[64];
+#pragma unroll
+                for (int e = 0; e < 64; ++e) xf[e] = __uint_as_float(v[e]);
+                if (has_epi) epilogue_chunk64(epi, xf, c0, g.K, oy0 + rh, ox0 + rw, g.P, g.Q);
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    uint32_t packed[4];
+#pragma unroll
+                    for (int e = 0; e < 8; e += 2) {
+                        __nv_bfloat162 b2 = __floats2bfloat162_rn(xf[jj * 8 + e], xf[jj * 8 + e + 1]);
+                        packed[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
+                    }
+                    st_shared_v4(stg_u + lane * 128 + ((jj ^ (lane & 7)) << 4),
+                                 make_uint4(packed[0], packed[1], packed[2], packed[3]));
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0 && !(g.debug & 4)) {
+                    // this warp's 32 rows = 2 output rows of the 16-wide rectangle
+                    tma_store_4d(&ymap, stg_u, c0, ox0, oy0 + q * 2, n);
+                    bulk_commit();
+                }
+                if (warp == 1) stamp(g, it, 7);
+                sbuf ^= 1;
+            }
+        }
+        if (lane == 0) bulk_wait_all();
+    } else {
+        // ---------------- builders: 2 groups, cp.async halo -> A rows in TMEM --------
+        const int grp = (warp - 5) >> 2;                    // tiles i with i % 2 == grp
+        const int gb = (warp - 5 - 4 * grp) * 32 + lane;    // thread index in the group
+        const int q = warp & 3;                             // TMEM lane quarter
+        const int m = q * 32 + lane;                        // tile pixel = TMEM lane
+        const uint32_t rowoff = ((m / kBw) * g.sh * g.HWp + (m % kBw)) * 8;
+        UnitOffsets uo0, uo1;  // units [0, 16) and [16, 32)
+        unit_offsets(g, 0, g.nchunks, rowoff, uo0);
+        unit_offsets(g, 16, g.nchunks, rowoff, uo1);
+        GroupHalo gh;
+        group_halo_slots(g, gb, gh);
+        const uint32_t ring = halo0 + grp * kGroupHaloStages * kHaloStageBytes;
+        TileWalk pf;  // prefetch walker: this group's tiles
+        pf.init(g, blockIdx.x + grp * gridDim.x, 2 * gridDim.x);
+        for (int s2 = 0; s2 < kGroupHaloStages - 1; ++s2) {
+            group_halo_issue(g, x, pf, gh, ring + s2 * kHaloStageBytes);
+            pf.next(g);
+        }
+        int k = 0;
+        for (int i = grp, t = blockIdx.x + grp * gridDim.x; t < g.total_tiles;
+             i += 2, t += 2 * gridDim.x, ++k) {
+            if (warp == 5) stamp(g, i, 8);
+            cp_async_wait<kGroupHaloStages - 2>();
+            named_sync(1 + grp, kGroupThreads);  // halo k landed; this group's build k-1 done
+            if (warp == 5) stamp(g, i, 9);
+            group_halo_issue(g, x, pf, gh,
+                             ring + ((k + kGroupHaloStages - 1) % kGroupHaloStages) * kHaloStageBytes);
+            pf.next(g);
+            const int stage = i % a_stages;
+            mbar_wait(&empty[stage], ((i / a_stages) & 1) ^ 1);
+            tc_fence_after();
+            if (warp == 5) stamp(g, i, 11);
+            if (!(g.debug & 2)) {
+                const uint32_t hbase = ring + (k % kGroupHaloStages) * kHaloStageBytes + rowoff;
+                const uint32_t ta = tmem_base + 2 * NP + stage * a_cols + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll
+                for (int g4 = 0; g4 < 8; ++g4) {
+                    if (4 * g4 >= g.nchunks) break;
+                    uint32_t v[16];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int u = 4 * g4 + e;
+                        const uint32_t o0 = u < 16 ? uo0.o0[u] : uo1.o0[u - 16];
+                        const uint32_t o1 = u < 16 ? uo0.o1[u] : uo1.o1[u - 16];
+                        const uint2 lo = ld_shared_v2(hbase + o0);
+                        const uint2 hi = ld_shared_v2(hbase + o1);
+                        v[4 * e + 0] = lo.x;
+                        v[4 * e + 1] = lo.y;
+                        v[4 * e + 2] = hi.x;
+                        v[4 * e + 3] = hi.y;
+                    }
+                    tmem_st16(ta + 16 * g4, v);
+                }
+                tmem_st_wait();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (warp == 5) stamp(g, i, 12);
+            if (lane == 0) mbar_arrive(&full[stage]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 512);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// backward weights
+//   warp 0: MMA issuer, warps 1-4: final TMEM drain, warps 5-12: builders
+//   (builder warp 5 lane 0 also issues the dY TMA loads)
+constexpr int kWgThreads = 32 * 13;
+
+template <int NP>
+struct WgSmem {
+    static constexpr int kAtom = kTile * 128;               // 64 kc x 128 pixels
+    static constexpr int kA = 4 * kAtom;                     // kc rows up to 256
+    static constexpr int kB = (NP / 64) * kAtom;             // dY: NP channels x 128 pixels
+    static constexpr int kStage = kA + kB;
+    static constexpr int kStages = 2;
+    static constexpr int kHaloOff = kStages * kStage;
+    static constexpr int kBarOff = kHaloOff + kHaloStages * kHaloStageBytes;
+    static constexpr int kBytes = kBarOff + 128 + 1024;
+};
+
+template <int NP>
+__global__ void __launch_bounds__(kWgThreads, 1)
+    stem_wgrad_kernel(const __grid_constant__ CUtensorMap dymap, const __nv_bfloat16* __restrict__ x,
+                      float* __restrict__ partial, const __grid_constant__ StemArgs g) {
+    using L = WgSmem<NP>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+    uint64_t* empty = full + L::kStages;
+    uint64_t* done = empty + L::kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    const uint32_t halo0 = smem_u32(smem + L::kHaloOff);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mtiles = g.kcm / 128;
+    constexpr uint32_t kColsNeed = 2 * NP;  // up to 2 M tiles (kc <= 256)
+    constexpr uint32_t kCols = kColsNeed <= 32 ? 32 : kColsNeed <= 64 ? 64 : kColsNeed <= 128 ? 128
+                               : kColsNeed <= 256 ? 256 : 512;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < L::kStages; ++i) {
+            mbar_init(&full[i], kBuilders / 32 + 1);  // 8 builder warps + the TMA arrival
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(done, 1);
+        fence_barrier_init();
+        tma_prefetch(&dymap);
+    }
+    if (warp == 0) tmem_alloc(tmem_slot, kCols);
+    if (warp >= 5) {
+        // kc rows beyond 8*nchunks stay zero in every stage
+        const int b = threadIdx.x - 5 * 32;
+        for (int s = 0; s < L::kStages; ++s) {
+            const uint32_t a_base = smem_u32(smem + s * L::kStage);
+            for (int i = b; i < (4 * 8 - g.nchunks) * kTile; i += kBuilders) {
+                const int j = g.nchunks + i / kTile, p = i % kTile;
+                st_shared_v4(a_base + (j >> 3) * L::kAtom + p * 128 + (((j & 7) ^ (p & 7)) << 4),
+                             make_uint4(0u, 0u, 0u, 0u));
+            }
+        }
+        halo_zero_words(halo0, b);
+        fence_proxy_async_smem();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int my_tiles = blockIdx.x < g.total_tiles
+                             ? (g.total_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+    if (warp == 0) {
+        // ---------------- MMA issuer: D[kc][k] += A[kc][pix] . dY[k][pix] ---------
+        constexpr uint32_t idesc = idesc_bf16_f32(kTile, NP, true, true);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int i = 0; i < my_tiles; ++i) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t a_base = smem_u32(smem + stage * L::kStage);
+                const uint32_t b_base = a_base + L::kA;
+                for (int mt = 0; mt < mtiles; ++mt)
+#pragma unroll
+                    for (int k = 0; k < kTile / 16; ++k) {
+                        const uint64_t ad =
+                            umma_desc_sw128(a_base + mt * 2 * L::kAtom + k * 2048, L::kAtom, 1024);
+                        const uint64_t bd = umma_desc_sw128(b_base + k * 2048, L::kAtom, 1024);
+                        mma_bf16(tmem_base + mt * NP, ad, bd, idesc, (i | k) != 0);
+                    }
+                mma_commit(&empty[stage]);
+                if (i == my_tiles - 1) mma_commit(done);
+            }
+            __syncwarp();
+            if (++stage == L::kStages) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+    } else if (warp <= 4) {
+        // ---------------- drain: partial[cta][k][kc] ------------------------------
+        const int q = warp & 3;
+        if (my_tiles > 0) {
+            mbar_wait(done, 0);
+            tc_fence_after();
+        }
+        for (int mt = 0; mt < mtiles; ++mt) {
+            const int kc = mt * 128 + q * 32 + lane;
+#pragma unroll 1
+            for (int c0 = 0; c0 < NP; c0 += 16) {
+                uint32_t v[16];
+                if (my_tiles > 0) {
+                    tmem_ld16(tmem_base + mt * NP + c0 + (static_cast<uint32_t>(q * 32) << 16), v);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) v[e] = 0u;
+                }
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    if (c0 + e < g.K)
+                        partial[((size_t)blockIdx.x * g.K + c0 + e) * g.kcm + kc] =
+                            __uint_as_float(v[e]);
+            }
+        }
+    } else {
+        // ---------------- builders: A[kc][pix] (MN-major, 128B swizzle) + dY TMA ---
+        const int b = threadIdx.x - 5 * 32;
+        HaloSlots hs;
+        halo_slots(g, b, hs);
+        BuildPlan bp;
+        build_plan<true>(g, warp - 5, lane, bp);
+        for (int i = 0; i < kHaloStages - 1; ++i)
+            halo_issue(g, x, blockIdx.x + i * gridDim.x, hs, halo0 + i * kHaloStageBytes);
+        int stage = 0;
+        uint32_t phase = 0;
+        int i = 0;
+        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++i) {
+            cp_async_wait<kHaloStages - 2>();
+            named_sync(1, kBuilders);
+            halo_issue(g, x, t + (kHaloStages - 1) * gridDim.x, hs,
+                       halo0 + ((i + kHaloStages - 1) % kHaloStages) * kHaloStageBytes);
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sbase = smem + stage * L::kStage;
+            if (b == 0) {
+                int n, oy0, ox0;
+                tile_origin(g, t, n, oy0, ox0);
+                mbar_arrive_expect_tx(&full[stage], L::kB);
+#pragma unroll
+                for (int a = 0; a < NP / 64; ++a)
+                    tma_load_4d(smem_u32(sbase + L::kA + a * L::kAtom), &dymap, &full[stage], a * 64,
+                                ox0, oy0, n);
+            }
+            build_tile(bp, smem_u32(sbase), halo0 + (i % kHaloStages) * kHaloStageBytes);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[stage]);
+            if (++stage == L::kStages) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, kCols);
+    }
+}
+
+// dw[k][r][s][c] = sum over CTAs (fixed order) of partial[cta][k][tap*4 + c]
+__global__ void stem_wgrad_finish_kernel(const float* __restrict__ partial, int ctas, int K,
+                                         int kcm, int taps, int f_pitch, int C,
+                                         __nv_bfloat16* __restrict__ dw) {
+    const long long total = (long long)K * taps * f_pitch;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c = (int)(i % f_pitch);
+        const long long kt = i / f_pitch;
+        const int tap = (int)(kt % taps), k = (int)(kt / taps);
+        float acc = 0.0f;
+        if (c < C) {
+            const float* p = partial + (size_t)k * kcm + tap * 4 + c;
+            for (int s = 0; s < ctas; ++s) acc += p[(size_t)s * K * kcm];
+        }
+        dw[i] = __float2bfloat16_rn(acc);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host
+
+bool stem_args(const pk_conv_geom* g, StemArgs& a) {
+    if (g->groups != 1 || g->transpose || g->c > 4 || g->x_pitch != 8 || g->f_pitch != 8)
+        return false;
+    if (g->r * g->s > kMaxTaps || (g->k != 64 && g->k != 128) || g->y_pitch != g->k)
+        return false;
+    a = StemArgs{};
+    a.N = g->n;
+    a.H = g->h;
+    a.W = g->w;
+    a.x_pitch = g->x_pitch;
+    a.P = g->p;
+    a.Q = g->q;
+    a.K = g->k;
+    a.n_pad = g->k;
+    a.R = g->r;
+    a.S = g->s;
+    a.sh = g->str_h;
+    a.sw = g->str_w;
+    a.dh = g->dil_h;
+    a.dw = g->dil_w;
+    a.ph = g->pad_h;
+    a.pw = g->pad_w;
+    a.C = g->c;
+    a.tiles_w = (g->q + kBw - 1) / kBw;
+    a.tiles_h = (g->p + kBh - 1) / kBh;
+    a.total_tiles = a.tiles_w * a.tiles_h * g->n;
+    a.HH = (kBh - 1) * a.sh + (a.R - 1) * a.dh + 1;
+    a.HW = (kBw - 1) * a.sw + (a.S - 1) * a.dw + 1;
+    a.HWp = (a.HW + a.sw - 1) / a.sw;
+    if (a.HH * a.HW > kBuilders * kHaloPer || a.sw * a.HH * a.HWp * 8 > kHaloStageBytes - 8) return false;
+    a.taps = a.R * a.S;
+    a.nchunks = (a.taps + 1) / 2;
+    a.nchunks += a.nchunks & 1;
+    a.kcm = (a.nchunks * 8 + 127) / 128 * 128;
+    a.nbox = (a.HW * a.x_pitch + 255) / 256;
+    a.box_px = (a.HW + a.nbox - 1) / a.nbox;
+    a.box_px += a.box_px & 1;  // even pixel count: 16-byte multiple rows for any pitch
+    static const int dbg = [] {
+        const char* v = std::getenv("PK_STEM_DEBUG");
+        return v ? std::atoi(v) : 0;
+    }();
+    a.debug = dbg;
+    static unsigned long long* trace = [] {
+        unsigned long long* p = nullptr;
+        if (std::getenv("PK_STEM_TRACE")) cudaMalloc(&p, 32 * 32 * 8);
+        return p;
+    }();
+    a.trace = trace;
+    for (int t = 0; t < a.taps; ++t) {
+        const int r = t / a.S, s = t % a.S;
+        a.tap_off[t] = ((s * a.dw) % a.sw) * a.HH * a.HWp + r * a.dh * a.HWp + (s * a.dw) / a.sw;
+    }
+    return true;
+}
+
+template <typename Kern>
+cudaError_t set_smem(Kern kern, int bytes, int* attr_dev) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (*attr_dev != dev) {
+        const cudaError_t err =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (err != cudaSuccess) return err;
+        *attr_dev = dev;
+    }
+    return cudaSuccess;
+}
+
+template <int NP>
+cudaError_t launch_stem_fprop(const CUtensorMap& ymap, const CUtensorMap& xmap, const void* x,
+                              void* y, const void* w, const StemArgs& a, const pk_epilogue& e,
+                              cudaStream_t st) {
+    static int attr_dev = -1;
+    auto kern = stem_fprop_kernel<NP>;
+    const int bytes = FwdLayout(a.nchunks, NP).bytes;
+    if (bytes > 227 * 1024) return cudaErrorNotSupported;
+    cudaError_t err = set_smem(kern, 227 * 1024, &attr_dev);
+    if (err != cudaSuccess) return err;
+    int grid = num_sms_of_current_device();
+    if (a.total_tiles < grid) grid = a.total_tiles;
+    kern<<<grid, kFwdThreads, bytes, st>>>(ymap, xmap, (const __nv_bfloat16*)x, (__nv_bfloat16*)y,
+                                                         (const __nv_bfloat16*)w, a, e);
+    count_launch();
+    if (a.trace) {
+        unsigned long long h[32 * 32];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost);
+        const unsigned long long t0 = h[0];
+        for (int i = 0; i < 32; ++i) {
+            fprintf(stderr, "tile %2d:", i);
+            for (int e = 0; e < 13; ++e) fprintf(stderr, " %7lld", (long long)(h[i * 32 + e] - t0));
+            fprintf(stderr, " | mma:");
+            for (int e = 16; e < 17; ++e)
+                fprintf(stderr, " %5lld", (long long)(h[i * 32 + e] - h[i * 32 + 2]));
+            fprintf(stderr, "\n");
+        }
+    }
+    return cudaGetLastError();
+}
+
+int stem_wgrad_ctas(const StemArgs& a, int num_sms) {
+    if (num_sms > 148) num_sms = 148;  // workspace is sized for 148 partials
+    return a.total_tiles < num_sms ? a.total_tiles : num_sms;
+}
+
+template <int NP>
+cudaError_t launch_stem_wgrad(const CUtensorMap& dymap, const void* x, float* partial,
+                              const StemArgs& a, int ctas, cudaStream_t st) {
+    static int attr_dev = -1;
+    auto kern = stem_wgrad_kernel<NP>;
+    cudaError_t err = set_smem(kern, WgSmem<NP>::kBytes, &attr_dev);
+    if (err != cudaSuccess) return err;
+    kern<<<ctas, kWgThreads, WgSmem<NP>::kBytes, st>>>(dymap, (const __nv_bfloat16*)x, partial, a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace
+}  // namespace pk
+
+using namespace pk;
+
+extern "C" {
+
+int pk_cuda_stem_fused_supported(const pk_conv_geom* g) {
+    StemArgs a;
+    return stem_args(g, a) && tc::encode_fn() != nullptr;
+}
+
+cudaError_t pk_cuda_stem_fused_fprop(const pk_conv_geom* g, const void* x, const void* w, void* y,
+                                const pk_epilogue* epi, cudaStream_t st) {
+    StemArgs a;
+    if (!stem_args(g, a)) return cudaErrorNotSupported;
+    CUtensorMap ymap{};
+    // one epilogue warp stores 32 rows = 2 output rows of 16 pixels
+    if (!tc::make_map_nhwc(&ymap, y, g->n, g->p, g->q, g->y_pitch, kBw, 2, 1))
+        return cudaErrorNotSupported;
+    pk_epilogue e{};
+    e.act = -1;
+    if (epi) e = *epi;
+    CUtensorMap xmap{};
+    if (a.nbox * ((a.HH * a.box_px * 16 + 127) / 128 * 128) > kRawStageBytes ||
+        !tc::make_map_pixel_rows(&xmap, x, g->n, g->h, g->w, g->x_pitch, a.box_px * g->x_pitch, a.HH))
+        return cudaErrorNotSupported;
+    switch (g->k) {
+        case 64: return launch_stem_fprop<64>(ymap, xmap, x, y, w, a, e, st);
+        case 128: return launch_stem_fprop<128>(ymap, xmap, x, y, w, a, e, st);
+        default: return cudaErrorNotSupported;
+    }
+}
+
+size_t pk_cuda_stem_fused_wgrad_workspace(const pk_conv_geom* g, int num_sms) {
+    StemArgs a;
+    if (!stem_args(g, a)) return 0;
+    return (size_t)stem_wgrad_ctas(a, num_sms) * g->k * a.kcm * 4;
+}
+
+cudaError_t pk_cuda_stem_fused_wgrad(const pk_conv_geom* g, const void* dy, const void* x, void* dw,
+                                void* workspace, int num_sms, cudaStream_t st) {
+    StemArgs a;
+    if (!stem_args(g, a) || a.kcm > 256) return cudaErrorNotSupported;
+    CUtensorMap dymap{};
+    if (!tc::make_map_nhwc(&dymap, dy, g->n, g->p, g->q, g->y_pitch, kBw, kBh, 1))
+        return cudaErrorNotSupported;
+    const int ctas = stem_wgrad_ctas(a, num_sms);
+    float* partial = static_cast<float*>(workspace);
+    cudaError_t err;
+    switch (g->k) {
+        case 64: err = launch_stem_wgrad<64>(dymap, x, partial, a, ctas, st); break;
+        case 128: err = launch_stem_wgrad<128>(dymap, x, partial, a, ctas, st); break;
+        default: return cudaErrorNotSupported;
+    }
+    if (err != cudaSuccess) return err;
+    const long long total = (long long)g->k * a.taps * g->f_pitch;
+    const unsigned blocks = (unsigned)((total + 255) / 256);
+    stem_wgrad_finish_kernel<<<blocks, 256, 0, st>>>(partial, ctas, g->k, a.kcm, a.taps,
+                                                     g->f_pitch, g->c, (__nv_bfloat16*)dw);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // extern "C"

@@ -70,6 +70,23 @@ inline bool make_map_nhwc(CUtensorMap* map, const void* base, int n, int h, int 
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D bf16 view of an NHWC tensor as rows of pixels: dims {w*pitch, h, n},
+// box {box_elems, box_rows, 1}, no swizzle (plain rows of box_elems*2 bytes).
+// Used for narrow-channel halos, where a per-pixel (16-byte) inner box
+// dimension would make the TMA engine move 16 bytes per element.
+inline bool make_map_pixel_rows(CUtensorMap* map, const void* base, int n, int h, int w, int pitch,
+                                int box_elems, int box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || box_elems > 256 || box_rows > 256 || (box_elems * 2) % 16) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)w * pitch, (cuuint64_t)h, (cuuint64_t)n};
+    cuuint64_t strides[2] = {(cuuint64_t)w * pitch * 2, (cuuint64_t)h * w * pitch * 2};
+    cuuint32_t box[3] = {(cuuint32_t)box_elems, (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Rectangular tile (bw x bh x bn pixels, product `rows`, powers of two) that
 // covers an (n, h, w) output volume with the least padding.
 struct RectTile {

@@ -12,6 +12,7 @@
 //              Im2colGemm   SIMT GEMM + col2im / image   igemm_tc_dgrad
 //   BwdWeights Direct       direct_bwd_weights           direct_bwd_weights
 //              Im2colGemm   im2col + SIMT GEMM / image   igemm_tc_wgrad (split-K)
+#include <cstdlib>
 #include <cstring>
 
 #include "../cuda/kernels.h"
@@ -160,7 +161,19 @@ pk_conv_geom gemm_geom(long long rows, int kred, int kout) {
     return m;
 }
 
+// Fused stem kernels (halo staged in smem, operand expanded on chip):
+// forward and backward-weights. PK_STEM_FUSED=0 selects the packing path.
+bool stem_fused(const pk_conv_geom& g, ConvDirection dir) {
+    static const bool enabled = [] {
+        const char* v = std::getenv("PK_STEM_FUSED");
+        return !(v && v[0] == '0');
+    }();
+    return enabled && dir != ConvDirection::BackwardData && pk_cuda_stem_fused_supported(&g);
+}
+
 std::size_t stem_workspace(const pk_conv_geom& g, ConvDirection dir) {
+    if (stem_fused(g, dir))
+        return dir == ConvDirection::Forward ? 0 : pk_cuda_stem_fused_wgrad_workspace(&g, 148);
     const std::size_t kcp = pk_stem_kc_pitch(&g);
     const std::size_t rows = (std::size_t)g.n * g.p * g.q;
     const std::size_t col = align256(rows * kcp * 2);
@@ -181,6 +194,13 @@ void run_stem(const pk_conv_geom& g, ConvDirection dir, const void* a, const voi
     const long long rows = (long long)g.n * g.p * g.q;
     char* col = static_cast<char*>(ws);
     char* aux = col + align256((std::size_t)rows * kcp * 2);
+    if (stem_fused(g, dir)) {
+        if (dir == ConvDirection::Forward)
+            ck(pk_cuda_stem_fused_fprop(&g, a, b, out, epi, st), "stem_fused_fprop");
+        else
+            ck(pk_cuda_stem_fused_wgrad(&g, a, b, out, ws, num_sms, st), "stem_fused_wgrad");
+        return;
+    }
     if (dir == ConvDirection::Forward) {
         // y = col . Wp^T
         ck(pk_cuda_im2col_pack(&g, a, col, st), "im2col_pack");
@@ -280,7 +300,7 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                 // measured faster (1.28 ms) than 16-byte-row TMA boxes
                 // (1.69 ms) for ResNet conv1 at N=256.
                 if (stem_eligible(g, dt, epi)) {
-                    kernel = "stem_pack+gemm_tc";
+                    kernel = stem_fused(g, dir) ? "stem_fused_tc" : "stem_pack+gemm_tc";
                     run_stem(g, dir, a, b, out, ws, epi, h.num_sms(), st);
                 } else if (dt == PK_BF16 && pk_tc_fwd_supported(&g)) {
                     kernel = "igemm_tc_fwd";
@@ -375,7 +395,7 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
             kernel = "direct_simt_bwd_weights";
             ck(pk_cuda_direct_bwd_weights(&g, dt, a, b, out, st), "direct_bwd_weights");
         } else if (stem_eligible(g, dt, nullptr)) {
-            kernel = "stem_pack+wgrad_tc";
+            kernel = stem_fused(g, dir) ? "stem_fused_wgrad_tc" : "stem_pack+wgrad_tc";
             run_stem(g, dir, a, b, out, ws, nullptr, h.num_sms(), st);
         } else if (dt == PK_BF16 && pk_tc_wgrad_supported(&g)) {
             kernel = "igemm_tc_wgrad";
