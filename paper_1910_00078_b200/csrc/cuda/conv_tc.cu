@@ -281,20 +281,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int kb = 0; kb < ti.nkb; ++kb) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
-                if (lane == 0) {
+                {
                     fence_proxy_async_smem();
                     const uint32_t a_base = smem_u32(smem + stage * L::kStage);
                     const uint32_t b_base = a_base + L::kA;
-#pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {
-                        const uint64_t ad = umma_desc_sw128(a_base + k * 32, 16, 1024);
-                        const uint64_t bd = umma_desc_sw128(b_base + k * 32, 16, 1024);
-                        mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
-                    }
-                    mma_commit(&empty[stage]);
-                    if (kb == ti.nkb - 1) mma_commit(&tmem_full[a]);
+                    const uint64_t ad0 = umma_desc_sw128(a_base, 16, 1024);
+                    const uint64_t bd0 = umma_desc_sw128(b_base, 16, 1024);
+                    mma4_bf16(d_tmem, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + 2, bd0 + 4, bd0 + 6,
+                              idesc, kb != 0);
+                    mma_commit_elect(&empty[stage]);
+                    if (kb == ti.nkb - 1) mma_commit_elect(&tmem_full[a]);
                 }
-                __syncwarp();
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;

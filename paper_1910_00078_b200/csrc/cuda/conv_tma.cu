@@ -213,23 +213,22 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
             for (int kb = 0; kb < nkb; ++kb) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
-                if (lane == 0) {
+                {
+                    // whole warp: 4 MMAs per asm block (elect inside); descriptor
+                    // start fields advance by byte offset >> 4
                     const uint32_t a_base = smem_u32(smem + stage * L::kStage);
                     const uint32_t b_base = a_base + L::kA;
-#pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {
-                        // NARROW: K step k covers boxes 2k, 2k+1 (2 KB apart, LBO),
-                        // 16-row core-matrix groups are 128 B apart (SBO)
-                        const uint64_t ad =
-                            NARROW ? umma_desc_noswz(a_base + k * 2 * (L::kA / 8), L::kA / 8, 128)
-                                   : umma_desc_sw128(a_base + k * 32, 16, 1024);
-                        const uint64_t bd = umma_desc_sw128(b_base + k * 32, 16, 1024);
-                        mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
-                    }
-                    mma_commit(&empty[stage]);
-                    if (kb == nkb - 1) mma_commit(&tmem_full[a]);
+                    // NARROW: K step k covers boxes 2k, 2k+1 (2 KB apart, LBO),
+                    // 16-row core-matrix groups are 128 B apart (SBO)
+                    const uint64_t ad0 = NARROW ? umma_desc_noswz(a_base, L::kA / 8, 128)
+                                                : umma_desc_sw128(a_base, 16, 1024);
+                    const uint64_t bd0 = umma_desc_sw128(b_base, 16, 1024);
+                    constexpr uint64_t as = NARROW ? (2 * (L::kA / 8)) >> 4 : 2;
+                    mma4_bf16(d_tmem, ad0, ad0 + as, ad0 + 2 * as, ad0 + 3 * as, bd0, bd0 + 2, bd0 + 4,
+                              bd0 + 6, idesc, kb != 0);
+                    mma_commit_elect(&empty[stage]);
+                    if (kb == nkb - 1) mma_commit_elect(&tmem_full[a]);
                 }
-                __syncwarp();
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
@@ -477,19 +476,17 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         for (int kb = kb_begin; kb < kb_end; ++kb) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            if (lane == 0) {
+            {
                 const uint32_t a_base = smem_u32(smem + stage * L::kStage);
                 const uint32_t b_base = a_base + L::kA;
-#pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                    const uint64_t ad = umma_desc_sw128(a_base + k * 2048, L::kAtom, 1024);
-                    const uint64_t bd = umma_desc_sw128(b_base + k * 2048, L::kAtom, 1024);
-                    mma_bf16(tmem_base, ad, bd, idesc, (kb != kb_begin) || (k != 0));
-                }
-                mma_commit(&empty[stage]);
-                if (kb == kb_end - 1) mma_commit(tmem_full);
+                const uint64_t ad0 = umma_desc_sw128(a_base, L::kAtom, 1024);
+                const uint64_t bd0 = umma_desc_sw128(b_base, L::kAtom, 1024);
+                constexpr uint64_t ks = 2048 >> 4;  // 16 MN-major K rows
+                mma4_bf16(tmem_base, ad0, ad0 + ks, ad0 + 2 * ks, ad0 + 3 * ks, bd0, bd0 + ks,
+                          bd0 + 2 * ks, bd0 + 3 * ks, idesc, kb != kb_begin);
+                mma_commit_elect(&empty[stage]);
+                if (kb == kb_end - 1) mma_commit_elect(tmem_full);
             }
-            __syncwarp();
             if (++stage == STAGES) {
                 stage = 0;
                 phase ^= 1;

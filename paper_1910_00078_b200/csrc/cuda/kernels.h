@@ -152,6 +152,10 @@ int pk_cuda_stem_fused_supported(const pk_conv_geom* g);
 cudaError_t pk_cuda_stem_fused_fprop(const pk_conv_geom* g, const void* x, const void* w, void* y,
                                      const pk_epilogue* epi, cudaStream_t st);
 size_t pk_cuda_stem_fused_wgrad_workspace(const pk_conv_geom* g, int num_sms);
+// backward data (gather formulation; dY channels K == 64): no workspace
+int pk_cuda_stem_fused_dgrad_supported(const pk_conv_geom* g);
+cudaError_t pk_cuda_stem_fused_dgrad(const pk_conv_geom* g, const void* dy, const void* w, void* dx,
+                                     cudaStream_t st);
 cudaError_t pk_cuda_stem_fused_wgrad(const pk_conv_geom* g, const void* dy, const void* x,
                                      void* dw, void* workspace, int num_sms, cudaStream_t st);
 

@@ -52,7 +52,6 @@ struct StemArgs {
     int kcm;                  // wgrad: padded kc rows (multiple of 128)
     unsigned long long* trace;  // PK_STEM_TRACE: per-role clock64 stamps of CTA 0 (profiling only)
     int debug;                // PK_STEM_DEBUG bits (profiling only): 1 no MMA, 2 no build, 4 no store, 8 no TMEM drain, 16 no halo
-    int box_px, nbox;         // halo TMA: boxes of box_px pixels per halo row
     int tap_off[kMaxTaps];    // halo word offset of tap t
 };
 
@@ -219,51 +218,6 @@ __device__ __forceinline__ void halo_zero_words(uint32_t halo0, int b) {
     if (b < kHaloStages) st_shared_v2(halo0 + b * kHaloStageBytes + kHaloZero, make_uint2(0u, 0u));
 }
 
-// ---------------------------------------------------------------------------
-// TMA-fed halo: one elected thread loads the input halo of a tile as sw
-// column-phase boxes (traversal stride sw, out-of-bounds zero fill = the
-// convolution padding) into a raw ring of 16-byte pixels; the builders then
-// compact it to 8-byte (4-channel) pixels so operand gathers hit consecutive
-// 8-byte words.
-constexpr int kRawStages = 4;
-constexpr int kRawStageBytes = 16384;
-constexpr int kCompactBytes = kHaloStageBytes;  // 2 compact buffers
-
-__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
-    uint4 v;
-    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "r"(addr));
-    return v;
-}
-
-__device__ __forceinline__ void halo_tma(const StemArgs& g, const CUtensorMap* xmap, int t,
-                                         uint32_t raw_u, uint64_t* bar) {
-    int n, oy0, ox0;
-    tile_origin(g, t, n, oy0, ox0);
-    const int iy0 = oy0 * g.sh - g.ph, ix0 = ox0 * g.sw - g.pw;
-    // raw [box][row][box_px pixels x 16 B]; box destinations 128-byte aligned
-    const int bstride = (g.HH * g.box_px * 16 + 127) / 128 * 128;
-    mbar_arrive_expect_tx(bar, g.nbox * g.HH * g.box_px * 16);
-    for (int bx = 0; bx < g.nbox; ++bx)
-        tma_load_3d(raw_u + bx * bstride, xmap, bar, (ix0 + bx * g.box_px) * g.x_pitch, iy0, n);
-}
-
-// raw halo pixel (row, col) 16 B -> compact [col % sw][row][col / sw] 8 B
-// (channels 0-3, column-phase split)
-__device__ __forceinline__ void halo_compact(const StemArgs& g, uint32_t raw_u, uint32_t cmp_u, int b) {
-    const int per_box = g.HH * g.box_px, total = g.nbox * per_box;
-    const int bstride = (per_box * 16 + 127) / 128 * 128;
-    for (int i = b; i < total; i += kBuilders) {
-        const int bx = i / per_box, rem = i - bx * per_box;
-        const int row = rem / g.box_px, col = bx * g.box_px + (rem - row * g.box_px);
-        if (col >= g.HW) continue;
-        const uint4 v = ld_shared_v4(raw_u + bx * bstride + rem * 16);
-        const int ph = col % g.sw, idx = col / g.sw;
-        st_shared_v2(cmp_u + ((ph * g.HH + row) * g.HWp + idx) * 8, make_uint2(v.x, v.y));
-    }
-}
-
 // Halo byte offsets (relative to the pixel's row base) of the two taps of each
 // unit this warp expands: units [u0, u0 + 16); invalid taps -> the zero word.
 struct UnitOffsets {
@@ -331,14 +285,6 @@ __device__ __forceinline__ void mma4_bf16_ts(uint32_t tmem_d, uint32_t a0, uint3
         : "memory");
 }
 
-__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
-            smem_u32(bar))
-        : "memory");
-}
 
 // Two builder groups (4 warps each, one per TMEM lane quarter) alternate
 // tiles, so two independent halo -> operand chains are in flight; each group
@@ -420,11 +366,10 @@ __device__ __forceinline__ void group_halo_issue(const StemArgs& g, const __nv_b
 
 // smem: resident filter (SW128 K-major), halo ring, epilogue staging, barriers
 struct FwdLayout {
-    int raw_off, halo_off, stg_off, bar_off, bytes;
+    int halo_off, stg_off, bar_off, bytes;
     __host__ __device__ FwdLayout(int nchunks, int np) {
         const int atoms = (nchunks + 7) / 8;
-        raw_off = atoms * np * 128;  // (unused)
-        halo_off = raw_off;
+        halo_off = atoms * np * 128;
         stg_off = halo_off + 2 * kGroupHaloStages * kHaloStageBytes;
         bar_off = stg_off + 4 * 2 * 4096;  // 4 epilogue warps x 2 staging buffers
         bytes = bar_off + 256 + 1024;
@@ -433,8 +378,7 @@ struct FwdLayout {
 
 template <int NP>
 __global__ void __launch_bounds__(kFwdThreads, 1)
-    stem_fprop_kernel(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap xmap,
-                      const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+    stem_fprop_kernel(const __grid_constant__ CUtensorMap ymap, const __nv_bfloat16* __restrict__ x,
                       const __nv_bfloat16* __restrict__ w, const __grid_constant__ StemArgs g,
                       const pk_epilogue epi) {
     const FwdLayout L(g.nchunks, NP);
@@ -445,11 +389,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     uint64_t* empty = full + kMaxAStages;
     uint64_t* tmem_full = empty + kMaxAStages;
     uint64_t* tmem_empty = tmem_full + 2;
-    uint64_t* raw_full = tmem_empty + 2;
-    uint64_t* raw_empty = raw_full + kRawStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + kRawStages);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
     const uint32_t halo0 = smem_u32(smem + L.halo_off);
-    const uint32_t raw0 = smem_u32(smem + L.raw_off);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // TMEM columns: [0, 2*NP) accumulators, then A stages of 4 columns per unit
     const int a_cols = (g.nchunks + 3) / 4 * 16;  // whole 4-unit (16-column) store groups
@@ -465,13 +406,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             mbar_init(&tmem_full[i], 1);
             mbar_init(&tmem_empty[i], 4);
         }
-        for (int i = 0; i < kRawStages; ++i) {
-            mbar_init(&raw_full[i], 1);
-            mbar_init(&raw_empty[i], kBuilders / 32);
-        }
         fence_barrier_init();
         tma_prefetch(&ymap);
-        tma_prefetch(&xmap);
     }
     if (warp == 0) tmem_alloc(tmem_slot, 512);
     if (warp >= 5) {
@@ -750,21 +686,23 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         for (int i = 0; i < my_tiles; ++i) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            if (lane == 0) {
+            {
                 const uint32_t a_base = smem_u32(smem + stage * L::kStage);
                 const uint32_t b_base = a_base + L::kA;
-                for (int mt = 0; mt < mtiles; ++mt)
+                constexpr uint64_t ks = 2048 >> 4;  // 16 MN-major K rows (pixels)
+                const uint64_t bd0 = umma_desc_sw128(b_base, L::kAtom, 1024);
+                for (int mt = 0; mt < mtiles; ++mt) {
+                    const uint64_t ad0 = umma_desc_sw128(a_base + mt * 2 * L::kAtom, L::kAtom, 1024);
 #pragma unroll
-                    for (int k = 0; k < kTile / 16; ++k) {
-                        const uint64_t ad =
-                            umma_desc_sw128(a_base + mt * 2 * L::kAtom + k * 2048, L::kAtom, 1024);
-                        const uint64_t bd = umma_desc_sw128(b_base + k * 2048, L::kAtom, 1024);
-                        mma_bf16(tmem_base + mt * NP, ad, bd, idesc, (i | k) != 0);
-                    }
-                mma_commit(&empty[stage]);
-                if (i == my_tiles - 1) mma_commit(done);
+                    for (int k = 0; k < kTile / 16; k += 4)
+                        mma4_bf16(tmem_base + mt * NP, ad0 + k * ks, ad0 + (k + 1) * ks,
+                                  ad0 + (k + 2) * ks, ad0 + (k + 3) * ks, bd0 + k * ks,
+                                  bd0 + (k + 1) * ks, bd0 + (k + 2) * ks, bd0 + (k + 3) * ks, idesc,
+                                  (i | k) != 0);
+                }
+                mma_commit_elect(&empty[stage]);
+                if (i == my_tiles - 1) mma_commit_elect(done);
             }
-            __syncwarp();
             if (++stage == L::kStages) {
                 stage = 0;
                 phase ^= 1;
@@ -862,6 +800,309 @@ __global__ void stem_wgrad_finish_kernel(const float* __restrict__ partial, int 
 }
 
 // ---------------------------------------------------------------------------
+// backward data (gather formulation, deterministic, no column matrix in HBM)
+//
+// A CTA owns a TY x TX rectangle of dX. The dY pixels whose taps reach it form
+// an HY x WX halo (11 x 19 for conv1 at 16 x 32), loaded by one TMA box as the
+// K-major A operand (K = the 64 dY channels). Two M=128 MMAs against the
+// resident packed filter B[kc][k] (kc = tap*4 + c) give the column block
+// colg[dY pixel][tap, c] in TMEM; 4 warps drain it to shared memory (fp32,
+// compact tap*C + c, odd row stride: conflict-free), then 8 warps gather each
+// dX pixel's taps (only those whose stride phase matches) and store 16-byte
+// pixels. MMA of the next tile overlaps the gather.
+//   warp 0: TMA producer + MMA issuer; warps 1-8: drain (1-4) + gather (1-8)
+constexpr int kDgThreads = 32 * 9;
+
+struct DgArgs {
+    int N, H, W, x_pitch, P, Q, K;
+    int R, S, sh, sw, dh, dw, ph, pw, C, taps;
+    int TY, TX, HY, WX;         // dX tile, dY halo box
+    int oy_lo0, ox_lo0;         // halo origin for tile (0, 0): oy_lo(Y0) = Y0/sh + oy_lo0
+    int tiles_w, tiles_h, total_tiles;
+    int npad;                   // MMA N = roundup(taps*4, 16)
+    int cstride;                // colg row stride (words, odd)
+    unsigned long long* trace;  // PK_STEM_TRACE (profiling only)
+};
+__device__ __forceinline__ void dstamp(const DgArgs& g, int it, int ev) {
+    if (g.trace && blockIdx.x == 0 && it < 32 && (threadIdx.x & 31) == 0)
+        g.trace[it * 32 + ev] = clock64();
+}
+
+struct DgLayout {
+    int a_stage, b_off, colg_off, bar_off, bytes;
+    __host__ __device__ DgLayout(const DgArgs& g) {
+        a_stage = 2 * kTile * 128;                 // 2 M tiles of 128 halo pixels x 64 ch
+        b_off = 2 * a_stage;                        // double-buffered A
+        colg_off = b_off + g.npad * 128;
+        bar_off = colg_off + (g.HY * g.WX * g.cstride * 4 + 1023) / 1024 * 1024;
+        bytes = bar_off + 128 + 1024;
+    }
+};
+
+__device__ __forceinline__ void st_shared_f32(uint32_t addr, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ float ld_shared_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ void dg_tile(const DgArgs& g, int t, int& n, int& Y0, int& X0) {
+    const int tx = t % g.tiles_w, rest = t / g.tiles_w;
+    Y0 = (rest % g.tiles_h) * g.TY;
+    n = rest / g.tiles_h;
+    X0 = tx * g.TX;
+}
+
+// C: input channels (<= 4); KR/KS/KSH/KSW: compile-time filter size and
+// stride (0 = runtime values from g) so the ResNet conv1 gather unrolls.
+template <int C, int KR, int KS, int KSH, int KSW>
+__global__ void __launch_bounds__(kDgThreads, 1)
+    stem_dgrad_kernel(const __grid_constant__ CUtensorMap dymap, const __nv_bfloat16* __restrict__ w,
+                      __nv_bfloat16* __restrict__ dx, const __grid_constant__ DgArgs g) {
+    const DgLayout L(g);
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+    uint64_t* a_empty = a_full + 2;
+    uint64_t* tmem_full = a_empty + 2;
+    uint64_t* tmem_empty = tmem_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+    const uint32_t colg_u = smem_u32(smem + L.colg_off);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&a_full[i], 1);
+            mbar_init(&a_empty[i], 1);
+        }
+        mbar_init(tmem_full, 1);
+        mbar_init(tmem_empty, 4);
+        fence_barrier_init();
+        tma_prefetch(&dymap);
+    }
+    if (warp == 0) tmem_alloc(tmem_slot, 512);
+    // packed filter B[kc][k] (kc = tap*4 + c, K-major SWIZZLE_128B, 64 k = one atom)
+    for (int i = threadIdx.x; i < g.npad * 8; i += blockDim.x) {
+        const int kc = i >> 3, j = i & 7;  // 16-byte unit j = k 8j..8j+7
+        const int tap = kc >> 2, c = kc & 3;
+        __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int k = j * 8 + e;
+            v[e] = (tap < g.taps && c < g.C && k < g.K)
+                       ? w[((size_t)k * g.taps + tap) * g.x_pitch + c]
+                       : __float2bfloat16_rn(0.0f);
+        }
+        st_shared_v4(smem_u32(smem + L.b_off) + kc * 128 + ((j ^ (kc & 7)) << 4),
+                     *reinterpret_cast<const uint4*>(v));
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer + MMA issuer --------------------------------
+        constexpr int kBoxBytes = 0;  // (unused)
+        (void)kBoxBytes;
+        const uint32_t box_bytes = g.HY * g.WX * 128;
+        const uint32_t idesc = idesc_bf16_f32(kTile, g.npad, false, false);
+        const uint64_t bd0 = umma_desc_sw128(smem_u32(smem + L.b_off), 16, 1024);
+        auto load = [&](int tt, int buf) {
+            int n, Y0, X0;
+            dg_tile(g, tt, n, Y0, X0);
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&a_full[buf], box_bytes);
+                tma_load_4d(smem_u32(smem + buf * L.a_stage), &dymap, &a_full[buf], 0,
+                            X0 / g.sw + g.ox_lo0, Y0 / g.sh + g.oy_lo0, n);
+            }
+        };
+        if (blockIdx.x < g.total_tiles) load(blockIdx.x, 0);
+        int i = 0;
+        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++i) {
+            const int buf = i & 1;
+            // prefetch tile i+1 once the MMA of tile i-1 released its buffer
+            if (t + (int)gridDim.x < g.total_tiles) {
+                if (i >= 1) mbar_wait(&a_empty[buf ^ 1], ((i - 1) >> 1) & 1);
+                load(t + gridDim.x, buf ^ 1);
+            }
+            dstamp(g, i, 0);
+            mbar_wait(&a_full[buf], (i >> 1) & 1);
+            dstamp(g, i, 1);
+            mbar_wait(tmem_empty, (i & 1) ^ 1);
+            dstamp(g, i, 2);
+            tc_fence_after();
+            const uint64_t ad0 = umma_desc_sw128(smem_u32(smem + buf * L.a_stage), 16, 1024);
+            for (int mt = 0; mt * kTile < g.HY * g.WX; ++mt) {
+                const uint64_t am = ad0 + (uint64_t)(mt * (kTile * 128 / 16));
+                mma4_bf16(tmem_base + mt * g.npad, am, am + 2, am + 4, am + 6, bd0, bd0 + 2, bd0 + 4,
+                          bd0 + 6, idesc, 0);
+            }
+            mma_commit_elect(&a_empty[buf]);
+            mma_commit_elect(tmem_full);
+            dstamp(g, i, 3);
+            __syncwarp();
+        }
+    } else {
+        // ---------------- drain (warps 1-4) + gather (warps 1-8) -------------------
+        const int rows = g.HY * g.WX;
+        const int gt = threadIdx.x - 32;  // 0..255
+        int i = 0;
+        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++i) {
+            int n, Y0, X0;
+            dg_tile(g, t, n, Y0, X0);
+            {
+                // 8 drain warps: lane quarter q = warp % 4, column chunks split in two
+                const int q = warp & 3, half = (warp - 1) >> 2;
+                const int nch = g.npad / 16, ch0 = half ? (nch + 1) / 2 : 0,
+                          ch1 = half ? nch : (nch + 1) / 2;
+                if (warp == 1) dstamp(g, i, 4);
+                mbar_wait(tmem_full, i & 1);
+                if (warp == 1) dstamp(g, i, 5);
+                tc_fence_after();
+                // colg rows hold all npad/4 taps (the padding taps are never read),
+                // so every chunk stores 4 taps x C values at immediate offsets
+                for (int mt = 0; mt * kTile < rows; ++mt) {
+                    const int row = mt * kTile + q * 32 + lane;
+                    const uint32_t dst = colg_u + row * g.cstride * 4;
+                    const bool live = row < rows;
+                    int cb = ch0;
+#pragma unroll 1
+                    for (; cb + 2 <= ch1; cb += 2) {
+                        uint32_t v[32];
+                        const uint32_t ta = tmem_base + mt * g.npad + cb * 16 +
+                                            (static_cast<uint32_t>(q * 32) << 16);
+                        tmem_ld16(ta, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+                        tmem_ld16(ta + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+                        tmem_ld_wait();
+                        if (live) {
+                            const uint32_t d = dst + cb * 4 * C * 4;
+#pragma unroll
+                            for (int e = 0; e < 32; ++e)
+                                if ((e & 3) < C) st_shared_f32(d + ((e >> 2) * C + (e & 3)) * 4, __uint_as_float(v[e]));
+                        }
+                    }
+                    if (cb < ch1) {
+                        uint32_t v[16];
+                        tmem_ld16(tmem_base + mt * g.npad + cb * 16 + (static_cast<uint32_t>(q * 32) << 16), v);
+                        tmem_ld_wait();
+                        if (live) {
+                            const uint32_t d = dst + cb * 4 * C * 4;
+#pragma unroll
+                            for (int e = 0; e < 16; ++e)
+                                if ((e & 3) < C) st_shared_f32(d + ((e >> 2) * C + (e & 3)) * 4, __uint_as_float(v[e]));
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0 && warp <= 4) {
+                    // tmem_empty counts 4 arrivals: one per quarter pair after both drained
+                }
+            }
+            if (warp == 1) dstamp(g, i, 6);
+            named_sync(1, 256);  // colg of tile i complete (all TMEM reads done too)
+            if (warp == 1) dstamp(g, i, 7);
+            if (warp <= 4 && lane == 0) mbar_arrive(tmem_empty);
+            const int oy_lo = Y0 / g.sh + g.oy_lo0, ox_lo = X0 / g.sw + g.ox_lo0;
+            const int TX = g.TX, npx = g.TY * TX;
+            const int sh = KSH ? KSH : g.sh, sw = KSW ? KSW : g.sw, R = KR ? KR : g.R,
+                      S = KS ? KS : g.S;
+            const int WX = g.WX, cs4 = g.cstride * 4;
+            for (int px = gt; px < npx; px += 256) {
+                const int iy = Y0 + px / TX, ix = X0 + px % TX;
+                if (iy >= g.H || ix >= g.W) continue;
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                // taps reaching (iy, ix): r = r0, r0 + sh, ... (dil 1) with dY row
+                // (iy + ph - r) / sh, i.e. one halo row up per step; dY outside the
+                // image is zero in the halo box, so no bounds checks
+                const int r0 = (iy + g.ph) % sh, s0 = (ix + g.pw) % sw;
+                const int lr = (iy + g.ph - r0) / sh - oy_lo, lc = (ix + g.pw - s0) / sw - ox_lo;
+                uint32_t rowa = colg_u + (lr * WX + lc) * cs4 + (r0 * S + s0) * C * 4;
+                if (KR) {
+                    // compile-time geometry: fixed trip counts, predicated tail taps
+                    constexpr int NR = KR ? (KR + KSH - 1) / KSH : 1, NS = KS ? (KS + KSW - 1) / KSW : 1;
+#pragma unroll
+                    for (int ri = 0; ri < NR; ++ri) {
+                        const bool rok = r0 + ri * KSH < KR;
+#pragma unroll
+                        for (int si = 0; si < NS; ++si) {
+                            const bool ok = rok && s0 + si * KSW < KS;
+                            const uint32_t a = rowa + ri * (KSH * KS * C * 4 - WX * cs4) +
+                                               si * (KSW * C * 4 - cs4);
+#pragma unroll
+                            for (int c = 0; c < C; ++c)
+                                if (ok) acc[c] += ld_shared_f32(a + c * 4);
+                        }
+                    }
+                } else {
+                    for (int r = r0; r < R; r += sh) {
+                        uint32_t a = rowa;
+                        for (int s = s0; s < S; s += sw) {
+#pragma unroll
+                            for (int c = 0; c < C; ++c) acc[c] += ld_shared_f32(a + c * 4);
+                            a += sw * C * 4 - cs4;  // next tap in the row: one halo pixel left
+                        }
+                        rowa += sh * S * C * 4 - WX * cs4;  // next tap row: one halo row up
+                    }
+                }
+                __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) o[c] = __float2bfloat16_rn(c < 4 ? acc[c & 3] : 0.0f);
+                *reinterpret_cast<uint4*>(dx + (((size_t)n * g.H + iy) * g.W + ix) * g.x_pitch) =
+                    *reinterpret_cast<const uint4*>(o);
+            }
+            if (warp == 1) dstamp(g, i, 8);
+            named_sync(1, 256);  // colg free for tile i+1
+            if (warp == 1) dstamp(g, i, 9);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 512);
+    }
+}
+
+__host__ __device__ inline int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+bool dg_args(const pk_conv_geom* g, DgArgs& a) {
+    if (g->groups != 1 || g->transpose || g->c > 4 || g->x_pitch != 8 || g->f_pitch != 8 ||
+        g->k != 64 || g->y_pitch != 64 || g->r * g->s > kMaxTaps || g->dil_h != 1 || g->dil_w != 1)
+        return false;
+    a = DgArgs{};
+    a.N = g->n; a.H = g->h; a.W = g->w; a.x_pitch = g->x_pitch; a.P = g->p; a.Q = g->q; a.K = g->k;
+    a.R = g->r; a.S = g->s; a.sh = g->str_h; a.sw = g->str_w; a.dh = g->dil_h; a.dw = g->dil_w;
+    a.ph = g->pad_h; a.pw = g->pad_w; a.C = g->c; a.taps = g->r * g->s;
+    a.npad = (a.taps * 4 + 15) / 16 * 16;
+    if (2 * a.npad > 512) return false;
+    a.cstride = ((a.npad / 4) * a.C) | 1;  // all padded taps stored; odd: conflict-free
+    static const int cand[][2] = {{16, 32}, {8, 32}, {16, 16}, {8, 16}, {8, 8}, {4, 8}};
+    for (const auto& c : cand) {
+        const int TY = c[0], TX = c[1];
+        if (TY % a.sh || TX % a.sw) continue;
+        // dY rows reaching dX rows [Y0, Y0 + TY) for Y0 = 0 (pattern repeats every tile)
+        const int lo_y = -floor_div(-(a.ph - (a.R - 1) * a.dh), a.sh);  // ceil
+        const int hi_y = floor_div(TY - 1 + a.ph, a.sh);
+        const int lo_x = -floor_div(-(a.pw - (a.S - 1) * a.dw), a.sw);
+        const int hi_x = floor_div(TX - 1 + a.pw, a.sw);
+        const int HY = hi_y - lo_y + 1, WX = hi_x - lo_x + 1;
+        if (HY * WX > 2 * kTile || HY > 256 || WX > 256) continue;
+        a.TY = TY; a.TX = TX; a.HY = HY; a.WX = WX; a.oy_lo0 = lo_y; a.ox_lo0 = lo_x;
+        a.tiles_w = (a.W + TX - 1) / TX;
+        a.tiles_h = (a.H + TY - 1) / TY;
+        a.total_tiles = a.tiles_w * a.tiles_h * a.N;
+        return DgLayout(a).bytes <= 227 * 1024;
+    }
+    return false;
+}
+
+// ---------------------------------------------------------------------------
 // host
 
 bool stem_args(const pk_conv_geom* g, StemArgs& a) {
@@ -898,9 +1139,6 @@ bool stem_args(const pk_conv_geom* g, StemArgs& a) {
     a.nchunks = (a.taps + 1) / 2;
     a.nchunks += a.nchunks & 1;
     a.kcm = (a.nchunks * 8 + 127) / 128 * 128;
-    a.nbox = (a.HW * a.x_pitch + 255) / 256;
-    a.box_px = (a.HW + a.nbox - 1) / a.nbox;
-    a.box_px += a.box_px & 1;  // even pixel count: 16-byte multiple rows for any pitch
     static const int dbg = [] {
         const char* v = std::getenv("PK_STEM_DEBUG");
         return v ? std::atoi(v) : 0;
@@ -933,8 +1171,7 @@ cudaError_t set_smem(Kern kern, int bytes, int* attr_dev) {
 }
 
 template <int NP>
-cudaError_t launch_stem_fprop(const CUtensorMap& ymap, const CUtensorMap& xmap, const void* x,
-                              void* y, const void* w, const StemArgs& a, const pk_epilogue& e,
+cudaError_t launch_stem_fprop(const CUtensorMap& ymap, const void* x, const void* w, const StemArgs& a, const pk_epilogue& e,
                               cudaStream_t st) {
     static int attr_dev = -1;
     auto kern = stem_fprop_kernel<NP>;
@@ -944,7 +1181,7 @@ cudaError_t launch_stem_fprop(const CUtensorMap& ymap, const CUtensorMap& xmap, 
     if (err != cudaSuccess) return err;
     int grid = num_sms_of_current_device();
     if (a.total_tiles < grid) grid = a.total_tiles;
-    kern<<<grid, kFwdThreads, bytes, st>>>(ymap, xmap, (const __nv_bfloat16*)x, (__nv_bfloat16*)y,
+    kern<<<grid, kFwdThreads, bytes, st>>>(ymap, (const __nv_bfloat16*)x,
                                                          (const __nv_bfloat16*)w, a, e);
     count_launch();
     if (a.trace) {
@@ -1004,14 +1241,59 @@ cudaError_t pk_cuda_stem_fused_fprop(const pk_conv_geom* g, const void* x, const
     pk_epilogue e{};
     e.act = -1;
     if (epi) e = *epi;
-    CUtensorMap xmap{};
-    if (a.nbox * ((a.HH * a.box_px * 16 + 127) / 128 * 128) > kRawStageBytes ||
-        !tc::make_map_pixel_rows(&xmap, x, g->n, g->h, g->w, g->x_pitch, a.box_px * g->x_pitch, a.HH))
-        return cudaErrorNotSupported;
     switch (g->k) {
-        case 64: return launch_stem_fprop<64>(ymap, xmap, x, y, w, a, e, st);
-        case 128: return launch_stem_fprop<128>(ymap, xmap, x, y, w, a, e, st);
+        case 64: return launch_stem_fprop<64>(ymap, x, w, a, e, st);
+        case 128: return launch_stem_fprop<128>(ymap, x, w, a, e, st);
         default: return cudaErrorNotSupported;
+    }
+}
+
+int pk_cuda_stem_fused_dgrad_supported(const pk_conv_geom* g) {
+    DgArgs a;
+    return dg_args(g, a) && tc::encode_fn() != nullptr;
+}
+
+cudaError_t pk_cuda_stem_fused_dgrad(const pk_conv_geom* g, const void* dy, const void* w, void* dx,
+                                     cudaStream_t st) {
+    DgArgs a;
+    if (!dg_args(g, a)) return cudaErrorNotSupported;
+    CUtensorMap dymap{};
+    if (!tc::make_map_nhwc(&dymap, dy, g->n, g->p, g->q, g->y_pitch, a.WX, a.HY, 1))
+        return cudaErrorNotSupported;
+    int grid = tc::num_sms_of_current_device();
+    if (a.total_tiles < grid) grid = a.total_tiles;
+    static unsigned long long* trace = [] {
+        unsigned long long* p = nullptr;
+        if (std::getenv("PK_STEM_TRACE")) cudaMalloc(&p, 32 * 32 * 8);
+        return p;
+    }();
+    a.trace = trace;
+    auto go = [&](auto kern, int* attr_dev) {
+        cudaError_t err = set_smem(kern, 227 * 1024, attr_dev);
+        if (err != cudaSuccess) return err;
+        kern<<<grid, kDgThreads, DgLayout(a).bytes, st>>>(dymap, (const __nv_bfloat16*)w,
+                                                          (__nv_bfloat16*)dx, a);
+        count_launch();
+        if (a.trace) {
+            unsigned long long h[32 * 32];
+            cudaStreamSynchronize(st);
+            cudaMemcpy(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost);
+            for (int i = 0; i < 12; ++i) {
+                fprintf(stderr, "dg tile %2d:", i);
+                for (int e = 0; e < 10; ++e) fprintf(stderr, " %8lld", (long long)(h[i * 32 + e] - h[0]));
+                fprintf(stderr, "\n");
+            }
+        }
+        return cudaGetLastError();
+    };
+    static int dev0 = -1, dev1 = -1, dev2 = -1, dev3 = -1, dev4 = -1;
+    if (a.C == 3 && a.R == 7 && a.S == 7 && a.sh == 2 && a.sw == 2)  // ResNet conv1
+        return go(stem_dgrad_kernel<3, 7, 7, 2, 2>, &dev0);
+    switch (a.C) {
+        case 1: return go(stem_dgrad_kernel<1, 0, 0, 0, 0>, &dev1);
+        case 2: return go(stem_dgrad_kernel<2, 0, 0, 0, 0>, &dev2);
+        case 3: return go(stem_dgrad_kernel<3, 0, 0, 0, 0>, &dev3);
+        default: return go(stem_dgrad_kernel<4, 0, 0, 0, 0>, &dev4);
     }
 }
 

@@ -182,22 +182,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = kb_begin; kb < kb_end; ++kb) {
             mbar_wait(&full[stage], phase);
             tc_fence_after();
-            if (lane == 0) {
+            {
                 fence_proxy_async_smem();
                 const uint32_t a_base = smem_u32(smem + stage * L::kStage);
                 const uint32_t b_base = a_base + L::kA;
-#pragma unroll
-                for (int k = 0; k < BK / 16; ++k) {
-                    // MN-major: 16 K rows = 2 core groups of 8 rows (SBO 1024 B);
-                    // the two 64-wide MN atoms are LBO = 8 KB apart.
-                    const uint64_t ad = umma_desc_sw128(a_base + k * 2048, L::kA / 2, 1024);
-                    const uint64_t bd = umma_desc_sw128(b_base + k * 2048, L::kB / 2, 1024);
-                    mma_bf16(tmem_base, ad, bd, idesc, (kb != kb_begin) || (k != 0));
-                }
-                mma_commit(&empty[stage]);
-                if (kb == kb_end - 1) mma_commit(tmem_full);
+                // MN-major: 16 K rows = 2 core groups of 8 rows (SBO 1024 B);
+                // the two 64-wide MN atoms are LBO = 8 KB apart.
+                const uint64_t ad0 = umma_desc_sw128(a_base, L::kA / 2, 1024);
+                const uint64_t bd0 = umma_desc_sw128(b_base, L::kB / 2, 1024);
+                constexpr uint64_t ks = 2048 >> 4;
+                mma4_bf16(tmem_base, ad0, ad0 + ks, ad0 + 2 * ks, ad0 + 3 * ks, bd0, bd0 + ks,
+                          bd0 + 2 * ks, bd0 + 3 * ks, idesc, kb != kb_begin);
+                mma_commit_elect(&empty[stage]);
+                if (kb == kb_end - 1) mma_commit_elect(tmem_full);
             }
-            __syncwarp();
             if (++stage == STAGES) {
                 stage = 0;
                 phase ^= 1;

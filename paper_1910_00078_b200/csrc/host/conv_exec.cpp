@@ -168,12 +168,14 @@ bool stem_fused(const pk_conv_geom& g, ConvDirection dir) {
         const char* v = std::getenv("PK_STEM_FUSED");
         return !(v && v[0] == '0');
     }();
-    return enabled && dir != ConvDirection::BackwardData && pk_cuda_stem_fused_supported(&g);
+    if (!enabled) return false;
+    return dir == ConvDirection::BackwardData ? pk_cuda_stem_fused_dgrad_supported(&g) != 0
+                                              : pk_cuda_stem_fused_supported(&g) != 0;
 }
 
 std::size_t stem_workspace(const pk_conv_geom& g, ConvDirection dir) {
     if (stem_fused(g, dir))
-        return dir == ConvDirection::Forward ? 0 : pk_cuda_stem_fused_wgrad_workspace(&g, 148);
+        return dir == ConvDirection::BackwardWeights ? pk_cuda_stem_fused_wgrad_workspace(&g, 148) : 0;
     const std::size_t kcp = pk_stem_kc_pitch(&g);
     const std::size_t rows = (std::size_t)g.n * g.p * g.q;
     const std::size_t col = align256(rows * kcp * 2);
@@ -197,6 +199,8 @@ void run_stem(const pk_conv_geom& g, ConvDirection dir, const void* a, const voi
     if (stem_fused(g, dir)) {
         if (dir == ConvDirection::Forward)
             ck(pk_cuda_stem_fused_fprop(&g, a, b, out, epi, st), "stem_fused_fprop");
+        else if (dir == ConvDirection::BackwardData)
+            ck(pk_cuda_stem_fused_dgrad(&g, a, b, out, st), "stem_fused_dgrad");
         else
             ck(pk_cuda_stem_fused_wgrad(&g, a, b, out, ws, num_sms, st), "stem_fused_wgrad");
         return;
@@ -370,7 +374,7 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
             kernel = "direct_simt_bwd_data";
             ck(pk_cuda_direct_bwd_data(&g, dt, a, b, out, st), "direct_bwd_data");
         } else if (stem_eligible(g, dt, nullptr)) {
-            kernel = "stem_gemm_tc+col2im";
+            kernel = stem_fused(g, dir) ? "stem_fused_dgrad_tc" : "stem_gemm_tc+col2im";
             run_stem(g, dir, a, b, out, ws, nullptr, h.num_sms(), st);
         } else if (dt == PK_BF16 && pk_tc_dgrad_supported(&g)) {
             kernel = "igemm_tc_dgrad";

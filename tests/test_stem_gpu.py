@@ -1,7 +1,8 @@
 """Fused narrow-channel (stem) tcgen05 kernels against the oracle: ResNet
 conv1 (3 -> 64, 7x7 stride 2 pad 3), VGG conv1_1 (3 -> 64, 3x3 pad 1) and
-ragged / dilated / 128-channel variants, forward (ImplicitGemm) and backward
-weights (Im2colGemm), plus the fused epilogue through a fusion plan.
+ragged / dilated / 128-channel variants, forward (ImplicitGemm), backward data
+and backward weights (Im2colGemm), plus the fused epilogue through a fusion
+plan.
 bf16 tolerance 1e-2 relative L2 against the fp32 oracle (north_star)."""
 import numpy as np
 import pytest
@@ -33,7 +34,7 @@ def _inputs(lib, p, rng):
 
 
 @pytest.mark.parametrize("si", range(len(STEMS)))
-@pytest.mark.parametrize("direction", [abi.FORWARD, abi.BACKWARD_WEIGHTS])
+@pytest.mark.parametrize("direction", [abi.FORWARD, abi.BACKWARD_DATA, abi.BACKWARD_WEIGHTS])
 def test_stem_fused(lib, si, direction):
     if direction == abi.FORWARD and STEMS[si].get("dilation", 1) > 1:
         pytest.skip("ImplicitGemm is forward, dilation 1 only (solver.cpp:167-171)")
@@ -43,9 +44,11 @@ def test_stem_fused(lib, si, direction):
     a, b = _inputs(lib, p, rng)
     solver = "ImplicitGemm" if direction == abi.FORWARD else "Im2colGemm"
     got = h.conv_run(p, solver, a, b)
+    if direction == abi.BACKWARD_DATA and (STEMS[si]["k"] != 64 or STEMS[si].get("dilation", 1) > 1):
+        pytest.skip("fused stem dgrad: 64 dY channels, dilation 1")
     assert h.last_kernel().startswith("stem_fused"), h.last_kernel()
-    want = (oracle.conv_forward(p, a, b) if direction == abi.FORWARD
-            else oracle.conv_backward_weights(p, a, b))
+    want = {abi.FORWARD: oracle.conv_forward, abi.BACKWARD_DATA: oracle.conv_backward_data,
+            abi.BACKWARD_WEIGHTS: oracle.conv_backward_weights}[direction](p, a, b)
     err = rel_l2(got, want)
     assert err <= 1e-2, err
     assert np.array_equal(oracle.round_bf16(got), got)
