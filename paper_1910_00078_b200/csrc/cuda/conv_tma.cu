@@ -1,3 +1,4 @@
+#include <cstdio>
 // TMA-fed tcgen05 convolution kernels (sm_100a) — the fast path for layers
 // whose channel pitches are multiples of 64 (every ResNet-50 / VGG-16 layer
 // except the 3-channel stem).
@@ -385,9 +386,11 @@ struct TmaWgArgs {
     int num_kb, kb_per_split;
 };
 
-template <int NB, int STAGES>
+// MT = output-channel tiles of 128 per CTA (2: M = 256 rows sharing every B
+// load, halving the L2 bytes per FLOP — the kernel is L2/TMA-throughput bound)
+template <int NB, int STAGES, int MT>
 struct WSmem {
-    static constexpr int kA = BM * BK * 2;   // two 64-channel MN atoms of dY
+    static constexpr int kA = MT * BM * BK * 2;   // 2*MT 64-channel MN atoms of dY
     static constexpr int kB = NB * BK * 2;   // NB/64 MN atoms of tap-shifted X
     static constexpr int kAtom = 64 * BK * 2;
     static constexpr int kStage = kA + kB;
@@ -395,12 +398,13 @@ struct WSmem {
     static constexpr int kBytes = kBarOff + (2 * STAGES + 1) * 8 + 16 + 1024;
 };
 
-template <int NB, int STAGES>
+template <int NB, int STAGES, int MT>
 __global__ void __launch_bounds__(kWgThreads, 1)
     conv_tma_wgrad_kernel(const __grid_constant__ CUtensorMap dymap,
                           const __grid_constant__ CUtensorMap xmap, float* __restrict__ partial,
                           const __grid_constant__ TmaWgArgs g) {
-    using L = WSmem<NB, STAGES>;
+    using L = WSmem<NB, STAGES, MT>;
+    constexpr uint32_t kCols = MT * NB;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -409,7 +413,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     uint64_t* tmem_full = empty + STAGES;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM;
+    const int m0 = blockIdx.x * BM * MT;
     const int n0 = blockIdx.y * NB;
     const int split = blockIdx.z;
     const int kb_begin = split * g.kb_per_split;
@@ -425,7 +429,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         tma_prefetch(&dymap);
         tma_prefetch(&xmap);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, NB);
+    if (warp == 1) tmem_alloc(tmem_slot, kCols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -456,8 +460,10 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sa = smem + stage * L::kStage;
                 mbar_arrive_expect_tx(&full[stage], L::kA + L::kB);
-                tma_load_4d(smem_u32(sa), &dymap, &full[stage], m0, q0, p0, img0);
-                tma_load_4d(smem_u32(sa + L::kA / 2), &dymap, &full[stage], m0 + 64, q0, p0, img0);
+#pragma unroll
+                for (int j = 0; j < 2 * MT; ++j)
+                    tma_load_4d(smem_u32(sa + j * L::kAtom), &dymap, &full[stage], m0 + 64 * j, q0, p0,
+                                img0);
 #pragma unroll
                 for (int a = 0; a < kAtoms; ++a)
                     tma_load_4d(smem_u32(sa + L::kA + a * L::kAtom), &xmap, &full[stage], bc[a],
@@ -479,11 +485,14 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             {
                 const uint32_t a_base = smem_u32(smem + stage * L::kStage);
                 const uint32_t b_base = a_base + L::kA;
-                const uint64_t ad0 = umma_desc_sw128(a_base, L::kAtom, 1024);
                 const uint64_t bd0 = umma_desc_sw128(b_base, L::kAtom, 1024);
                 constexpr uint64_t ks = 2048 >> 4;  // 16 MN-major K rows
-                mma4_bf16(tmem_base, ad0, ad0 + ks, ad0 + 2 * ks, ad0 + 3 * ks, bd0, bd0 + ks,
-                          bd0 + 2 * ks, bd0 + 3 * ks, idesc, kb != kb_begin);
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) {
+                    const uint64_t ad0 = umma_desc_sw128(a_base + mt * 2 * L::kAtom, L::kAtom, 1024);
+                    mma4_bf16(tmem_base + mt * NB, ad0, ad0 + ks, ad0 + 2 * ks, ad0 + 3 * ks, bd0,
+                              bd0 + ks, bd0 + 2 * ks, bd0 + 3 * ks, idesc, kb != kb_begin);
+                }
                 mma_commit_elect(&empty[stage]);
                 if (kb == kb_end - 1) mma_commit_elect(tmem_full);
             }
@@ -499,12 +508,14 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             mbar_wait(tmem_full, 0);
             tc_fence_after();
         }
-        const int k = m0 + q * 32 + lane;
+#pragma unroll 1
+        for (int mt = 0; mt < MT; ++mt) {
+        const int k = m0 + mt * BM + q * 32 + lane;
 #pragma unroll 1
         for (int c0 = 0; c0 < NB; c0 += 16) {
             uint32_t v[16];
             if (live) {
-                tmem_ld16(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + c0, v);
+                tmem_ld16(tmem_base + mt * NB + (static_cast<uint32_t>(q * 32) << 16) + c0, v);
                 tmem_ld_wait();
             } else {
 #pragma unroll
@@ -523,12 +534,13 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 for (int e = 0; e < 16 && nn + e < g.Nn; ++e) dst[e] = __uint_as_float(v[e]);
             }
         }
+        }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, NB);
+        tmem_dealloc(tmem_base, kCols);
     }
 }
 
@@ -710,46 +722,72 @@ cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, cons
                   : dispatch_fprop<false, false>(bn, amap, bmap, ymap, out, t, e, st);
 }
 
+// One wave: split-K so that tiles x splits fills the SMs once (no tail wave);
+// at least 4 k-blocks per split.
 static int tma_wgrad_splits(int tiles_mn, int num_kb, int num_sms) {
-    int splits = (2 * num_sms + tiles_mn - 1) / tiles_mn;
+    int splits = num_sms / tiles_mn;
     const int max_splits = num_kb / 4 > 1 ? num_kb / 4 : 1;
     if (splits > max_splits) splits = max_splits;
     return splits < 1 ? 1 : splits;
 }
 
-// Filter-position tile width: 256 for spatial filters (more MMA work per byte
-// of X/dY pulled through L2; measured 0.236 -> 0.182 ms on conv2_x 3x3), 128
-// for 1x1 filters (HBM-bound; the wider tile only halves the CTA count there).
-static int wgrad_nb(const pk_conv_geom* g) {
-    return (g->r * g->s > 1 && g->r * g->s * g->x_pitch >= 256) ? 256 : 128;
+// Filter-position tile width 256 and two output-channel tiles per CTA
+// (M = 256) whenever the layer is wide enough: more MMA work per byte pulled
+// through L2 (the bound of this kernel). PK_WG_TILE=128x1 etc. overrides.
+struct WgTile {
+    int nb, mt;
+};
+static WgTile wgrad_tile(const pk_conv_geom* g) {
+    static const char* env = std::getenv("PK_WG_TILE");
+    const int nn = g->r * g->s * g->x_pitch;
+    WgTile t{nn >= 256 ? 256 : 128, g->k >= 256 ? 2 : 1};
+    if (env) {
+        int nb = 0, mt = 0;
+        if (std::sscanf(env, "%dx%d", &nb, &mt) == 2 && (nb == 128 || nb == 256) && (mt == 1 || mt == 2))
+            t = {nb, mt};
+    }
+    return t;
+}
+
+// 1x1, stride 1, no padding: the reduction runs over plain pixel ranges, so
+// both operands are contiguous [pixels][channels] matrices (64-pixel boxes of
+// 8 KB, no rectangle padding or short runs).
+static bool wgrad_linear(const pk_conv_geom* g) {
+    return g->r == 1 && g->s == 1 && g->str_h == 1 && g->str_w == 1 && g->pad_h == 0 &&
+           g->pad_w == 0 && (long long)g->n * g->p * g->q < (1LL << 31);
 }
 
 static void wgrad_geometry(const pk_conv_geom* g, int* tiles_mn, int* num_kb, RectTile* rt) {
-    *rt = tc::best_rect(g->n, g->p, g->q, BK);
-    const int tw = (g->q + rt->bw - 1) / rt->bw, th = (g->p + rt->bh - 1) / rt->bh;
-    const int tn = (g->n + rt->bn - 1) / rt->bn;
-    *num_kb = tw * th * tn;
+    if (wgrad_linear(g)) {
+        *rt = RectTile{BK, 1, 1};
+        *num_kb = (int)(((long long)g->n * g->p * g->q + BK - 1) / BK);
+    } else {
+        *rt = tc::best_rect(g->n, g->p, g->q, BK);
+        const int tw = (g->q + rt->bw - 1) / rt->bw, th = (g->p + rt->bh - 1) / rt->bh;
+        const int tn = (g->n + rt->bn - 1) / rt->bn;
+        *num_kb = tw * th * tn;
+    }
     const int nn = g->r * g->s * g->x_pitch;
-    const int nb = wgrad_nb(g);
-    *tiles_mn = ((g->k + BM - 1) / BM) * ((nn + nb - 1) / nb);
+    const WgTile wt = wgrad_tile(g);
+    *tiles_mn = ((g->k + BM * wt.mt - 1) / (BM * wt.mt)) * ((nn + wt.nb - 1) / wt.nb);
 }
 
-template <int NB, int STAGES>
+template <int NB, int STAGES, int MT>
 cudaError_t launch_wgrad(const CUtensorMap& dymap, const CUtensorMap& xmap, float* partial,
                          const TmaWgArgs& w, int splits, cudaStream_t st) {
-    using L = WSmem<NB, STAGES>;
+    using L = WSmem<NB, STAGES, MT>;
     static int attr_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
     if (attr_dev != dev) {
-        cudaError_t err = cudaFuncSetAttribute(conv_tma_wgrad_kernel<NB, STAGES>,
+        cudaError_t err = cudaFuncSetAttribute(conv_tma_wgrad_kernel<NB, STAGES, MT>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                L::kBytes);
         if (err != cudaSuccess) return err;
         attr_dev = dev;
     }
-    dim3 grid((w.K + BM - 1) / BM, (w.Nn + NB - 1) / NB, splits);
-    conv_tma_wgrad_kernel<NB, STAGES><<<grid, kWgThreads, L::kBytes, st>>>(dymap, xmap, partial, w);
+    dim3 grid((w.K + BM * MT - 1) / (BM * MT), (w.Nn + NB - 1) / NB, splits);
+    conv_tma_wgrad_kernel<NB, STAGES, MT><<<grid, kWgThreads, L::kBytes, st>>>(dymap, xmap, partial, w);
     return cudaGetLastError();
 }
 
@@ -786,23 +824,31 @@ cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, v
     w.str_w = g->str_w;
     w.dil_h = g->dil_h;
     w.dil_w = g->dil_w;
+    const bool lin = wgrad_linear(g);
+    // linear: one image of one row holding all N*P*Q pixels
+    const int vn = lin ? 1 : g->n, vp = lin ? 1 : g->p, vq = lin ? g->n * g->p * g->q : g->q;
     w.rw = rt.bw;
     w.rh = rt.bh;
     w.rn = rt.bn;
-    w.tw = (g->q + rt.bw - 1) / rt.bw;
-    w.th = (g->p + rt.bh - 1) / rt.bh;
+    w.tw = (vq + rt.bw - 1) / rt.bw;
+    w.th = (vp + rt.bh - 1) / rt.bh;
     w.num_kb = num_kb;
     const int splits = tma_wgrad_splits(tiles_mn, num_kb, num_sms);
     w.kb_per_split = (num_kb + splits - 1) / splits;
     CUtensorMap dymap{}, xmap{};
-    if (!tc::make_map_nhwc(&dymap, dy, g->n, g->p, g->q, g->y_pitch, rt.bw, rt.bh, rt.bn))
+    if (!tc::make_map_nhwc(&dymap, dy, vn, vp, vq, g->y_pitch, rt.bw, rt.bh, rt.bn))
         return cudaErrorNotSupported;
-    if (!tc::make_map_nhwc(&xmap, x, g->n, g->h, g->w, g->x_pitch, rt.bw, rt.bh, rt.bn, g->str_w,
-                           g->str_h))
+    if (!tc::make_map_nhwc(&xmap, x, lin ? 1 : g->n, lin ? 1 : g->h, lin ? vq : g->w, g->x_pitch,
+                           rt.bw, rt.bh, rt.bn, g->str_w, g->str_h))
         return cudaErrorNotSupported;
-    const cudaError_t le =
-        wgrad_nb(g) == 256 ? launch_wgrad<256, 4>(dymap, xmap, (float*)workspace, w, splits, st)
-                           : launch_wgrad<128, 6>(dymap, xmap, (float*)workspace, w, splits, st);
+    const WgTile wt = wgrad_tile(g);
+    cudaError_t le;
+    if (wt.mt == 2)
+        le = wt.nb == 256 ? launch_wgrad<256, 3, 2>(dymap, xmap, (float*)workspace, w, splits, st)
+                          : launch_wgrad<128, 4, 2>(dymap, xmap, (float*)workspace, w, splits, st);
+    else
+        le = wt.nb == 256 ? launch_wgrad<256, 4, 1>(dymap, xmap, (float*)workspace, w, splits, st)
+                          : launch_wgrad<128, 6, 1>(dymap, xmap, (float*)workspace, w, splits, st);
     if (le != cudaSuccess) return le;
     const long long total = (long long)w.K * w.Nn;
     long long blocks = (total + 255) / 256;
