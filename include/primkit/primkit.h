@@ -266,6 +266,41 @@ PRIMKIT_API primkit_status primkit_batchnorm_backward_device(
     const float* saved_mean, const float* saved_invstd, void* dx, float* dgamma, float* dbeta,
     int relu);
 
+/* Convolution forward fused with training-mode spatial batch-norm (+ReLU)
+ * (BASELINE cfg4): the convolution epilogue stores the bf16 conv output
+ * `conv_out` (kept for the backward pass) and accumulates the per-channel
+ * batch statistics of exactly those stored values, so the BN statistics need
+ * no extra read of conv_out; one vectorised pass then writes
+ * y = gamma*(conv_out-mean)*invstd+beta (ReLU if relu != 0). Semantics of the
+ * statistics / running update: primitives.cpp:61-96. Device NHWC tensors;
+ * gamma/beta/running/saved vectors are f32 [K]. workspace >=
+ * primkit_conv_bn_workspace() bytes. Tensor-core (bf16) convolutions fuse;
+ * other element types / kernels run conv then the standalone BN. */
+PRIMKIT_API primkit_status primkit_conv_bn_workspace(primkit_handle* handle,
+                                                     const primkit_conv_problem* problem,
+                                                     const char* solver_name, uint64_t* out_bytes);
+PRIMKIT_API primkit_status primkit_conv_bn_forward_train_device(
+    primkit_handle* handle, const primkit_conv_problem* problem, const char* solver_name,
+    const void* x, const void* w, const float* gamma, const float* beta, float* running_mean,
+    float* running_var, float epsilon, float momentum, void* conv_out, void* y,
+    float* saved_mean, float* saved_invstd, int relu, void* workspace, size_t workspace_bytes);
+
+/* Backward counterpart (cfg4 bwd): a backward-data convolution whose output
+ * dz is the gradient w.r.t. the output of a preceding training BN (+ReLU)
+ * layer, with that BN's backward reductions (sum d, sum d*xhat, d = dz*mask)
+ * accumulated in the convolution epilogue from the stored dz and the BN input
+ * `bn_x`; one vectorised pass then writes bn_dx = dL/d(bn_x) and dgamma /
+ * dbeta (primitives.cpp:113-152 semantics; ReLU mask recomputed from bn_x).
+ * problem: the BackwardData convolution (operands dy, w as in
+ * primkit_conv_run); bn_* vectors f32 [C]. workspace >=
+ * primkit_conv_bn_workspace(problem) bytes. bf16 tensor-core dgrad fuses;
+ * otherwise dgrad then the standalone BN backward. */
+PRIMKIT_API primkit_status primkit_conv_backward_data_bn_device(
+    primkit_handle* handle, const primkit_conv_problem* problem, const char* solver_name,
+    const void* dy, const void* w, void* dz, const void* bn_x, const float* gamma,
+    const float* beta, const float* saved_mean, const float* saved_invstd, int relu, void* bn_dx,
+    float* dgamma, float* dbeta, void* workspace, size_t workspace_bytes);
+
 /* Pointwise activation (ref primitives.hpp:55-60), host NCHW buffers. */
 PRIMKIT_API primkit_status primkit_activation_forward(primkit_handle* handle,
                                                       primkit_activation kind, float alpha,

@@ -491,6 +491,134 @@ primkit_status primkit_conv_run_device(primkit_handle* h, const primkit_conv_pro
     });
 }
 
+// Per-CTA fp32 partials (+ 2 x C finalize scratch) over the channels of the
+// convolution OUTPUT (K forward, C backward data).
+static std::size_t conv_bn_stats_bytes(const primkit::ConvProblem& p) {
+    const std::size_t ch = p.direction == primkit::ConvDirection::BackwardData ? p.c : p.k;
+    return ((std::size_t)pk_stats_slots() + 1) * ch * 2 * sizeof(float);
+}
+
+primkit_status primkit_conv_bn_workspace(primkit_handle* h, const primkit_conv_problem* pp,
+                                         const char* solver_name, uint64_t* out) {
+    return guarded([&] {
+        const primkit::ConvProblem p = to_problem(pp);
+        const primkit::Solver& s = select_solver(h, p, solver_name);
+        auto plan = H(h).cached_build(p, s, nullptr);
+        const std::size_t conv = (plan->device_workspace_bytes() + 255) / 256 * 256;
+        *need(out, "output") = conv + conv_bn_stats_bytes(p);
+    });
+}
+
+primkit_status primkit_conv_bn_forward_train_device(
+    primkit_handle* h, const primkit_conv_problem* pp, const char* solver_name, const void* x,
+    const void* w, const float* gamma, const float* beta, float* running_mean, float* running_var,
+    float eps, float momentum, void* conv_out, void* y, float* saved_mean, float* saved_invstd,
+    int relu, void* workspace, size_t ws_bytes) {
+    return guarded([&] {
+        if (eps <= 0.0f)
+            primkit::throw_error(primkit::ErrorCode::InvalidEpsilon, "epsilon must be positive");
+        const primkit::ConvProblem p = to_problem(pp);
+        if (p.direction != primkit::ConvDirection::Forward || p.mode != primkit::ConvMode::Convolution)
+            primkit::throw_error(primkit::ErrorCode::InvalidValue,
+                                 "conv+BN fusion needs a forward convolution");
+        const primkit::Solver& s = select_solver(h, p, solver_name);
+        auto plan = H(h).cached_build(p, s, nullptr);
+        primkit::Handle& hd = H(h);
+        hd.activate();
+        const std::size_t conv = (plan->device_workspace_bytes() + 255) / 256 * 256;
+        if (ws_bytes < conv + conv_bn_stats_bytes(p))
+            primkit::throw_error(primkit::ErrorCode::WorkspaceTooSmall, "workspace below requested size");
+        const primkit::ConvShapes sh = primkit::resolve_shapes(p.input_desc(), p.filter_desc(),
+                                                                p.conv_desc());
+        const int n = (int)sh.n, k = (int)sh.k, hw = (int)(sh.oh * sh.ow);
+        const int dt = p.etype == primkit::ElementType::BF16 ? PK_BF16 : PK_F32;
+        float* part = reinterpret_cast<float*>(static_cast<char*>(workspace) + conv);
+        const bool fused = dt == PK_BF16 && plan->fuses_stats();
+        cudaStream_t st = hd.stream();
+        if (fused) {
+            primkit::check_cuda(cudaMemsetAsync(part, 0, conv_bn_stats_bytes(p), st), "memset");
+            pk_epilogue e{};
+            e.act = -1;
+            e.stats = part;
+            plan->run(hd, need(x, "x"), need(w, "w"), need(conv_out, "conv_out"), workspace, conv, &e);
+            primkit::check_cuda(pk_cuda_bn_finalize_apply(part, pk_stats_slots(), conv_out, need(y, "y"),
+                                                          n, k, hw, pk_pitch(k), dt, gamma, beta,
+                                                          running_mean, running_var, eps, momentum,
+                                                          saved_mean, saved_invstd, relu, st),
+                                "bn_finalize_apply");
+            hd.last_kernel = hd.last_kernel + "+bn_stats_epilogue";
+        } else {
+            plan->run(hd, need(x, "x"), need(w, "w"), need(conv_out, "conv_out"), workspace, conv);
+            void* scratch = hd.scratch(7, pk_bn_scratch_bytes(n, k, hw, 0));
+            primkit::check_cuda(pk_cuda_bn_fwd_train(conv_out, need(y, "y"), n, k, hw, pk_pitch(k), dt,
+                                                     0, gamma, beta, running_mean, running_var, eps,
+                                                     momentum, saved_mean, saved_invstd, relu,
+                                                     scratch, st),
+                                "bn_fwd_train");
+        }
+    });
+}
+
+primkit_status primkit_conv_backward_data_bn_device(
+    primkit_handle* h, const primkit_conv_problem* pp, const char* solver_name, const void* dy,
+    const void* w, void* dz, const void* bn_x, const float* gamma, const float* beta,
+    const float* saved_mean, const float* saved_invstd, int relu, void* bn_dx, float* dgamma,
+    float* dbeta, void* workspace, size_t ws_bytes) {
+    return guarded([&] {
+        const primkit::ConvProblem p = to_problem(pp);
+        if (p.direction != primkit::ConvDirection::BackwardData ||
+            p.mode != primkit::ConvMode::Convolution)
+            primkit::throw_error(primkit::ErrorCode::InvalidValue,
+                                 "dgrad+BN fusion needs a backward-data convolution");
+        const primkit::Solver& s = select_solver(h, p, solver_name);
+        auto plan = H(h).cached_build(p, s, nullptr);
+        primkit::Handle& hd = H(h);
+        hd.activate();
+        const std::size_t conv = (plan->device_workspace_bytes() + 255) / 256 * 256;
+        if (ws_bytes < conv + conv_bn_stats_bytes(p))
+            primkit::throw_error(primkit::ErrorCode::WorkspaceTooSmall, "workspace below requested size");
+        const int n = (int)p.n, c = (int)p.c, hw = (int)(p.h * p.w);
+        const int dt = p.etype == primkit::ElementType::BF16 ? PK_BF16 : PK_F32;
+        float* part = reinterpret_cast<float*>(static_cast<char*>(workspace) + conv);
+        float* tot = part + (std::size_t)pk_stats_slots() * c * 2;
+        cudaStream_t st = hd.stream();
+        if (dt == PK_BF16 && plan->fuses_stats()) {
+            primkit::check_cuda(cudaMemsetAsync(part, 0, (std::size_t)pk_stats_slots() * c * 2 * 4, st),
+                                "memset");
+            pk_epilogue e{};
+            e.act = -1;
+            e.stats = part;
+            e.bnb_y = need(bn_x, "bn_x");
+            e.bnb_gamma = gamma;
+            e.bnb_beta = beta;
+            e.bnb_mean = saved_mean;
+            e.bnb_invstd = saved_invstd;
+            e.bnb_relu = relu;
+            plan->run(hd, need(dy, "dy"), need(w, "w"), need(dz, "dz"), workspace, conv, &e);
+            primkit::check_cuda(pk_cuda_bn_bwd_finalize_apply(part, pk_stats_slots(), dz, bn_x,
+                                                              need(bn_dx, "bn_dx"), n, c, hw,
+                                                              pk_pitch(c), dt, gamma, beta,
+                                                              saved_mean, saved_invstd, relu,
+                                                              dgamma, dbeta, tot, st),
+                                "bn_bwd_finalize_apply");
+            hd.last_kernel = hd.last_kernel + "+bn_bwd_stats_epilogue";
+        } else {
+            plan->run(hd, need(dy, "dy"), need(w, "w"), need(dz, "dz"), workspace, conv);
+            // standalone BN backward needs the BN output for the ReLU mask:
+            // rebuild it into bn_dx first (same shape), then run in place
+            void* scratch = hd.scratch(7, pk_bn_scratch_bytes(n, c, hw, 0));
+            void* ybuf = hd.scratch(8, (std::size_t)n * hw * pk_pitch(c) * (dt == PK_BF16 ? 2 : 4));
+            primkit::check_cuda(pk_cuda_bn_apply_stats(bn_x, ybuf, n, c, hw, pk_pitch(c), dt, gamma,
+                                                       beta, saved_mean, saved_invstd, relu, st),
+                                "bn_apply");
+            primkit::check_cuda(pk_cuda_bn_bwd(bn_x, ybuf, dz, need(bn_dx, "bn_dx"), n, c, hw,
+                                               pk_pitch(c), dt, 0, gamma, saved_mean, saved_invstd,
+                                               dgamma, dbeta, relu, dt == PK_BF16, scratch, st),
+                                "bn_bwd");
+        }
+    });
+}
+
 primkit_status primkit_fusion_execute_device(primkit_handle* h, primkit_fusion_plan* plan,
                                              const void* input, void* output, int unfused) {
     return guarded([&] {

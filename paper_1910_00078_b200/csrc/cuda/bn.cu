@@ -206,6 +206,123 @@ __global__ void bn_dx_kernel(const T* __restrict__ x, const T* __restrict__ y,
     }
 }
 
+// Per-CTA fp32 partials (sum, sumsq) of the conv epilogue -> batch stats.
+__global__ void bn_finalize_partials_kernel(const float* __restrict__ part, int slots, int c,
+                                            double m, float eps, float momentum,
+                                            float* __restrict__ running_mean,
+                                            float* __restrict__ running_var,
+                                            float* __restrict__ saved_mean,
+                                            float* __restrict__ saved_invstd) {
+    const int ch = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ch >= c) return;
+    double s = 0.0, sq = 0.0;
+    for (int k = 0; k < slots; ++k) {
+        s += part[((size_t)k * c + ch) * 2 + 0];
+        sq += part[((size_t)k * c + ch) * 2 + 1];
+    }
+    const double mu = s / m;
+    const double var = fmax(0.0, sq / m - mu * mu);
+    saved_mean[ch] = (float)mu;
+    saved_invstd[ch] = (float)(1.0 / sqrt(var + (double)eps));
+    if (running_mean) {
+        running_mean[ch] = (1.0f - momentum) * running_mean[ch] + momentum * (float)mu;
+        running_var[ch] = (1.0f - momentum) * running_var[ch] + momentum * (float)var;
+    }
+}
+
+// y = gamma * (x - mu) * invstd + beta (+ReLU) on bf16 NHWC, 8 channels (16 B)
+// per thread; pad lanes stay zero.
+__global__ void bn_apply_bf16x8_kernel(const uint4* __restrict__ x, uint4* __restrict__ y,
+                                       long long vecs, int c, int pitch_vecs,
+                                       const float* __restrict__ gamma,
+                                       const float* __restrict__ beta,
+                                       const float* __restrict__ mean,
+                                       const float* __restrict__ invstd, int relu) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < vecs;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c0 = (int)(i % pitch_vecs) * 8;
+        uint4 v = __ldg(x + i);
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            float2 f = __bfloat1622float2(h[e]);
+            const int ch = c0 + 2 * e;
+            float a = 0.f, b = 0.f;
+            if (ch < c) {
+                a = gamma[ch] * (f.x - mean[ch]) * invstd[ch] + beta[ch];
+                if (relu && !(a > 0.0f)) a = 0.0f;
+            }
+            if (ch + 1 < c) {
+                b = gamma[ch + 1] * (f.y - mean[ch + 1]) * invstd[ch + 1] + beta[ch + 1];
+                if (relu && !(b > 0.0f)) b = 0.0f;
+            }
+            h[e] = __floats2bfloat162_rn(a, b);
+        }
+        y[i] = v;
+    }
+}
+
+// dgrad-epilogue partials -> dbeta = sum d, dgamma = sum d*xhat (double),
+// rounded to the element type like the reference (primitives.cpp:145-146).
+__global__ void bn_bwd_finalize_partials_kernel(const float* __restrict__ part, int slots, int c,
+                                                int round_bf16, float* __restrict__ dgamma,
+                                                float* __restrict__ dbeta,
+                                                float* __restrict__ tot) {
+    const int ch = blockIdx.x * blockDim.x + threadIdx.x;
+    if (ch >= c) return;
+    double s = 0.0, t = 0.0;
+    for (int k = 0; k < slots; ++k) {
+        s += part[((size_t)k * c + ch) * 2 + 0];
+        t += part[((size_t)k * c + ch) * 2 + 1];
+    }
+    float fs = (float)s, ft = (float)t;
+    tot[2 * ch] = fs;
+    tot[2 * ch + 1] = ft;
+    if (round_bf16) {
+        fs = __bfloat162float(__float2bfloat16_rn(fs));
+        ft = __bfloat162float(__float2bfloat16_rn(ft));
+    }
+    if (dbeta) dbeta[ch] = fs;
+    if (dgamma) dgamma[ch] = ft;
+}
+
+// dx = gamma*invstd/m * (m*d - sum d - xhat * sum d*xhat), d = dz * mask,
+// 8 bf16 channels per thread.
+__global__ void bn_bwd_apply_bf16x8_kernel(const uint4* __restrict__ dz, const uint4* __restrict__ y,
+                                           uint4* __restrict__ dx, long long vecs, int c,
+                                           int pitch_vecs, float m, const float* __restrict__ gamma,
+                                           const float* __restrict__ beta,
+                                           const float* __restrict__ mean,
+                                           const float* __restrict__ invstd,
+                                           const float* __restrict__ tot, int relu) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < vecs;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int c0 = (int)(i % pitch_vecs) * 8;
+        uint4 dv = __ldg(dz + i), yv = __ldg(y + i), ov;
+        const __nv_bfloat162* dh = reinterpret_cast<const __nv_bfloat162*>(&dv);
+        const __nv_bfloat162* yh = reinterpret_cast<const __nv_bfloat162*>(&yv);
+        __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&ov);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float2 d2 = __bfloat1622float2(dh[e]), y2 = __bfloat1622float2(yh[e]);
+            float o[2] = {0.f, 0.f};
+            const float dd[2] = {d2.x, d2.y}, yy[2] = {y2.x, y2.y};
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int ch = c0 + 2 * e + u;
+                if (ch >= c) continue;
+                float d = dd[u];
+                const float g = gamma[ch], mu = mean[ch], inv = invstd[ch];
+                if (relu && !(g * (yy[u] - mu) * inv + beta[ch] > 0.0f)) d = 0.f;
+                const float xhat = (yy[u] - mu) * inv;
+                o[u] = (g * inv / m) * (m * d - tot[2 * ch] - xhat * tot[2 * ch + 1]);
+            }
+            oh[e] = __floats2bfloat162_rn(o[0], o[1]);
+        }
+        dx[i] = ov;
+    }
+}
+
 inline unsigned gsz(long long total) {
     long long b = (total + 255) / 256;
     if (b > 148LL * 32) b = 148LL * 32;
@@ -217,6 +334,68 @@ inline unsigned gsz(long long total) {
 using namespace pk;
 
 extern "C" {
+
+cudaError_t pk_cuda_bn_finalize_apply(const float* part, int slots, const void* x, void* y, int n,
+                                      int c, int hw, int pitch, int dtype, const float* gamma,
+                                      const float* beta, float* running_mean, float* running_var,
+                                      float eps, float momentum, float* saved_mean,
+                                      float* saved_invstd, int relu, cudaStream_t st) {
+    const long long rows = (long long)n * hw;
+    bn_finalize_partials_kernel<<<(c + 127) / 128, 128, 0, st>>>(
+        part, slots, c, (double)rows, eps, momentum, running_mean, running_var, saved_mean,
+        saved_invstd);
+    if (dtype == PK_BF16 && pitch % 8 == 0) {
+        const long long vecs = rows * pitch / 8;
+        bn_apply_bf16x8_kernel<<<gsz(vecs), 256, 0, st>>>((const uint4*)x, (uint4*)y, vecs, c,
+                                                            pitch / 8, gamma, beta, saved_mean,
+                                                            saved_invstd, relu);
+    } else {
+        PK_DISPATCH_DTYPE(dtype, T,
+                          bn_apply_kernel<T><<<gsz(rows * pitch), 256, 0, st>>>(
+                              (const T*)x, (T*)y, rows, c, hw, pitch, 0, gamma, beta, saved_mean,
+                              saved_invstd, relu));
+    }
+    count_launch(2);
+    return cudaGetLastError();
+}
+
+cudaError_t pk_cuda_bn_bwd_finalize_apply(const float* part, int slots, const void* dz,
+                                          const void* y, void* dx, int n, int c, int hw, int pitch,
+                                          int dtype, const float* gamma, const float* beta,
+                                          const float* mean, const float* invstd, int relu,
+                                          float* dgamma, float* dbeta, float* tot_scratch,
+                                          cudaStream_t st) {
+    if (dtype != PK_BF16 || pitch % 8) return cudaErrorNotSupported;
+    const long long rows = (long long)n * hw;
+    bn_bwd_finalize_partials_kernel<<<(c + 127) / 128, 128, 0, st>>>(part, slots, c, 1, dgamma,
+                                                                      dbeta, tot_scratch);
+    const long long vecs = rows * pitch / 8;
+    bn_bwd_apply_bf16x8_kernel<<<gsz(vecs), 256, 0, st>>>(
+        (const uint4*)dz, (const uint4*)y, (uint4*)dx, vecs, c, pitch / 8, (float)rows, gamma, beta,
+        mean, invstd, tot_scratch, relu);
+    count_launch(2);
+    return cudaGetLastError();
+}
+
+cudaError_t pk_cuda_bn_apply_stats(const void* x, void* y, int n, int c, int hw, int pitch,
+                                   int dtype, const float* gamma, const float* beta,
+                                   const float* mean, const float* invstd, int relu,
+                                   cudaStream_t st) {
+    const long long rows = (long long)n * hw;
+    if (dtype == PK_BF16 && pitch % 8 == 0) {
+        const long long vecs = rows * pitch / 8;
+        bn_apply_bf16x8_kernel<<<gsz(vecs), 256, 0, st>>>((const uint4*)x, (uint4*)y, vecs, c,
+                                                            pitch / 8, gamma, beta, mean, invstd,
+                                                            relu);
+    } else {
+        PK_DISPATCH_DTYPE(dtype, T,
+                          bn_apply_kernel<T><<<gsz(rows * pitch), 256, 0, st>>>(
+                              (const T*)x, (T*)y, rows, c, hw, pitch, 0, gamma, beta, mean, invstd,
+                              relu));
+    }
+    count_launch();
+    return cudaGetLastError();
+}
 
 size_t pk_bn_scratch_bytes(int n, int c, int hw, int per_act) {
     if (per_act) return (size_t)c * hw * 2 * sizeof(double);

@@ -134,6 +134,98 @@ __device__ __forceinline__ void epilogue_chunk64(const pk_epilogue& e, float (&x
     }
 }
 
+// BN statistics of a staged 32-row x 64-channel bf16 tile (128-byte rows,
+// 16-byte chunks XOR-swizzled by row & 7, as the tcgen05 epilogues stage
+// them): lane l sums channels ch0 + 2l, ch0 + 2l + 1 over the rows set in
+// `rows_ok` and adds (sum, sumsq) into part[channel][2].
+__device__ __forceinline__ void epilogue_stats64(uint32_t stg_u, int lane, unsigned rows_ok,
+                                                 float* part, int ch0, int n_out) {
+    float s0 = 0.f, s1 = 0.f, q0 = 0.f, q1 = 0.f;
+    const uint32_t wb = (lane & 3) << 2;
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) {
+        if (!((rows_ok >> r) & 1u)) continue;
+        uint32_t wv;
+        asm volatile("ld.shared.b32 %0, [%1];"
+                     : "=r"(wv)
+                     : "r"(stg_u + r * 128 + ((((lane >> 2) ^ (r & 7)) << 4) | wb)));
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv));
+        s0 += f.x;
+        q0 = fmaf(f.x, f.x, q0);
+        s1 += f.y;
+        q1 = fmaf(f.y, f.y, q1);
+    }
+    const int ch = ch0 + 2 * lane;
+    if (ch < n_out) {
+        atomicAdd(part + 2 * ch, s0);
+        atomicAdd(part + 2 * ch + 1, q0);
+    }
+    if (ch + 1 < n_out) {
+        atomicAdd(part + 2 * ch + 2, s1);
+        atomicAdd(part + 2 * ch + 3, q1);
+    }
+}
+
+// Backward variant: dz from the staged tile, y (the preceding BN's input) from
+// global memory at the same pixel / channels (lane l: channels ch0+2l, +1;
+// `pix` = this lane's own row pixel, broadcast per row).
+__device__ __forceinline__ void epilogue_bnbwd_stats64(const pk_epilogue& e, uint32_t stg_u,
+                                                       int lane, unsigned rows_ok, long long pix,
+                                                       float* part, int ch0, int n_out,
+                                                       int pitch) {
+    const int ch = ch0 + 2 * lane;
+    const bool v0 = ch < n_out, v1 = ch + 1 < n_out;
+    const float g0 = v0 ? e.bnb_gamma[ch] : 0.f, g1 = v1 ? e.bnb_gamma[ch + 1] : 0.f;
+    const float b0 = v0 ? e.bnb_beta[ch] : 0.f, b1 = v1 ? e.bnb_beta[ch + 1] : 0.f;
+    const float m0 = v0 ? e.bnb_mean[ch] : 0.f, m1 = v1 ? e.bnb_mean[ch + 1] : 0.f;
+    const float i0 = v0 ? e.bnb_invstd[ch] : 0.f, i1 = v1 ? e.bnb_invstd[ch + 1] : 0.f;
+    const __nv_bfloat16* y = static_cast<const __nv_bfloat16*>(e.bnb_y);
+    float s0 = 0.f, s1 = 0.f, t0 = 0.f, t1 = 0.f;
+    const uint32_t wb = (lane & 3) << 2;
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+        const long long rp = __shfl_sync(0xffffffffu, pix, r);
+        if (!((rows_ok >> r) & 1u)) continue;
+        uint32_t wv, yv = 0u;
+        asm volatile("ld.shared.b32 %0, [%1];"
+                     : "=r"(wv)
+                     : "r"(stg_u + r * 128 + ((((lane >> 2) ^ (r & 7)) << 4) | wb)));
+        if (v0) yv = __ldg(reinterpret_cast<const unsigned int*>(y + rp * pitch + ch));
+        const float2 dz = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv));
+        const float2 yy = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&yv));
+        float d0 = dz.x, d1 = dz.y;
+        if (e.bnb_relu) {
+            // the forward mask, recomputed exactly as bn_apply_bf16x8_kernel does
+            if (!(g0 * (yy.x - m0) * i0 + b0 > 0.0f)) d0 = 0.f;
+            if (!(g1 * (yy.y - m1) * i1 + b1 > 0.0f)) d1 = 0.f;
+        }
+        s0 += d0;
+        t0 = fmaf(d0, (yy.x - m0) * i0, t0);
+        s1 += d1;
+        t1 = fmaf(d1, (yy.y - m1) * i1, t1);
+    }
+    if (v0) {
+        atomicAdd(part + 2 * ch, s0);
+        atomicAdd(part + 2 * ch + 1, t0);
+    }
+    if (v1) {
+        atomicAdd(part + 2 * ch + 2, s1);
+        atomicAdd(part + 2 * ch + 3, t1);
+    }
+}
+
+// Forward or backward BN statistics of a staged tile (see pk_epilogue).
+__device__ __forceinline__ void epilogue_bn_stats(const pk_epilogue& e, uint32_t stg_u, int lane,
+                                                  bool row_ok, long long pix, int ch0, int n_out,
+                                                  int pitch) {
+    const unsigned ok = __ballot_sync(0xffffffffu, row_ok);
+    float* part = e.stats + (size_t)blockIdx.x * n_out * 2;
+    if (e.bnb_y)
+        epilogue_bnbwd_stats64(e, stg_u, lane, ok, pix, part, ch0, n_out, pitch);
+    else
+        epilogue_stats64(stg_u, lane, ok, part, ch0, n_out);
+}
+
 inline unsigned ceil_div(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
 }  // namespace pk

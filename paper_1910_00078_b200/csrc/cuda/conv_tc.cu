@@ -398,9 +398,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tma_store_2d(&ymap, stg_u, n0 + c0, ti.m0 + q * 32);
                         bulk_commit();
                     }
+                    if (epi.stats && live) {
+                        long long pix = 0;
+                        if (my_m < ti.rows) {
+                            int pn, py, px;
+                            row_coords<MODE>(g, ti.phase, my_m, pn, py, px);
+                            pix = ((long long)pn * g.Ho + py) * g.Wo + px;
+                        }
+                        epilogue_bn_stats(epi, stg_u, lane, my_m < ti.rows, pix, n0 + c0, g.n_out,
+                                          g.out_pitch);
+                    }
                     sbuf ^= 1;
                 } else {
                     __syncwarp();
+                    if (epi.stats && live) {
+                        long long pix = 0;
+                        if (my_m < ti.rows) {
+                            int pn, py, px;
+                            row_coords<MODE>(g, ti.phase, my_m, pn, py, px);
+                            pix = ((long long)pn * g.Ho + py) * g.Wo + px;
+                        }
+                        epilogue_bn_stats(epi, stg_u, lane, my_m < ti.rows, pix, n0 + c0, g.n_out,
+                                          g.out_pitch);
+                    }
                     // coalesced stores: 4 rows x 128 B per instruction
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
@@ -593,7 +613,8 @@ cudaError_t pk_cuda_igemm_tc_fwd(const pk_conv_geom* g, const void* x, const voi
 }
 
 cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const void* f, void* dx,
-                                   void* workspace, const pk_tc_config* cfg, cudaStream_t st) {
+                                   void* workspace, const pk_tc_config* cfg, cudaStream_t st,
+                                   const pk_epilogue* stats_epi) {
     if (!pk_tc_dgrad_supported(g) || !aligned16(dy) || !aligned16(dx)) return cudaErrorNotSupported;
     // B operand: Wt[c][r][s][k] = W[k][r][s][c]
     cudaError_t err = pk_cuda_filter_to_dgrad(g, PK_BF16, f, workspace, st);
@@ -624,6 +645,15 @@ cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const 
     t.total_tiles = ((t.M + BM - 1) / BM) * t.n_tiles_n;
     pk_epilogue e{};
     e.act = -1;
+    if (stats_epi) {  // BN statistics only: the dgrad output is never transformed
+        e.stats = stats_epi->stats;
+        e.bnb_y = stats_epi->bnb_y;
+        e.bnb_gamma = stats_epi->bnb_gamma;
+        e.bnb_beta = stats_epi->bnb_beta;
+        e.bnb_mean = stats_epi->bnb_mean;
+        e.bnb_invstd = stats_epi->bnb_invstd;
+        e.bnb_relu = stats_epi->bnb_relu;
+    }
     CUtensorMap amap{}, bmap{};
     if (!tc::make_map_2d(&bmap, workspace, g->c, t.kred, t.kred, bn)) return cudaErrorInvalidValue;
     const bool plain = g->r == 1 && g->s == 1 && g->str_h == 1 && g->str_w == 1 &&
@@ -632,7 +662,7 @@ cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const 
         if (!tc::make_map_2d(&amap, dy, t.M, g->y_pitch, g->y_pitch, BM)) return cudaErrorInvalidValue;
         return dispatch_bn<PLAIN>(bn, amap, bmap, dy, dx, t, e, st);
     }
-    const cudaError_t te = pk_tma_conv(g, true, dy, workspace, dx, nullptr,
+    const cudaError_t te = pk_tma_conv(g, true, dy, workspace, dx, stats_epi ? &e : nullptr,
                                        cfg ? cfg->block_n : 256, st);
     if (te != cudaErrorNotSupported) return te;
     if ((g->str_h > 1 || g->str_w > 1) && build_phases(t, g->n, g->h, g->w))

@@ -340,9 +340,17 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                         tma_store_4d(&ymap, stg_u, n0c + c0, ri.w0 + qw, ri.h0 + qh, ri.n0 + qn);
                         bulk_commit();
                     }
+                    if (epi.stats && live)
+                        epilogue_bn_stats(epi, stg_u, lane, row_ok,
+                                          ((long long)pn * g.Ho + oy) * g.Wo + ox, n0c + c0,
+                                          g.n_out, g.out_pitch);
                     if (L::kStgBufs == 2) sbuf ^= 1;
                 } else {
                     __syncwarp();
+                    if (epi.stats && live)
+                        epilogue_bn_stats(epi, stg_u, lane, row_ok,
+                                          ((long long)pn * g.Ho + oy) * g.Wo + ox, n0c + c0,
+                                          g.n_out, g.out_pitch);
                     // each lane owns its row: write the 128-byte chunk back from
                     // staging as 8 x 16 B (rows are strided in the output)
                     if (row_ok) {

@@ -57,7 +57,26 @@ typedef struct pk_epilogue {
     // tensor-core epilogues (bf16 outputs) in place of bias/bn_* when set.
     const float* ch_scale;
     const float* ch_shift;
+    // Optional batch-norm (training) statistics of the STORED outputs: when
+    // set, every CTA adds per-channel sum and sum of squares of its
+    // bf16-rounded outputs into stats[blockIdx.x][channel][2] (fp32, zeroed by
+    // the caller; pk_stats_slots() slices). Spatial mode only.
+    float* stats;
+    // Backward variant (a dgrad producing dz = dL/d(BN output) of a preceding
+    // training BN): with bnb_y = that BN's input (same NHWC layout as this
+    // output), the epilogue instead accumulates per channel
+    //   stats[cta][ch][0] += d,  stats[cta][ch][1] += d * xhat,
+    //   d = dz * mask (mask = bnb_relu ? BN(y) > 0 : 1), xhat = (y - mean) * invstd.
+    const void* bnb_y;
+    const float* bnb_gamma;
+    const float* bnb_beta;
+    const float* bnb_mean;
+    const float* bnb_invstd;
+    int bnb_relu;
 } pk_epilogue;
+
+// Per-CTA slices of pk_epilogue.stats (persistent conv grids use <= this many CTAs).
+static inline int pk_stats_slots(void) { return 148; }
 
 // ---- layout conversion ------------------------------------------------------
 // NCHW f32 [n][c][hw] <-> NHWC [n][hw][pitch] of dtype (RNE on bf16 stores).
@@ -131,7 +150,8 @@ cudaError_t pk_cuda_igemm_tc_fwd(const pk_conv_geom* g, const void* x, const voi
                                  const pk_epilogue* epi, const pk_tc_config* cfg,
                                  cudaStream_t st);
 cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const void* f, void* dx,
-                                   void* workspace, const pk_tc_config* cfg, cudaStream_t st);
+                                   void* workspace, const pk_tc_config* cfg, cudaStream_t st,
+                                   const pk_epilogue* stats_epi);
 cudaError_t pk_cuda_igemm_tc_wgrad(const pk_conv_geom* g, const void* dy, const void* x, void* dw,
                                    void* workspace, int num_sms, const pk_tc_config* cfg,
                                    cudaStream_t st);
@@ -174,6 +194,29 @@ cudaError_t pk_cuda_bn_fwd_train(const void* x, void* y, int n, int c, int hw, i
                                  float* running_mean, float* running_var, float eps,
                                  float momentum, float* saved_mean, float* saved_invstd,
                                  int relu, void* scratch, cudaStream_t st);
+// Finalize training BN from per-CTA fp32 partials [slots][c][2] (sum, sumsq)
+// of m values per channel: reference semantics (double, biased var clamped,
+// running stats update), then y = BN(x) (+ReLU) with 16-byte vector accesses.
+cudaError_t pk_cuda_bn_finalize_apply(const float* part, int slots, const void* x, void* y, int n,
+                                      int c, int hw, int pitch, int dtype, const float* gamma,
+                                      const float* beta, float* running_mean, float* running_var,
+                                      float eps, float momentum, float* saved_mean,
+                                      float* saved_invstd, int relu, cudaStream_t st);
+// y = gamma*(x-mean)*invstd+beta (+ReLU) with given batch statistics.
+cudaError_t pk_cuda_bn_apply_stats(const void* x, void* y, int n, int c, int hw, int pitch,
+                                   int dtype, const float* gamma, const float* beta,
+                                   const float* mean, const float* invstd, int relu,
+                                   cudaStream_t st);
+// BN backward from per-CTA fp32 partials [slots][c][2] (sum d, sum d*xhat)
+// of a dgrad epilogue: dgamma/dbeta (rounded to bf16 when dtype is bf16, the
+// reference's etype rule) and dx = gamma*invstd/m * (m*d - dbeta - xhat*dgamma)
+// with d = dz * mask, vectorised over bf16 NHWC.
+cudaError_t pk_cuda_bn_bwd_finalize_apply(const float* part, int slots, const void* dz,
+                                          const void* y, void* dx, int n, int c, int hw, int pitch,
+                                          int dtype, const float* gamma, const float* beta,
+                                          const float* mean, const float* invstd, int relu,
+                                          float* dgamma, float* dbeta, float* tot_scratch,
+                                          cudaStream_t st);
 cudaError_t pk_cuda_bn_bwd(const void* x, const void* y, const void* dy, void* dx, int n, int c,
                            int hw, int pitch, int dtype, int per_act, const float* gamma,
                            const float* saved_mean, const float* saved_invstd, float* dgamma,

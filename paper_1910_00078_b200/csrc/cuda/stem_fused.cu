@@ -535,6 +535,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                     tma_store_4d(&ymap, stg_u, c0, ox0, oy0 + q * 2, n);
                     bulk_commit();
                 }
+                if (epi.stats)
+                    epilogue_stats64(stg_u, lane,
+                                     __ballot_sync(0xffffffffu, oy0 + rh < g.P && ox0 + rw < g.Q),
+                                     epi.stats + (size_t)blockIdx.x * g.K * 2, c0, g.K);
                 if (warp == 1) stamp(g, it, 7);
                 sbuf ^= 1;
             }

@@ -232,6 +232,17 @@ void run_stem(const pk_conv_geom& g, ConvDirection dir, const void* a, const voi
 
 OpCounters conv_counters(const ConvProblem& p, ConvAlgo algo) { return counters_for(p, algo); }
 
+bool ConvPlan::fuses_stats() const {
+    const pk_conv_geom g = make_geom(problem_);
+    if (problem_.etype != ElementType::BF16 || g.transpose || g.groups != 1) return false;
+    if (problem_.direction == ConvDirection::Forward)
+        return algo_ == ConvAlgo::ImplicitGemm && pk_tc_fwd_supported(&g);
+    if (problem_.direction == ConvDirection::BackwardData)
+        return algo_ == ConvAlgo::Im2colGemm && !stem_eligible(g, PK_BF16, nullptr) &&
+               pk_tc_dgrad_supported(&g);
+    return false;
+}
+
 std::size_t ConvPlan::device_workspace_bytes() const {
     const pk_conv_geom g = make_geom(problem_);
     const int dt = dtype_of(problem_.etype);
@@ -378,7 +389,9 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
             run_stem(g, dir, a, b, out, ws, nullptr, h.num_sms(), st);
         } else if (dt == PK_BF16 && pk_tc_dgrad_supported(&g)) {
             kernel = "igemm_tc_dgrad";
-            ck(pk_cuda_igemm_tc_dgrad(&g, a, b, out, ws, &kDefaultTc, st), "igemm_tc_dgrad");
+            ck(pk_cuda_igemm_tc_dgrad(&g, a, b, out, ws, &kDefaultTc, st,
+                                      (epi && epi->stats) ? epi : nullptr),
+               "igemm_tc_dgrad");
         } else {
             kernel = "gemm_simt+col2im";
             float* col = static_cast<float*>(ws);
