@@ -102,6 +102,12 @@ SECTION2 = {
                                                     C.c_float, P, P, P, C.c_int]),
     "primkit_batchnorm_backward_device": (ST, [P, I64P, C.c_int, P, P, P, P, P, P, P, P, P, P,
                                                C.c_int]),
+    "primkit_conv_bn_workspace": (ST, [P, C.POINTER(ConvProblem), C.c_char_p, C.POINTER(C.c_uint64)]),
+    "primkit_conv_bn_forward_train_device": (ST, [P, C.POINTER(ConvProblem), C.c_char_p, P, P, P, P,
+                                                  P, P, C.c_float, C.c_float, P, P, P, P, C.c_int,
+                                                  P, C.c_size_t]),
+    "primkit_conv_backward_data_bn_device": (ST, [P, C.POINTER(ConvProblem), C.c_char_p, P, P, P,
+                                                  P, P, P, P, P, C.c_int, P, P, P, P, C.c_size_t]),
     "primkit_activation_forward": (ST, [P, C.c_int, C.c_float, I64P, C.c_int, FP, FP]),
     "primkit_activation_backward": (ST, [P, C.c_int, C.c_float, I64P, C.c_int, FP, FP, FP]),
     "primkit_nchw_to_device": (ST, [P, I64P, C.c_int, P, P]),
