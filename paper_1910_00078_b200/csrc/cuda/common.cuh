@@ -134,97 +134,128 @@ __device__ __forceinline__ void epilogue_chunk64(const pk_epilogue& e, float (&x
     }
 }
 
-// BN statistics of a staged 32-row x 64-channel bf16 tile (128-byte rows,
-// 16-byte chunks XOR-swizzled by row & 7, as the tcgen05 epilogues stage
-// them): lane l sums channels ch0 + 2l, ch0 + 2l + 1 over the rows set in
-// `rows_ok` and adds (sum, sumsq) into part[channel][2].
-__device__ __forceinline__ void epilogue_stats64(uint32_t stg_u, int lane, unsigned rows_ok,
-                                                 float* part, int ch0, int n_out) {
-    float s0 = 0.f, s1 = 0.f, q0 = 0.f, q1 = 0.f;
-    const uint32_t wb = (lane & 3) << 2;
-#pragma unroll 8
-    for (int r = 0; r < 32; ++r) {
-        if (!((rows_ok >> r) & 1u)) continue;
-        uint32_t wv;
-        asm volatile("ld.shared.b32 %0, [%1];"
-                     : "=r"(wv)
-                     : "r"(stg_u + r * 128 + ((((lane >> 2) ^ (r & 7)) << 4) | wb)));
-        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv));
-        s0 += f.x;
-        q0 = fmaf(f.x, f.x, q0);
-        s1 += f.y;
-        q1 = fmaf(f.y, f.y, q1);
-    }
-    const int ch = ch0 + 2 * lane;
-    if (ch < n_out) {
-        atomicAdd(part + 2 * ch, s0);
-        atomicAdd(part + 2 * ch + 1, q0);
-    }
-    if (ch + 1 < n_out) {
-        atomicAdd(part + 2 * ch + 2, s1);
-        atomicAdd(part + 2 * ch + 3, q1);
-    }
+// ---- batch-norm statistics in the tensor-core epilogues -------------------
+// A staged tile is 32 rows x 64 channels of bf16 (128-byte rows, 16-byte
+// chunks XOR-swizzled by row & 7). Lane l owns channels ch0 + 2l, ch0 + 2l + 1
+// and sums them over the valid rows. Sums are kept in registers per channel
+// block (persistent CTAs keep their channel block: 148 % n_tiles_n == 0 for
+// n_tiles_n in {1, 2, 4}) and flushed to the CTA's slice of pk_epilogue.stats
+// only when the block changes and at the end — one atomic per channel per
+// CTA instead of one per tile.
+
+__device__ __forceinline__ uint32_t staged_word(uint32_t stg_u, int r, int lane) {
+    uint32_t wv;
+    asm volatile("ld.shared.b32 %0, [%1];"
+                 : "=r"(wv)
+                 : "r"(stg_u + r * 128 + ((((lane >> 2) ^ (r & 7)) << 4) | ((lane & 3) << 2))));
+    return wv;
 }
 
-// Backward variant: dz from the staged tile, y (the preceding BN's input) from
-// global memory at the same pixel / channels (lane l: channels ch0+2l, +1;
-// `pix` = this lane's own row pixel, broadcast per row).
-__device__ __forceinline__ void epilogue_bnbwd_stats64(const pk_epilogue& e, uint32_t stg_u,
-                                                       int lane, unsigned rows_ok, long long pix,
-                                                       float* part, int ch0, int n_out,
-                                                       int pitch) {
+// forward: (sum, sumsq) of the stored values for both channels of the lane
+__device__ __forceinline__ float4 stats64_fwd(uint32_t stg_u, int lane, unsigned ok) {
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) {
+        if (!((ok >> r) & 1u)) continue;
+        const uint32_t wv = staged_word(stg_u, r, lane);
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv));
+        a.x += f.x;
+        a.y = fmaf(f.x, f.x, a.y);
+        a.z += f.y;
+        a.w = fmaf(f.y, f.y, a.w);
+    }
+    return a;
+}
+
+// backward (see pk_epilogue.bnb_*): (sum d, sum d*xhat) for both channels;
+// y rows are fetched 8 at a time so the loads overlap
+__device__ __forceinline__ float4 stats64_bwd(const pk_epilogue& e, uint32_t stg_u, int lane,
+                                              unsigned ok, long long pix, int ch0, int n_out,
+                                              int pitch) {
     const int ch = ch0 + 2 * lane;
     const bool v0 = ch < n_out, v1 = ch + 1 < n_out;
     const float g0 = v0 ? e.bnb_gamma[ch] : 0.f, g1 = v1 ? e.bnb_gamma[ch + 1] : 0.f;
     const float b0 = v0 ? e.bnb_beta[ch] : 0.f, b1 = v1 ? e.bnb_beta[ch + 1] : 0.f;
     const float m0 = v0 ? e.bnb_mean[ch] : 0.f, m1 = v1 ? e.bnb_mean[ch + 1] : 0.f;
     const float i0 = v0 ? e.bnb_invstd[ch] : 0.f, i1 = v1 ? e.bnb_invstd[ch + 1] : 0.f;
+    const float sc0 = g0 * i0, sh0 = b0 - m0 * sc0, sc1 = g1 * i1, sh1 = b1 - m1 * sc1;
     const __nv_bfloat16* y = static_cast<const __nv_bfloat16*>(e.bnb_y);
-    float s0 = 0.f, s1 = 0.f, t0 = 0.f, t1 = 0.f;
-    const uint32_t wb = (lane & 3) << 2;
-#pragma unroll 4
-    for (int r = 0; r < 32; ++r) {
-        const long long rp = __shfl_sync(0xffffffffu, pix, r);
-        if (!((rows_ok >> r) & 1u)) continue;
-        uint32_t wv, yv = 0u;
-        asm volatile("ld.shared.b32 %0, [%1];"
-                     : "=r"(wv)
-                     : "r"(stg_u + r * 128 + ((((lane >> 2) ^ (r & 7)) << 4) | wb)));
-        if (v0) yv = __ldg(reinterpret_cast<const unsigned int*>(y + rp * pitch + ch));
-        const float2 dz = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv));
-        const float2 yy = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&yv));
-        float d0 = dz.x, d1 = dz.y;
-        if (e.bnb_relu) {
-            // the forward mask, recomputed exactly as bn_apply_bf16x8_kernel does
-            if (!(g0 * (yy.x - m0) * i0 + b0 > 0.0f)) d0 = 0.f;
-            if (!(g1 * (yy.y - m1) * i1 + b1 > 0.0f)) d1 = 0.f;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+    for (int r0 = 0; r0 < 32; r0 += 8) {
+        uint32_t yv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const long long rp = __shfl_sync(0xffffffffu, pix, r0 + u);
+            yv[u] = (v0 && ((ok >> (r0 + u)) & 1u))
+                        ? __ldg(reinterpret_cast<const unsigned int*>(y + rp * pitch + ch))
+                        : 0u;
         }
-        s0 += d0;
-        t0 = fmaf(d0, (yy.x - m0) * i0, t0);
-        s1 += d1;
-        t1 = fmaf(d1, (yy.y - m1) * i1, t1);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int r = r0 + u;
+            if (!((ok >> r) & 1u)) continue;
+            const uint32_t wv = staged_word(stg_u, r, lane);
+            const float2 dz = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv));
+            const float2 yy = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&yv[u]));
+            float d0 = dz.x, d1 = dz.y;
+            if (e.bnb_relu) {
+                // the forward ReLU mask, recomputed exactly as bn_apply_bf16x8_kernel
+                // does (folded affine, bn_fold in bn.cu)
+                if (!(fmaf(yy.x, sc0, sh0) > 0.0f)) d0 = 0.f;
+                if (!(fmaf(yy.y, sc1, sh1) > 0.0f)) d1 = 0.f;
+            }
+            a.x += d0;
+            a.y = fmaf(d0, (yy.x - m0) * i0, a.y);
+            a.z += d1;
+            a.w = fmaf(d1, (yy.y - m1) * i1, a.w);
+        }
     }
-    if (v0) {
-        atomicAdd(part + 2 * ch, s0);
-        atomicAdd(part + 2 * ch + 1, t0);
-    }
-    if (v1) {
-        atomicAdd(part + 2 * ch + 2, s1);
-        atomicAdd(part + 2 * ch + 3, t1);
-    }
+    return a;
 }
 
-// Forward or backward BN statistics of a staged tile (see pk_epilogue).
-__device__ __forceinline__ void epilogue_bn_stats(const pk_epilogue& e, uint32_t stg_u, int lane,
-                                                  bool row_ok, long long pix, int ch0, int n_out,
-                                                  int pitch) {
-    const unsigned ok = __ballot_sync(0xffffffffu, row_ok);
-    float* part = e.stats + (size_t)blockIdx.x * n_out * 2;
-    if (e.bnb_y)
-        epilogue_bnbwd_stats64(e, stg_u, lane, ok, pix, part, ch0, n_out, pitch);
-    else
-        epilogue_stats64(stg_u, lane, ok, part, ch0, n_out);
-}
+struct BnStatAcc {
+    int base[2];
+    float4 a[2];
+    __device__ __forceinline__ void init() {
+        base[0] = base[1] = -1;
+        a[0] = a[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __device__ __forceinline__ void flush(const pk_epilogue& e, int s, int lane, int n_out) {
+        if (base[s] < 0) return;
+        float* part = e.stats + (size_t)blockIdx.x * n_out * 2;
+        const int ch = base[s] + 2 * lane;
+        if (ch < n_out) {
+            atomicAdd(part + 2 * ch, a[s].x);
+            atomicAdd(part + 2 * ch + 1, a[s].y);
+        }
+        if (ch + 1 < n_out) {
+            atomicAdd(part + 2 * ch + 2, a[s].z);
+            atomicAdd(part + 2 * ch + 3, a[s].w);
+        }
+        a[s] = make_float4(0.f, 0.f, 0.f, 0.f);
+        base[s] = -1;
+    }
+    // slot: which of the warp's (at most two) channel blocks this chunk is
+    __device__ __forceinline__ void add(const pk_epilogue& e, uint32_t stg_u, int lane, bool row_ok,
+                                        long long pix, int slot, int ch0, int n_out, int pitch) {
+        const unsigned ok = __ballot_sync(0xffffffffu, row_ok);
+        if (base[slot] != ch0) {
+            flush(e, slot, lane, n_out);
+            base[slot] = ch0;
+        }
+        const float4 v = e.bnb_y ? stats64_bwd(e, stg_u, lane, ok, pix, ch0, n_out, pitch)
+                                 : stats64_fwd(stg_u, lane, ok);
+        a[slot].x += v.x;
+        a[slot].y += v.y;
+        a[slot].z += v.z;
+        a[slot].w += v.w;
+    }
+    __device__ __forceinline__ void finish(const pk_epilogue& e, int lane, int n_out) {
+        flush(e, 0, lane, n_out);
+        flush(e, 1, lane, n_out);
+    }
+};
 
 inline unsigned ceil_div(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 

@@ -310,6 +310,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint8_t* stg_base = smem + L::kStagingOff + ew * 2 * 4096;
         int sbuf = 0;
         const bool has_epi = epilogue_active(&epi);
+        BnStatAcc bacc;
+        bacc.init();
         int it = 0;
         for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
             const TileInfo ti = tile_info<MODE>(g, t);
@@ -405,8 +407,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                             row_coords<MODE>(g, ti.phase, my_m, pn, py, px);
                             pix = ((long long)pn * g.Ho + py) * g.Wo + px;
                         }
-                        epilogue_bn_stats(epi, stg_u, lane, my_m < ti.rows, pix, n0 + c0, g.n_out,
-                                          g.out_pitch);
+                        bacc.add(epi, stg_u, lane, my_m < ti.rows, pix, (ci >> 1) & 1, n0 + c0,
+                                 g.n_out, g.out_pitch);
                     }
                     sbuf ^= 1;
                 } else {
@@ -418,8 +420,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                             row_coords<MODE>(g, ti.phase, my_m, pn, py, px);
                             pix = ((long long)pn * g.Ho + py) * g.Wo + px;
                         }
-                        epilogue_bn_stats(epi, stg_u, lane, my_m < ti.rows, pix, n0 + c0, g.n_out,
-                                          g.out_pitch);
+                        bacc.add(epi, stg_u, lane, my_m < ti.rows, pix, (ci >> 1) & 1, n0 + c0,
+                                 g.n_out, g.out_pitch);
                     }
                     // coalesced stores: 4 rows x 128 B per instruction
 #pragma unroll
@@ -443,6 +445,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
+        if (epi.stats) bacc.finish(epi, lane, g.n_out);
         if (kTmaStore && lane == 0) bulk_wait_all();
     }
     tc_fence_before();

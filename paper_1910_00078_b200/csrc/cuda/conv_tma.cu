@@ -244,6 +244,8 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
         uint8_t* stg_base = smem + L::kStagingOff + ew * L::kStgBufs * 4096;
         int sbuf = 0;
         const bool has_epi = epilogue_active(&epi);
+        BnStatAcc bacc;
+        bacc.init();
         // this lane's row inside the rectangle, and the quarter's sub-box origin
         const int row = q * 32 + lane;
         const int rw = row % g.bw, rh = (row / g.bw) % g.bh, rn = row / (g.bw * g.bh);
@@ -341,16 +343,14 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                         bulk_commit();
                     }
                     if (epi.stats && live)
-                        epilogue_bn_stats(epi, stg_u, lane, row_ok,
-                                          ((long long)pn * g.Ho + oy) * g.Wo + ox, n0c + c0,
-                                          g.n_out, g.out_pitch);
+                        bacc.add(epi, stg_u, lane, row_ok, ((long long)pn * g.Ho + oy) * g.Wo + ox,
+                                 (ci >> 1) & 1, n0c + c0, g.n_out, g.out_pitch);
                     if (L::kStgBufs == 2) sbuf ^= 1;
                 } else {
                     __syncwarp();
                     if (epi.stats && live)
-                        epilogue_bn_stats(epi, stg_u, lane, row_ok,
-                                          ((long long)pn * g.Ho + oy) * g.Wo + ox, n0c + c0,
-                                          g.n_out, g.out_pitch);
+                        bacc.add(epi, stg_u, lane, row_ok, ((long long)pn * g.Ho + oy) * g.Wo + ox,
+                                 (ci >> 1) & 1, n0c + c0, g.n_out, g.out_pitch);
                     // each lane owns its row: write the 128-byte chunk back from
                     // staging as 8 x 16 B (rows are strided in the output)
                     if (row_ok) {
@@ -371,6 +371,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                 }
             }
         }
+        if (epi.stats) bacc.finish(epi, lane, g.n_out);
         if (!PHASED && lane == 0) bulk_wait_all();
     }
     tc_fence_before();

@@ -486,6 +486,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const bool has_epi = epilogue_active(&epi);
         const int row = q * 32 + lane;
         const int rw = row % kBw, rh = row / kBw;
+        BnStatAcc bacc;
+        bacc.init();
         int it = 0;
         for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++it) {
             int n, oy0, ox0;
@@ -536,13 +538,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                     bulk_commit();
                 }
                 if (epi.stats)
-                    epilogue_stats64(stg_u, lane,
-                                     __ballot_sync(0xffffffffu, oy0 + rh < g.P && ox0 + rw < g.Q),
-                                     epi.stats + (size_t)blockIdx.x * g.K * 2, c0, g.K);
+                    bacc.add(epi, stg_u, lane, oy0 + rh < g.P && ox0 + rw < g.Q, 0, (c0 >> 6) & 1, c0,
+                             g.K, g.K);
                 if (warp == 1) stamp(g, it, 7);
                 sbuf ^= 1;
             }
         }
+        if (epi.stats) bacc.finish(epi, lane, g.K);
         if (lane == 0) bulk_wait_all();
     } else {
         // ---------------- builders: 2 groups, cp.async halo -> A rows in TMEM --------
