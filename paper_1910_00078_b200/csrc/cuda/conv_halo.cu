@@ -1,0 +1,401 @@
+// Halo-reuse tcgen05 convolution for stride-1 spatial filters (3x3 layers of
+// ResNet/VGG, forward and backward-data).
+//
+// The rectangle kernel (conv_tma.cu) fetches one shifted A box per filter
+// tap, so a 3x3 layer pulls every input pixel through L2 nine times — the
+// kernel is L2-bound for narrow layers (64-128 channels). Here the output is
+// tiled along the ROW-MAJOR PADDED GRID of each image (rows H + 2*pad, columns
+// Wg = W + 2*pad): tile = 128 consecutive grid positions p. The input of tap
+// (r, s) for position p is grid position p + r*Wg + s, so for every tap the
+// A operand is the SAME halo buffer (whole padded grid rows, one TMA box with
+// out-of-bounds zero fill) viewed from a different starting row — the tensor
+// core applies the 128B swizzle on absolute smem address bits, so a
+// descriptor may start at any 128-byte row (verified, tools/probes/
+// shift_probe.cu). Each 64-channel chunk of input is loaded once per tile;
+// only the filter slice streams per tap. Positions in the last S-1 grid
+// columns are not outputs (3.4% of a 56-wide tile row) and are dropped by the
+// epilogue.
+//
+// Backward data at stride 1 is the same convolution of dY with the
+// transposed filter, taps flipped (grid pad R-1-pad).
+#include <cstdlib>
+
+#include "common.cuh"
+#include "tc_host.cuh"
+#include "tc_internal.h"
+#include "tc_ptx.cuh"
+
+namespace pk {
+namespace {
+
+using namespace pk::tc;
+
+constexpr int kM = 128;
+constexpr int kHThreads = 320;  // producer, MMA, 8 epilogue warps
+constexpr int kHaloBufs = 2;
+
+struct HaloArgs {
+    int N, Hg, Wg, Ho, Wo;       // grid rows/cols per image, output extent
+    int pad_h, pad_w;            // grid origin in input coordinates
+    int R, S;
+    int red_ch, cpt;             // reduction channel pitch, 64-channel chunks
+    int n_out, out_pitch;
+    int tiles_img, total_tiles, n_tiles_n;
+    int NR;                      // halo rows per tile (box height)
+    int flip;                    // dgrad: tap (r,s) uses filter tap (R-1-r, S-1-s)
+};
+
+// RESB: the whole filter slice of the tile's output channels is resident in
+// smem (loaded once per CTA) — used when it fits (taps x chunks x BN x 128 B
+// <= kResMax) and the grid has one output-channel tile; streaming a small
+// (tap, chunk) slice per MMA group leaves the tensor core waiting on TMA
+// latency.
+constexpr int kResMax = 80 * 1024;
+
+template <int BN, int BSTAGES, bool RESB>
+struct HSmem {
+    static constexpr int kHalo = 448 * 128;            // up to 448 grid rows x 128 B
+    static constexpr int kB = BN * 128;                // one (tap, chunk) filter slice
+    static constexpr int kBOff = kHaloBufs * kHalo;
+    static constexpr int kStgOff = kBOff + (RESB ? kResMax : BSTAGES * kB);
+    static constexpr int kStaging = 8 * 4096;
+    static constexpr int kBarOff = kStgOff + kStaging;
+    static constexpr int kBytes = kBarOff + (2 * kHaloBufs + 2 * BSTAGES + 4) * 8 + 16 + 1024;
+};
+
+struct HTile {
+    int n, p0, nt, row0;
+};
+__device__ __forceinline__ HTile htile(const HaloArgs& g, int t) {
+    HTile h;
+    h.nt = t % g.n_tiles_n;
+    const int mt = t / g.n_tiles_n;
+    h.n = mt / g.tiles_img;
+    h.p0 = (mt - h.n * g.tiles_img) * kM;
+    h.row0 = h.p0 / g.Wg;
+    return h;
+}
+
+template <int BN, int BSTAGES, bool RESB>
+__global__ void __launch_bounds__(kHThreads, 1)
+    conv_halo_kernel(const __grid_constant__ CUtensorMap amap,
+                     const __grid_constant__ CUtensorMap bmap, __nv_bfloat16* __restrict__ out,
+                     const __grid_constant__ HaloArgs g, const pk_epilogue epi) {
+    using L = HSmem<BN, BSTAGES, RESB>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* h_full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+    uint64_t* h_empty = h_full + kHaloBufs;
+    uint64_t* b_full = h_empty + kHaloBufs;
+    uint64_t* b_empty = b_full + BSTAGES;
+    uint64_t* tmem_full = b_empty + BSTAGES;
+    uint64_t* tmem_empty = tmem_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr uint32_t kCols = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+    const int taps = g.R * g.S;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kHaloBufs; ++i) {
+            mbar_init(&h_full[i], 1);
+            mbar_init(&h_empty[i], 1);
+        }
+        for (int i = 0; i < BSTAGES; ++i) {
+            mbar_init(&b_full[i], 1);
+            mbar_init(&b_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tmem_full[i], 1);
+            mbar_init(&tmem_empty[i], 8);
+        }
+        fence_barrier_init();
+        tma_prefetch(&amap);
+        tma_prefetch(&bmap);
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, kCols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer: halo per chunk, filter slice per tap ----
+        if (lane == 0) {
+            int hs = 0, bs = 0;
+            uint32_t hph = 0, bph = 0;
+            const uint32_t halo_bytes = g.NR * g.Wg * 128;
+            if (RESB) {  // whole filter slice once: (chunk, tap) blocks of BN x 128 B
+                mbar_arrive_expect_tx(&b_full[0], g.cpt * taps * L::kB);
+                for (int ck = 0; ck < g.cpt; ++ck)
+                    for (int tap = 0; tap < taps; ++tap) {
+                        const int ft = g.flip ? taps - 1 - tap : tap;
+                        tma_load_2d(smem_u32(smem + L::kBOff + (ck * taps + tap) * L::kB), &bmap,
+                                    &b_full[0], ft * g.red_ch + ck * 64, 0);
+                    }
+            }
+            for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
+                const HTile ht = htile(g, t);
+                for (int ck = 0; ck < g.cpt; ++ck) {
+                    mbar_wait(&h_empty[hs], hph ^ 1);
+                    mbar_arrive_expect_tx(&h_full[hs], halo_bytes);
+                    tma_load_4d(smem_u32(smem + hs * L::kHalo), &amap, &h_full[hs], ck * 64,
+                                -g.pad_w, ht.row0 - g.pad_h, ht.n);
+                    if (++hs == kHaloBufs) {
+                        hs = 0;
+                        hph ^= 1;
+                    }
+                    for (int tap = 0; tap < (RESB ? 0 : taps); ++tap) {
+                        const int ft = g.flip ? taps - 1 - tap : tap;
+                        mbar_wait(&b_empty[bs], bph ^ 1);
+                        mbar_arrive_expect_tx(&b_full[bs], L::kB);
+                        tma_load_2d(smem_u32(smem + L::kBOff + bs * L::kB), &bmap, &b_full[bs],
+                                    ft * g.red_ch + ck * 64, ht.nt * BN);
+                        if (++bs == BSTAGES) {
+                            bs = 0;
+                            bph ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer: A = shifted halo view per tap --------------
+        constexpr uint32_t idesc = idesc_bf16_f32(kM, BN, false, false);
+        int hs = 0, bs = 0;
+        uint32_t hph = 0, bph = 0;
+        int it = 0;
+        if (RESB) mbar_wait(&b_full[0], 0);
+        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++it) {
+            const HTile ht = htile(g, t);
+            const int a = it & 1;
+            mbar_wait(&tmem_empty[a], ((it >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + a * BN;
+            const int base_row = ht.p0 - ht.row0 * g.Wg;
+            for (int ck = 0; ck < g.cpt; ++ck) {
+                mbar_wait(&h_full[hs], hph);
+                tc_fence_after();
+                const uint32_t halo_u = smem_u32(smem + hs * L::kHalo);
+                for (int tap = 0; tap < taps; ++tap) {
+                    const int r = tap / g.S, s = tap - r * g.S;
+                    if (!RESB) {
+                        mbar_wait(&b_full[bs], bph);
+                        tc_fence_after();
+                    }
+                    const uint64_t ad0 =
+                        umma_desc_sw128(halo_u + (base_row + r * g.Wg + s) * 128, 16, 1024);
+                    const uint64_t bd0 = umma_desc_sw128(
+                        smem_u32(smem + L::kBOff + (RESB ? ck * taps + tap : bs) * L::kB), 16, 1024);
+                    mma4_bf16(d_tmem, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + 2, bd0 + 4, bd0 + 6,
+                              idesc, (ck | tap) != 0);
+                    if (!RESB) {
+                        mma_commit_elect(&b_empty[bs]);
+                        if (++bs == BSTAGES) {
+                            bs = 0;
+                            bph ^= 1;
+                        }
+                    }
+                }
+                mma_commit_elect(&h_empty[hs]);
+                if (++hs == kHaloBufs) {
+                    hs = 0;
+                    hph ^= 1;
+                }
+            }
+            mma_commit_elect(&tmem_full[a]);
+        }
+    } else {
+        // ---------------- epilogue (8 warps): direct 16-byte stores ---------------
+        const int ew = warp - 2;
+        const int q = warp & 3;
+        const int half = ew >> 2;
+        uint8_t* stg = smem + L::kStgOff + ew * 4096;
+        const uint32_t stg_u = smem_u32(stg);
+        const bool has_epi = epilogue_active(&epi);
+        BnStatAcc bacc;
+        bacc.init();
+        int it = 0;
+        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++it) {
+            const HTile ht = htile(g, t);
+            const int n0c = ht.nt * BN;
+            const int p = ht.p0 + q * 32 + lane;  // this lane's grid position
+            const int oy = p / g.Wg, ox = p - oy * g.Wg;
+            const bool row_ok = oy < g.Ho && ox < g.Wo;
+            const long long pix = ((long long)ht.n * g.Ho + oy) * g.Wo + ox;
+            const int a = it & 1;
+            mbar_wait(&tmem_full[a], (it >> 1) & 1);
+            tc_fence_after();
+            const int span = min(BN, g.out_pitch - n0c);
+            const int nchunks = (span + 63) / 64;
+            int my_last = -1;
+            for (int ci = half; ci < nchunks; ci += 2) my_last = ci;
+            if (my_last < 0) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tmem_empty[a]);
+            }
+#pragma unroll 1
+            for (int ci = half; ci < nchunks; ci += 2) {
+                const int c0 = ci * 64;
+                uint32_t v[64];
+                const uint32_t ta = tmem_base + a * BN + c0 + (static_cast<uint32_t>(q * 32) << 16);
+                tmem_ld16(ta + 0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+                tmem_ld16(ta + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+                tmem_ld16(ta + 32, *reinterpret_cast<uint32_t(*)[16]>(&v[32]));
+                tmem_ld16(ta + 48, *reinterpret_cast<uint32_t(*)[16]>(&v[48]));
+                tmem_ld_wait();
+                if (ci == my_last) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tmem_empty[a]);
+                }
+                float xf[64];
+#pragma unroll
+                for (int e = 0; e < 64; ++e) xf[e] = __uint_as_float(v[e]);
+                if (has_epi) epilogue_chunk64(epi, xf, n0c + c0, g.n_out, oy, ox, g.Ho, g.Wo);
+                uint4 pk[8];
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    uint32_t w4[4];
+#pragma unroll
+                    for (int e = 0; e < 8; e += 2) {
+                        const int ch = n0c + c0 + jj * 8 + e;
+                        const float x0 = ch < g.n_out ? xf[jj * 8 + e] : 0.0f;
+                        const float x1 = ch + 1 < g.n_out ? xf[jj * 8 + e + 1] : 0.0f;
+                        __nv_bfloat162 b2 = __floats2bfloat162_rn(x0, x1);
+                        w4[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
+                    }
+                    pk[jj] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+                }
+                // stage the rounded 32 x 64 tile (128-byte rows, swizzled), then
+                // store 4 full rows per instruction (8 lanes x 16 B per row)
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj)
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                     stg_u + lane * 128 + ((jj ^ (lane & 7)) << 4)),
+                                 "r"(pk[jj].x), "r"(pk[jj].y), "r"(pk[jj].z), "r"(pk[jj].w)
+                                 : "memory");
+                __syncwarp();
+                {
+                    const int sj = lane & 7;
+                    const int ch = n0c + c0 + sj * 8;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int row = (lane >> 3) + 4 * i;
+                        const int pr = ht.p0 + q * 32 + row;
+                        const int ry = pr / g.Wg, rx = pr - ry * g.Wg;
+                        uint4 val;
+                        asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                     : "=r"(val.x), "=r"(val.y), "=r"(val.z), "=r"(val.w)
+                                     : "r"(stg_u + row * 128 + ((sj ^ (row & 7)) << 4)));
+                        if (ry < g.Ho && rx < g.Wo && ch < g.out_pitch)
+                            *reinterpret_cast<uint4*>(
+                                out + (((long long)ht.n * g.Ho + ry) * g.Wo + rx) * g.out_pitch + ch) = val;
+                    }
+                }
+                if (epi.stats)
+                    bacc.add(epi, stg_u, lane, row_ok, pix, (ci >> 1) & 1, n0c + c0, g.n_out,
+                             g.out_pitch);
+                __syncwarp();  // staging reused by the next chunk
+            }
+        }
+        if (epi.stats) bacc.finish(epi, lane, g.n_out);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, kCols);
+    }
+}
+
+template <int BN, int BSTAGES, bool RESB>
+cudaError_t launch_halo(const CUtensorMap& amap, const CUtensorMap& bmap, void* out,
+                        const HaloArgs& g, const pk_epilogue& e, cudaStream_t st) {
+    using L = HSmem<BN, BSTAGES, RESB>;
+    auto kern = conv_halo_kernel<BN, BSTAGES, RESB>;
+    static int attr_dev = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
+        const cudaError_t err =
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kBytes);
+        if (err != cudaSuccess) return err;
+        attr_dev = dev;
+    }
+    int grid = num_sms_of_current_device();
+    if (g.total_tiles < grid) grid = g.total_tiles;
+    kern<<<grid, kHThreads, L::kBytes, st>>>(amap, bmap, (__nv_bfloat16*)out, g, e);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace
+}  // namespace pk
+
+using namespace pk;
+
+// Stride-1 spatial convolution (forward, or backward data when dgrad) through
+// the halo-reuse kernel. cudaErrorNotSupported (nothing launched) when the
+// geometry does not fit: stride/dilation 1, filters > 1x1, channel pitches
+// multiples of 64, padded grid width <= 256, halo <= 448 rows, N <= 256.
+cudaError_t pk_halo_conv(const pk_conv_geom* g, bool dgrad, const void* src, const void* filt,
+                         void* out, const pk_epilogue* epi, cudaStream_t st) {
+    static const bool enabled = [] {
+        const char* v = std::getenv("PK_HALO");
+        return !(v && v[0] == '0');
+    }();
+    if (!enabled || g->groups != 1 || g->transpose || g->str_h != 1 || g->str_w != 1 ||
+        g->dil_h != 1 || g->dil_w != 1 || g->r * g->s < 2)
+        return cudaErrorNotSupported;
+    const int src_pitch = dgrad ? g->y_pitch : g->x_pitch;
+    const int out_pitch = dgrad ? g->x_pitch : g->y_pitch;
+    const int n_out = dgrad ? g->c : g->k;
+    if (src_pitch % 64 || out_pitch % 8 || n_out > 256) return cudaErrorNotSupported;
+    // grid of the source (dgrad: dY padded by R-1-pad, which reproduces dX's extent)
+    const int Hs = dgrad ? g->p : g->h, Ws = dgrad ? g->q : g->w;
+    const int pad_h = dgrad ? g->r - 1 - g->pad_h : g->pad_h;
+    const int pad_w = dgrad ? g->s - 1 - g->pad_w : g->pad_w;
+    if (pad_h < 0 || pad_w < 0) return cudaErrorNotSupported;
+    HaloArgs a{};
+    a.N = g->n;
+    a.Hg = Hs + 2 * pad_h;
+    a.Wg = Ws + 2 * pad_w;
+    a.Ho = a.Hg - g->r + 1;
+    a.Wo = a.Wg - g->s + 1;
+    if (a.Ho != (dgrad ? g->h : g->p) || a.Wo != (dgrad ? g->w : g->q)) return cudaErrorNotSupported;
+    a.pad_h = pad_h;
+    a.pad_w = pad_w;
+    a.R = g->r;
+    a.S = g->s;
+    a.red_ch = src_pitch;
+    a.cpt = src_pitch / 64;
+    a.n_out = n_out;
+    a.out_pitch = out_pitch;
+    a.flip = dgrad ? 1 : 0;
+    // halo of 128 positions: rows touched by [p0, p0 + 127 + (R-1)Wg + S-1]
+    a.NR = (127 + (g->r - 1) * a.Wg + g->s - 1 + a.Wg - 1) / a.Wg + 1;
+    if (a.Wg > 256 || a.NR > 256 || a.NR * a.Wg > 448) return cudaErrorNotSupported;
+    a.tiles_img = (a.Ho * a.Wg + kM - 1) / kM;
+    // small images waste most of a tile on padding columns: leave them to the
+    // rectangle kernel (valid fraction below ~80%)
+    if ((long long)a.Ho * a.Wo * 10 < (long long)a.tiles_img * kM * 8) return cudaErrorNotSupported;
+    const int bn = out_pitch <= 64 ? 64 : out_pitch <= 128 ? 128 : 256;
+    a.n_tiles_n = (out_pitch + bn - 1) / bn;
+    a.total_tiles = a.tiles_img * g->n * a.n_tiles_n;
+    CUtensorMap amap{}, bmap{};
+    if (!tc::make_map_nhwc(&amap, src, g->n, Hs, Ws, src_pitch, a.Wg, a.NR, 1))
+        return cudaErrorNotSupported;
+    const long long kred = (long long)g->r * g->s * src_pitch;
+    if (!tc::make_map_2d(&bmap, filt, n_out, kred, kred, bn)) return cudaErrorNotSupported;
+    pk_epilogue e{};
+    e.act = -1;
+    if (epi) e = *epi;
+    // only the resident-filter form beats the rectangle kernel (measured: the
+    // streamed per-tap filter slices leave the MMA waiting on TMA latency)
+    const bool resb = a.n_tiles_n == 1 && (long long)a.cpt * g->r * g->s * bn * 128 <= kResMax;
+    if (!resb) return cudaErrorNotSupported;
+    if (bn == 64) return launch_halo<64, 8, true>(amap, bmap, out, a, e, st);
+    return launch_halo<128, 4, true>(amap, bmap, out, a, e, st);
+}

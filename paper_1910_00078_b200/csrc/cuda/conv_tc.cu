@@ -609,6 +609,9 @@ cudaError_t pk_cuda_igemm_tc_fwd(const pk_conv_geom* g, const void* x, const voi
         if (!tc::make_map_2d(&amap, x, t.M, g->x_pitch, g->x_pitch, BM)) return cudaErrorInvalidValue;
         return dispatch_bn<PLAIN>(bn, amap, bmap, x, y, t, e, st);
     }
+    // stride-1 spatial filters: halo-reuse tiles (input loaded once per tile)
+    const cudaError_t he = pk_halo_conv(g, false, x, f, y, &e, st);
+    if (he != cudaErrorNotSupported) return he;
     // TMA rectangle tiles when the channel pitch is a multiple of 64
     const cudaError_t te = pk_tma_conv(g, false, x, f, y, &e, cfg ? cfg->block_n : 256, st);
     if (te != cudaErrorNotSupported) return te;
@@ -665,6 +668,8 @@ cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const 
         if (!tc::make_map_2d(&amap, dy, t.M, g->y_pitch, g->y_pitch, BM)) return cudaErrorInvalidValue;
         return dispatch_bn<PLAIN>(bn, amap, bmap, dy, dx, t, e, st);
     }
+    const cudaError_t he = pk_halo_conv(g, true, dy, workspace, dx, stats_epi ? &e : nullptr, st);
+    if (he != cudaErrorNotSupported) return he;
     const cudaError_t te = pk_tma_conv(g, true, dy, workspace, dx, stats_epi ? &e : nullptr,
                                        cfg ? cfg->block_n : 256, st);
     if (te != cudaErrorNotSupported) return te;

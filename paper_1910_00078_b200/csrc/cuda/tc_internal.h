@@ -15,3 +15,8 @@ bool pk_tma_wgrad_supported(const pk_conv_geom* g);
 size_t pk_tma_wgrad_workspace(const pk_conv_geom* g, int num_sms);
 cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, void* dw,
                          void* workspace, int num_sms, cudaStream_t st);
+
+// Halo-reuse path for stride-1 spatial filters (conv_halo.cu): forward, or
+// backward data (filt = transposed filter [C][R][S][pitch K]) when dgrad.
+cudaError_t pk_halo_conv(const pk_conv_geom* g, bool dgrad, const void* src, const void* filt,
+                         void* out, const pk_epilogue* epi, cudaStream_t st);
