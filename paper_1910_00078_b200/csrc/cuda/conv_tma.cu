@@ -553,13 +553,45 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     }
 }
 
+// dW = sum over splits of the fp32 partials (fixed order: deterministic), four
+// outputs per thread and eight splits' loads in flight before the adds.
 __global__ void wgrad_sum_kernel(const float* __restrict__ partial, int splits, long long total,
                                  __nv_bfloat16* __restrict__ dw) {
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+    const long long quads = total / 4;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < quads;
          i += (long long)gridDim.x * blockDim.x) {
-        float acc = 0.0f;
-        for (int s = 0; s < splits; ++s) acc += partial[(size_t)s * total + i];
-        dw[i] = __float2bfloat16_rn(acc);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4* p = reinterpret_cast<const float4*>(partial) + i;
+        int s = 0;
+        for (; s + 8 <= splits; s += 8) {
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(p + (size_t)(s + u) * quads);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                acc.x += v[u].x;
+                acc.y += v[u].y;
+                acc.z += v[u].z;
+                acc.w += v[u].w;
+            }
+        }
+        for (; s < splits; ++s) {
+            const float4 v = __ldg(p + (size_t)s * quads);
+            acc.x += v.x;
+            acc.y += v.y;
+            acc.z += v.z;
+            acc.w += v.w;
+        }
+        __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
+        reinterpret_cast<uint2*>(dw)[i] = make_uint2(*reinterpret_cast<uint32_t*>(&lo),
+                                                     *reinterpret_cast<uint32_t*>(&hi));
+    }
+    // tail (total not a multiple of 4)
+    for (long long i = quads * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        float a = 0.f;
+        for (int s = 0; s < splits; ++s) a += partial[(size_t)s * total + i];
+        dw[i] = __float2bfloat16_rn(a);
     }
 }
 

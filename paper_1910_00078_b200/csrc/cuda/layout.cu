@@ -69,6 +69,31 @@ __global__ void filter_to_dgrad_kernel(pk_conv_geom g, const T* __restrict__ f, 
     }
 }
 
+// Tiled transpose per filter tap: D[c][tap][k] = F[k][tap][c] through a 32x33
+// smem tile (coalesced reads along c, coalesced writes along k).
+template <typename T>
+__global__ void __launch_bounds__(256) filter_to_dgrad_tiled_kernel(pk_conv_geom g,
+                                                                     const T* __restrict__ f,
+                                                                     T* __restrict__ d, int kp) {
+    __shared__ T tile[32][33];
+    const int taps = g.r * g.s, tap = blockIdx.z;
+    const int c0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+#pragma unroll
+    for (int i = ty; i < 32; i += 8) {
+        const int k = k0 + i, c = c0 + tx;
+        float v = 0.0f;
+        if (k < g.k && c < g.c) v = ld(f + ((size_t)k * taps + tap) * g.f_pitch + c);
+        st(&tile[i][tx], v);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = ty; i < 32; i += 8) {
+        const int c = c0 + i, k = k0 + tx;
+        if (c < g.c && k < kp) d[((size_t)c * taps + tap) * kp + k] = tile[tx][i];
+    }
+}
+
 // 8 channels per thread (one 16-byte bf16 / two 16-byte f32 vectors).
 template <typename T>
 __global__ void pointwise_kernel(const T* __restrict__ x, T* __restrict__ y, long long rows,
@@ -184,6 +209,14 @@ cudaError_t pk_cuda_nhwc_to_nchw(const void* src, float* dst, int n, int c, int 
 cudaError_t pk_cuda_filter_to_dgrad(const pk_conv_geom* g, int dtype, const void* f, void* dst,
                                     cudaStream_t st) {
     const int kp = pk_pitch(g->k);
+    if (g->groups == 1 && !g->transpose && g->r * g->s <= 65535) {
+        const dim3 grid((g->c + 31) / 32, (kp + 31) / 32, g->r * g->s);
+        PK_DISPATCH_DTYPE(dtype, T,
+                          filter_to_dgrad_tiled_kernel<T><<<grid, 256, 0, st>>>(
+                              *g, (const T*)f, (T*)dst, kp));
+        count_launch();
+        return cudaGetLastError();
+    }
     const long long total = (long long)g->c * g->r * g->s * kp;
     PK_DISPATCH_DTYPE(dtype, T,
                       filter_to_dgrad_kernel<T><<<grid_for(total), 256, 0, st>>>(
