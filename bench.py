@@ -354,6 +354,25 @@ def roofline(torch, lib, handle, net, peaks):
     return res
 
 
+def ncu_family_traffic(family: str):
+    """DRAM bytes (read + write) per step of the kernels of a direction family,
+    from the committed ncu launch list of one step (profiles/*launches_step.csv,
+    `--metrics ...,dram__bytes_read.sum,dram__bytes_write.sum`); None if absent."""
+    import csv
+    import glob
+    keys = {"igemm_tc_wgrad": ("wgrad",), "igemm_tc_fprop": ("fprop", "stem_fprop"),
+            "igemm_tc_dgrad": ("dgrad", "filter_to_dgrad")}[family]
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*launches_step.csv")))
+    if not files:
+        return None, None
+    total = 0.0
+    with open(files[-1]) as f:
+        for row in csv.DictReader(f):
+            if any(k in row["kernel"] for k in keys):
+                total += float(row["dram__bytes_read.sum"]) + float(row["dram__bytes_write.sum"])
+    return total, os.path.basename(files[-1])
+
+
 def layer_report(torch, lib, handle, net, peaks, path):
     """Per (layer, direction) device time and roofline position."""
     rows = []
@@ -506,7 +525,9 @@ def main():
             "kernel": "%s family (all 53 ResNet-50 convs of that direction, N=%d; largest share "
                       "of the step)" % (dom_name, args.batch),
             "achieved": dom["tflops"], "peak": peak, "unit": "TFLOP/s",
-            "frac": dom["tflops"] / peak, "traffic": None,
+            "frac": dom["tflops"] / peak, "traffic": ncu_family_traffic(dom_name)[0],
+            "traffic_unit": "bytes per step (DRAM read+write of the family's kernels)",
+            "traffic_source": ncu_family_traffic(dom_name)[1],
             "peak_source": f"{peak_kind} bf16_tflops_sustained (MEASURED_PEAKS.json)",
             "per_direction": rf}
         if rank == 0:
