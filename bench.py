@@ -220,6 +220,13 @@ class Net:
     def flops(self) -> float:
         return 3.0 * sum(L.flops(self.n) for L in self.layers)
 
+    def algorithmic_bytes(self) -> float:
+        """|x| + |y| + |w| (bf16, padded pitch) over the 53 layers: the minimum
+        DRAM traffic of one direction's pass."""
+        p = lambda c: (c + 7) // 8 * 8  # noqa: E731
+        return float(sum(2 * (self.n * L.h * L.h * p(L.c) + self.n * L.out_h * L.out_h * p(L.k) +
+                              L.k * L.r * L.r * p(L.c)) for L in self.layers))
+
 
 def run_conv(lib, handle, p, solver, a, b, out, ws):
     st = lib.lib.primkit_conv_run_device(handle.ptr, C.byref(p), solver, C.c_void_p(a.data_ptr()),
@@ -355,22 +362,38 @@ def roofline(torch, lib, handle, net, peaks):
 
 
 def ncu_family_traffic(family: str):
-    """DRAM bytes (read + write) per step of the kernels of a direction family,
-    from the committed ncu launch list of one step (profiles/*launches_step.csv,
-    `--metrics ...,dram__bytes_read.sum,dram__bytes_write.sum`); None if absent."""
+    """DRAM bytes (read + write) per step of one direction's kernels, from the
+    committed ncu launch list of one step (profiles/*launches_step.csv,
+    `--metrics ...,dram__bytes_read.sum,dram__bytes_write.sum`, launch order).
+    step() runs every forward conv first, then per layer (reversed) dgrad =
+    [filter_to_dgrad, conv kernel] or stem_dgrad, and wgrad = the *wgrad*
+    kernels; launches are classified by that order. None if absent."""
     import csv
     import glob
-    keys = {"igemm_tc_wgrad": ("wgrad",), "igemm_tc_fprop": ("fprop", "stem_fprop"),
-            "igemm_tc_dgrad": ("dgrad", "filter_to_dgrad")}[family]
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*launches_step.csv")))
     if not files:
         return None, None
-    total = 0.0
     with open(files[-1]) as f:
-        for row in csv.DictReader(f):
-            if any(k in row["kernel"] for k in keys):
-                total += float(row["dram__bytes_read.sum"]) + float(row["dram__bytes_write.sum"])
-    return total, os.path.basename(files[-1])
+        rows = list(csv.DictReader(f))
+    tot = {"igemm_tc_fprop": 0.0, "igemm_tc_dgrad": 0.0, "igemm_tc_wgrad": 0.0}
+    backward, after_transpose = False, False
+    for row in rows:
+        name = row["kernel"]
+        b = float(row["dram__bytes_read.sum"]) + float(row["dram__bytes_write.sum"])
+        if "filter_to_dgrad" in name or "stem_dgrad" in name:
+            backward = True
+        if not backward:
+            tot["igemm_tc_fprop"] += b
+        elif "wgrad" in name:
+            tot["igemm_tc_wgrad"] += b
+        elif "filter_to_dgrad" in name:
+            tot["igemm_tc_dgrad"] += b
+            after_transpose = True
+            continue
+        else:  # the dgrad conv launched right after its filter transpose (or stem_dgrad)
+            tot["igemm_tc_dgrad"] += b
+        after_transpose = False
+    return tot[family], os.path.basename(files[-1])
 
 
 def layer_report(torch, lib, handle, net, peaks, path):
@@ -527,6 +550,7 @@ def main():
             "achieved": dom["tflops"], "peak": peak, "unit": "TFLOP/s",
             "frac": dom["tflops"] / peak, "traffic": ncu_family_traffic(dom_name)[0],
             "traffic_unit": "bytes per step (DRAM read+write of the family's kernels)",
+            "algorithmic_bytes": net.algorithmic_bytes(),
             "traffic_source": ncu_family_traffic(dom_name)[1],
             "peak_source": f"{peak_kind} bf16_tflops_sustained (MEASURED_PEAKS.json)",
             "per_direction": rf}
