@@ -134,6 +134,45 @@ __device__ __forceinline__ void epilogue_chunk64(const pk_epilogue& e, float (&x
     }
 }
 
+// Round a lane's 64 fp32 outputs to bf16 and stage them as one 128-byte row
+// (16-byte chunks XOR-swizzled by lane & 7) for a TMA / coalesced store.
+// Channels at or beyond `valid` are written as zero; the common full chunk
+// takes the mask-free path (the per-element selects cost 3x the packing).
+__device__ __forceinline__ void pack_stage64(const float (&xf)[64], uint32_t stg_u, int lane,
+                                             int valid) {
+    if (valid >= 64) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(xf[jj * 8 + 2 * e], xf[jj * 8 + 2 * e + 1]);
+                w[e] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                             stg_u + lane * 128 + ((jj ^ (lane & 7)) << 4)),
+                         "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                         : "memory");
+        }
+    } else {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int c = jj * 8 + 2 * e;
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(c < valid ? xf[c] : 0.0f,
+                                                          c + 1 < valid ? xf[c + 1] : 0.0f);
+                w[e] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                             stg_u + lane * 128 + ((jj ^ (lane & 7)) << 4)),
+                         "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                         : "memory");
+        }
+    }
+}
+
 // ---- batch-norm statistics in the tensor-core epilogues -------------------
 // A staged tile is 32 rows x 64 channels of bf16 (128-byte rows, 16-byte
 // chunks XOR-swizzled by row & 7). Lane l owns channels ch0 + 2l, ch0 + 2l + 1

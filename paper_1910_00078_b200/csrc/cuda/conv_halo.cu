@@ -254,28 +254,9 @@ __global__ void __launch_bounds__(kHThreads, 1)
 #pragma unroll
                 for (int e = 0; e < 64; ++e) xf[e] = __uint_as_float(v[e]);
                 if (has_epi) epilogue_chunk64(epi, xf, n0c + c0, g.n_out, oy, ox, g.Ho, g.Wo);
-                uint4 pk[8];
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    uint32_t w4[4];
-#pragma unroll
-                    for (int e = 0; e < 8; e += 2) {
-                        const int ch = n0c + c0 + jj * 8 + e;
-                        const float x0 = ch < g.n_out ? xf[jj * 8 + e] : 0.0f;
-                        const float x1 = ch + 1 < g.n_out ? xf[jj * 8 + e + 1] : 0.0f;
-                        __nv_bfloat162 b2 = __floats2bfloat162_rn(x0, x1);
-                        w4[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
-                    }
-                    pk[jj] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-                }
                 // stage the rounded 32 x 64 tile (128-byte rows, swizzled), then
                 // store 4 full rows per instruction (8 lanes x 16 B per row)
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj)
-                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
-                                     stg_u + lane * 128 + ((jj ^ (lane & 7)) << 4)),
-                                 "r"(pk[jj].x), "r"(pk[jj].y), "r"(pk[jj].z), "r"(pk[jj].w)
-                                 : "memory");
+                pack_stage64(xf, stg_u, lane, g.n_out - (n0c + c0));
                 __syncwarp();
                 {
                     const int sj = lane & 7;

@@ -1,3 +1,4 @@
+#include <cstdio>
 #include <cstdlib>
 // tcgen05 implicit-GEMM convolution, forward and backward-data (sm_100a).
 //
@@ -58,7 +59,13 @@ struct ConvTcArgs {
     int ph_h0[kMaxPhases], ph_w0[kMaxPhases];
     int ph_tap_start[kMaxPhases + 1];
     unsigned short taps[kMaxTaps];  // (r << 8) | s
+    int debug;             // PK_TC_DEBUG (profiling only): 1 no MMA, 2 no TMEM load, 4 no store, 8 no math
+    unsigned long long* trace;  // PK_TC_TRACE: clock64 stamps of CTA 0 (profiling only)
 };
+__device__ __forceinline__ void tcstamp(const ConvTcArgs& g, int it, int ev) {
+    if (g.trace && blockIdx.x == 0 && it < 32 && (threadIdx.x & 31) == 0)
+        g.trace[it * 16 + ev] = clock64();
+}
 
 template <int BN, int STAGES>
 struct Smem {
@@ -195,7 +202,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const int tap0 = MODE == PHASE_DGRAD ? g.ph_tap_start[ti.phase] : 0;
             for (int kb = 0; kb < ti.nkb; ++kb) {
+                if (kb == 0 && warp == 0) tcstamp(g, (t - blockIdx.x) / gridDim.x, 0);
                 mbar_wait(&empty[stage], phase ^ 1);
+                if (kb == 0 && warp == 0) tcstamp(g, (t - blockIdx.x) / gridDim.x, 1);
                 uint8_t* sa = smem + stage * L::kStage;
                 int r = 0, s = 0, c8 = 0, bcol = kb * BK;
                 bool kvalid = true;
@@ -275,11 +284,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int a = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
             ++it;
+            tcstamp(g, it - 1, 2);
             mbar_wait(&tmem_empty[a], aphase ^ 1);
+            tcstamp(g, it - 1, 3);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + a * BN;
             for (int kb = 0; kb < ti.nkb; ++kb) {
                 mbar_wait(&full[stage], phase);
+                if (kb == 0) tcstamp(g, it - 1, 4);
                 tc_fence_after();
                 {
                     fence_proxy_async_smem();
@@ -287,8 +299,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t b_base = a_base + L::kA;
                     const uint64_t ad0 = umma_desc_sw128(a_base, 16, 1024);
                     const uint64_t bd0 = umma_desc_sw128(b_base, 16, 1024);
-                    mma4_bf16(d_tmem, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + 2, bd0 + 4, bd0 + 6,
-                              idesc, kb != 0);
+                    if (!(g.debug & 1))
+                        mma4_bf16(d_tmem, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + 2, bd0 + 4,
+                                  bd0 + 6, idesc, kb != 0);
                     mma_commit_elect(&empty[stage]);
                     if (kb == ti.nkb - 1) mma_commit_elect(&tmem_full[a]);
                 }
@@ -325,7 +338,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 a = it & 1;
                 const uint32_t aphase = (it >> 1) & 1;
                 ++it;
+                if (warp == 5) tcstamp(g, it - 1, 5);
                 mbar_wait(&tmem_full[a], aphase);
+                if (warp == 5) tcstamp(g, it - 1, 6);
                 tc_fence_after();
             }
             // 64-column chunks that reach the output (warp-uniform)
@@ -343,7 +358,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int ci = half; ci < nchunks; ci += 2) {
                 const int c0 = ci * 64;
                 uint32_t v[64];
-                if (live) {
+                if (live && (g.debug & 2)) {
+#pragma unroll
+                    for (int e = 0; e < 64; ++e) v[e] = lane + e;
+                    if (ci == my_last) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tmem_empty[a]);
+                    }
+                } else if (live) {
                     const uint32_t ta = tmem_base + a * BN + c0 + (static_cast<uint32_t>(q * 32) << 16);
                     tmem_ld16(ta + 0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
                     if (BN >= 32) tmem_ld16(ta + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
@@ -375,29 +398,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int e = 0; e < 64; ++e) xf[e] = __uint_as_float(v[e]);
                 if (has_epi) epilogue_chunk64(epi, xf, n0 + c0, g.n_out, my_oy, my_ox, g.Ho, g.Wo);
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    uint32_t packed[4];
-#pragma unroll
-                    for (int e = 0; e < 8; e += 2) {
-                        const int ch = n0 + c0 + jj * 8 + e;
-                        float x0 = xf[jj * 8 + e];
-                        float x1 = xf[jj * 8 + e + 1];
-                        if (ch >= g.n_out || c0 + jj * 8 + e >= BN) x0 = 0.0f;
-                        if (ch + 1 >= g.n_out || c0 + jj * 8 + e + 1 >= BN) x1 = 0.0f;
-                        __nv_bfloat162 b2 = __floats2bfloat162_rn(x0, x1);
-                        packed[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
-                    }
-                    const uint32_t dst = stg_u + lane * 128 + ((jj ^ (lane & 7)) << 4);
-                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst),
-                                 "r"(packed[0]), "r"(packed[1]), "r"(packed[2]), "r"(packed[3])
-                                 : "memory");
-                }
+                pack_stage64(xf, stg_u, lane, min(g.n_out - (n0 + c0), BN - c0));
                 if (kTmaStore) {
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        tma_store_2d(&ymap, stg_u, n0 + c0, ti.m0 + q * 32);
+                        if (!(g.debug & 4)) tma_store_2d(&ymap, stg_u, n0 + c0, ti.m0 + q * 32);
                         bulk_commit();
                     }
                     if (epi.stats && live) {
@@ -411,6 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  g.n_out, g.out_pitch);
                     }
                     sbuf ^= 1;
+                    if (warp == 5) tcstamp(g, it - 1, 7 + (ci >> 1));
                 } else {
                     __syncwarp();
                     if (epi.stats && live) {
@@ -476,6 +483,16 @@ cudaError_t launch(const CUtensorMap& amap, const CUtensorMap& bmap, const CUten
     if (grid < 1) grid = 1;
     kern<<<grid, kThreads, L::kBytes, st>>>(amap, bmap, ymap, (const __nv_bfloat16*)src,
                                             (__nv_bfloat16*)out, g, e);
+    if (g.trace) {
+        unsigned long long h[32 * 16];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, g.trace, sizeof(h), cudaMemcpyDeviceToHost);
+        for (int i = 0; i < 12; ++i) {
+            fprintf(stderr, "tc tile %2d:", i);
+            for (int e = 0; e < 9; ++e) fprintf(stderr, " %7lld", (long long)(h[i * 16 + e] - h[0]));
+            fprintf(stderr, "\n");
+        }
+    }
     count_launch();
     return cudaGetLastError();
 }
@@ -503,6 +520,17 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 void base_args(ConvTcArgs& t, int bn) {
     t.n_tiles_n = (t.out_pitch + bn - 1) / bn;
+    static const int dbg = [] {
+        const char* v = std::getenv("PK_TC_DEBUG");
+        return v ? std::atoi(v) : 0;
+    }();
+    t.debug = dbg;
+    static unsigned long long* trace = [] {
+        unsigned long long* p = nullptr;
+        if (std::getenv("PK_TC_TRACE")) cudaMalloc(&p, 32 * 16 * 8);
+        return p;
+    }();
+    t.trace = trace;
 }
 
 // Sub-pixel phase tables for backward data with stride > 1.

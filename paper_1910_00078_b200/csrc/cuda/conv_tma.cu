@@ -317,24 +317,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
 #pragma unroll
                 for (int e = 0; e < 64; ++e) xf[e] = __uint_as_float(v[e]);
                 if (has_epi) epilogue_chunk64(epi, xf, n0c + c0, g.n_out, oy, ox, g.Ho, g.Wo);
-#pragma unroll
-                for (int jj = 0; jj < 8; ++jj) {
-                    uint32_t packed[4];
-#pragma unroll
-                    for (int e = 0; e < 8; e += 2) {
-                        const int ch = n0c + c0 + jj * 8 + e;
-                        float x0 = xf[jj * 8 + e];
-                        float x1 = xf[jj * 8 + e + 1];
-                        if (ch >= g.n_out || c0 + jj * 8 + e >= BN) x0 = 0.0f;
-                        if (ch + 1 >= g.n_out || c0 + jj * 8 + e + 1 >= BN) x1 = 0.0f;
-                        __nv_bfloat162 b2 = __floats2bfloat162_rn(x0, x1);
-                        packed[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
-                    }
-                    const uint32_t dst = stg_u + lane * 128 + ((jj ^ (lane & 7)) << 4);
-                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst),
-                                 "r"(packed[0]), "r"(packed[1]), "r"(packed[2]), "r"(packed[3])
-                                 : "memory");
-                }
+                pack_stage64(xf, stg_u, lane, min(g.n_out - (n0c + c0), BN - c0));
                 if (!PHASED) {
                     fence_proxy_async_smem();
                     __syncwarp();
