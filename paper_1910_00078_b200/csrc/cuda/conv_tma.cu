@@ -376,7 +376,12 @@ struct TmaWgArgs {
     int rw, rh, rn;            // reduction rectangle (product 64)
     int tw, th;                // rectangles per row / column
     int num_kb, kb_per_split;
+    unsigned long long* trace;  // PK_WG_TRACE: clock64 stamps of CTA (0,0,0) (profiling only)
 };
+__device__ __forceinline__ void wgstamp(const TmaWgArgs& g, int ev) {
+    if (g.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (threadIdx.x & 31) == 0)
+        g.trace[ev] = clock64();
+}
 
 // MT = output-channel tiles of 128 per CTA (2: M = 256 rows sharing every B
 // load, halving the L2 bytes per FLOP — the kernel is L2/TMA-throughput bound)
@@ -471,8 +476,10 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         constexpr uint32_t idesc = idesc_bf16_f32(BM, NB, true, true);
         int stage = 0;
         uint32_t phase = 0;
+        wgstamp(g, 0);
         for (int kb = kb_begin; kb < kb_end; ++kb) {
             mbar_wait(&full[stage], phase);
+            if (kb - kb_begin < 8) wgstamp(g, 8 + kb - kb_begin);
             tc_fence_after();
             {
                 const uint32_t a_base = smem_u32(smem + stage * L::kStage);
@@ -488,6 +495,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 mma_commit_elect(&empty[stage]);
                 if (kb == kb_end - 1) mma_commit_elect(tmem_full);
             }
+            if (kb == kb_end - 1) wgstamp(g, 1);
             if (++stage == STAGES) {
                 stage = 0;
                 phase ^= 1;
@@ -498,35 +506,60 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         const bool live = kb_end > kb_begin;
         if (live) {
             mbar_wait(tmem_full, 0);
+            if (warp == 2) wgstamp(g, 2);
             tc_fence_after();
         }
+        // drain: 64 TMEM columns per round (one wait), staged through the now
+        // idle pipeline smem so every global store writes two full 256-byte
+        // row segments of the partial (coalesced) instead of 32 scattered 16 B
+        float* stg = reinterpret_cast<float*>(smem) + (warp - 2) * 32 * 68;
+        const uint32_t stg_u = smem_u32(stg);
 #pragma unroll 1
         for (int mt = 0; mt < MT; ++mt) {
-        const int k = m0 + mt * BM + q * 32 + lane;
 #pragma unroll 1
-        for (int c0 = 0; c0 < NB; c0 += 16) {
-            uint32_t v[16];
-            if (live) {
-                tmem_ld16(tmem_base + mt * NB + (static_cast<uint32_t>(q * 32) << 16) + c0, v);
-                tmem_ld_wait();
-            } else {
+            for (int c0 = 0; c0 < NB; c0 += 64) {
+                uint32_t v[64];
+                if (live) {
+                    const uint32_t ta = tmem_base + mt * NB + c0 + (static_cast<uint32_t>(q * 32) << 16);
+                    tmem_ld16(ta + 0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+                    tmem_ld16(ta + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+                    tmem_ld16(ta + 32, *reinterpret_cast<uint32_t(*)[16]>(&v[32]));
+                    tmem_ld16(ta + 48, *reinterpret_cast<uint32_t(*)[16]>(&v[48]));
+                    tmem_ld_wait();
+                } else {
 #pragma unroll
-                for (int e = 0; e < 16; ++e) v[e] = 0u;
-            }
-            const int nn = n0 + c0;
-            if (k >= g.K || nn >= g.Nn) continue;
-            float* dst = partial + ((size_t)split * g.K + k) * g.Nn + nn;
-            if (nn + 16 <= g.Nn) {
+                    for (int e = 0; e < 64; ++e) v[e] = 0u;
+                }
 #pragma unroll
-                for (int e = 0; e < 16; e += 4)
-                    *reinterpret_cast<float4*>(dst + e) =
-                        make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]),
-                                    __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
-            } else {
-                for (int e = 0; e < 16 && nn + e < g.Nn; ++e) dst[e] = __uint_as_float(v[e]);
+                for (int e = 0; e < 64; e += 4)
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                                     stg_u + (lane * 68 + e) * 4),
+                                 "r"(v[e]), "r"(v[e + 1]), "r"(v[e + 2]), "r"(v[e + 3])
+                                 : "memory");
+                __syncwarp();
+                const int col = (lane & 15) * 4, nn = n0 + c0 + col;
+#pragma unroll 4
+                for (int i = 0; i < 16; ++i) {
+                    const int r = (lane >> 4) + 2 * i;
+                    const int k = m0 + mt * BM + q * 32 + r;
+                    float4 val;
+                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(val.x), "=f"(val.y), "=f"(val.z), "=f"(val.w)
+                                 : "r"(stg_u + (r * 68 + col) * 4));
+                    if (k < g.K && nn < g.Nn) {
+                        float* dst = partial + ((size_t)split * g.K + k) * g.Nn + nn;
+                        if (nn + 4 <= g.Nn) {
+                            *reinterpret_cast<float4*>(dst) = val;
+                        } else {
+                            const float vv[4] = {val.x, val.y, val.z, val.w};
+                            for (int e = 0; e < 4 && nn + e < g.Nn; ++e) dst[e] = vv[e];
+                        }
+                    }
+                }
+                __syncwarp();
             }
         }
-        }
+        if (warp == 2) wgstamp(g, 3);
     }
     tc_fence_before();
     __syncthreads();
@@ -765,6 +798,9 @@ static WgTile wgrad_tile(const pk_conv_geom* g) {
     static const char* env = std::getenv("PK_WG_TILE");
     const int nn = g->r * g->s * g->x_pitch;
     WgTile t{nn >= 256 ? 256 : 128, g->k >= 256 ? 2 : 1};
+    // measured (B200, all ResNet-50 layers): 1x1 stride-1 layers are fastest
+    // with 128-wide filter tiles (smaller fp32 partials to drain and sum)
+    if (g->r == 1 && g->s == 1 && g->str_h == 1 && g->str_w == 1) t.nb = 128;
     if (env) {
         int nb = 0, mt = 0;
         if (std::sscanf(env, "%dx%d", &nb, &mt) == 2 && (nb == 128 || nb == 256) && (mt == 1 || mt == 2))
@@ -857,6 +893,12 @@ cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, v
     w.tw = (vq + rt.bw - 1) / rt.bw;
     w.th = (vp + rt.bh - 1) / rt.bh;
     w.num_kb = num_kb;
+    static unsigned long long* trace = [] {
+        unsigned long long* p = nullptr;
+        if (std::getenv("PK_WG_TRACE")) cudaMalloc(&p, 32 * 8);
+        return p;
+    }();
+    w.trace = trace;
     const int splits = tma_wgrad_splits(tiles_mn, num_kb, num_sms);
     w.kb_per_split = (num_kb + splits - 1) / splits;
     CUtensorMap dymap{}, xmap{};
@@ -874,6 +916,15 @@ cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, v
         le = wt.nb == 256 ? launch_wgrad<256, 4, 1>(dymap, xmap, (float*)workspace, w, splits, st)
                           : launch_wgrad<128, 6, 1>(dymap, xmap, (float*)workspace, w, splits, st);
     if (le != cudaSuccess) return le;
+    if (w.trace) {
+        unsigned long long h[32];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, w.trace, sizeof(h), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "wg: kb/split %d, mma start 0, last commit %lld, drain start %lld end %lld | first kb fulls:",
+                w.kb_per_split, (long long)(h[1] - h[0]), (long long)(h[2] - h[0]), (long long)(h[3] - h[0]));
+        for (int e = 8; e < 16; ++e) fprintf(stderr, " %lld", (long long)(h[e] - h[0]));
+        fprintf(stderr, "\n");
+    }
     const long long total = (long long)w.K * w.Nn;
     long long blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
