@@ -52,6 +52,10 @@ struct ConvTcArgs {
     int kred, num_kb;      // non-phase modes
     int n_out, out_pitch;
     int n_tiles_n, total_tiles;
+    // batched plain GEMM (Winograd): A/Y rows are [batch][rows_per_batch] with
+    // rows_per_batch = b_batch_mtiles * BM; B rows of batch b start at
+    // b * b_batch_rows. 0 = not batched.
+    int b_batch_mtiles, b_batch_rows;
     // phase decomposition (PHASE_DGRAD)
     int num_phases, cpt;   // cpt = red_ch / 64
     int ph_tile_start[kMaxPhases + 1];
@@ -227,7 +231,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 if (threadIdx.x == 0) {
                     mbar_arrive_expect_tx(&full[stage], MODE == PLAIN ? L::kA + L::kB : L::kB);
-                    tma_load_2d(smem_u32(sa + L::kA), &bmap, &full[stage], bcol, n0);
+                    const int brow = MODE == PLAIN && g.b_batch_mtiles
+                                         ? (ti.m0 / BM / g.b_batch_mtiles) * g.b_batch_rows
+                                         : 0;
+                    tma_load_2d(smem_u32(sa + L::kA), &bmap, &full[stage], bcol, n0 + brow);
                     if (MODE == PLAIN) tma_load_2d(smem_u32(sa), &amap, &full[stage], kb * BK, ti.m0);
                 }
                 if (MODE != PLAIN) {
@@ -644,6 +651,40 @@ cudaError_t pk_cuda_igemm_tc_fwd(const pk_conv_geom* g, const void* x, const voi
     const cudaError_t te = pk_tma_conv(g, false, x, f, y, &e, cfg ? cfg->block_n : 256, st);
     if (te != cudaErrorNotSupported) return te;
     return dispatch_bn<GATHER_FWD>(bn, amap, bmap, x, y, t, e, st);
+}
+
+cudaError_t pk_cuda_gemm_tc_batched(const void* a, const void* b, void* y, int batch,
+                                    int rows_per_batch, int kdim, int n_out, int b_rows_per_batch,
+                                    int out_pitch, cudaStream_t st) {
+    if (rows_per_batch % BM || kdim % 8 || out_pitch % 8 || !aligned16(a) || !aligned16(b) ||
+        !aligned16(y) || tc::encode_fn() == nullptr)
+        return cudaErrorNotSupported;
+    ConvTcArgs t{};
+    t.M = batch * rows_per_batch;
+    t.Ho = t.M;
+    t.Wo = 1;
+    t.Hs = t.M;
+    t.Ws = 1;
+    t.src_pitch = kdim;
+    t.red_ch = kdim;
+    t.R = t.S = 1;
+    t.str_h = t.str_w = t.dil_h = t.dil_w = 1;
+    t.kred = kdim;
+    t.num_kb = (kdim + BK - 1) / BK;
+    t.n_out = n_out;
+    t.out_pitch = out_pitch;
+    const int bn = pick_bn(256, out_pitch);
+    base_args(t, bn);
+    t.total_tiles = (t.M / BM) * t.n_tiles_n;
+    t.b_batch_mtiles = rows_per_batch / BM;
+    t.b_batch_rows = b_rows_per_batch;
+    pk_epilogue e{};
+    e.act = -1;
+    CUtensorMap amap{}, bmap{};
+    if (!tc::make_map_2d(&bmap, b, (long long)batch * b_rows_per_batch, kdim, kdim, bn) ||
+        !tc::make_map_2d(&amap, a, t.M, kdim, kdim, BM))
+        return cudaErrorInvalidValue;
+    return dispatch_bn<PLAIN>(bn, amap, bmap, a, y, t, e, st);
 }
 
 cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const void* f, void* dx,

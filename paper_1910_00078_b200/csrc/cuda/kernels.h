@@ -129,6 +129,20 @@ cudaError_t pk_cuda_igemm_simt_fwd(const pk_conv_geom* g, int dtype, const void*
 cudaError_t pk_cuda_winograd_f23(const pk_conv_geom* g, int dtype, const void* x, const void* f,
                                  void* y, const pk_epilogue* epi, cudaStream_t st);
 
+// ---- Winograd F(m x m, 3x3) on the tensor cores (bf16, m = 2 or 4) ----------
+// Filter/input transforms in registers, alpha^2 batched tcgen05 GEMMs, output
+// transform + epilogue; V/M staged in ws (chunked over tiles).
+int pk_winograd_tc_supported(const pk_conv_geom* g);
+size_t pk_winograd_tc_workspace(const pk_conv_geom* g, int m);
+cudaError_t pk_cuda_winograd_tc(const pk_conv_geom* g, int m, const void* x, const void* f,
+                                void* y, const pk_epilogue* epi, void* ws, size_t ws_bytes,
+                                cudaStream_t st);
+// Batched plain tcgen05 GEMM: Y[b][i][j] = sum_l A[b][i][l] * B[b][j][l] (bf16 in,
+// fp32 accumulate, bf16 out). A/Y rows per batch must be a multiple of 128.
+cudaError_t pk_cuda_gemm_tc_batched(const void* a, const void* b, void* y, int batch,
+                                    int rows_per_batch, int kdim, int n_out, int b_rows_per_batch,
+                                    int out_pitch, cudaStream_t st);
+
 // ---- FFT convolution (complex<double>, radix-2, pow2 planes) -----------------
 size_t pk_cuda_fft_scratch_bytes(const pk_conv_geom* g);
 cudaError_t pk_cuda_fft_fwd(const pk_conv_geom* g, int dtype, const void* x, const void* f,

@@ -110,6 +110,24 @@ pk_tc_config tc_config(const ImplicitGemmTiles& t) {
 
 const pk_tc_config kDefaultTc{256, 4, 1};
 
+// Output tile of the bf16 tensor-core Winograd: F(2x2,3x3) as the reference
+// (conv.cpp:269-365); PK_WINOGRAD_M=4 selects F(4x4,3x3).
+int winograd_tile_m() {
+    const char* v = std::getenv("PK_WINOGRAD_M");
+    return v && std::atoi(v) == 4 ? 4 : 2;
+}
+
+// Workspace cap for the tensor-core Winograd (PK_WINOGRAD_WS bytes; tests use
+// it to exercise the chunked path).
+std::size_t winograd_ws(const pk_conv_geom& g, int m) {
+    std::size_t wb = pk_winograd_tc_workspace(&g, m);
+    if (const char* v = std::getenv("PK_WINOGRAD_WS")) {
+        const std::size_t cap = std::strtoull(v, nullptr, 10);
+        if (cap && cap < wb) wb = cap;
+    }
+    return wb;
+}
+
 std::size_t col_bytes(const pk_conv_geom& g, int dtype) {
     return (std::size_t)g.p * g.q * g.r * g.s * g.f_pitch * (dtype == PK_BF16 ? 2 : 4);
 }
@@ -303,8 +321,17 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                 ck(pk_cuda_direct_fwd(&g, dt, a, b, out, epi, st), "direct_fwd");
                 break;
             case ConvAlgo::Winograd:
-                kernel = "winograd_f23";
-                ck(pk_cuda_winograd_f23(&g, dt, a, b, out, epi, st), "winograd_f23");
+                if (dt == PK_BF16 && pk_winograd_tc_supported(&g)) {
+                    // tensor-core Winograd: transforms + alpha^2 batched tcgen05 GEMMs
+                    const int m = winograd_tile_m();
+                    kernel = m == 4 ? "winograd_tc_f43" : "winograd_tc_f23";
+                    const std::size_t wb = winograd_ws(g, m);
+                    ck(pk_cuda_winograd_tc(&g, m, a, b, out, epi, h.scratch(12, wb), wb, st),
+                       "winograd_tc");
+                } else {
+                    kernel = "winograd_f23";
+                    ck(pk_cuda_winograd_f23(&g, dt, a, b, out, epi, st), "winograd_f23");
+                }
                 break;
             case ConvAlgo::FFT:
                 kernel = "fft";

@@ -1,0 +1,100 @@
+"""Tensor-core Winograd (bf16): F(2x2,3x3) — the reference's algorithm
+(proj/src/core/conv.cpp:269-365) — and F(4x4,3x3), transforms on CUDA cores,
+the alpha^2 element-wise products as one batched tcgen05 GEMM launch.
+
+Checked through the C ABI (`primkit_conv_run`, solver "Winograd") against the
+fp32 oracle on the same bf16-rounded inputs: <= 1e-2 relative L2 (north_star
+bf16 tolerance), outputs exactly bf16 values, edge tiles cropped, pad lanes
+zero, and the chunked-workspace path equal to the single-chunk result."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1910_00078_b200 import abi
+from paper_1910_00078_b200.primkit import problem
+
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+# F(2,3): the north_star bf16 tolerance. F(4,3) with bf16 GEMM operands is
+# numerically outside it (each of the V, U, M roundings alone costs ~1.8e-2
+# relative L2 through the 6x6 transforms: measured 2.9e-2 on the B200), so the
+# Winograd solver never selects it; it is opt-in (PK_WINOGRAD_M=4) and held
+# to its own measured bound here.
+TOL = {2: 1e-2, 4: 5e-2}
+
+SHAPES = [
+    dict(n=2, c=64, h=14, w=14, k=64, y=3, x=3, pad=1),
+    dict(n=1, c=3, h=17, w=13, k=5, y=3, x=3, pad=1),      # pitch-8 channels, odd edges
+    dict(n=2, c=24, h=9, w=11, k=40, y=3, x=3, pad=0),     # no padding, ragged tiles
+    dict(n=1, c=128, h=28, w=28, k=256, y=3, x=3, pad=1),
+    dict(n=3, c=256, h=7, w=7, k=128, y=3, x=3, pad=1),
+    dict(n=1, c=16, h=3, w=3, k=8, y=3, x=3, pad=1),        # single tile
+]
+
+
+@pytest.fixture
+def wino_env():
+    saved = {k: os.environ.get(k) for k in ("PK_WINOGRAD_M", "PK_WINOGRAD_WS")}
+    yield os.environ
+    for k, v in saved.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
+
+
+def _run(lib, p, x, w):
+    h = lib.handle()
+    y = h.conv_run(p, "Winograd", x, w)
+    return y, h.last_kernel()
+
+
+@pytest.mark.parametrize("m", [2, 4])
+@pytest.mark.parametrize("si", range(len(SHAPES)))
+def test_winograd_tc_parity(lib, wino_env, m, si):
+    wino_env["PK_WINOGRAD_M"] = str(m)
+    rng = np.random.default_rng(40 + si)
+    s = SHAPES[si]
+    p = problem(**s, etype=abi.BF16)
+    x = oracle.round_bf16(rng.uniform(-1, 1, (s["n"], s["c"], s["h"], s["w"])).astype(np.float32))
+    w = oracle.round_bf16(rng.uniform(-1, 1, (s["k"], s["c"], 3, 3)).astype(np.float32))
+    y, kern = _run(lib, p, x, w)
+    assert kern == f"winograd_tc_f{m}3", kern
+    want = oracle.conv_forward(p, x, w)
+    assert y.shape == want.shape
+    err = rel_l2(y, want)
+    assert err <= TOL[m], f"F({m},3) rel-L2 {err:.3e}"
+    assert np.array_equal(oracle.round_bf16(y), y)
+
+
+@pytest.mark.parametrize("m", [2, 4])
+def test_winograd_tc_chunked(lib, wino_env, m):
+    """A workspace cap forces several tile chunks; results must not change."""
+    wino_env["PK_WINOGRAD_M"] = str(m)
+    rng = np.random.default_rng(7)
+    p = problem(n=4, c=32, h=30, w=30, k=48, y=3, x=3, pad=1, etype=abi.BF16)
+    x = oracle.round_bf16(rng.uniform(-1, 1, (4, 32, 30, 30)).astype(np.float32))
+    w = oracle.round_bf16(rng.uniform(-1, 1, (48, 32, 3, 3)).astype(np.float32))
+    full, _ = _run(lib, p, x, w)
+    al = (m + 2) ** 2
+    per_tile = al * (32 + 48) * 2
+    wino_env["PK_WINOGRAD_WS"] = str(al * 48 * 32 * 2 + 256 + 128 * per_tile + 5)
+    chunked, _ = _run(lib, p, x, w)
+    assert np.array_equal(full, chunked)
+    assert rel_l2(full, oracle.conv_forward(p, x, w)) <= TOL[m]
+
+
+def test_winograd_tc_counters_keep_reference_semantics(lib, ref):
+    """The op counters stay the reference's (16 multiplies per tile, channel, k)."""
+    rng = np.random.default_rng(3)
+    p = problem(n=1, c=8, h=6, w=6, k=8, y=3, x=3, pad=1, etype=abi.BF16)
+    x = oracle.round_bf16(rng.uniform(-1, 1, (1, 8, 6, 6)).astype(np.float32))
+    w = oracle.round_bf16(rng.uniform(-1, 1, (8, 8, 3, 3)).astype(np.float32))
+    h, hr = lib.handle(), ref.handle()
+    h.conv_run(p, "Winograd", x, w)
+    hr.conv_run(p, "Winograd", x, w)
+    assert h.counters() == hr.counters()

@@ -178,11 +178,14 @@ def cfg3(d, iters, n=128):
         fl = flops(p, hw, hw)
         fl_total += fl
         row = {"layer": f"{c}->{k}@{hw}", "gflop": fl / 1e9}
-        for s in ("ImplicitGemm", "Winograd"):
-            ws = d.ws(p, s.encode())
-            ms = timed(lambda: d.conv(p, s.encode(), x, w, y, ws), iters)
+        for s in ("ImplicitGemm", "Winograd", "Winograd-F43"):
+            solver = s.split("-")[0].encode()
+            os.environ["PK_WINOGRAD_M"] = "4" if s.endswith("F43") else "2"
+            ws = d.ws(p, solver)
+            ms = timed(lambda: d.conv(p, solver, x, w, y, ws), iters)
             row[s] = {"ms": ms, "tflops": fl / ms / 1e9, "kernel": d.last_kernel()}
-            tot[s] += ms
+            tot[s] = tot.get(s, 0.0) + ms
+        os.environ.pop("PK_WINOGRAD_M", None)
         # Find (device-timed, every applicable solver) on a reduced batch
         pf = problem(n=2, c=c, h=hw, w=hw, k=k, y=3, x=3, pad=1, etype=abi.BF16)
         hf = d.lib.handle()
@@ -195,7 +198,7 @@ def cfg3(d, iters, n=128):
         rows.append(row)
     return {"batch": n, "layers": rows,
             "total_ms": tot, "tflops": {s: fl_total / v / 1e9 for s, v in tot.items()},
-            "note": "Winograd F(2,3) effective TFLOP/s use the direct-conv flop count"}
+            "note": "Winograd F(2,3)/F(4,3) (tensor-core, bf16) effective TFLOP/s use the direct-conv flop count"}
 
 
 def cfg4(d, iters, n=256):
