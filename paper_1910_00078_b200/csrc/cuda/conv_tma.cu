@@ -52,6 +52,7 @@ struct TmaConvArgs {
     int qbw, qbh, qbn;        // per-epilogue-warp quarter sub-box
     int n_tiles_n, total_tiles;
     int num_phases;
+    int phase_tma;            // PHASED: 1 = per-phase TMA store maps (num_phases <= kStoreMaps)
     int ph_tw[kMaxPhases], ph_th[kMaxPhases], ph_tn[kMaxPhases];
     int ph_tile_start[kMaxPhases + 1];
     int ph_hp[kMaxPhases], ph_wp[kMaxPhases], ph_h0[kMaxPhases], ph_w0[kMaxPhases];
@@ -76,6 +77,14 @@ struct FSmem {
 
 struct RectInfo {
     int phase, n0, h0, w0, nt, ntaps, tap0;
+};
+
+// Output store maps: one 4-D map per sub-pixel phase (strided views of dX,
+// so phased backward-data tiles also leave through TMA stores); only m[0]
+// for unphased convolutions.
+constexpr int kStoreMaps = 4;
+struct alignas(64) YMaps {
+    CUtensorMap m[kStoreMaps];
 };
 
 __device__ __forceinline__ RectInfo rect_info(const TmaConvArgs& g, int t) {
@@ -110,7 +119,7 @@ template <int BN, int STAGES, bool PHASED, bool NARROW>
 __global__ void __launch_bounds__(kFpropThreads, 1)
     conv_tma_fprop_kernel(const __grid_constant__ CUtensorMap amap,
                           const __grid_constant__ CUtensorMap bmap,
-                          const __grid_constant__ CUtensorMap ymap, __nv_bfloat16* __restrict__ out,
+                          const __grid_constant__ YMaps ymaps, __nv_bfloat16* __restrict__ out,
                           const __grid_constant__ TmaConvArgs g, const pk_epilogue epi) {
     using L = FSmem<BN, STAGES>;
     extern __shared__ uint8_t smem_raw[];
@@ -137,7 +146,8 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
         fence_barrier_init();
         tma_prefetch(&amap);
         tma_prefetch(&bmap);
-        if (!PHASED) tma_prefetch(&ymap);
+        if (!PHASED || g.phase_tma)
+            for (int i = 0; i < (PHASED ? g.num_phases : 1); ++i) tma_prefetch(&ymaps.m[i]);
     }
     if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
     tc_fence_before();
@@ -244,6 +254,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
         uint8_t* stg_base = smem + L::kStagingOff + ew * L::kStgBufs * 4096;
         int sbuf = 0;
         const bool has_epi = epilogue_active(&epi);
+        const bool tma_st = !PHASED || g.phase_tma;
         BnStatAcc bacc;
         bacc.init();
         // this lane's row inside the rectangle, and the quarter's sub-box origin
@@ -304,7 +315,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                     for (int e = 0; e < 64; ++e) v[e] = 0u;
                 }
                 const uint32_t stg_u = smem_u32(stg_base + sbuf * 4096);
-                if (!PHASED) {
+                if (tma_st) {
                     if (lane == 0) {
                         if (L::kStgBufs == 2)
                             bulk_wait_read<1>();
@@ -318,11 +329,11 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                 for (int e = 0; e < 64; ++e) xf[e] = __uint_as_float(v[e]);
                 if (has_epi) epilogue_chunk64(epi, xf, n0c + c0, g.n_out, oy, ox, g.Ho, g.Wo);
                 pack_stage64(xf, stg_u, lane, min(g.n_out - (n0c + c0), BN - c0));
-                if (!PHASED) {
+                if (tma_st) {
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        tma_store_4d(&ymap, stg_u, n0c + c0, ri.w0 + qw, ri.h0 + qh, ri.n0 + qn);
+                        tma_store_4d(&ymaps.m[PHASED ? ri.phase : 0], stg_u, n0c + c0, ri.w0 + qw, ri.h0 + qh, ri.n0 + qn);
                         bulk_commit();
                     }
                     if (epi.stats && live)
@@ -355,7 +366,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
             }
         }
         if (epi.stats) bacc.finish(epi, lane, g.n_out);
-        if (!PHASED && lane == 0) bulk_wait_all();
+        if (tma_st && lane == 0) bulk_wait_all();
     }
     tc_fence_before();
     __syncthreads();
@@ -615,7 +626,7 @@ __global__ void wgrad_sum_kernel(const float* __restrict__ partial, int splits, 
 // host
 
 template <int BN, int STAGES, bool PHASED, bool NARROW>
-cudaError_t launch_fprop(const CUtensorMap& amap, const CUtensorMap& bmap, const CUtensorMap& ymap,
+cudaError_t launch_fprop(const CUtensorMap& amap, const CUtensorMap& bmap, const YMaps& ymap,
                          void* out, const TmaConvArgs& g, const pk_epilogue& e, cudaStream_t st) {
     using L = FSmem<BN, STAGES>;
     auto kern = conv_tma_fprop_kernel<BN, STAGES, PHASED, NARROW>;
@@ -638,7 +649,7 @@ cudaError_t launch_fprop(const CUtensorMap& amap, const CUtensorMap& bmap, const
 
 template <bool PHASED, bool NARROW>
 cudaError_t dispatch_fprop(int bn, const CUtensorMap& amap, const CUtensorMap& bmap,
-                           const CUtensorMap& ymap, void* out, const TmaConvArgs& g,
+                           const YMaps& ymap, void* out, const TmaConvArgs& g,
                            const pk_epilogue& e, cudaStream_t st) {
     if (bn == 64) return launch_fprop<64, 6, PHASED, NARROW>(amap, bmap, ymap, out, g, e, st);
     if (bn == 128) return launch_fprop<128, 5, PHASED, NARROW>(amap, bmap, ymap, out, g, e, st);
@@ -758,7 +769,8 @@ cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, cons
     if (!fill_phases(t, g->n, t.Ho, t.Wo, sh, sw, g->r, g->s, g->pad_h, g->pad_w, g->dil_h,
                      g->dil_w, dgrad))
         return cudaErrorNotSupported;
-    CUtensorMap amap{}, bmap{}, ymap{};
+    CUtensorMap amap{}, bmap{};
+    YMaps ymap{};
     const int Hs = dgrad ? g->p : g->h, Ws = dgrad ? g->q : g->w;
     if (!tc::make_map_nhwc(&amap, src, g->n, Hs, Ws, src_pitch, t.bw, t.bh, t.bn, t.mult_w,
                            t.mult_h, narrow ? 8 : 64))
@@ -767,8 +779,24 @@ cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, cons
     if (!tc::make_map_2d(&bmap, filt, t.n_out, kred, kred, bn)) return cudaErrorInvalidValue;
     const bool phased = sh > 1 || sw > 1;
     if (!phased &&
-        !tc::make_map_nhwc(&ymap, out, g->n, t.Ho, t.Wo, out_pitch, t.qbw, t.qbh, t.qbn))
+        !tc::make_map_nhwc(&ymap.m[0], out, g->n, t.Ho, t.Wo, out_pitch, t.qbw, t.qbh, t.qbn))
         return cudaErrorInvalidValue;
+    if (phased && t.num_phases <= kStoreMaps) {
+        // phase (ph, pw) of dX as a strided 4-D view: dims (pitch, wp, hp, n)
+        t.phase_tma = 1;
+        for (int i = 0; i < t.num_phases; ++i) {
+            if (t.ph_hp[i] == 0 || t.ph_wp[i] == 0) continue;  // no tiles in this phase
+            const void* base = static_cast<const __nv_bfloat16*>(out) +
+                               ((size_t)t.ph_h0[i] * t.Wo + t.ph_w0[i]) * out_pitch;
+            if (!tc::make_map_nhwc_strided(&ymap.m[i], base, g->n, t.ph_hp[i], t.ph_wp[i],
+                                           out_pitch, (long long)sw * out_pitch,
+                                           (long long)sh * t.Wo * out_pitch,
+                                           (long long)t.Ho * t.Wo * out_pitch, t.qbw, t.qbh, t.qbn)) {
+                t.phase_tma = 0;
+                break;
+            }
+        }
+    }
     pk_epilogue e{};
     e.act = -1;
     if (epi) e = *epi;

@@ -70,6 +70,24 @@ inline bool make_map_nhwc(CUtensorMap* map, const void* base, int n, int h, int 
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 4-D bf16 view with explicit element strides per dimension (w, h, n): a
+// sub-pixel phase of an NHWC tensor for TMA stores (box {64, bw, bh, bn}).
+inline bool make_map_nhwc_strided(CUtensorMap* map, const void* base, int n, int h, int w,
+                                  int pitch, long long w_stride, long long h_stride,
+                                  long long n_stride, int bw, int bh, int bn) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)pitch, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+    cuuint64_t strides[3] = {(cuuint64_t)w_stride * 2, (cuuint64_t)h_stride * 2,
+                             (cuuint64_t)n_stride * 2};
+    cuuint32_t box[4] = {64, (cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)bn};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+              box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // 3-D bf16 view of an NHWC tensor as rows of pixels: dims {w*pitch, h, n},
 // box {box_elems, box_rows, 1}, no swizzle (plain rows of box_elems*2 bytes).
 // Used for narrow-channel halos, where a per-pixel (16-byte) inner box
