@@ -40,7 +40,16 @@ constexpr int kThreads = 416;  // 4 producer + 1 MMA + 8 epilogue warps
 constexpr int kMaxPhases = 16;
 constexpr int kMaxTaps = 1024;
 
-enum Mode { GATHER_FWD = 0, GATHER_DGRAD = 1, PHASE_DGRAD = 2, PLAIN = 3 };
+// PLAIN_RES / PLAIN_RES_BIG: plain GEMM with the CTA's whole B slice (filter
+// rows of its fixed N tile, <= kResB bytes) loaded once and kept resident in
+// shared memory; the pipeline stages carry A only. Cuts the TMA traffic of 1x1
+// layers (B was re-read for every 128-pixel tile) to the activations.
+enum Mode { GATHER_FWD = 0, GATHER_DGRAD = 1, PHASE_DGRAD = 2, PLAIN = 3, PLAIN_RES = 4,
+            PLAIN_RES_BIG = 5 };
+template <int MODE>
+constexpr bool is_plain() { return MODE == PLAIN || MODE == PLAIN_RES || MODE == PLAIN_RES_BIG; }
+template <int MODE>
+constexpr bool is_res() { return MODE == PLAIN_RES || MODE == PLAIN_RES_BIG; }
 
 struct ConvTcArgs {
     int M;                 // output rows (non-phase modes)
@@ -63,6 +72,7 @@ struct ConvTcArgs {
     int ph_h0[kMaxPhases], ph_w0[kMaxPhases];
     int ph_tap_start[kMaxPhases + 1];
     unsigned short taps[kMaxTaps];  // (r << 8) | s
+    int debug_nores;       // PK_TC_NORES=1: disable the resident-B plain path (A/B comparisons)
     int debug;             // PK_TC_DEBUG (profiling only): 1 no MMA, 2 no TMEM load, 4 no store, 8 no math
     unsigned long long* trace;  // PK_TC_TRACE: clock64 stamps of CTA 0 (profiling only)
 };
@@ -71,15 +81,19 @@ __device__ __forceinline__ void tcstamp(const ConvTcArgs& g, int it, int ev) {
         g.trace[it * 16 + ev] = clock64();
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int MODE = PLAIN>
 struct Smem {
     static constexpr int kA = BM * BK * 2;
     static constexpr int kB = BN * BK * 2;
-    static constexpr int kStage = kA + kB;
-    static constexpr int kStaging = 8 * 2 * 32 * 128;  // 8 epilogue warps x 2 buffers x 32 x 128 B
-    static constexpr int kStagingOff = STAGES * kStage;
+    static constexpr int kStage = is_res<MODE>() ? kA : kA + kB;
+    // resident B slice (PLAIN_RES*): 64 KB, or 128 KB with single staging
+    static constexpr int kResB = MODE == PLAIN_RES_BIG ? 128 * 1024 : MODE == PLAIN_RES ? 64 * 1024 : 0;
+    static constexpr int kStgBufs = MODE == PLAIN_RES_BIG ? 1 : 2;
+    static constexpr int kResOff = STAGES * kStage;
+    static constexpr int kStaging = 8 * kStgBufs * 32 * 128;  // 8 epilogue warps x bufs x 32 x 128 B
+    static constexpr int kStagingOff = kResOff + kResB;
     static constexpr int kBarOff = kStagingOff + kStaging;
-    static constexpr int kBytes = kBarOff + (2 * STAGES + 4) * 8 + 16 + 1024;
+    static constexpr int kBytes = kBarOff + (2 * STAGES + 5) * 8 + 16 + 1024;
 };
 
 struct TileInfo {
@@ -136,7 +150,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap ymap,
                    const __nv_bfloat16* __restrict__ src, __nv_bfloat16* __restrict__ out,
                    const __grid_constant__ ConvTcArgs g, const pk_epilogue epi) {
-    using L = Smem<BN, STAGES>;
+    using L = Smem<BN, STAGES, MODE>;
+    constexpr bool kPlain = is_plain<MODE>();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -144,7 +159,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* empty = full + STAGES;
     uint64_t* tmem_full = empty + STAGES;   // [2]
     uint64_t* tmem_empty = tmem_full + 2;   // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+    uint64_t* bfull = tmem_empty + 2;       // resident B loaded
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int kAccCols = 2 * BN;  // double-buffered accumulator
@@ -153,16 +169,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < STAGES; ++i) {
-            mbar_init(&full[i], MODE == PLAIN ? 1 : 128 + 1);
+            mbar_init(&full[i], kPlain ? 1 : 128 + 1);
             mbar_init(&empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tmem_full[i], 1);
             mbar_init(&tmem_empty[i], 8);
         }
+        mbar_init(bfull, 1);
         fence_barrier_init();
         tma_prefetch(&bmap);
-        if (MODE == PLAIN) tma_prefetch(&amap);
+        if (kPlain) tma_prefetch(&amap);
         if (MODE != PHASE_DGRAD) tma_prefetch(&ymap);
     }
     if (warp == 4) tmem_alloc(tmem_slot, kTmemCols);
@@ -183,7 +200,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (ti.nkb == 0) continue;
             const int n0 = ti.n0 * BN;
             int row_img[8], row_h[8], row_w[8];
-            if (MODE != PLAIN) {
+            if (!kPlain) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     const int m = ti.m0 + rbase + 4 * i;
@@ -219,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     s = rs & 0xff;
                     c8 = chunk * 8 + j;
                     bcol = (r * g.S + s) * g.red_ch + chunk * BK;
-                } else if (MODE != PLAIN) {
+                } else if (!kPlain) {
                     const int k8 = kb * (BK / 8) + j;
                     kvalid = k8 * 8 < g.kred;
                     if (kvalid) {
@@ -230,14 +247,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 if (threadIdx.x == 0) {
-                    mbar_arrive_expect_tx(&full[stage], MODE == PLAIN ? L::kA + L::kB : L::kB);
-                    const int brow = MODE == PLAIN && g.b_batch_mtiles
-                                         ? (ti.m0 / BM / g.b_batch_mtiles) * g.b_batch_rows
-                                         : 0;
-                    tma_load_2d(smem_u32(sa + L::kA), &bmap, &full[stage], bcol, n0 + brow);
-                    if (MODE == PLAIN) tma_load_2d(smem_u32(sa), &amap, &full[stage], kb * BK, ti.m0);
+                    if (is_res<MODE>()) {
+                        if (t == (int)blockIdx.x && kb == 0) {
+                            // this CTA's N tile never changes (grid % n_tiles_n == 0):
+                            // load its whole B slice once
+                            mbar_arrive_expect_tx(bfull, ti.nkb * L::kB);
+                            for (int k = 0; k < ti.nkb; ++k)
+                                tma_load_2d(smem_u32(smem + L::kResOff + k * L::kB), &bmap, bfull,
+                                            k * BK, n0);
+                        }
+                        mbar_arrive_expect_tx(&full[stage], L::kA);
+                    } else {
+                        mbar_arrive_expect_tx(&full[stage], kPlain ? L::kA + L::kB : L::kB);
+                        const int brow = kPlain && g.b_batch_mtiles
+                                             ? (ti.m0 / BM / g.b_batch_mtiles) * g.b_batch_rows
+                                             : 0;
+                        tma_load_2d(smem_u32(sa + L::kA), &bmap, &full[stage], bcol, n0 + brow);
+                    }
+                    if (kPlain) tma_load_2d(smem_u32(sa), &amap, &full[stage], kb * BK, ti.m0);
                 }
-                if (MODE != PLAIN) {
+                if (!kPlain) {
                     const uint32_t sa_u = smem_u32(sa);
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
@@ -285,6 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
+        if (is_res<MODE>() && (int)blockIdx.x < g.total_tiles) mbar_wait(bfull, 0);
         for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
             const TileInfo ti = tile_info<MODE>(g, t);
             if (ti.nkb == 0) continue;
@@ -303,7 +333,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 {
                     fence_proxy_async_smem();
                     const uint32_t a_base = smem_u32(smem + stage * L::kStage);
-                    const uint32_t b_base = a_base + L::kA;
+                    const uint32_t b_base = is_res<MODE>()
+                                                ? smem_u32(smem + L::kResOff + kb * L::kB)
+                                                : a_base + L::kA;
                     const uint64_t ad0 = umma_desc_sw128(a_base, 16, 1024);
                     const uint64_t bd0 = umma_desc_sw128(b_base, 16, 1024);
                     if (!(g.debug & 1))
@@ -327,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ew = warp - 5;
         const int q = warp & 3;
         const int half = ew >> 2;
-        uint8_t* stg_base = smem + L::kStagingOff + ew * 2 * 4096;
+        uint8_t* stg_base = smem + L::kStagingOff + ew * L::kStgBufs * 4096;
         int sbuf = 0;
         const bool has_epi = epilogue_active(&epi);
         BnStatAcc bacc;
@@ -397,7 +429,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (kTmaStore) {
                     // the store issued from this buffer two chunks ago must have
                     // finished reading it
-                    if (lane == 0) bulk_wait_read<1>();
+                    if (lane == 0) {
+                        if (L::kStgBufs == 2)
+                            bulk_wait_read<1>();
+                        else
+                            bulk_wait_read<0>();
+                    }
                     __syncwarp();
                 }
                 // math + pack into the swizzled staging row of this lane
@@ -423,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         bacc.add(epi, stg_u, lane, my_m < ti.rows, pix, (ci >> 1) & 1, n0 + c0,
                                  g.n_out, g.out_pitch);
                     }
-                    sbuf ^= 1;
+                    if (L::kStgBufs == 2) sbuf ^= 1;
                     if (warp == 5) tcstamp(g, it - 1, 7 + (ci >> 1));
                 } else {
                     __syncwarp();
@@ -474,7 +511,8 @@ template <int BN, int STAGES, int MODE>
 cudaError_t launch(const CUtensorMap& amap, const CUtensorMap& bmap, const CUtensorMap& ymap,
                    const void* src, void* out, const ConvTcArgs& g, const pk_epilogue& e,
                    cudaStream_t st) {
-    using L = Smem<BN, STAGES>;
+    using L = Smem<BN, STAGES, MODE>;
+    static_assert(L::kBytes <= 227 * 1024, "smem");
     auto kern = conv_tc_kernel<BN, STAGES, MODE>;
     static int attr_dev = -1;
     int dev = 0;
@@ -486,6 +524,7 @@ cudaError_t launch(const CUtensorMap& amap, const CUtensorMap& bmap, const CUten
         attr_dev = dev;
     }
     int grid = num_sms_of_current_device();
+    if (is_res<MODE>()) grid = grid / g.n_tiles_n * g.n_tiles_n;  // fixed N tile per CTA
     if (g.total_tiles < grid) grid = g.total_tiles;
     if (grid < 1) grid = 1;
     kern<<<grid, kThreads, L::kBytes, st>>>(amap, bmap, ymap, (const __nv_bfloat16*)src,
@@ -511,6 +550,20 @@ cudaError_t dispatch_bn(int bn, const CUtensorMap& amap, const CUtensorMap& bmap
     if (MODE != PHASE_DGRAD &&
         !tc::make_map_2d(&ymap, out, g.M, g.out_pitch, g.out_pitch, 32))
         return cudaErrorInvalidValue;
+    if (MODE == PLAIN && !g.b_batch_mtiles && !g.debug_nores && bn >= 64) {
+        // resident B slice when it fits (num_kb x BN x 128 bytes)
+        const long long resb = (long long)g.num_kb * bn * BK * 2;
+        if (resb <= 64 * 1024) {
+            if (bn == 64) return launch<64, 6, PLAIN_RES>(amap, bmap, ymap, src, out, g, e, st);
+            if (bn == 128) return launch<128, 6, PLAIN_RES>(amap, bmap, ymap, src, out, g, e, st);
+            return launch<256, 6, PLAIN_RES>(amap, bmap, ymap, src, out, g, e, st);
+        }
+        if (resb <= 128 * 1024) {
+            if (bn == 64) return launch<64, 4, PLAIN_RES_BIG>(amap, bmap, ymap, src, out, g, e, st);
+            if (bn == 128) return launch<128, 4, PLAIN_RES_BIG>(amap, bmap, ymap, src, out, g, e, st);
+            return launch<256, 4, PLAIN_RES_BIG>(amap, bmap, ymap, src, out, g, e, st);
+        }
+    }
     if (bn == 32) return launch<32, 8, MODE>(amap, bmap, ymap, src, out, g, e, st);
     if (bn == 64) return launch<64, 6, MODE>(amap, bmap, ymap, src, out, g, e, st);
     if (bn == 128) return launch<128, 5, MODE>(amap, bmap, ymap, src, out, g, e, st);
@@ -532,6 +585,7 @@ void base_args(ConvTcArgs& t, int bn) {
         return v ? std::atoi(v) : 0;
     }();
     t.debug = dbg;
+    t.debug_nores = std::getenv("PK_TC_NORES") != nullptr;
     static unsigned long long* trace = [] {
         unsigned long long* p = nullptr;
         if (std::getenv("PK_TC_TRACE")) cudaMalloc(&p, 32 * 16 * 8);
