@@ -408,7 +408,18 @@ def layer_report(torch, lib, handle, net, peaks, path):
         for d, (a, b, o) in ((0, (x, w, y)), (1, (dy, w, dx)), (2, (dy, x, dw))):
             p, s = probs[d]
             run_conv(lib, handle, p, s, a, b, o, net.ws)
-            ms = time_region(torch, lambda: run_conv(lib, handle, p, s, a, b, o, net.ws), 10) / 10
+            eager_ms = time_region(torch, lambda: run_conv(lib, handle, p, s, a, b, o, net.ws), 10) / 10
+            # device time without host launch overhead: 10 launches in one graph
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                lib.check(lib.lib.primkit_handle_set_stream(
+                    handle.ptr, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+                for _ in range(10):
+                    run_conv(lib, handle, p, s, a, b, o, net.ws)
+            lib.check(lib.lib.primkit_handle_set_stream(
+                handle.ptr, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+            g.replay()
+            ms = time_region(torch, g.replay, 3) / 30
             fl = L.flops(net.n)
             byts = 2 * (a.numel() + b.numel() + o.numel())
             bound_ms = max(fl / tc, byts / hbm) * 1e3
@@ -416,7 +427,8 @@ def layer_report(torch, lib, handle, net, peaks, path):
             lib.lib.primkit_handle_last_kernel(handle.ptr, kname, 64)
             rows.append({"layer": L.name, "dir": ["fwd", "bwd_data", "bwd_weights"][d],
                          "c": L.c, "k": L.k, "h": L.h, "r": L.r, "stride": L.stride,
-                         "kernel": kname.value.decode(), "ms": ms, "tflops": fl / ms / 1e9,
+                         "kernel": kname.value.decode(), "ms": ms, "eager_ms": eager_ms,
+                         "tflops": fl / ms / 1e9,
                          "roofline_ms": bound_ms, "frac_of_roofline": bound_ms / ms,
                          "bound": "tensor" if fl / tc > byts / hbm else "hbm"})
     with open(path, "w") as f:
