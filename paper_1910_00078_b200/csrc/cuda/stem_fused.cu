@@ -827,6 +827,8 @@ struct DgArgs {
     int tiles_w, tiles_h, total_tiles;
     int npad;                   // MMA N = roundup(taps*4, 16)
     int cstride;                // colg row stride (words, odd)
+    int v2;                     // 1: pipelined kernel (halo <= one M tile)
+    int debug;                  // PK_STEM_DEBUG (v2, profiling only): 1 no MMA, 2 no drain, 4 no gather
     unsigned long long* trace;  // PK_STEM_TRACE (profiling only)
 };
 __device__ __forceinline__ void dstamp(const DgArgs& g, int it, int ev) {
@@ -1075,6 +1077,249 @@ __global__ void __launch_bounds__(kDgThreads, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// backward data, pipelined (v2): the halo of a tile fits one M=128 MMA, so the
+// TMEM accumulator and the colg buffer are both double-buffered and the three
+// stages run on separate warps, overlapping tile by tile:
+//   warp 0     dY halo TMA (one tile ahead) + MMA issue into TMEM[buf]
+//   warps 1-8  drain TMEM[buf] (lane quarter = warp % 4, column halves split
+//              between the two warps of a quarter) -> colg[buf] (fp32)
+//   warps 9-16 gather colg[buf] -> dX (each dX pixel sums its taps; bf16 store)
+constexpr int kDg2Threads = 32 * 17;
+constexpr int kDg2Stages = 3;    // dY halo ring: two tiles of TMA latency in flight
+constexpr int kDg2Prefetch = 0;  // L2 prefetch distance beyond the ring (measured: no gain)
+
+struct Dg2Layout {
+    int a_stage, b_off, colg_off, colg_bytes, bar_off, bytes;
+    __host__ __device__ Dg2Layout(const DgArgs& g) {
+        a_stage = kTile * 128;                      // 128 halo pixels x 64 dY channels
+        b_off = kDg2Stages * a_stage;
+        colg_off = b_off + (g.npad * 128 + 1023) / 1024 * 1024;
+        colg_bytes = (g.HY * g.WX * g.cstride * 4 + 127) / 128 * 128;
+        bar_off = colg_off + 2 * colg_bytes;
+        bytes = bar_off + 128 + 1024;
+    }
+};
+
+template <int C, int KR, int KS, int KSH, int KSW>
+__global__ void __launch_bounds__(kDg2Threads, 1)
+    stem_dgrad2_kernel(const __grid_constant__ CUtensorMap dymap, const __nv_bfloat16* __restrict__ w,
+                       __nv_bfloat16* __restrict__ dx, const __grid_constant__ DgArgs g) {
+    const Dg2Layout L(g);
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+    uint64_t* a_empty = a_full + kDg2Stages;
+    uint64_t* tmem_full = a_empty + kDg2Stages;
+    uint64_t* tmem_empty = tmem_full + 2;
+    uint64_t* colg_full = tmem_empty + 2;
+    uint64_t* colg_empty = colg_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(colg_empty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kDg2Stages; ++i) {
+            mbar_init(&a_full[i], 1);
+            mbar_init(&a_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tmem_full[i], 1);
+            mbar_init(&tmem_empty[i], 8);
+            mbar_init(&colg_full[i], 256);
+            mbar_init(&colg_empty[i], 256);
+        }
+        fence_barrier_init();
+        tma_prefetch(&dymap);
+    }
+    if (warp == 0) tmem_alloc(tmem_slot, 512);
+    // packed filter B[kc][k] (kc = tap*C + c dense, K-major SWIZZLE_128B, 64 k = one atom):
+    // the accumulator row of a halo pixel is then exactly its colg row
+    for (int i = threadIdx.x; i < g.npad * 8; i += blockDim.x) {
+        const int kc = i >> 3, j = i & 7;
+        const int tap = kc / C, c = kc - tap * C;
+        __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int k = j * 8 + e;
+            v[e] = (tap < g.taps && c < g.C && k < g.K)
+                       ? w[((size_t)k * g.taps + tap) * g.x_pitch + c]
+                       : __float2bfloat16_rn(0.0f);
+        }
+        st_shared_v4(smem_u32(smem + L.b_off) + kc * 128 + ((j ^ (kc & 7)) << 4),
+                     *reinterpret_cast<const uint4*>(v));
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- TMA producer + MMA issuer --------------------------------
+        const uint32_t box_bytes = g.HY * g.WX * 128;
+        const uint32_t idesc = idesc_bf16_f32(kTile, g.npad, false, false);
+        const uint64_t bd0 = umma_desc_sw128(smem_u32(smem + L.b_off), 16, 1024);
+        auto load = [&](int tt, int buf) {
+            int n, Y0, X0;
+            dg_tile(g, tt, n, Y0, X0);
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&a_full[buf], box_bytes);
+                tma_load_4d(smem_u32(smem + buf * L.a_stage), &dymap, &a_full[buf], 0,
+                            X0 / g.sw + g.ox_lo0, Y0 / g.sh + g.oy_lo0, n);
+            }
+        };
+        auto prefetch = [&](int tt) {
+            int n, Y0, X0;
+            dg_tile(g, tt, n, Y0, X0);
+            if (lane == 0)
+                tma_prefetch_4d(&dymap, 0, X0 / g.sw + g.ox_lo0, Y0 / g.sh + g.oy_lo0, n);
+        };
+        // L2 prefetch runs kDg2Prefetch tiles ahead of the smem loads
+        for (int j = kDg2Stages - 1; j < kDg2Stages - 1 + kDg2Prefetch; ++j)
+            if ((int)blockIdx.x + j * (int)gridDim.x < g.total_tiles) prefetch(blockIdx.x + j * gridDim.x);
+        (void)prefetch;
+        // ring of kDg2Stages halo buffers: tile j uses stage j % S (use count j / S)
+        for (int j = 0; j < kDg2Stages - 1; ++j)
+            if ((int)blockIdx.x + j * (int)gridDim.x < g.total_tiles)
+                load(blockIdx.x + j * gridDim.x, j);
+        int i = 0;
+        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++i) {
+            const int buf = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            const int jn = i + kDg2Stages - 1;  // tile to prefetch now
+            if (t + (kDg2Stages - 1) * (int)gridDim.x < g.total_tiles) {
+                if (jn >= kDg2Stages) mbar_wait(&a_empty[jn % kDg2Stages], ((jn / kDg2Stages) - 1) & 1);
+                load(t + (kDg2Stages - 1) * gridDim.x, jn % kDg2Stages);
+            }
+            if (kDg2Prefetch && t + (kDg2Stages - 1 + kDg2Prefetch) * (int)gridDim.x < g.total_tiles)
+                prefetch(t + (kDg2Stages - 1 + kDg2Prefetch) * gridDim.x);
+            const int as = i % kDg2Stages;
+            mbar_wait(&a_full[as], (i / kDg2Stages) & 1);
+            mbar_wait(&tmem_empty[buf], ph ^ 1);
+            tc_fence_after();
+            const uint64_t ad0 = umma_desc_sw128(smem_u32(smem + as * L.a_stage), 16, 1024);
+            if (!(g.debug & 1))
+                mma4_bf16(tmem_base + buf * 256, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + 2,
+                          bd0 + 4, bd0 + 6, idesc, 0);
+            mma_commit_elect(&a_empty[as]);
+            mma_commit_elect(&tmem_full[buf]);
+            __syncwarp();
+        }
+    } else if (warp <= 8) {
+        // ---------------- drain: TMEM[buf] -> colg[buf] ----------------------------
+        const int q = warp & 3, half = (warp - 1) >> 2;
+        const int rows = g.HY * g.WX;
+        const int row = q * 32 + lane;
+        const int nall = g.npad / 16, nh = ((nall + 1) / 2 + 1) & ~1;  // even split point
+        const int cb0 = half ? nh : 0, nch = half ? nall : (nh < nall ? nh : nall);
+        int i = 0;
+        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++i) {
+            const int buf = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            mbar_wait(&tmem_full[buf], ph);
+            tc_fence_after();
+            mbar_wait(&colg_empty[buf], ph ^ 1);
+            const uint32_t dst = smem_u32(smem + L.colg_off + buf * L.colg_bytes) + row * g.cstride * 4;
+            const bool live = row < rows && !(g.debug & 2);
+            const uint32_t ta0 = tmem_base + buf * 256 + (static_cast<uint32_t>(q * 32) << 16);
+            int cb = cb0;
+#pragma unroll 1
+            for (; cb + 2 <= nch; cb += 2) {
+                uint32_t v[32];
+                tmem_ld16(ta0 + cb * 16, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+                tmem_ld16(ta0 + cb * 16 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+                tmem_ld_wait();
+                if (live) {
+#pragma unroll
+                    for (int q4 = 0; q4 < 8; ++q4)
+                        if (cb * 16 + q4 * 4 < g.cstride)
+                            st_shared_v4(dst + (cb * 16 + q4 * 4) * 4,
+                                         make_uint4(v[q4 * 4], v[q4 * 4 + 1], v[q4 * 4 + 2], v[q4 * 4 + 3]));
+                }
+            }
+            if (cb < nch) {
+                uint32_t v[16];
+                tmem_ld16(ta0 + cb * 16, v);
+                tmem_ld_wait();
+                if (live) {
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4)
+                        if (cb * 16 + q4 * 4 < g.cstride)
+                            st_shared_v4(dst + (cb * 16 + q4 * 4) * 4,
+                                         make_uint4(v[q4 * 4], v[q4 * 4 + 1], v[q4 * 4 + 2], v[q4 * 4 + 3]));
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tmem_empty[buf]);
+            mbar_arrive(&colg_full[buf]);
+        }
+    } else {
+        // ---------------- gather: colg[buf] -> dX ---------------------------------
+        const int gt = threadIdx.x - 288;  // 0..255
+        const int sh = KSH ? KSH : g.sh, sw = KSW ? KSW : g.sw, R = KR ? KR : g.R,
+                  S = KS ? KS : g.S;
+        const int WX = g.WX, cs4 = g.cstride * 4, TX = g.TX, npx = g.TY * g.TX;
+        int i = 0;
+        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++i) {
+            const int buf = i & 1;
+            const uint32_t ph = (i >> 1) & 1;
+            int n, Y0, X0;
+            dg_tile(g, t, n, Y0, X0);
+            const int oy_lo = Y0 / g.sh + g.oy_lo0, ox_lo = X0 / g.sw + g.ox_lo0;
+            const uint32_t colg_u = smem_u32(smem + L.colg_off + buf * L.colg_bytes);
+            mbar_wait(&colg_full[buf], ph);
+            for (int px = gt; px < (g.debug & 4 ? 0 : npx); px += 256) {
+                const int iy = Y0 + px / TX, ix = X0 + px % TX;
+                if (iy >= g.H || ix >= g.W) continue;
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                const int r0 = (iy + g.ph) % sh, s0 = (ix + g.pw) % sw;
+                const int lr = (iy + g.ph - r0) / sh - oy_lo, lc = (ix + g.pw - s0) / sw - ox_lo;
+                uint32_t rowa = colg_u + (lr * WX + lc) * cs4 + (r0 * S + s0) * C * 4;
+                if (KR) {
+                    constexpr int NR = KR ? (KR + KSH - 1) / KSH : 1, NS = KS ? (KS + KSW - 1) / KSW : 1;
+#pragma unroll
+                    for (int ri = 0; ri < NR; ++ri) {
+                        const bool rok = r0 + ri * KSH < KR;
+#pragma unroll
+                        for (int si = 0; si < NS; ++si) {
+                            const bool ok = rok && s0 + si * KSW < KS;
+                            const uint32_t a = rowa + ri * (KSH * KS * C * 4 - WX * cs4) +
+                                               si * (KSW * C * 4 - cs4);
+#pragma unroll
+                            for (int c = 0; c < C; ++c)
+                                if (ok) acc[c] += ld_shared_f32(a + c * 4);
+                        }
+                    }
+                } else {
+                    for (int r = r0; r < R; r += sh) {
+                        uint32_t a = rowa;
+                        for (int s2 = s0; s2 < S; s2 += sw) {
+#pragma unroll
+                            for (int c = 0; c < C; ++c) acc[c] += ld_shared_f32(a + c * 4);
+                            a += sw * C * 4 - cs4;
+                        }
+                        rowa += sh * S * C * 4 - WX * cs4;
+                    }
+                }
+                __align__(16) __nv_bfloat16 o[8];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) o[c] = __float2bfloat16_rn(c < 4 ? acc[c & 3] : 0.0f);
+                *reinterpret_cast<uint4*>(dx + (((size_t)n * g.H + iy) * g.W + ix) * g.x_pitch) =
+                    *reinterpret_cast<const uint4*>(o);
+            }
+            mbar_arrive(&colg_empty[buf]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 512);
+    }
+}
+
 __host__ __device__ inline int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
 bool dg_args(const pk_conv_geom* g, DgArgs& a) {
@@ -1089,6 +1334,33 @@ bool dg_args(const pk_conv_geom* g, DgArgs& a) {
     if (2 * a.npad > 512) return false;
     a.cstride = ((a.npad / 4) * a.C) | 1;  // all padded taps stored; odd: conflict-free
     static const int cand[][2] = {{16, 32}, {8, 32}, {16, 16}, {8, 16}, {8, 8}, {4, 8}};
+    // pipelined v2 first: the largest tile whose halo fits one 128-row MMA
+    static const bool v2_off = std::getenv("PK_STEM_DG_V1") != nullptr;
+    for (const auto& c : cand) {
+        if (v2_off || (a.taps * a.C + 15) / 16 * 16 > 256) break;
+        const int TY = c[0], TX = c[1];
+        if (TY % a.sh || TX % a.sw) continue;
+        const int lo_y = -floor_div(-(a.ph - (a.R - 1) * a.dh), a.sh);
+        const int hi_y = floor_div(TY - 1 + a.ph, a.sh);
+        const int lo_x = -floor_div(-(a.pw - (a.S - 1) * a.dw), a.sw);
+        const int hi_x = floor_div(TX - 1 + a.pw, a.sw);
+        const int HY = hi_y - lo_y + 1, WX = hi_x - lo_x + 1;
+        if (HY * WX > kTile || HY > 256 || WX > 256) continue;
+        DgArgs b = a;
+        // v2: dense kc = tap*C + c; colg rows of roundup4(taps*C) words with an odd
+        // number of 16-byte units (conflict-free vector drain stores)
+        b.npad = (a.taps * a.C + 15) / 16 * 16;
+        b.cstride = (a.taps * a.C + 3) / 4 * 4;
+        if ((b.cstride / 4) % 2 == 0) b.cstride += 4;
+        b.TY = TY; b.TX = TX; b.HY = HY; b.WX = WX; b.oy_lo0 = lo_y; b.ox_lo0 = lo_x;
+        b.tiles_w = (b.W + TX - 1) / TX;
+        b.tiles_h = (b.H + TY - 1) / TY;
+        b.total_tiles = b.tiles_w * b.tiles_h * b.N;
+        b.v2 = 1;
+        if (Dg2Layout(b).bytes > 227 * 1024) continue;
+        a = b;
+        return true;
+    }
     for (const auto& c : cand) {
         const int TY = c[0], TX = c[1];
         if (TY % a.sh || TX % a.sw) continue;
@@ -1274,11 +1546,16 @@ cudaError_t pk_cuda_stem_fused_dgrad(const pk_conv_geom* g, const void* dy, cons
         return p;
     }();
     a.trace = trace;
+    if (const char* v = std::getenv("PK_STEM_DEBUG")) a.debug = std::atoi(v);
     auto go = [&](auto kern, int* attr_dev) {
         cudaError_t err = set_smem(kern, 227 * 1024, attr_dev);
         if (err != cudaSuccess) return err;
-        kern<<<grid, kDgThreads, DgLayout(a).bytes, st>>>(dymap, (const __nv_bfloat16*)w,
-                                                          (__nv_bfloat16*)dx, a);
+        if (a.v2)
+            kern<<<grid, kDg2Threads, Dg2Layout(a).bytes, st>>>(dymap, (const __nv_bfloat16*)w,
+                                                                (__nv_bfloat16*)dx, a);
+        else
+            kern<<<grid, kDgThreads, DgLayout(a).bytes, st>>>(dymap, (const __nv_bfloat16*)w,
+                                                              (__nv_bfloat16*)dx, a);
         count_launch();
         if (a.trace) {
             unsigned long long h[32 * 32];
@@ -1293,6 +1570,17 @@ cudaError_t pk_cuda_stem_fused_dgrad(const pk_conv_geom* g, const void* dy, cons
         return cudaGetLastError();
     };
     static int dev0 = -1, dev1 = -1, dev2 = -1, dev3 = -1, dev4 = -1;
+    static int e0 = -1, e1 = -1, e2 = -1, e3 = -1, e4 = -1;
+    if (a.v2) {
+        if (a.C == 3 && a.R == 7 && a.S == 7 && a.sh == 2 && a.sw == 2)  // ResNet conv1
+            return go(stem_dgrad2_kernel<3, 7, 7, 2, 2>, &e0);
+        switch (a.C) {
+            case 1: return go(stem_dgrad2_kernel<1, 0, 0, 0, 0>, &e1);
+            case 2: return go(stem_dgrad2_kernel<2, 0, 0, 0, 0>, &e2);
+            case 3: return go(stem_dgrad2_kernel<3, 0, 0, 0, 0>, &e3);
+            default: return go(stem_dgrad2_kernel<4, 0, 0, 0, 0>, &e4);
+        }
+    }
     if (a.C == 3 && a.R == 7 && a.S == 7 && a.sh == 2 && a.sw == 2)  // ResNet conv1
         return go(stem_dgrad_kernel<3, 7, 7, 2, 2>, &dev0);
     switch (a.C) {
