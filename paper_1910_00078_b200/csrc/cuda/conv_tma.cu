@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                           const __grid_constant__ CUtensorMap xmap, float* __restrict__ partial,
                           const __grid_constant__ TmaWgArgs g) {
     using L = WSmem<NB, STAGES, MT>;
-    constexpr uint32_t kCols = MT * NB;
+    constexpr uint32_t kCols = MT * NB <= 128 ? 128 : MT * NB <= 256 ? 256 : 512;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -467,11 +467,15 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 const int q0 = wi * g.rw, p0 = hi * g.rh, img0 = ni * g.rn;
                 mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sa = smem + stage * L::kStage;
-                mbar_arrive_expect_tx(&full[stage], L::kA + L::kB);
+                // dY atoms past K (e.g. K = 64 in an M = 128 tile) are not loaded:
+                // the MMA rows they feed are never stored
+                const int a_atoms = min(2 * MT, (g.K - m0 + 63) / 64);
+                mbar_arrive_expect_tx(&full[stage], a_atoms * L::kAtom + L::kB);
 #pragma unroll
                 for (int j = 0; j < 2 * MT; ++j)
-                    tma_load_4d(smem_u32(sa + j * L::kAtom), &dymap, &full[stage], m0 + 64 * j, q0, p0,
-                                img0);
+                    if (j < a_atoms)
+                        tma_load_4d(smem_u32(sa + j * L::kAtom), &dymap, &full[stage], m0 + 64 * j,
+                                    q0, p0, img0);
 #pragma unroll
                 for (int a = 0; a < kAtoms; ++a)
                     tma_load_4d(smem_u32(sa + L::kA + a * L::kAtom), &xmap, &full[stage], bc[a],
@@ -826,12 +830,16 @@ static WgTile wgrad_tile(const pk_conv_geom* g) {
     static const char* env = std::getenv("PK_WG_TILE");
     const int nn = g->r * g->s * g->x_pitch;
     WgTile t{nn >= 256 ? 256 : 128, g->k >= 256 ? 2 : 1};
+    // 3 taps x 64 channels (3x3 filters on 64-channel inputs): 192-wide tiles
+    // cover the 576 filter positions exactly (256-wide ones waste 25%)
+    if (nn % 256 != 0 && nn % 192 == 0 && nn <= 768 && t.mt == 1) t.nb = 192;
     // measured (B200, all ResNet-50 layers): 1x1 stride-1 layers are fastest
     // with 128-wide filter tiles (smaller fp32 partials to drain and sum)
     if (g->r == 1 && g->s == 1 && g->str_h == 1 && g->str_w == 1) t.nb = 128;
     if (env) {
         int nb = 0, mt = 0;
-        if (std::sscanf(env, "%dx%d", &nb, &mt) == 2 && (nb == 128 || nb == 256) && (mt == 1 || mt == 2))
+        if (std::sscanf(env, "%dx%d", &nb, &mt) == 2 && (nb == 128 || nb == 256 || (nb == 192 && mt == 1)) &&
+            (mt == 1 || mt == 2))
             t = {nb, mt};
     }
     return t;
@@ -940,6 +948,8 @@ cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, v
     if (wt.mt == 2)
         le = wt.nb == 256 ? launch_wgrad<256, 3, 2>(dymap, xmap, (float*)workspace, w, splits, st)
                           : launch_wgrad<128, 4, 2>(dymap, xmap, (float*)workspace, w, splits, st);
+    else if (wt.nb == 192)
+        le = launch_wgrad<192, 5, 1>(dymap, xmap, (float*)workspace, w, splits, st);
     else
         le = wt.nb == 256 ? launch_wgrad<256, 4, 1>(dymap, xmap, (float*)workspace, w, splits, st)
                           : launch_wgrad<128, 6, 1>(dymap, xmap, (float*)workspace, w, splits, st);
