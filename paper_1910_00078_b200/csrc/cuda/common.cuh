@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "kernels.h"
 
 namespace pk {
@@ -297,6 +299,36 @@ struct BnStatAcc {
 };
 
 inline unsigned ceil_div(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+// Programmatic dependent launch (PDL). Step kernels are launched with
+// programmatic stream serialization, so kernel i+1 may be scheduled while
+// kernel i drains: it runs its prologue (barrier init, TMEM alloc, tensor-map
+// prefetch) and then blocks in pdl_wait() until kernel i has COMPLETED and its
+// memory is visible. Every kernel launched through pk_launch calls pdl_wait()
+// before its first global memory access, then pdl_trigger() so its own
+// successor can be scheduled. Both are no-ops for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled();  // PK_PDL=0 disables (A/B comparisons)
+
+template <typename... KArgs, typename... Args>
+cudaError_t pk_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 }  // namespace pk
 

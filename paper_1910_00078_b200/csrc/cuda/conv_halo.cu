@@ -118,6 +118,8 @@ __global__ void __launch_bounds__(kHThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();  // predecessor complete: inputs ready, outputs free
+    pdl_trigger();
 
     if (warp == 0) {
         // ---------------- TMA producer: halo per chunk, filter slice per tap ----
@@ -307,7 +309,9 @@ cudaError_t launch_halo(const CUtensorMap& amap, const CUtensorMap& bmap, void* 
     }
     int grid = num_sms_of_current_device();
     if (g.total_tiles < grid) grid = g.total_tiles;
-    kern<<<grid, kHThreads, L::kBytes, st>>>(amap, bmap, (__nv_bfloat16*)out, g, e);
+    cudaError_t le = pk_launch(kern, dim3(grid), dim3(kHThreads), L::kBytes, st, amap, bmap,
+                               (__nv_bfloat16*)out, g, e);
+    if (le != cudaSuccess) return le;
     count_launch();
     return cudaGetLastError();
 }

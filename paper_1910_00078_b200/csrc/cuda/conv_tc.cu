@@ -187,6 +187,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();  // predecessor complete: inputs ready, outputs free
+    pdl_trigger();
 
     if (warp < 4) {
         // ======================= producers ==================================
@@ -527,8 +529,9 @@ cudaError_t launch(const CUtensorMap& amap, const CUtensorMap& bmap, const CUten
     if (is_res<MODE>()) grid = grid / g.n_tiles_n * g.n_tiles_n;  // fixed N tile per CTA
     if (g.total_tiles < grid) grid = g.total_tiles;
     if (grid < 1) grid = 1;
-    kern<<<grid, kThreads, L::kBytes, st>>>(amap, bmap, ymap, (const __nv_bfloat16*)src,
-                                            (__nv_bfloat16*)out, g, e);
+    cudaError_t le = pk_launch(kern, dim3(grid), dim3(kThreads), L::kBytes, st, amap, bmap, ymap,
+                               (const __nv_bfloat16*)src, (__nv_bfloat16*)out, g, e);
+    if (le != cudaSuccess) return le;
     if (g.trace) {
         unsigned long long h[32 * 16];
         cudaStreamSynchronize(st);

@@ -154,6 +154,8 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();  // predecessor complete: inputs ready, outputs free
+    pdl_trigger();
 
     if (warp == 0) {
         // ---------------- TMA producer (one elected lane) -------------------
@@ -442,6 +444,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();  // predecessor complete: inputs ready, outputs free
+    pdl_trigger();
 
     if (warp == 0) {
         if (lane == 0) {
@@ -588,6 +592,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 // outputs per thread and eight splits' loads in flight before the adds.
 __global__ void wgrad_sum_kernel(const float* __restrict__ partial, int splits, long long total,
                                  __nv_bfloat16* __restrict__ dw) {
+    pdl_wait();
+    pdl_trigger();
     const long long quads = total / 4;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < quads;
          i += (long long)gridDim.x * blockDim.x) {
@@ -646,7 +652,9 @@ cudaError_t launch_fprop(const CUtensorMap& amap, const CUtensorMap& bmap, const
     int grid = num_sms_of_current_device();
     if (g.total_tiles < grid) grid = g.total_tiles;
     if (grid < 1) grid = 1;
-    kern<<<grid, kFpropThreads, L::kBytes, st>>>(amap, bmap, ymap, (__nv_bfloat16*)out, g, e);
+    cudaError_t le = pk_launch(kern, dim3(grid), dim3(kFpropThreads), L::kBytes, st, amap, bmap,
+                               ymap, (__nv_bfloat16*)out, g, e);
+    if (le != cudaSuccess) return le;
     count_launch();
     return cudaGetLastError();
 }
@@ -883,7 +891,9 @@ cudaError_t launch_wgrad(const CUtensorMap& dymap, const CUtensorMap& xmap, floa
         attr_dev = dev;
     }
     dim3 grid((w.K + BM * MT - 1) / (BM * MT), (w.Nn + NB - 1) / NB, splits);
-    conv_tma_wgrad_kernel<NB, STAGES, MT><<<grid, kWgThreads, L::kBytes, st>>>(dymap, xmap, partial, w);
+    cudaError_t le = pk_launch(conv_tma_wgrad_kernel<NB, STAGES, MT>, grid, dim3(kWgThreads),
+                               L::kBytes, st, dymap, xmap, partial, w);
+    if (le != cudaSuccess) return le;
     return cudaGetLastError();
 }
 
@@ -966,8 +976,8 @@ cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, v
     const long long total = (long long)w.K * w.Nn;
     long long blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
-    wgrad_sum_kernel<<<(unsigned)blocks, 256, 0, st>>>((const float*)workspace, splits, total,
-                                                       (__nv_bfloat16*)dw);
+    le = pk_launch(wgrad_sum_kernel, dim3((unsigned)blocks), dim3(256), 0, st, (const float*)workspace,
+                   splits, total, (__nv_bfloat16*)dw);
     count_launch(2);
-    return cudaGetLastError();
+    return le != cudaSuccess ? le : cudaGetLastError();
 }

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Layout conversion and pointwise kernels (HBM-bound; coalesced through a
 // shared-memory transpose tile, one pass over the data).
 #include <atomic>
@@ -9,6 +10,14 @@ namespace pk {
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("PK_PDL");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
 
 // [n][c][hw] f32 -> [n][hw][pitch] T. Tile: 32 channels x 32 pixels.
 template <typename T>
@@ -79,6 +88,8 @@ __global__ void __launch_bounds__(256) filter_to_dgrad_tiled_kernel(pk_conv_geom
     const int taps = g.r * g.s, tap = blockIdx.z;
     const int c0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    pdl_wait();
+    pdl_trigger();
 #pragma unroll
     for (int i = ty; i < 32; i += 8) {
         const int k = k0 + i, c = c0 + tx;
@@ -212,8 +223,10 @@ cudaError_t pk_cuda_filter_to_dgrad(const pk_conv_geom* g, int dtype, const void
     if (g->groups == 1 && !g->transpose && g->r * g->s <= 65535) {
         const dim3 grid((g->c + 31) / 32, (kp + 31) / 32, g->r * g->s);
         PK_DISPATCH_DTYPE(dtype, T,
-                          filter_to_dgrad_tiled_kernel<T><<<grid, 256, 0, st>>>(
-                              *g, (const T*)f, (T*)dst, kp));
+                          const cudaError_t le = pk_launch(filter_to_dgrad_tiled_kernel<T>, grid,
+                                                           dim3(256), 0, st, *g, (const T*)f,
+                                                           (T*)dst, kp);
+                          if (le != cudaSuccess) return le);
         count_launch();
         return cudaGetLastError();
     }

@@ -381,6 +381,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     stem_fprop_kernel(const __grid_constant__ CUtensorMap ymap, const __nv_bfloat16* __restrict__ x,
                       const __nv_bfloat16* __restrict__ w, const __grid_constant__ StemArgs g,
                       const pk_epilogue epi) {
+    pdl_wait();
+    pdl_trigger();
     const FwdLayout L(g.nchunks, NP);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -638,6 +640,8 @@ template <int NP>
 __global__ void __launch_bounds__(kWgThreads, 1)
     stem_wgrad_kernel(const __grid_constant__ CUtensorMap dymap, const __nv_bfloat16* __restrict__ x,
                       float* __restrict__ partial, const __grid_constant__ StemArgs g) {
+    pdl_wait();
+    pdl_trigger();
     using L = WgSmem<NP>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -790,6 +794,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 __global__ void stem_wgrad_finish_kernel(const float* __restrict__ partial, int ctas, int K,
                                          int kcm, int taps, int f_pitch, int C,
                                          __nv_bfloat16* __restrict__ dw) {
+    pdl_wait();
+    pdl_trigger();
     const long long total = (long long)K * taps * f_pitch;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
          i += (long long)gridDim.x * blockDim.x) {
@@ -869,6 +875,8 @@ template <int C, int KR, int KS, int KSH, int KSW>
 __global__ void __launch_bounds__(kDgThreads, 1)
     stem_dgrad_kernel(const __grid_constant__ CUtensorMap dymap, const __nv_bfloat16* __restrict__ w,
                       __nv_bfloat16* __restrict__ dx, const __grid_constant__ DgArgs g) {
+    pdl_wait();
+    pdl_trigger();
     const DgLayout L(g);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -1105,6 +1113,8 @@ template <int C, int KR, int KS, int KSH, int KSW>
 __global__ void __launch_bounds__(kDg2Threads, 1)
     stem_dgrad2_kernel(const __grid_constant__ CUtensorMap dymap, const __nv_bfloat16* __restrict__ w,
                        __nv_bfloat16* __restrict__ dx, const __grid_constant__ DgArgs g) {
+    pdl_wait();
+    pdl_trigger();
     const Dg2Layout L(g);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -1459,8 +1469,9 @@ cudaError_t launch_stem_fprop(const CUtensorMap& ymap, const void* x, const void
     if (err != cudaSuccess) return err;
     int grid = num_sms_of_current_device();
     if (a.total_tiles < grid) grid = a.total_tiles;
-    kern<<<grid, kFwdThreads, bytes, st>>>(ymap, (const __nv_bfloat16*)x,
-                                                         (const __nv_bfloat16*)w, a, e);
+    cudaError_t le = pk_launch(kern, dim3(grid), dim3(kFwdThreads), bytes, st, ymap,
+                               (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, a, e);
+    if (le != cudaSuccess) return le;
     count_launch();
     if (a.trace) {
         unsigned long long h[32 * 32];
@@ -1491,7 +1502,9 @@ cudaError_t launch_stem_wgrad(const CUtensorMap& dymap, const void* x, float* pa
     auto kern = stem_wgrad_kernel<NP>;
     cudaError_t err = set_smem(kern, WgSmem<NP>::kBytes, &attr_dev);
     if (err != cudaSuccess) return err;
-    kern<<<ctas, kWgThreads, WgSmem<NP>::kBytes, st>>>(dymap, (const __nv_bfloat16*)x, partial, a);
+    cudaError_t le = pk_launch(kern, dim3(ctas), dim3(kWgThreads), WgSmem<NP>::kBytes, st, dymap,
+                               (const __nv_bfloat16*)x, partial, a);
+    if (le != cudaSuccess) return le;
     count_launch();
     return cudaGetLastError();
 }
@@ -1551,11 +1564,12 @@ cudaError_t pk_cuda_stem_fused_dgrad(const pk_conv_geom* g, const void* dy, cons
         cudaError_t err = set_smem(kern, 227 * 1024, attr_dev);
         if (err != cudaSuccess) return err;
         if (a.v2)
-            kern<<<grid, kDg2Threads, Dg2Layout(a).bytes, st>>>(dymap, (const __nv_bfloat16*)w,
-                                                                (__nv_bfloat16*)dx, a);
+            err = pk_launch(kern, dim3(grid), dim3(kDg2Threads), Dg2Layout(a).bytes, st, dymap,
+                            (const __nv_bfloat16*)w, (__nv_bfloat16*)dx, a);
         else
-            kern<<<grid, kDgThreads, DgLayout(a).bytes, st>>>(dymap, (const __nv_bfloat16*)w,
-                                                              (__nv_bfloat16*)dx, a);
+            err = pk_launch(kern, dim3(grid), dim3(kDgThreads), DgLayout(a).bytes, st, dymap,
+                            (const __nv_bfloat16*)w, (__nv_bfloat16*)dx, a);
+        if (err != cudaSuccess) return err;
         count_launch();
         if (a.trace) {
             unsigned long long h[32 * 32];
@@ -1615,10 +1629,10 @@ cudaError_t pk_cuda_stem_fused_wgrad(const pk_conv_geom* g, const void* dy, cons
     if (err != cudaSuccess) return err;
     const long long total = (long long)g->k * a.taps * g->f_pitch;
     const unsigned blocks = (unsigned)((total + 255) / 256);
-    stem_wgrad_finish_kernel<<<blocks, 256, 0, st>>>(partial, ctas, g->k, a.kcm, a.taps,
-                                                     g->f_pitch, g->c, (__nv_bfloat16*)dw);
+    err = pk_launch(stem_wgrad_finish_kernel, dim3(blocks), dim3(256), 0, st, (const float*)partial,
+                    ctas, g->k, a.kcm, a.taps, g->f_pitch, g->c, (__nv_bfloat16*)dw);
     count_launch();
-    return cudaGetLastError();
+    return err != cudaSuccess ? err : cudaGetLastError();
 }
 
 }  // extern "C"
