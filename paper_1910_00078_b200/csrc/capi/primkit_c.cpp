@@ -79,6 +79,110 @@ primkit::TensorDescriptor result_desc(const primkit::ConvProblem& p) {
     return p.filter_desc();
 }
 
+// ---- overlapped host-buffer path ------------------------------------------
+// primkit_conv_run with PINNED host buffers and a forward / backward-data
+// problem: the batch is processed in image chunks so that the host->device
+// copy of chunk j+1, the compute of chunk j and the device->host copy of
+// chunk j-1 run concurrently (PCIe is full duplex; the copies dominate this
+// ABI). Results are identical to the single-shot path (per-image kernels);
+// the op counters advance once for the whole problem, as in the reference.
+bool is_pinned(const void* p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+int host_chunk_images(const primkit::ConvProblem& p, const float* a, const float* out) {
+    using D = primkit::ConvDirection;
+    if (p.direction == D::BackwardWeights || p.n < 2) return 0;
+    const auto da = operand_descs(p).first;
+    const auto dr = result_desc(p);
+    const double per_img = 4.0 * std::max(da.elem_count() / p.n, dr.elem_count() / p.n);
+    double target = 48.0 * 1024 * 1024;  // bytes per chunk transfer
+    if (const char* v = std::getenv("PK_HOST_CHUNK_KB")) target = std::atof(v) * 1024;
+    if (target <= 0) return 0;
+    const long long nc = std::max<long long>(1, (long long)(target / per_img));
+    if (nc * 2 > p.n) return 0;  // fewer than two chunks: nothing to overlap
+    if (!is_pinned(a) || !is_pinned(out)) return 0;
+    return (int)nc;
+}
+
+void conv_run_chunked(primkit::Handle& hd, const primkit::ConvProblem& p,
+                      const primkit::Solver& solver, const primkit::PerfConfig& cfg, const float* a,
+                      const float* b, float* out, int nc) {
+    const auto [da, db] = operand_descs(p);
+    const primkit::TensorDescriptor dr = result_desc(p);
+    const int dt = p.etype == primkit::ElementType::BF16 ? PK_BF16 : PK_F32;
+    const size_t esz = p.etype == primkit::ElementType::BF16 ? 2 : 4;
+    const int ca = (int)da.dims[1], co = (int)dr.dims[1];
+    const long long hwa = da.dims[2] * da.dims[3], hwo = dr.dims[2] * dr.dims[3];
+    const size_t img_a_host = (size_t)ca * hwa, img_o_host = (size_t)co * hwo;  // floats
+    const size_t img_a_dev = (size_t)hwa * pk_pitch(ca) * esz, img_o_dev = (size_t)hwo * pk_pitch(co) * esz;
+    char* dva = static_cast<char*>(hd.scratch(1, primkit::device_bytes(da)));
+    void* dvb = hd.scratch(2, primkit::device_bytes(db));
+    char* dvo = static_cast<char*>(hd.scratch(3, primkit::device_bytes(dr)));
+    float* in_stage[2] = {static_cast<float*>(hd.scratch(30, img_a_host * nc * 4)),
+                          static_cast<float*>(hd.scratch(31, img_a_host * nc * 4))};
+    float* out_stage[2] = {static_cast<float*>(hd.scratch(32, img_o_host * nc * 4)),
+                           static_cast<float*>(hd.scratch(33, img_o_host * nc * 4))};
+    cudaStream_t cs = hd.stream(), up = hd.copy_stream(0), down = hd.copy_stream(1);
+    auto ck = [](cudaError_t e, const char* w) { primkit::check_cuda(e, w); };
+    // the filter goes first, on the compute stream (small)
+    primkit::upload_nchw(hd, db, need(b, "operand b"), dvb);
+    // copy streams start after everything already queued on the compute stream
+    cudaEvent_t start = hd.event(0);
+    ck(cudaEventRecord(start, cs), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(up, start, 0), "cudaStreamWaitEvent");
+    ck(cudaStreamWaitEvent(down, start, 0), "cudaStreamWaitEvent");
+    const primkit::OpCounters saved = hd.counters();
+    std::string kernel;
+    const int chunks = (int)((p.n + nc - 1) / nc);
+    for (int j = 0; j < chunks; ++j) {
+        const int s = j & 1;
+        const int n0 = j * nc, nj = (int)std::min<long long>(nc, p.n - n0);
+        cudaEvent_t h2d = hd.event(1 + s), consumed = hd.event(3 + s), conv_out = hd.event(5 + s),
+                    d2h = hd.event(7 + s);
+        if (j >= 2) ck(cudaStreamWaitEvent(up, consumed, 0), "cudaStreamWaitEvent");
+        ck(cudaMemcpyAsync(in_stage[s], a + (size_t)n0 * img_a_host, (size_t)nj * img_a_host * 4,
+                           cudaMemcpyHostToDevice, up),
+           "cudaMemcpyAsync");
+        ck(cudaEventRecord(h2d, up), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(cs, h2d, 0), "cudaStreamWaitEvent");
+        ck(pk_cuda_nchw_to_nhwc(in_stage[s], dva + (size_t)n0 * img_a_dev, nj, ca, (int)hwa,
+                                pk_pitch(ca), dt, cs),
+           "nchw_to_nhwc");
+        ck(cudaEventRecord(consumed, cs), "cudaEventRecord");
+        primkit::ConvProblem pj = p;
+        pj.n = nj;
+        auto plan = hd.cached_build(pj, solver, &cfg);
+        const size_t dws = plan->device_workspace_bytes();
+        void* ws = hd.scratch(0, dws);
+        plan->run(hd, dva + (size_t)n0 * img_a_dev, dvb, dvo + (size_t)n0 * img_o_dev, ws, dws);
+        kernel = hd.last_kernel;
+        if (j >= 2) ck(cudaStreamWaitEvent(cs, d2h, 0), "cudaStreamWaitEvent");
+        ck(pk_cuda_nhwc_to_nchw(dvo + (size_t)n0 * img_o_dev, out_stage[s], nj, co, (int)hwo,
+                                pk_pitch(co), dt, cs),
+           "nhwc_to_nchw");
+        ck(cudaEventRecord(conv_out, cs), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(down, conv_out, 0), "cudaStreamWaitEvent");
+        ck(cudaMemcpyAsync(out + (size_t)n0 * img_o_host, out_stage[s], (size_t)nj * img_o_host * 4,
+                           cudaMemcpyDeviceToHost, down),
+           "cudaMemcpyAsync");
+        ck(cudaEventRecord(d2h, down), "cudaEventRecord");
+    }
+    // the compute stream (and so later work on it) waits for the last copies
+    cudaEvent_t done = hd.event(9);
+    ck(cudaEventRecord(done, down), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(cs, done, 0), "cudaStreamWaitEvent");
+    ck(cudaStreamSynchronize(down), "cudaStreamSynchronize");
+    hd.counters() = saved;
+    hd.counters() += hd.cached_build(p, solver, &cfg)->op_counters();
+    hd.last_kernel = kernel;
+}
+
 void copy_name(char* buf, size_t len, const std::string& name) {
     if (!buf || len == 0) primkit::throw_error(primkit::ErrorCode::InvalidValue, "null output buffer");
     if (name.size() + 1 > len)
@@ -268,6 +372,10 @@ primkit_status primkit_conv_run(primkit_handle* h, const primkit_conv_problem* p
         if (solver.workspace_bytes(p, &cfg) > ws_bytes)
             primkit::throw_error(primkit::ErrorCode::WorkspaceTooSmall,
                                  "workspace too small for " + solver.name());
+        if (const int nc = host_chunk_images(p, need(a, "operand a"), need(output, "output"))) {
+            conv_run_chunked(hd, p, solver, cfg, a, b, output, nc);
+            return;
+        }
         const auto [da, db] = operand_descs(p);
         const primkit::TensorDescriptor dr = result_desc(p);
         void* dva = hd.scratch(1, primkit::device_bytes(da));

@@ -467,4 +467,6 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
     h.counters() += counters_for(problem_, algo_);
 }
 
+OpCounters ConvPlan::op_counters() const { return counters_for(problem_, algo_); }
+
 }  // namespace primkit

@@ -82,6 +82,10 @@ Handle::~Handle() {
         cudaSetDevice(device_);
         if (ev0_) cudaEventDestroy(ev0_);
         if (ev1_) cudaEventDestroy(ev1_);
+        for (cudaStream_t s : copy_streams_)
+            if (s) cudaStreamDestroy(s);
+        for (cudaEvent_t e : events_)
+            if (e) cudaEventDestroy(e);
     }
     scratch_.clear();
 }
@@ -108,6 +112,22 @@ void Handle::init_device(int device) {
 void Handle::activate() const {
     if (device_ < 0) const_cast<Handle*>(this)->init_device(-1);
     check_cuda(cudaSetDevice(device_), "cudaSetDevice");
+}
+
+cudaStream_t Handle::copy_stream(int i) {
+    activate();
+    if (!copy_streams_[i])
+        check_cuda(cudaStreamCreateWithFlags(&copy_streams_[i], cudaStreamNonBlocking),
+                   "cudaStreamCreate");
+    return copy_streams_[i];
+}
+
+cudaEvent_t Handle::event(int i) {
+    activate();
+    if ((int)events_.size() <= i) events_.resize(i + 1, nullptr);
+    if (!events_[i])
+        check_cuda(cudaEventCreateWithFlags(&events_[i], cudaEventDisableTiming), "cudaEventCreate");
+    return events_[i];
 }
 
 void* Handle::scratch(int slot, std::size_t bytes) {

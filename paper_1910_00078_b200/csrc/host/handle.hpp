@@ -103,6 +103,10 @@ public:
     // workspace, 1..: staging for host-ABI operands).
     void* scratch(int slot, std::size_t bytes);
     void sync() const;
+    // Non-blocking copy streams (0: host->device, 1: device->host) and a pool
+    // of timing-free events for the overlapped host-buffer path; lazily made.
+    cudaStream_t copy_stream(int i);
+    cudaEvent_t event(int i);
 
     // Times `fn` (one enqueue of device work) in ms: CUDA events on the
     // handle's stream, or the injected clock.
@@ -130,6 +134,8 @@ private:
     int num_sms_ = 148;
     cudaStream_t stream_ = nullptr;
     cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+    cudaStream_t copy_streams_[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> events_;
     std::map<int, DeviceBuffer> scratch_;
     double last_device_ms_ = 0.0;
 };
