@@ -52,6 +52,7 @@ struct TmaConvArgs {
     int qbw, qbh, qbn;        // per-epilogue-warp quarter sub-box
     int n_tiles_n, total_tiles;
     int num_phases;
+    int mt;                   // 128-pixel M tiles per rectangle (1 or 2)
     int phase_tma;            // PHASED: 1 = per-phase TMA store maps (num_phases <= kStoreMaps)
     int ph_tw[kMaxPhases], ph_th[kMaxPhases], ph_tn[kMaxPhases];
     int ph_tile_start[kMaxPhases + 1];
@@ -61,9 +62,12 @@ struct TmaConvArgs {
     short off_h[kMaxTaps], off_w[kMaxTaps];
 };
 
-template <int BN, int STAGES>
+// MT = 128-pixel M tiles per CTA tile (2: a 256-pixel rectangle whose two
+// halves are two M=128 MMAs sharing every filter (B) stage — half the B bytes
+// per FLOP through TMA; needs 2 x MT x BN <= 512 TMEM columns, so BN <= 128)
+template <int BN, int STAGES, int MT = 1>
 struct FSmem {
-    static constexpr int kA = BM * BK * 2;
+    static constexpr int kA = MT * BM * BK * 2;
     static constexpr int kB = BN * BK * 2;
     static constexpr int kStage = kA + kB;
     // epilogue staging per warp: double-buffered, except BN=256 where the
@@ -115,13 +119,14 @@ __device__ __forceinline__ int tile_kblocks(const TmaConvArgs& g, const RectInfo
     return NARROW ? (ri.ntaps * g.cpt + 7) / 8 : ri.ntaps * g.cpt;
 }
 
-template <int BN, int STAGES, bool PHASED, bool NARROW>
+template <int BN, int STAGES, bool PHASED, bool NARROW, int MT>
 __global__ void __launch_bounds__(kFpropThreads, 1)
     conv_tma_fprop_kernel(const __grid_constant__ CUtensorMap amap,
                           const __grid_constant__ CUtensorMap bmap,
                           const __grid_constant__ YMaps ymaps, __nv_bfloat16* __restrict__ out,
                           const __grid_constant__ TmaConvArgs g, const pk_epilogue epi) {
-    using L = FSmem<BN, STAGES>;
+    using L = FSmem<BN, STAGES, MT>;
+    static_assert(2 * MT * BN <= 512, "TMEM");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -131,8 +136,9 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
     uint64_t* tmem_empty = tmem_full + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr uint32_t kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128
-                                   : 2 * BN <= 256 ? 256 : 512;
+    constexpr int kAcc = 2 * MT * BN;
+    constexpr uint32_t kTmemCols = kAcc <= 32 ? 32 : kAcc <= 64 ? 64 : kAcc <= 128 ? 128
+                                   : kAcc <= 256 ? 256 : 512;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < STAGES; ++i) {
@@ -222,7 +228,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
             ++it;
             mbar_wait(&tmem_empty[a], aphase ^ 1);
             tc_fence_after();
-            const uint32_t d_tmem = tmem_base + a * BN;
+            const uint32_t d_tmem = tmem_base + a * (MT * BN);
             for (int kb = 0; kb < nkb; ++kb) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
@@ -231,14 +237,17 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                     // start fields advance by byte offset >> 4
                     const uint32_t a_base = smem_u32(smem + stage * L::kStage);
                     const uint32_t b_base = a_base + L::kA;
-                    // NARROW: K step k covers boxes 2k, 2k+1 (2 KB apart, LBO),
-                    // 16-row core-matrix groups are 128 B apart (SBO)
-                    const uint64_t ad0 = NARROW ? umma_desc_noswz(a_base, L::kA / 8, 128)
-                                                : umma_desc_sw128(a_base, 16, 1024);
                     const uint64_t bd0 = umma_desc_sw128(b_base, 16, 1024);
-                    constexpr uint64_t as = NARROW ? (2 * (L::kA / 8)) >> 4 : 2;
-                    mma4_bf16(d_tmem, ad0, ad0 + as, ad0 + 2 * as, ad0 + 3 * as, bd0, bd0 + 2, bd0 + 4,
-                              bd0 + 6, idesc, kb != 0);
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        // NARROW: K step k covers boxes 2k, 2k+1 (2 KB apart, LBO),
+                        // 16-row core-matrix groups are 128 B apart (SBO)
+                        const uint64_t ad0 = NARROW ? umma_desc_noswz(a_base, L::kA / 8, 128)
+                                                    : umma_desc_sw128(a_base + mt * BM * 128, 16, 1024);
+                        constexpr uint64_t as = NARROW ? (2 * (L::kA / 8)) >> 4 : 2;
+                        mma4_bf16(d_tmem + mt * BN, ad0, ad0 + as, ad0 + 2 * as, ad0 + 3 * as, bd0,
+                                  bd0 + 2, bd0 + 4, bd0 + 6, idesc, kb != 0);
+                    }
                     mma_commit_elect(&empty[stage]);
                     if (kb == nkb - 1) mma_commit_elect(&tmem_full[a]);
                 }
@@ -259,24 +268,11 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
         const bool tma_st = !PHASED || g.phase_tma;
         BnStatAcc bacc;
         bacc.init();
-        // this lane's row inside the rectangle, and the quarter's sub-box origin
-        const int row = q * 32 + lane;
-        const int rw = row % g.bw, rh = (row / g.bw) % g.bh, rn = row / (g.bw * g.bh);
-        const int q0 = q * 32;
-        const int qw = q0 % g.bw, qh = (q0 / g.bw) % g.bh, qn = q0 / (g.bw * g.bh);
         int it = 0;
         for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
             const RectInfo ri = rect_info(g, t);
             const int n0c = ri.nt * BN;
             const bool live = ri.ntaps > 0;
-            // output coordinates of this lane's row
-            const int pn = ri.n0 + rn, ph_ = ri.h0 + rh, pw_ = ri.w0 + rw;
-            int oy = ph_, ox = pw_;
-            bool row_ok = pn < g.N && ph_ < g.ph_hp[ri.phase] && pw_ < g.ph_wp[ri.phase];
-            if (PHASED) {
-                oy = ph_ * g.str_h + g.ph_h0[ri.phase];
-                ox = pw_ * g.str_w + g.ph_w0[ri.phase];
-            }
             int a = 0;
             if (live) {
                 a = it & 1;
@@ -285,11 +281,27 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                 mbar_wait(&tmem_full[a], aphase);
                 tc_fence_after();
             }
+#pragma unroll 1
+          for (int mt = 0; mt < MT; ++mt) {
+            // this lane's row inside the rectangle, and the quarter's sub-box origin
+            const int row = mt * BM + q * 32 + lane;
+            const int rw = row % g.bw, rh = (row / g.bw) % g.bh, rn = row / (g.bw * g.bh);
+            const int q0 = mt * BM + q * 32;
+            const int qw = q0 % g.bw, qh = (q0 / g.bw) % g.bh, qn = q0 / (g.bw * g.bh);
+            // output coordinates of this lane's row
+            const int pn = ri.n0 + rn, ph_ = ri.h0 + rh, pw_ = ri.w0 + rw;
+            int oy = ph_, ox = pw_;
+            bool row_ok = pn < g.N && ph_ < g.ph_hp[ri.phase] && pw_ < g.ph_wp[ri.phase];
+            if (PHASED) {
+                oy = ph_ * g.str_h + g.ph_h0[ri.phase];
+                ox = pw_ * g.str_w + g.ph_w0[ri.phase];
+            }
             const int span = min(BN, g.out_pitch - n0c);
             const int nchunks = (span + 63) / 64;
             int my_last = -1;
-            for (int ci = half; ci < nchunks; ci += 2) my_last = ci;
-            if (live && my_last < 0) {
+            if (mt == MT - 1)
+                for (int ci = half; ci < nchunks; ci += 2) my_last = ci;
+            if (live && mt == MT - 1 && my_last < 0) {
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tmem_empty[a]);
@@ -299,7 +311,8 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                 const int c0 = ci * 64;
                 uint32_t v[64];
                 if (live) {
-                    const uint32_t ta = tmem_base + a * BN + c0 + (static_cast<uint32_t>(q * 32) << 16);
+                    const uint32_t ta = tmem_base + a * (MT * BN) + mt * BN + c0 +
+                                        (static_cast<uint32_t>(q * 32) << 16);
                     tmem_ld16(ta + 0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
                     if (BN >= 32) tmem_ld16(ta + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
                     if (BN >= 64) {
@@ -366,6 +379,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                     __syncwarp();
                 }
             }
+          }  // mt
         }
         if (epi.stats) bacc.finish(epi, lane, g.n_out);
         if (tma_st && lane == 0) bulk_wait_all();
@@ -635,11 +649,12 @@ __global__ void wgrad_sum_kernel(const float* __restrict__ partial, int splits, 
 // ---------------------------------------------------------------------------
 // host
 
-template <int BN, int STAGES, bool PHASED, bool NARROW>
+template <int BN, int STAGES, bool PHASED, bool NARROW, int MT = 1>
 cudaError_t launch_fprop(const CUtensorMap& amap, const CUtensorMap& bmap, const YMaps& ymap,
                          void* out, const TmaConvArgs& g, const pk_epilogue& e, cudaStream_t st) {
-    using L = FSmem<BN, STAGES>;
-    auto kern = conv_tma_fprop_kernel<BN, STAGES, PHASED, NARROW>;
+    using L = FSmem<BN, STAGES, MT>;
+    static_assert(L::kBytes <= 227 * 1024, "smem");
+    auto kern = conv_tma_fprop_kernel<BN, STAGES, PHASED, NARROW, MT>;
     static int attr_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -663,6 +678,10 @@ template <bool PHASED, bool NARROW>
 cudaError_t dispatch_fprop(int bn, const CUtensorMap& amap, const CUtensorMap& bmap,
                            const YMaps& ymap, void* out, const TmaConvArgs& g,
                            const pk_epilogue& e, cudaStream_t st) {
+    if (g.mt == 2 && !PHASED && !NARROW) {
+        if (bn == 64) return launch_fprop<64, 4, false, false, 2>(amap, bmap, ymap, out, g, e, st);
+        if (bn == 128) return launch_fprop<128, 3, false, false, 2>(amap, bmap, ymap, out, g, e, st);
+    }
     if (bn == 64) return launch_fprop<64, 6, PHASED, NARROW>(amap, bmap, ymap, out, g, e, st);
     if (bn == 128) return launch_fprop<128, 5, PHASED, NARROW>(amap, bmap, ymap, out, g, e, st);
     return launch_fprop<256, 4, PHASED, NARROW>(amap, bmap, ymap, out, g, e, st);
@@ -766,17 +785,21 @@ cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, cons
     t.mult_h = dgrad ? 1 : g->str_h;
     t.mult_w = dgrad ? 1 : g->str_w;
     const int hp0 = (t.Ho + sh - 1) / sh, wp0 = (t.Wo + sw - 1) / sw;
-    const RectTile rt = tc::best_rect(g->n, hp0, wp0, BM);
-    t.bw = rt.bw;
-    t.bh = rt.bh;
-    t.bn = rt.bn;
-    quarter_box(t);
     // PK_TMA_BN (64/128/256) overrides the tile width for tuning experiments
     static const int env_bn = [] {
         const char* v = std::getenv("PK_TMA_BN");
         return v ? std::atoi(v) : 0;
     }();
     const int bn = choose_bn(env_bn ? env_bn : bn_want, out_pitch);
+    // 256-pixel rectangles (two M=128 MMAs per filter stage) when the tile
+    // width leaves TMEM room for two double-buffered accumulators
+    static const bool mt_off = std::getenv("PK_TMA_MT1") != nullptr;
+    t.mt = (!mt_off && !narrow && sh == 1 && sw == 1 && bn <= 128) ? 2 : 1;
+    const RectTile rt = tc::best_rect(g->n, hp0, wp0, BM * t.mt);
+    t.bw = rt.bw;
+    t.bh = rt.bh;
+    t.bn = rt.bn;
+    quarter_box(t);
     t.n_tiles_n = (out_pitch + bn - 1) / bn;
     if (!fill_phases(t, g->n, t.Ho, t.Wo, sh, sw, g->r, g->s, g->pad_h, g->pad_w, g->dil_h,
                      g->dil_w, dgrad))
