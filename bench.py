@@ -566,6 +566,18 @@ def main():
             "traffic_source": ncu_family_traffic(dom_name)[1],
             "peak_source": f"{peak_kind} bf16_tflops_sustained (MEASURED_PEAKS.json)",
             "per_direction": rf}
+        # per-layer roofline (each conv bounded by max(FLOPs / tensor peak, bytes / HBM
+        # peak), bytes = x + w + y in bf16): the family's attainable time vs measured
+        pitch = lambda c: (c + 7) // 8 * 8  # noqa: E731
+        roof_ms = 0.0
+        for L in net.layers:
+            byts = 2.0 * (args.batch * L.h * L.h * pitch(L.c) + L.k * L.r * L.r * pitch(L.c) +
+                          args.batch * L.out_h * L.out_h * pitch(L.k))
+            roof_ms += max(L.flops(args.batch) / (peak * 1e12),
+                           byts / (peaks["hbm_gbs"] * 1e9)) * 1e3
+        extras["roofline"]["layer_roofline_ms"] = roof_ms
+        extras["roofline"]["frac_of_layer_roofline"] = roof_ms / dom["ms"]
+        extras["roofline"]["step_frac_of_layer_roofline"] = 3 * roof_ms / ms_step
         if rank == 0:
             extras["fusion"] = fusion_speedup(torch, lib, handle, device)
             with mp.get_context("fork").Pool(os.cpu_count() or 1) as pool:
