@@ -191,6 +191,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     pdl_trigger();
 
     if (warp < 4) {
+      // plain GEMMs: only thread 0 of warp 0 issues TMA; warps 1-3 stay idle
+      // instead of polling the stage barriers
+      if (!kPlain || warp == 0) {
         // ======================= producers ==================================
         int stage = 0;
         uint32_t phase = 0;
@@ -310,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
+      }
     } else if (warp == 4) {
         // ======================= MMA issuer ==================================
         constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, false, false);
@@ -574,6 +578,11 @@ cudaError_t dispatch_bn(int bn, const CUtensorMap& amap, const CUtensorMap& bmap
 }
 
 int pick_bn(int want, int out_pitch) {
+    static const int env_bn = [] {  // PK_TC_BN: tile-width experiments only
+        const char* v = std::getenv("PK_TC_BN");
+        return v ? std::atoi(v) : 0;
+    }();
+    if (env_bn) want = env_bn;
     int bn = want <= 64 ? 64 : want <= 128 ? 128 : 256;
     const int need = out_pitch <= 32 ? 32 : out_pitch <= 64 ? 64 : out_pitch <= 128 ? 128 : 256;
     return bn < need ? bn : need;
