@@ -101,7 +101,7 @@ int host_chunk_images(const primkit::ConvProblem& p, const float* a, const float
     const auto da = operand_descs(p).first;
     const auto dr = result_desc(p);
     const double per_img = 4.0 * std::max(da.elem_count() / p.n, dr.elem_count() / p.n);
-    double target = 48.0 * 1024 * 1024;  // bytes per chunk transfer
+    double target = 16.0 * 1024 * 1024;  // bytes per chunk transfer (measured best of 8-48 MB)
     if (const char* v = std::getenv("PK_HOST_CHUNK_KB")) target = std::atof(v) * 1024;
     if (target <= 0) return 0;
     const long long nc = std::max<long long>(1, (long long)(target / per_img));
