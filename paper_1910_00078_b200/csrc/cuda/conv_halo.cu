@@ -43,6 +43,7 @@ struct HaloArgs {
     int tiles_img, total_tiles, n_tiles_n;
     int NR;                      // halo rows per tile (box height)
     int flip;                    // dgrad: tap (r,s) uses filter tap (R-1-r, S-1-s)
+    int debug;                   // PK_HALO_DEBUG (timing experiments only): 1 = 8-row-aligned tap views
 };
 
 // RESB: the whole filter slice of the tile's output channels is resident in
@@ -52,15 +53,23 @@ struct HaloArgs {
 // latency.
 constexpr int kResMax = 80 * 1024;
 
-template <int BN, int BSTAGES, bool RESB>
+// HB = halo buffers. 3 (BN = 64 only): a third halo load in flight — with two,
+// the next tile's halo is requested only when the current tile's MMAs start,
+// so every tile waited ~one TMA latency (measured 0.083 ms vs 0.041 of MMA on
+// ResNet conv2_x); paid for by smaller halo buffers (352 rows), an exact-size
+// resident filter (<= 74 KB) and staging for the 4 epilogue warps that work
+// when BN = 64.
+constexpr int kHaloRows3 = 352;
+constexpr int kResMax3 = 74 * 1024;
+template <int BN, int BSTAGES, bool RESB, int HB = kHaloBufs>
 struct HSmem {
-    static constexpr int kHalo = 448 * 128;            // up to 448 grid rows x 128 B
+    static constexpr int kHalo = (HB == 3 ? kHaloRows3 : 448) * 128;  // grid rows x 128 B
     static constexpr int kB = BN * 128;                // one (tap, chunk) filter slice
-    static constexpr int kBOff = kHaloBufs * kHalo;
-    static constexpr int kStgOff = kBOff + (RESB ? kResMax : BSTAGES * kB);
-    static constexpr int kStaging = 8 * 4096;
+    static constexpr int kBOff = HB * kHalo;
+    static constexpr int kStgOff = kBOff + (RESB ? (HB == 3 ? kResMax3 : kResMax) : BSTAGES * kB);
+    static constexpr int kStaging = (HB == 3 ? 4 : 8) * 4096;
     static constexpr int kBarOff = kStgOff + kStaging;
-    static constexpr int kBytes = kBarOff + (2 * kHaloBufs + 2 * BSTAGES + 4) * 8 + 16 + 1024;
+    static constexpr int kBytes = kBarOff + (2 * HB + 2 * BSTAGES + 4) * 8 + 16 + 1024;
 };
 
 struct HTile {
@@ -76,18 +85,19 @@ __device__ __forceinline__ HTile htile(const HaloArgs& g, int t) {
     return h;
 }
 
-template <int BN, int BSTAGES, bool RESB>
+template <int BN, int BSTAGES, bool RESB, int HB>
 __global__ void __launch_bounds__(kHThreads, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap amap,
                      const __grid_constant__ CUtensorMap bmap, __nv_bfloat16* __restrict__ out,
                      const __grid_constant__ HaloArgs g, const pk_epilogue epi) {
-    using L = HSmem<BN, BSTAGES, RESB>;
+    using L = HSmem<BN, BSTAGES, RESB, HB>;
+    static_assert(HB == 2 || BN == 64, "3 halo buffers: BN = 64 only");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     uint64_t* h_full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
-    uint64_t* h_empty = h_full + kHaloBufs;
-    uint64_t* b_full = h_empty + kHaloBufs;
+    uint64_t* h_empty = h_full + HB;
+    uint64_t* b_full = h_empty + HB;
     uint64_t* b_empty = b_full + BSTAGES;
     uint64_t* tmem_full = b_empty + BSTAGES;
     uint64_t* tmem_empty = tmem_full + 2;
@@ -97,7 +107,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
     const int taps = g.R * g.S;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kHaloBufs; ++i) {
+        for (int i = 0; i < HB; ++i) {
             mbar_init(&h_full[i], 1);
             mbar_init(&h_empty[i], 1);
         }
@@ -126,7 +136,9 @@ __global__ void __launch_bounds__(kHThreads, 1)
         if (lane == 0) {
             int hs = 0, bs = 0;
             uint32_t hph = 0, bph = 0;
-            const uint32_t halo_bytes = g.NR * g.Wg * 128;
+            // PK_HALO_DEBUG=2 (timing only): in-bounds boxes of the unpadded width
+            const bool inb = g.debug & 2;
+            const uint32_t halo_bytes = g.NR * (inb ? g.Wg - 2 * g.pad_w : g.Wg) * 128;
             if (RESB) {  // whole filter slice once: (chunk, tap) blocks of BN x 128 B
                 mbar_arrive_expect_tx(&b_full[0], g.cpt * taps * L::kB);
                 for (int ck = 0; ck < g.cpt; ++ck)
@@ -141,9 +153,13 @@ __global__ void __launch_bounds__(kHThreads, 1)
                 for (int ck = 0; ck < g.cpt; ++ck) {
                     mbar_wait(&h_empty[hs], hph ^ 1);
                     mbar_arrive_expect_tx(&h_full[hs], halo_bytes);
-                    tma_load_4d(smem_u32(smem + hs * L::kHalo), &amap, &h_full[hs], ck * 64,
-                                -g.pad_w, ht.row0 - g.pad_h, ht.n);
-                    if (++hs == kHaloBufs) {
+                    if (inb)
+                        tma_load_4d(smem_u32(smem + hs * L::kHalo), &amap, &h_full[hs], ck * 64, 0,
+                                    max(0, min(ht.row0 - g.pad_h, g.Hg - 2 * g.pad_h - g.NR)), ht.n);
+                    else
+                        tma_load_4d(smem_u32(smem + hs * L::kHalo), &amap, &h_full[hs], ck * 64,
+                                    -g.pad_w, ht.row0 - g.pad_h, ht.n);
+                    if (++hs == HB) {
                         hs = 0;
                         hph ^= 1;
                     }
@@ -179,18 +195,46 @@ __global__ void __launch_bounds__(kHThreads, 1)
                 mbar_wait(&h_full[hs], hph);
                 tc_fence_after();
                 const uint32_t halo_u = smem_u32(smem + hs * L::kHalo);
-                for (int tap = 0; tap < taps; ++tap) {
+                if (RESB && !(g.debug & ~24)) {
+                    // resident filter: descriptors are the tile base plus a per-tap
+                    // offset (start field in 16-byte units), two taps per issue block;
+                    // keeps the issuing thread ahead of N=64 MMAs (48 clk each)
+                    const uint64_t at = umma_desc_sw128(
+                        halo_u + ((g.debug & 16) ? 0 : base_row * 128), 16, 1024);
+                    const uint64_t bt = umma_desc_sw128(
+                        smem_u32(smem + L::kBOff + ck * taps * L::kB), 16, 1024);
+                    int r0 = 0, s0 = 0;
+                    int tap = 0;
+                    for (; tap + 2 <= taps; tap += 2) {
+                        const int al = (g.debug & 16) ? ~63 : ~0;  // timing: 8-row-aligned views
+                        const uint64_t a0 = at + (uint64_t)(((r0 * g.Wg + s0) * 8) & al);
+                        if (++s0 == g.S) { s0 = 0; ++r0; }
+                        const uint64_t a1 = at + (uint64_t)(((r0 * g.Wg + s0) * 8) & al);
+                        if (++s0 == g.S) { s0 = 0; ++r0; }
+                        const uint64_t b0 = bt + (uint64_t)(tap * (L::kB >> 4));
+                        mma8_bf16(d_tmem, a0, b0, a1, b0 + (L::kB >> 4), idesc, (ck | tap) != 0);
+                    }
+                    if (tap < taps) {
+                        const uint64_t a0 = at + (uint64_t)((r0 * g.Wg + s0) * 8);
+                        const uint64_t b0 = bt + (uint64_t)(tap * (L::kB >> 4));
+                        mma4_bf16(d_tmem, a0, a0 + 2, a0 + 4, a0 + 6, b0, b0 + 2, b0 + 4, b0 + 6, idesc,
+                                  (ck | tap) != 0);
+                    }
+                }
+                for (int tap = 0; tap < ((RESB && !(g.debug & ~24)) ? 0 : taps); ++tap) {
                     const int r = tap / g.S, s = tap - r * g.S;
                     if (!RESB) {
                         mbar_wait(&b_full[bs], bph);
                         tc_fence_after();
                     }
+                    const int arow = base_row + r * g.Wg + s;
                     const uint64_t ad0 =
-                        umma_desc_sw128(halo_u + (base_row + r * g.Wg + s) * 128, 16, 1024);
+                        umma_desc_sw128(halo_u + ((g.debug & 1) ? (arow & ~7) : arow) * 128, 16, 1024);
                     const uint64_t bd0 = umma_desc_sw128(
                         smem_u32(smem + L::kBOff + (RESB ? ck * taps + tap : bs) * L::kB), 16, 1024);
-                    mma4_bf16(d_tmem, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + 2, bd0 + 4, bd0 + 6,
-                              idesc, (ck | tap) != 0);
+                    if (!(g.debug & 4))
+                        mma4_bf16(d_tmem, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + 2, bd0 + 4,
+                                  bd0 + 6, idesc, (ck | tap) != 0);
                     if (!RESB) {
                         mma_commit_elect(&b_empty[bs]);
                         if (++bs == BSTAGES) {
@@ -200,7 +244,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
                     }
                 }
                 mma_commit_elect(&h_empty[hs]);
-                if (++hs == kHaloBufs) {
+                if (++hs == HB) {
                     hs = 0;
                     hph ^= 1;
                 }
@@ -212,7 +256,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
         const int ew = warp - 2;
         const int q = warp & 3;
         const int half = ew >> 2;
-        uint8_t* stg = smem + L::kStgOff + ew * 4096;
+        uint8_t* stg = smem + L::kStgOff + (HB == 3 ? q : ew) * 4096;
         const uint32_t stg_u = smem_u32(stg);
         const bool has_epi = epilogue_active(&epi);
         BnStatAcc bacc;
@@ -236,6 +280,14 @@ __global__ void __launch_bounds__(kHThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tmem_empty[a]);
+            }
+            if (g.debug & 8) {  // timing experiments: no epilogue work
+                if (my_last >= 0) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tmem_empty[a]);
+                }
+                continue;
             }
 #pragma unroll 1
             for (int ci = half; ci < nchunks; ci += 2) {
@@ -293,11 +345,12 @@ __global__ void __launch_bounds__(kHThreads, 1)
     }
 }
 
-template <int BN, int BSTAGES, bool RESB>
+template <int BN, int BSTAGES, bool RESB, int HB = kHaloBufs>
 cudaError_t launch_halo(const CUtensorMap& amap, const CUtensorMap& bmap, void* out,
                         const HaloArgs& g, const pk_epilogue& e, cudaStream_t st) {
-    using L = HSmem<BN, BSTAGES, RESB>;
-    auto kern = conv_halo_kernel<BN, BSTAGES, RESB>;
+    using L = HSmem<BN, BSTAGES, RESB, HB>;
+    static_assert(L::kBytes <= 227 * 1024, "smem");
+    auto kern = conv_halo_kernel<BN, BSTAGES, RESB, HB>;
     static int attr_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -359,6 +412,7 @@ cudaError_t pk_halo_conv(const pk_conv_geom* g, bool dgrad, const void* src, con
     a.n_out = n_out;
     a.out_pitch = out_pitch;
     a.flip = dgrad ? 1 : 0;
+    if (const char* v = std::getenv("PK_HALO_DEBUG")) a.debug = std::atoi(v);
     // halo of 128 positions: rows touched by [p0, p0 + 127 + (R-1)Wg + S-1]
     a.NR = (127 + (g->r - 1) * a.Wg + g->s - 1 + a.Wg - 1) / a.Wg + 1;
     if (a.Wg > 256 || a.NR > 256 || a.NR * a.Wg > 448) return cudaErrorNotSupported;
@@ -370,7 +424,7 @@ cudaError_t pk_halo_conv(const pk_conv_geom* g, bool dgrad, const void* src, con
     a.n_tiles_n = (out_pitch + bn - 1) / bn;
     a.total_tiles = a.tiles_img * g->n * a.n_tiles_n;
     CUtensorMap amap{}, bmap{};
-    if (!tc::make_map_nhwc(&amap, src, g->n, Hs, Ws, src_pitch, a.Wg, a.NR, 1))
+    if (!tc::make_map_nhwc(&amap, src, g->n, Hs, Ws, src_pitch, (a.debug & 2) ? Ws : a.Wg, a.NR, 1))
         return cudaErrorNotSupported;
     const long long kred = (long long)g->r * g->s * src_pitch;
     if (!tc::make_map_2d(&bmap, filt, n_out, kred, kred, bn)) return cudaErrorNotSupported;
@@ -381,6 +435,10 @@ cudaError_t pk_halo_conv(const pk_conv_geom* g, bool dgrad, const void* src, con
     // streamed per-tap filter slices leave the MMA waiting on TMA latency)
     const bool resb = a.n_tiles_n == 1 && (long long)a.cpt * g->r * g->s * bn * 128 <= kResMax;
     if (!resb) return cudaErrorNotSupported;
+    static const bool hb2 = std::getenv("PK_HALO_HB2") != nullptr;
+    if (bn == 64 && !hb2 && a.NR * a.Wg <= kHaloRows3 &&
+        (long long)a.cpt * g->r * g->s * bn * 128 <= kResMax3)
+        return launch_halo<64, 8, true, 3>(amap, bmap, out, a, e, st);
     if (bn == 64) return launch_halo<64, 8, true>(amap, bmap, out, a, e, st);
     return launch_halo<128, 4, true>(amap, bmap, out, a, e, st);
 }

@@ -212,6 +212,30 @@ __device__ __forceinline__ void mma4_bf16(uint32_t tmem_d, uint64_t a0, uint64_t
         "r"(accumulate)
         : "memory");
 }
+// Two K=64 blocks (8 MMAs, K=16 each) with one elect: A/B descriptors of the
+// first K=16 step of each block; later steps advance the start field by 32 B.
+__device__ __forceinline__ void mma8_bf16(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint64_t a1,
+                                          uint64_t b1, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 x1, x2, x3, y1, y2, y3, u1, u2, u3, v1, v2, v3;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "add.s64 x1, %1, 2;\n\tadd.s64 x2, %1, 4;\n\tadd.s64 x3, %1, 6;\n\t"
+        "add.s64 y1, %2, 2;\n\tadd.s64 y2, %2, 4;\n\tadd.s64 y3, %2, 6;\n\t"
+        "add.s64 u1, %3, 2;\n\tadd.s64 u2, %3, 4;\n\tadd.s64 u3, %3, 6;\n\t"
+        "add.s64 v1, %4, 2;\n\tadd.s64 v2, %4, 4;\n\tadd.s64 v3, %4, 6;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], x1, y1, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], x2, y2, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], x3, y3, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %4, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], u1, v1, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], u2, v2, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], u3, v3, %5, 1;\n\t}" ::"r"(tmem_d),
+        "l"(a0), "l"(b0), "l"(a1), "l"(b1), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
