@@ -617,6 +617,22 @@ primkit_status primkit_conv_bn_workspace(primkit_handle* h, const primkit_conv_p
     });
 }
 
+// Statistics in the conv epilogue pay off only when the convolution leaves
+// the epilogue slack: spatial filters, or 1x1 layers of high arithmetic
+// intensity. On HBM-bound 1x1 layers the epilogue is the critical path and the
+// per-channel reductions there cost more than the separate statistics read
+// they save (measured, ResNet-50 N=256: conv2_1c 0.388 ms fused vs 0.348 ms
+// conv + standalone BN; conv4_2a 0.080 vs 0.090). PK_CBN_FUSE=1 / 0 forces.
+bool stats_epilogue_pays(const primkit::ConvProblem& p, const primkit::ConvShapes& sh) {
+    if (const char* v = std::getenv("PK_CBN_FUSE")) return v[0] != '0';
+    if (sh.y * sh.x > 1) return true;
+    const double flops = 2.0 * sh.n * sh.k * sh.cg * sh.y * sh.x * sh.oh * sh.ow;
+    const double bytes = 2.0 * ((double)sh.n * sh.h * sh.w * pk_pitch((int)sh.c) +
+                                (double)sh.k * sh.y * sh.x * pk_pitch((int)sh.cg) +
+                                (double)sh.n * sh.oh * sh.ow * pk_pitch((int)sh.k));
+    return flops / bytes >= 180.0;
+}
+
 primkit_status primkit_conv_bn_forward_train_device(
     primkit_handle* h, const primkit_conv_problem* pp, const char* solver_name, const void* x,
     const void* w, const float* gamma, const float* beta, float* running_mean, float* running_var,
@@ -641,7 +657,7 @@ primkit_status primkit_conv_bn_forward_train_device(
         const int n = (int)sh.n, k = (int)sh.k, hw = (int)(sh.oh * sh.ow);
         const int dt = p.etype == primkit::ElementType::BF16 ? PK_BF16 : PK_F32;
         float* part = reinterpret_cast<float*>(static_cast<char*>(workspace) + conv);
-        const bool fused = dt == PK_BF16 && plan->fuses_stats();
+        const bool fused = dt == PK_BF16 && plan->fuses_stats() && stats_epilogue_pays(p, sh);
         cudaStream_t st = hd.stream();
         if (fused) {
             primkit::check_cuda(cudaMemsetAsync(part, 0, conv_bn_stats_bytes(p), st), "memset");

@@ -192,19 +192,27 @@ __device__ __forceinline__ uint32_t staged_word(uint32_t stg_u, int r, int lane)
     return wv;
 }
 
-// forward: (sum, sumsq) of the stored values for both channels of the lane
+// forward: (sum, sumsq) of the stored values for both channels of the lane.
+// Packed f32x2 arithmetic (FADD2 / FFMA2): a bf16 pair widens to an f32 pair
+// with two bit ops, then one add and one fma cover both channels.
 __device__ __forceinline__ float4 stats64_fwd(uint32_t stg_u, int lane, unsigned ok) {
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+    unsigned long long sum = 0ull, sq = 0ull;  // (ch0, ch1) f32 pairs
 #pragma unroll 8
     for (int r = 0; r < 32; ++r) {
-        if (!((ok >> r) & 1u)) continue;
         const uint32_t wv = staged_word(stg_u, r, lane);
-        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv));
-        a.x += f.x;
-        a.y = fmaf(f.x, f.x, a.y);
-        a.z += f.y;
-        a.w = fmaf(f.y, f.y, a.w);
+        // rows past the tile (ok bit clear) contribute zeros
+        const uint32_t w = ((ok >> r) & 1u) ? wv : 0u;
+        unsigned long long f;
+        asm("{\n\t.reg .b32 lo, hi;\n\tshl.b32 lo, %1, 16;\n\tand.b32 hi, %1, 0xffff0000;\n\t"
+            "mov.b64 %0, {lo, hi};\n\t}"
+            : "=l"(f)
+            : "r"(w));
+        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(sum) : "l"(f));
+        asm("fma.rn.f32x2 %0, %1, %1, %0;" : "+l"(sq) : "l"(f));
     }
+    float4 a;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.z) : "l"(sum));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a.y), "=f"(a.w) : "l"(sq));
     return a;
 }
 

@@ -7,6 +7,8 @@ output the kernel stored (isolates the fused statistics from conv rounding).
 Also: fused == unfused (conv, then standalone BN) on the same device tensors."""
 import ctypes as C
 
+import os
+
 import numpy as np
 import pytest
 
@@ -95,7 +97,11 @@ def test_conv_bn_forward_train(lib, si, relu):
     rm = rng.uniform(-1, 1, p.k).astype(np.float32)
     rv = (1 + np.abs(rng.uniform(-1, 1, p.k))).astype(np.float32)
     h = lib.handle()
-    conv, y, sm, sinv, rm_out, rv_out = _run(lib, h, p, x, w, gamma, beta, rm, rv, relu)
+    os.environ["PK_CBN_FUSE"] = "1"  # always the epilogue-statistics path here
+    try:
+        conv, y, sm, sinv, rm_out, rv_out = _run(lib, h, p, x, w, gamma, beta, rm, rv, relu)
+    finally:
+        os.environ.pop("PK_CBN_FUSE", None)
     assert "bn_stats_epilogue" in h.last_kernel(), h.last_kernel()
     # the convolution itself: bf16 tolerance vs the fp32 oracle
     assert rel_l2(conv, oracle.conv_forward(p, xn, wn)) <= 1e-2
