@@ -707,6 +707,11 @@ cudaError_t pk_cuda_igemm_tc_fwd(const pk_conv_geom* g, const void* x, const voi
     const bool plain = g->r == 1 && g->s == 1 && g->str_h == 1 && g->str_w == 1 &&
                        g->pad_h == 0 && g->pad_w == 0 && g->x_pitch == g->f_pitch;
     if (plain) {
+        // filter slice too large to stay resident: CTA-pair kernel (half the B bytes)
+        static const bool pair_all = std::getenv("PK_TC2_ALL") != nullptr;  // A/B experiments
+        if (bn == 256 && (t.kred > 256 || pair_all) && !e.stats && !t.debug_nores &&
+            pk_gemm_pair_eligible(t.M, t.kred, g->k, g->y_pitch))
+            return pk_gemm_pair(x, f, y, t.M, t.kred, g->k, g->y_pitch, g->p, g->q, &e, st);
         if (!tc::make_map_2d(&amap, x, t.M, g->x_pitch, g->x_pitch, BM)) return cudaErrorInvalidValue;
         return dispatch_bn<PLAIN>(bn, amap, bmap, x, y, t, e, st);
     }
@@ -800,6 +805,11 @@ cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const 
     const bool plain = g->r == 1 && g->s == 1 && g->str_h == 1 && g->str_w == 1 &&
                        g->pad_h == 0 && g->pad_w == 0;
     if (plain) {
+        static const bool pair_all = std::getenv("PK_TC2_ALL") != nullptr;
+        if (bn == 256 && (t.kred > 256 || pair_all) && !e.stats && !t.debug_nores &&
+            pk_gemm_pair_eligible(t.M, t.kred, g->c, g->x_pitch))
+            return pk_gemm_pair(dy, workspace, dx, t.M, t.kred, g->c, g->x_pitch, g->h, g->w, nullptr,
+                                st);
         if (!tc::make_map_2d(&amap, dy, t.M, g->y_pitch, g->y_pitch, BM)) return cudaErrorInvalidValue;
         return dispatch_bn<PLAIN>(bn, amap, bmap, dy, dx, t, e, st);
     }

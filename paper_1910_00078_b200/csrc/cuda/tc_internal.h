@@ -20,3 +20,9 @@ cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, v
 // backward data (filt = transposed filter [C][R][S][pitch K]) when dgrad.
 cudaError_t pk_halo_conv(const pk_conv_geom* g, bool dgrad, const void* src, const void* filt,
                          void* out, const pk_epilogue* epi, cudaStream_t st);
+
+// CTA-pair (cta_group::2) plain GEMM for 1x1 layers whose filter slice cannot
+// stay resident (conv_tc2.cu): y[M][out_pitch] = a[M][kdim] . b[n_out][kdim]^T.
+int pk_gemm_pair_eligible(int M, int kdim, int n_out, int out_pitch);
+cudaError_t pk_gemm_pair(const void* a, const void* b, void* y, int M, int kdim, int n_out,
+                         int out_pitch, int P, int Q, const pk_epilogue* epi, cudaStream_t st);

@@ -224,6 +224,8 @@ def test_bf16_large_tensor_core_paths(lib):
                 dict(n=2, c=128, h=15, w=13, k=64, y=3, x=3, pad=1),    # MT=2, ragged, BN=64
                 dict(n=2, c=64, h=56, w=56, k=128, y=1, x=1),           # resident-filter 1x1
                 dict(n=2, c=512, h=7, w=7, k=128, y=1, x=1),            # resident 128 KB slice
+                dict(n=8, c=512, h=56, w=56, k=256, y=1, x=1),          # CTA-pair GEMM (fwd)
+                dict(n=8, c=256, h=56, w=56, k=512, y=1, x=1),          # CTA-pair GEMM (dgrad)
                 dict(n=2, c=512, h=14, w=14, k=1024, y=1, x=1, stride=2),
                 dict(n=2, c=3, h=32, w=32, k=64, y=7, x=7, pad=3, stride=2),
                 dict(n=1, c=256, h=13, w=13, k=512, y=1, x=1, stride=2)):
