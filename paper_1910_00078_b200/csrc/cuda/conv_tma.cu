@@ -412,22 +412,27 @@ __device__ __forceinline__ void wgstamp(const TmaWgArgs& g, int ev) {
 
 // MT = output-channel tiles of 128 per CTA (2: M = 256 rows sharing every B
 // load, halving the L2 bytes per FLOP — the kernel is L2/TMA-throughput bound)
-template <int NB, int STAGES, int MT>
+template <int NB, int STAGES, int MT, bool PAIR = false>
 struct WSmem {
     static constexpr int kA = MT * BM * BK * 2;   // 2*MT 64-channel MN atoms of dY
-    static constexpr int kB = NB * BK * 2;   // NB/64 MN atoms of tap-shifted X
+    static constexpr int kB = (PAIR ? NB / 2 : NB) * BK * 2;   // MN atoms of tap-shifted X
     static constexpr int kAtom = 64 * BK * 2;
     static constexpr int kStage = kA + kB;
     static constexpr int kBarOff = STAGES * kStage;
     static constexpr int kBytes = kBarOff + (2 * STAGES + 1) * 8 + 16 + 1024;
 };
 
-template <int NB, int STAGES, int MT>
+// PAIR: a CTA pair (cluster of 2, cta_group::2) owns a 256 x NB tile: each CTA
+// loads its 128 output-channel rows of dY and HALF of the NB filter-position
+// columns of X; the leader issues M=256 MMAs (half the TMA bytes per FLOP of
+// the M=256 single-CTA form, which re-reads every X column per CTA).
+template <int NB, int STAGES, int MT, bool PAIR>
 __global__ void __launch_bounds__(kWgThreads, 1)
     conv_tma_wgrad_kernel(const __grid_constant__ CUtensorMap dymap,
                           const __grid_constant__ CUtensorMap xmap, float* __restrict__ partial,
                           const __grid_constant__ TmaWgArgs g) {
-    using L = WSmem<NB, STAGES, MT>;
+    using L = WSmem<NB, STAGES, MT, PAIR>;
+    static_assert(!PAIR || MT == 1, "pair tiles: 128 rows per CTA");
     constexpr uint32_t kCols = MT * NB <= 128 ? 128 : MT * NB <= 256 ? 256 : 512;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -437,7 +442,9 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     uint64_t* tmem_full = empty + STAGES;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM * MT;
+    uint32_t rank = 0;
+    if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const int m0 = PAIR ? (blockIdx.x >> 1) * 2 * BM + (int)rank * BM : blockIdx.x * BM * MT;
     const int n0 = blockIdx.y * NB;
     const int split = blockIdx.z;
     const int kb_begin = split * g.kb_per_split;
@@ -453,9 +460,21 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         tma_prefetch(&dymap);
         tma_prefetch(&xmap);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, kCols);
+    if (warp == 1) {
+        if (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(kCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            tmem_alloc(tmem_slot, kCols);
+        }
+    }
     tc_fence_before();
     __syncthreads();
+    if (PAIR)  // the peer's barriers exist before any cross-CTA signal
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                         : "memory");
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_wait();  // predecessor complete: inputs ready, outputs free
@@ -463,12 +482,12 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            // the NB/64 column blocks of B: (tap, channel chunk) each
-            constexpr int kAtoms = NB / 64;
+            // the column blocks of B this CTA loads: (tap, channel chunk) each
+            constexpr int kAtoms = (PAIR ? NB / 2 : NB) / 64;
             int bc[kAtoms], bs[kAtoms], br[kAtoms];
 #pragma unroll
             for (int a = 0; a < kAtoms; ++a) {
-                const int nidx = n0 + a * 64;
+                const int nidx = n0 + (PAIR ? (int)rank * (NB / 2) : 0) + a * 64;
                 const int tap = nidx / g.Cp;
                 bc[a] = nidx - tap * g.Cp;
                 br[a] = tap / g.S;
@@ -485,6 +504,20 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 const int q0 = wi * g.rw, p0 = hi * g.rh, img0 = ni * g.rn;
                 mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sa = smem + stage * L::kStage;
+                if (PAIR) {
+                    // both CTAs' loads complete on the leader's stage barrier
+                    const uint32_t fb = smem_u32(&full[stage]) & 0xFEFFFFFFu;
+                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (L::kA + L::kB));
+#pragma unroll
+                    for (int j = 0; j < 2; ++j)
+                        tma_load_4d_pair(smem_u32(sa + j * L::kAtom), &dymap, fb, m0 + 64 * j, q0, p0,
+                                         img0);
+#pragma unroll
+                    for (int a = 0; a < kAtoms; ++a)
+                        tma_load_4d_pair(smem_u32(sa + L::kA + a * L::kAtom), &xmap, fb, bc[a],
+                                         q0 * g.str_w - g.pad_w + bs[a] * g.dil_w,
+                                         p0 * g.str_h - g.pad_h + br[a] * g.dil_h, img0);
+                } else {
                 // dY atoms past K (e.g. K = 64 in an M = 128 tile) are not loaded:
                 // the MMA rows they feed are never stored
                 const int a_atoms = min(2 * MT, (g.K - m0 + 63) / 64);
@@ -499,6 +532,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     tma_load_4d(smem_u32(sa + L::kA + a * L::kAtom), &xmap, &full[stage], bc[a],
                                 q0 * g.str_w - g.pad_w + bs[a] * g.dil_w,
                                 p0 * g.str_h - g.pad_h + br[a] * g.dil_h, img0);
+                }
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
@@ -506,7 +540,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             }
         }
     } else if (warp == 1) {
-        constexpr uint32_t idesc = idesc_bf16_f32(BM, NB, true, true);
+      if (!PAIR || rank == 0) {
+        constexpr uint32_t idesc = idesc_bf16_f32(PAIR ? 2 * BM : BM, NB, true, true);
         int stage = 0;
         uint32_t phase = 0;
         wgstamp(g, 0);
@@ -519,6 +554,13 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 const uint32_t b_base = a_base + L::kA;
                 const uint64_t bd0 = umma_desc_sw128(b_base, L::kAtom, 1024);
                 constexpr uint64_t ks = 2048 >> 4;  // 16 MN-major K rows
+                if (PAIR) {
+                    const uint64_t ad0 = umma_desc_sw128(a_base, L::kAtom, 1024);
+                    mma4_bf16_pair(tmem_base, ad0, ad0 + ks, ad0 + 2 * ks, ad0 + 3 * ks, bd0, bd0 + ks,
+                                   bd0 + 2 * ks, bd0 + 3 * ks, idesc, kb != kb_begin);
+                    mma_commit_pair(&empty[stage]);
+                    if (kb == kb_end - 1) mma_commit_pair(tmem_full);
+                } else {
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt) {
                     const uint64_t ad0 = umma_desc_sw128(a_base + mt * 2 * L::kAtom, L::kAtom, 1024);
@@ -527,6 +569,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 }
                 mma_commit_elect(&empty[stage]);
                 if (kb == kb_end - 1) mma_commit_elect(tmem_full);
+                }
             }
             if (kb == kb_end - 1) wgstamp(g, 1);
             if (++stage == STAGES) {
@@ -534,6 +577,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 phase ^= 1;
             }
         }
+      }
     } else {
         const int q = warp & 3;
         const bool live = kb_end > kb_begin;
@@ -596,9 +640,16 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (PAIR)
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                         : "memory");
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, kCols);
+        if (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(kCols));
+        else
+            tmem_dealloc(tmem_base, kCols);
     }
 }
 
@@ -856,11 +907,12 @@ static int tma_wgrad_splits(int tiles_mn, int num_kb, int num_sms) {
 // through L2 (the bound of this kernel). PK_WG_TILE=128x1 etc. overrides.
 struct WgTile {
     int nb, mt;
+    bool pair;  // CTA-pair M=256 tiles (cta_group::2): nb = 256, mt = 1 per CTA
 };
 static WgTile wgrad_tile(const pk_conv_geom* g) {
     static const char* env = std::getenv("PK_WG_TILE");
     const int nn = g->r * g->s * g->x_pitch;
-    WgTile t{nn >= 256 ? 256 : 128, g->k >= 256 ? 2 : 1};
+    WgTile t{nn >= 256 ? 256 : 128, g->k >= 256 ? 2 : 1, false};
     // 3 taps x 64 channels (3x3 filters on 64-channel inputs): 192-wide tiles
     // cover the 576 filter positions exactly (256-wide ones waste 25%)
     if (nn % 256 != 0 && nn % 192 == 0 && nn <= 768 && t.mt == 1) t.nb = 192;
@@ -876,8 +928,16 @@ static WgTile wgrad_tile(const pk_conv_geom* g) {
         int nb = 0, mt = 0;
         if (std::sscanf(env, "%dx%d", &nb, &mt) == 2 && (nb == 128 || nb == 256 || (nb == 192 && mt == 1)) &&
             (mt == 1 || mt == 2))
-            t = {nb, mt};
+            t = {nb, mt, false};
     }
+    // CTA pairs: each SM loads its 128 dY rows and half of a 256-wide X tile
+    static const int pair_env = [] {
+        const char* v = std::getenv("PK_WG_PAIR");
+        return v ? std::atoi(v) : -1;
+    }();
+    // measured (ResNet-50 N=256): 1x1 layers gain 3-15% (conv3_1ds 71 -> 61 us), 3x3 lose
+    const bool pair_ok = g->k % 256 == 0 && nn % 256 == 0;
+    if (pair_ok && (pair_env == 1 || (pair_env != 0 && g->r * g->s == 1))) t = {256, 1, true};
     return t;
 }
 
@@ -904,23 +964,25 @@ static void wgrad_geometry(const pk_conv_geom* g, int* tiles_mn, int* num_kb, Re
     *tiles_mn = ((g->k + BM * wt.mt - 1) / (BM * wt.mt)) * ((nn + wt.nb - 1) / wt.nb);
 }
 
-template <int NB, int STAGES, int MT>
+template <int NB, int STAGES, int MT, bool PAIR = false>
 cudaError_t launch_wgrad(const CUtensorMap& dymap, const CUtensorMap& xmap, float* partial,
                          const TmaWgArgs& w, int splits, cudaStream_t st) {
-    using L = WSmem<NB, STAGES, MT>;
+    using L = WSmem<NB, STAGES, MT, PAIR>;
+    static_assert(L::kBytes <= 227 * 1024, "smem");
     static int attr_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
     if (attr_dev != dev) {
-        cudaError_t err = cudaFuncSetAttribute(conv_tma_wgrad_kernel<NB, STAGES, MT>,
+        cudaError_t err = cudaFuncSetAttribute(conv_tma_wgrad_kernel<NB, STAGES, MT, PAIR>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                L::kBytes);
         if (err != cudaSuccess) return err;
         attr_dev = dev;
     }
-    dim3 grid((w.K + BM * MT - 1) / (BM * MT), (w.Nn + NB - 1) / NB, splits);
-    cudaError_t le = pk_launch(conv_tma_wgrad_kernel<NB, STAGES, MT>, grid, dim3(kWgThreads),
-                               L::kBytes, st, dymap, xmap, partial, w);
+    dim3 grid(PAIR ? 2 * ((w.K + 2 * BM - 1) / (2 * BM)) : (w.K + BM * MT - 1) / (BM * MT),
+              (w.Nn + NB - 1) / NB, splits);
+    cudaError_t le = pk_launch(conv_tma_wgrad_kernel<NB, STAGES, MT, PAIR>, grid, dim3(kWgThreads),
+                               L::kBytes, st, PAIR ? 2 : 1, dymap, xmap, partial, w);
     if (le != cudaSuccess) return le;
     return cudaGetLastError();
 }
@@ -986,6 +1048,8 @@ cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, v
     if (wt.mt == 2)
         le = wt.nb == 256 ? launch_wgrad<256, 3, 2>(dymap, xmap, (float*)workspace, w, splits, st)
                           : launch_wgrad<128, 4, 2>(dymap, xmap, (float*)workspace, w, splits, st);
+    else if (wt.pair)
+        le = launch_wgrad<256, 6, 1, true>(dymap, xmap, (float*)workspace, w, splits, st);
     else if (wt.nb == 192)
         le = launch_wgrad<192, 5, 1>(dymap, xmap, (float*)workspace, w, splits, st);
     else

@@ -236,6 +236,43 @@ __device__ __forceinline__ void mma8_bf16(uint32_t tmem_d, uint64_t a0, uint64_t
         : "memory");
 }
 
+// ---- CTA pair (cta_group::2) ----
+// TMA load by either CTA of a pair whose completion is signalled on the
+// LEADER's barrier (bar = this CTA's barrier address with the peer bit cleared).
+__device__ __forceinline__ void tma_load_4d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                                 int c0, int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+        : "memory");
+}
+// Four M=256 MMAs (leader CTA; each CTA holds 128 A rows and half of B).
+__device__ __forceinline__ void mma4_bf16_pair(uint32_t tmem_d, uint64_t a0, uint64_t a1, uint64_t a2,
+                                               uint64_t a3, uint64_t b0, uint64_t b1, uint64_t b2,
+                                               uint64_t b3, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %10, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %5, %9, p;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %6, %9, 1;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %3, %7, %9, 1;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %4, %8, %9, 1;\n\t}" ::"r"(tmem_d),
+        "l"(a0), "l"(a1), "l"(a2), "l"(a3), "l"(b0), "l"(b1), "l"(b2), "l"(b3), "r"(idesc),
+        "r"(accumulate)
+        : "memory");
+}
+// Commit of the pair's MMAs, arriving on the barrier at this offset in BOTH CTAs.
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+        "[%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
