@@ -53,6 +53,7 @@ struct TmaConvArgs {
     int n_tiles_n, total_tiles;
     int num_phases;
     int mt;                   // 128-pixel M tiles per rectangle (1 or 2)
+    int m_tiles, total_pairs; // PAIR: rectangle tiles (M) and pair tiles ceil(m/2) x n
     int phase_tma;            // PHASED: 1 = per-phase TMA store maps (num_phases <= kStoreMaps)
     int ph_tw[kMaxPhases], ph_th[kMaxPhases], ph_tn[kMaxPhases];
     int ph_tile_start[kMaxPhases + 1];
@@ -65,10 +66,10 @@ struct TmaConvArgs {
 // MT = 128-pixel M tiles per CTA tile (2: a 256-pixel rectangle whose two
 // halves are two M=128 MMAs sharing every filter (B) stage — half the B bytes
 // per FLOP through TMA; needs 2 x MT x BN <= 512 TMEM columns, so BN <= 128)
-template <int BN, int STAGES, int MT = 1>
+template <int BN, int STAGES, int MT = 1, bool PAIR = false>
 struct FSmem {
     static constexpr int kA = MT * BM * BK * 2;
-    static constexpr int kB = BN * BK * 2;
+    static constexpr int kB = (PAIR ? BN / 2 : BN) * BK * 2;  // PAIR: this CTA's half of B
     static constexpr int kStage = kA + kB;
     // epilogue staging per warp: double-buffered, except BN=256 where the
     // smem goes to a 4th pipeline stage instead
@@ -119,13 +120,27 @@ __device__ __forceinline__ int tile_kblocks(const TmaConvArgs& g, const RectInfo
     return NARROW ? (ri.ntaps * g.cpt + 7) / 8 : ri.ntaps * g.cpt;
 }
 
-template <int BN, int STAGES, bool PHASED, bool NARROW, int MT>
+// PAIR (cluster of 2, cta_group::2; BN = 256, unphased, MT = 1): the pair owns
+// two consecutive rectangles of one output-channel tile; each CTA loads its own
+// rectangle's tap boxes and HALF of the 256 filter rows, the leader issues
+// M=256 MMAs, commits are multicast and both epilogues release the leader's
+// accumulator remotely.
+template <int BN, int STAGES, bool PHASED, bool NARROW, int MT, bool PAIR = false>
 __global__ void __launch_bounds__(kFpropThreads, 1)
     conv_tma_fprop_kernel(const __grid_constant__ CUtensorMap amap,
                           const __grid_constant__ CUtensorMap bmap,
                           const __grid_constant__ YMaps ymaps, __nv_bfloat16* __restrict__ out,
                           const __grid_constant__ TmaConvArgs g, const pk_epilogue epi) {
-    using L = FSmem<BN, STAGES, MT>;
+    using L = FSmem<BN, STAGES, MT, PAIR>;
+    static_assert(!PAIR || (MT == 1 && !PHASED && !NARROW && BN == 256), "pair variant");
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    // tile loop: this CTA's rectangle tile of pair tile pt (PAIR) or tile pt
+    const int t_first = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int t_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    const int t_end = PAIR ? g.total_pairs : g.total_tiles;
+    auto my_tile = [&](int pt) {
+        return PAIR ? ((pt / g.n_tiles_n) * 2 + (int)rank) * g.n_tiles_n + pt % g.n_tiles_n : pt;
+    };
     static_assert(2 * MT * BN <= 512, "TMEM");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -147,7 +162,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tmem_full[i], 1);
-            mbar_init(&tmem_empty[i], 8);
+            mbar_init(&tmem_empty[i], PAIR ? 16 : 8);
         }
         fence_barrier_init();
         tma_prefetch(&amap);
@@ -155,9 +170,19 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
         if (!PHASED || g.phase_tma)
             for (int i = 0; i < (PHASED ? g.num_phases : 1); ++i) tma_prefetch(&ymaps.m[i]);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, kTmemCols);
+    if (warp == 1) {
+        if (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(kTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            tmem_alloc(tmem_slot, kTmemCols);
+        }
+    }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_wait();  // predecessor complete: inputs ready, outputs free
@@ -168,13 +193,30 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
-                const RectInfo ri = rect_info(g, t);
+            for (int pt = t_first; pt < t_end; pt += t_step) {
+                const RectInfo ri = rect_info(g, my_tile(pt));
                 const int nkb = tile_kblocks<NARROW>(g, ri);
                 const int ys = ri.h0 * g.mult_h, xs = ri.w0 * g.mult_w;
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * L::kStage;
+                    if (PAIR) {
+                        const int tap = kb / g.cpt, chunk = kb - tap * g.cpt;
+                        const int ti = ri.tap0 + tap;
+                        const unsigned short rs = g.taps[ti];
+                        const uint32_t fb = smem_u32(&full[stage]) & 0xFEFFFFFFu;  // leader's
+                        if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (L::kA + L::kB));
+                        tma_load_4d_pair(smem_u32(sa), &amap, fb, chunk * BK, xs + g.off_w[ti],
+                                         ys + g.off_h[ti], ri.n0);
+                        tma_load_2d_pair(smem_u32(sa + L::kA), &bmap, fb,
+                                         ((rs >> 8) * g.S + (rs & 0xff)) * g.red_ch + chunk * BK,
+                                         ri.nt * BN + (int)rank * (BN / 2));
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                        continue;
+                    }
                     mbar_arrive_expect_tx(&full[stage], L::kA + L::kB);
                     if (NARROW) {
                         // eight 16-byte-row boxes, one per (tap, 8-channel group);
@@ -215,12 +257,13 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------------------------------
-        constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, false, false);
+      if (!PAIR || rank == 0) {
+        constexpr uint32_t idesc = idesc_bf16_f32(PAIR ? 2 * BM : BM, BN, false, false);
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
-        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
-            const RectInfo ri = rect_info(g, t);
+        for (int pt = t_first; pt < t_end; pt += t_step) {
+            const RectInfo ri = rect_info(g, my_tile(pt));
             const int nkb = tile_kblocks<NARROW>(g, ri);
             if (nkb == 0) continue;
             const int a = it & 1;
@@ -238,6 +281,18 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                     const uint32_t a_base = smem_u32(smem + stage * L::kStage);
                     const uint32_t b_base = a_base + L::kA;
                     const uint64_t bd0 = umma_desc_sw128(b_base, 16, 1024);
+                    if (PAIR) {
+                        const uint64_t ad0 = umma_desc_sw128(a_base, 16, 1024);
+                        mma4_bf16_pair(d_tmem, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + 2, bd0 + 4,
+                                       bd0 + 6, idesc, kb != 0);
+                        mma_commit_pair(&empty[stage]);
+                        if (kb == nkb - 1) mma_commit_pair(&tmem_full[a]);
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                        continue;
+                    }
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt) {
                         // NARROW: K step k covers boxes 2k, 2k+1 (2 KB apart, LBO),
@@ -257,6 +312,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                 }
             }
         }
+      }
     } else {
         // ---------------- epilogue (8 warps) ---------------------------------
         const int ew = warp - 2;
@@ -269,8 +325,8 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
         BnStatAcc bacc;
         bacc.init();
         int it = 0;
-        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
-            const RectInfo ri = rect_info(g, t);
+        for (int pt = t_first; pt < t_end; pt += t_step) {
+            const RectInfo ri = rect_info(g, my_tile(pt));
             const int n0c = ri.nt * BN;
             const bool live = ri.ntaps > 0;
             int a = 0;
@@ -304,7 +360,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
             if (live && mt == MT - 1 && my_last < 0) {
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tmem_empty[a]);
+                if (lane == 0) { if (PAIR) mbar_arrive_leader(&tmem_empty[a]); else mbar_arrive(&tmem_empty[a]); }
             }
 #pragma unroll 1
             for (int ci = half; ci < nchunks; ci += 2) {
@@ -323,7 +379,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                     if (ci == my_last) {
                         tc_fence_before();
                         __syncwarp();
-                        if (lane == 0) mbar_arrive(&tmem_empty[a]);
+                        if (lane == 0) { if (PAIR) mbar_arrive_leader(&tmem_empty[a]); else mbar_arrive(&tmem_empty[a]); }
                     }
                 } else {
 #pragma unroll
@@ -386,9 +442,14 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, kTmemCols);
+        if (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(kTmemCols));
+        else
+            tmem_dealloc(tmem_base, kTmemCols);
     }
 }
 
@@ -700,12 +761,12 @@ __global__ void wgrad_sum_kernel(const float* __restrict__ partial, int splits, 
 // ---------------------------------------------------------------------------
 // host
 
-template <int BN, int STAGES, bool PHASED, bool NARROW, int MT = 1>
+template <int BN, int STAGES, bool PHASED, bool NARROW, int MT = 1, bool PAIR = false>
 cudaError_t launch_fprop(const CUtensorMap& amap, const CUtensorMap& bmap, const YMaps& ymap,
                          void* out, const TmaConvArgs& g, const pk_epilogue& e, cudaStream_t st) {
-    using L = FSmem<BN, STAGES, MT>;
+    using L = FSmem<BN, STAGES, MT, PAIR>;
     static_assert(L::kBytes <= 227 * 1024, "smem");
-    auto kern = conv_tma_fprop_kernel<BN, STAGES, PHASED, NARROW, MT>;
+    auto kern = conv_tma_fprop_kernel<BN, STAGES, PHASED, NARROW, MT, PAIR>;
     static int attr_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -716,10 +777,15 @@ cudaError_t launch_fprop(const CUtensorMap& amap, const CUtensorMap& bmap, const
         attr_dev = dev;
     }
     int grid = num_sms_of_current_device();
-    if (g.total_tiles < grid) grid = g.total_tiles;
+    if (PAIR) {
+        grid = grid / 2 * 2;
+        if (2 * g.total_pairs < grid) grid = 2 * g.total_pairs;
+    } else if (g.total_tiles < grid) {
+        grid = g.total_tiles;
+    }
     if (grid < 1) grid = 1;
-    cudaError_t le = pk_launch(kern, dim3(grid), dim3(kFpropThreads), L::kBytes, st, amap, bmap,
-                               ymap, (__nv_bfloat16*)out, g, e);
+    cudaError_t le = pk_launch(kern, dim3(grid), dim3(kFpropThreads), L::kBytes, st, PAIR ? 2 : 1,
+                               amap, bmap, ymap, (__nv_bfloat16*)out, g, e);
     if (le != cudaSuccess) return le;
     count_launch();
     return cudaGetLastError();
@@ -729,6 +795,8 @@ template <bool PHASED, bool NARROW>
 cudaError_t dispatch_fprop(int bn, const CUtensorMap& amap, const CUtensorMap& bmap,
                            const YMaps& ymap, void* out, const TmaConvArgs& g,
                            const pk_epilogue& e, cudaStream_t st) {
+    if (g.total_pairs > 0 && !PHASED && !NARROW && bn == 256)
+        return launch_fprop<256, 6, false, false, 1, true>(amap, bmap, ymap, out, g, e, st);
     if (g.mt == 2 && !PHASED && !NARROW) {
         if (bn == 64) return launch_fprop<64, 4, false, false, 2>(amap, bmap, ymap, out, g, e, st);
         if (bn == 128) return launch_fprop<128, 3, false, false, 2>(amap, bmap, ymap, out, g, e, st);
@@ -862,7 +930,18 @@ cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, cons
                            t.mult_h, narrow ? 8 : 64))
         return cudaErrorNotSupported;
     const long long kred = (long long)g->r * g->s * src_pitch;
-    if (!tc::make_map_2d(&bmap, filt, t.n_out, kred, kred, bn)) return cudaErrorInvalidValue;
+    // CTA pairs for 256-wide tiles of unphased spatial convolutions (PK_TMA_PAIR=0 disables)
+    static const bool pair_off = [] {
+        const char* v = std::getenv("PK_TMA_PAIR");
+        return v && v[0] == '0';
+    }();
+    t.m_tiles = t.n_tiles_n ? t.total_tiles / t.n_tiles_n : 0;
+    t.total_pairs = 0;
+    if (!pair_off && !narrow && sh == 1 && sw == 1 && bn == 256 && t.mt == 1 && g->r * g->s > 1 &&
+        (!epi || !epi->stats) && (long long)((t.m_tiles + 1) / 2) * t.n_tiles_n >= 74)
+        t.total_pairs = (t.m_tiles + 1) / 2 * t.n_tiles_n;
+    if (!tc::make_map_2d(&bmap, filt, t.n_out, kred, kred, t.total_pairs ? bn / 2 : bn))
+        return cudaErrorInvalidValue;
     const bool phased = sh > 1 || sw > 1;
     if (!phased &&
         !tc::make_map_nhwc(&ymap.m[0], out, g->n, t.Ho, t.Wo, out_pitch, t.qbw, t.qbh, t.qbn))
