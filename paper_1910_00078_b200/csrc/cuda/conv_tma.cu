@@ -1067,6 +1067,8 @@ cudaError_t launch_wgrad(const CUtensorMap& dymap, const CUtensorMap& xmap, floa
 }
 
 size_t pk_tma_wgrad_workspace(const pk_conv_geom* g, int num_sms) {
+    if (const int hs = pk_halo_wgrad_splits(g, num_sms))
+        return (size_t)hs * g->k * g->r * g->s * g->x_pitch * 4;
     int tiles_mn, num_kb;
     RectTile rt;
     wgrad_geometry(g, &tiles_mn, &num_kb, &rt);
@@ -1085,6 +1087,20 @@ bool pk_tma_wgrad_supported(const pk_conv_geom* g) {
 cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, void* dw,
                          void* workspace, int num_sms, cudaStream_t st) {
     if (!pk_tma_wgrad_supported(g)) return cudaErrorNotSupported;
+    if (const int hs = pk_halo_wgrad_splits(g, num_sms)) {
+        // 64-channel spatial filters: padded-grid halo kernel + deterministic split sum
+        cudaError_t le = pk_halo_wgrad(g, dy, x, static_cast<float*>(workspace), hs, st);
+        if (le != cudaErrorNotSupported) {
+            if (le != cudaSuccess) return le;
+            const long long total = (long long)g->k * g->r * g->s * g->x_pitch;
+            long long blocks = (total + 255) / 256;
+            if (blocks > 148 * 16) blocks = 148 * 16;
+            le = pk_launch(wgrad_sum_kernel, dim3((unsigned)blocks), dim3(256), 0, st,
+                           (const float*)workspace, hs, total, (__nv_bfloat16*)dw);
+            count_launch();
+            return le != cudaSuccess ? le : cudaGetLastError();
+        }
+    }
     int tiles_mn, num_kb;
     RectTile rt;
     wgrad_geometry(g, &tiles_mn, &num_kb, &rt);

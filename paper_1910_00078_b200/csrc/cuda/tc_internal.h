@@ -26,3 +26,10 @@ cudaError_t pk_halo_conv(const pk_conv_geom* g, bool dgrad, const void* src, con
 int pk_gemm_pair_eligible(int M, int kdim, int n_out, int out_pitch);
 cudaError_t pk_gemm_pair(const void* a, const void* b, void* y, int M, int kdim, int n_out,
                          int out_pitch, int P, int Q, const pk_epilogue* epi, cudaStream_t st);
+
+// Padded-grid halo backward weights for stride-1 spatial filters on 64-channel
+// tensors (wgrad_halo.cu): fp32 partials [splits][K][R*S*64]; splits = 0 when
+// the geometry is not eligible.
+int pk_halo_wgrad_splits(const pk_conv_geom* g, int num_sms);
+cudaError_t pk_halo_wgrad(const pk_conv_geom* g, const void* dy, const void* x, float* partial,
+                          int splits, cudaStream_t st);
