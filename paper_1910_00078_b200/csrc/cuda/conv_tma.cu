@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                     const uint32_t a_base = smem_u32(smem + stage * L::kStage);
                     const uint32_t b_base = a_base + L::kA;
                     const uint64_t bd0 = umma_desc_sw128(b_base, 16, 1024);
-                    if (PAIR) {
+                    if constexpr (PAIR) {
                         const uint64_t ad0 = umma_desc_sw128(a_base, 16, 1024);
                         mma4_bf16_pair(d_tmem, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + 2, bd0 + 4,
                                        bd0 + 6, idesc, kb != 0);
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                             phase ^= 1;
                         }
                         continue;
-                    }
+                    } else {
 #pragma unroll
                     for (int mt = 0; mt < MT; ++mt) {
                         // NARROW: K step k covers boxes 2k, 2k+1 (2 KB apart, LBO),
@@ -305,6 +305,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                     }
                     mma_commit_elect(&empty[stage]);
                     if (kb == nkb - 1) mma_commit_elect(&tmem_full[a]);
+                    }
                 }
                 if (++stage == STAGES) {
                     stage = 0;
