@@ -322,6 +322,76 @@ __device__ __forceinline__ void pdl_trigger() {
 
 bool pdl_enabled();  // PK_PDL=0 disables (A/B comparisons)
 
+// ---- in-kernel split-K finish (wgrad) ----------------------------------------
+// The CTAs of a split-K wgrad grid each write an fp32 partial [split][total];
+// instead of a separate sum launch, every CTA arrives on a grid barrier and then
+// sums a slice of the output over all splits in FIXED split order (deterministic,
+// bit-identical to wgrad_sum_kernel) and stores bf16. Only for grids whose CTAs
+// are all co-resident (grid <= SMs, one CTA per SM): the host checks. sync[0]
+// counts arrivals, sync[1] departures; the last CTA to leave resets both, so a
+// slot is reusable by the next launch (stream-ordered) and by graph replays.
+__device__ __forceinline__ void splitk_finish(const float* __restrict__ partial, int splits,
+                                              long long total, __nv_bfloat16* __restrict__ dw,
+                                              unsigned int* sync) {
+    const unsigned nctas = gridDim.x * gridDim.y * gridDim.z;
+    const unsigned cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    __threadfence();  // this CTA's partial stores before its arrival
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicAdd(&sync[0], 1u);
+        unsigned seen;
+        do {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(seen) : "l"(sync) : "memory");
+            if (seen < nctas) __nanosleep(64);
+        } while (seen < nctas);
+    }
+    __syncthreads();
+    const long long quads = total / 4;
+    const long long per = (quads + nctas - 1) / nctas;
+    const long long q0 = (long long)cta * per, q1 = q0 + per < quads ? q0 + per : quads;
+    const float4* p = reinterpret_cast<const float4*>(partial);
+    for (long long i = q0 + threadIdx.x; i < q1; i += blockDim.x) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        int s = 0;
+        for (; s + 8 <= splits; s += 8) {  // eight loads in flight, then the adds in order
+            float4 v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + (size_t)(s + u) * quads + i);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                acc.x += v[u].x;
+                acc.y += v[u].y;
+                acc.z += v[u].z;
+                acc.w += v[u].w;
+            }
+        }
+        for (; s < splits; ++s) {
+            const float4 v = __ldcg(p + (size_t)s * quads + i);
+            acc.x += v.x;
+            acc.y += v.y;
+            acc.z += v.z;
+            acc.w += v.w;
+        }
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
+        reinterpret_cast<uint2*>(dw)[i] =
+            make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi));
+    }
+    if (cta == 0)  // tail (total not a multiple of 4)
+        for (long long i = quads * 4 + threadIdx.x; i < total; i += blockDim.x) {
+            float a = 0.f;
+            for (int s = 0; s < splits; ++s) a += __ldcg(partial + (size_t)s * total + i);
+            dw[i] = __float2bfloat16_rn(a);
+        }
+    __syncthreads();
+    if (threadIdx.x == 0 && atomicAdd(&sync[1], 1u) == nctas - 1) {
+        sync[0] = 0u;
+        sync[1] = 0u;
+        __threadfence();
+    }
+}
+// A free barrier slot (round-robin over a static pool) or nullptr if unavailable.
+unsigned int* splitk_sync_slot();
+
 template <typename... KArgs, typename... Args>
 cudaError_t pk_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                       Args&&... args) {

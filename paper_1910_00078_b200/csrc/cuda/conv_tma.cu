@@ -466,6 +466,12 @@ struct TmaWgArgs {
     int tw, th;                // rectangles per row / column
     int num_kb, kb_per_split;
     unsigned long long* trace;  // PK_WG_TRACE: clock64 stamps of CTA (0,0,0) (profiling only)
+    // in-kernel split-K finish (single-CTA tiles, co-resident grid): barrier slot,
+    // output and split count; sync == nullptr -> the host launches wgrad_sum_kernel
+    unsigned int* sync;
+    __nv_bfloat16* dw;
+    int splits;
+    long long total;
 };
 __device__ __forceinline__ void wgstamp(const TmaWgArgs& g, int ev) {
     if (g.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (threadIdx.x & 31) == 0)
@@ -700,6 +706,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         }
         if (warp == 2) wgstamp(g, 3);
     }
+    if (!PAIR && g.sync) splitk_finish(partial, g.splits, g.total, g.dw, g.sync);
     tc_fence_before();
     __syncthreads();
     if (PAIR)
@@ -1090,9 +1097,12 @@ cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, v
     if (!pk_tma_wgrad_supported(g)) return cudaErrorNotSupported;
     if (const int hs = pk_halo_wgrad_splits(g, num_sms)) {
         // 64-channel spatial filters: padded-grid halo kernel + deterministic split sum
-        cudaError_t le = pk_halo_wgrad(g, dy, x, static_cast<float*>(workspace), hs, st);
+        unsigned int* sync = splitk_sync_slot();
+        cudaError_t le = pk_halo_wgrad(g, dy, x, static_cast<float*>(workspace), hs, st,
+                                       static_cast<__nv_bfloat16*>(dw), sync);
         if (le != cudaErrorNotSupported) {
             if (le != cudaSuccess) return le;
+            if (sync) return cudaSuccess;  // finished in-kernel
             const long long total = (long long)g->k * g->r * g->s * g->x_pitch;
             long long blocks = (total + 255) / 256;
             if (blocks > 148 * 16) blocks = 148 * 16;
@@ -1140,6 +1150,13 @@ cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, v
                            rt.bw, rt.bh, rt.bn, g->str_w, g->str_h))
         return cudaErrorNotSupported;
     const WgTile wt = wgrad_tile(g);
+    w.dw = static_cast<__nv_bfloat16*>(dw);
+    w.splits = splits;
+    w.total = (long long)w.K * w.Nn;
+    // in-kernel finish pays for small outputs (launch saved); large ones want the
+    // full-GPU sum kernel (measured: conv2 wgrads -7 us each, conv4/5 3x3 +8 us)
+    if (!wt.pair && (long long)tiles_mn * splits <= num_sms && w.total <= 65536)
+        w.sync = splitk_sync_slot();
     cudaError_t le;
     if (wt.mt == 2)
         le = wt.nb == 256 ? launch_wgrad<256, 3, 2>(dymap, xmap, (float*)workspace, w, splits, st)
@@ -1160,6 +1177,10 @@ cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, v
                 w.kb_per_split, (long long)(h[1] - h[0]), (long long)(h[2] - h[0]), (long long)(h[3] - h[0]));
         for (int e = 8; e < 16; ++e) fprintf(stderr, " %lld", (long long)(h[e] - h[0]));
         fprintf(stderr, "\n");
+    }
+    if (w.sync && !wt.pair) {  // finished in-kernel
+        count_launch();
+        return cudaGetLastError();
     }
     const long long total = (long long)w.K * w.Nn;
     long long blocks = (total + 255) / 256;

@@ -11,6 +11,25 @@ namespace pk {
 static std::atomic<uint64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
+// Split-K grid-barrier slots (zero-initialised at module load; every use
+// leaves its slot zeroed again).
+__device__ unsigned int g_splitk_sync[64][2];
+
+unsigned int* splitk_sync_slot() {
+    static unsigned int* base = [] {
+        void* p = nullptr;
+        if (std::getenv("PK_SPLITK_FUSE") && std::getenv("PK_SPLITK_FUSE")[0] == '0') return (unsigned int*)nullptr;
+        if (cudaGetSymbolAddress(&p, g_splitk_sync) != cudaSuccess) {
+            cudaGetLastError();
+            return (unsigned int*)nullptr;
+        }
+        return static_cast<unsigned int*>(p);
+    }();
+    static std::atomic<unsigned> next{0};
+    if (!base) return nullptr;
+    return base + 2 * (next.fetch_add(1, std::memory_order_relaxed) % 64);
+}
+
 bool pdl_enabled() {
     static const bool on = [] {
         const char* v = std::getenv("PK_PDL");

@@ -31,5 +31,7 @@ cudaError_t pk_gemm_pair(const void* a, const void* b, void* y, int M, int kdim,
 // tensors (wgrad_halo.cu): fp32 partials [splits][K][R*S*64]; splits = 0 when
 // the geometry is not eligible.
 int pk_halo_wgrad_splits(const pk_conv_geom* g, int num_sms);
+// dw/sync: when sync is non-null the kernel finishes the split-K sum itself
+// (grid barrier, fixed split order) and writes bf16 dW.
 cudaError_t pk_halo_wgrad(const pk_conv_geom* g, const void* dy, const void* x, float* partial,
-                          int splits, cudaStream_t st);
+                          int splits, cudaStream_t st, void* dw, unsigned int* sync);

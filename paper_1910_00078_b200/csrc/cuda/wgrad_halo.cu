@@ -46,6 +46,9 @@ struct HwArgs {
     int blocks_img, total_kb, kb_per;
     int taps, mtiles;
     int tap_off[16];         // grid-row offset r*Wg + s of tap t
+    unsigned int* sync;      // in-kernel split-K finish (nullptr: separate sum kernel)
+    __nv_bfloat16* dw;
+    int splits;
 };
 
 __global__ void __launch_bounds__(kHwThreads, 1)
@@ -173,6 +176,7 @@ __global__ void __launch_bounds__(kHwThreads, 1)
             }
         }
     }
+    if (g.sync) splitk_finish(partial, g.splits, (long long)g.K * g.Nn, g.dw, g.sync);
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -226,10 +230,13 @@ int pk_halo_wgrad_splits(const pk_conv_geom* g, int num_sms) {
 }
 
 cudaError_t pk_halo_wgrad(const pk_conv_geom* g, const void* dy, const void* x, float* partial,
-                          int splits, cudaStream_t st) {
+                          int splits, cudaStream_t st, void* dw, unsigned int* sync) {
     HwArgs a;
     if (!halo_args(g, a) || splits < 1) return cudaErrorNotSupported;
     a.kb_per = (a.total_kb + splits - 1) / splits;
+    a.sync = sync;  // grid = splits <= SMs, one CTA per SM: co-resident
+    a.dw = static_cast<__nv_bfloat16*>(dw);
+    a.splits = splits;
     CUtensorMap xmap{}, dymap{};
     if (!tc::make_map_nhwc(&xmap, x, g->n, g->h, g->w, 64, a.Wg, a.KBR + a.R - 1, 1) ||
         !tc::make_map_nhwc(&dymap, dy, g->n, g->p, g->q, 64, a.Wg, a.KBR, 1))
