@@ -65,6 +65,9 @@ struct ConvTcArgs {
     // rows_per_batch = b_batch_mtiles * BM; B rows of batch b start at
     // b * b_batch_rows. 0 = not batched.
     int b_batch_mtiles, b_batch_rows;
+    // plain modes: B given MN-major (the filter W[K][C] itself for backward data,
+    // no transpose launch): BN/64 atoms of 64 output channels x 64 k per k-block
+    int b_mn;
     // phase decomposition (PHASE_DGRAD)
     int num_phases, cpt;   // cpt = red_ch / 64
     int ph_tile_start[kMaxPhases + 1];
@@ -257,9 +260,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                             // this CTA's N tile never changes (grid % n_tiles_n == 0):
                             // load its whole B slice once
                             mbar_arrive_expect_tx(bfull, ti.nkb * L::kB);
-                            for (int k = 0; k < ti.nkb; ++k)
-                                tma_load_2d(smem_u32(smem + L::kResOff + k * L::kB), &bmap, bfull,
-                                            k * BK, n0);
+                            for (int k = 0; k < ti.nkb; ++k) {
+                                if (g.b_mn) {
+                                    for (int j = 0; j < BN / 64; ++j)
+                                        tma_load_2d(smem_u32(smem + L::kResOff + k * L::kB + j * 8192),
+                                                    &bmap, bfull, n0 + 64 * j, k * BK);
+                                } else {
+                                    tma_load_2d(smem_u32(smem + L::kResOff + k * L::kB), &bmap, bfull,
+                                                k * BK, n0);
+                                }
+                            }
                         }
                         mbar_arrive_expect_tx(&full[stage], L::kA);
                     } else {
@@ -267,7 +277,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int brow = kPlain && g.b_batch_mtiles
                                              ? (ti.m0 / BM / g.b_batch_mtiles) * g.b_batch_rows
                                              : 0;
-                        tma_load_2d(smem_u32(sa + L::kA), &bmap, &full[stage], bcol, n0 + brow);
+                        if (kPlain && g.b_mn) {
+                            for (int j = 0; j < BN / 64; ++j)
+                                tma_load_2d(smem_u32(sa + L::kA + j * 8192), &bmap, &full[stage],
+                                            n0 + 64 * j, kb * BK);
+                        } else {
+                            tma_load_2d(smem_u32(sa + L::kA), &bmap, &full[stage], bcol, n0 + brow);
+                        }
                     }
                     if (kPlain) tma_load_2d(smem_u32(sa), &amap, &full[stage], kb * BK, ti.m0);
                 }
@@ -316,7 +332,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     } else if (warp == 4) {
         // ======================= MMA issuer ==================================
-        constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, false, false);
+        const uint32_t idesc = idesc_bf16_f32(BM, BN, false, kPlain && g.b_mn);
+        // B k-step (16 k): K-major +32 B, MN-major +16 rows (2048 B); atoms 8 KB apart
+        const uint64_t bks = kPlain && g.b_mn ? 128 : 2;
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
@@ -343,10 +361,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                 ? smem_u32(smem + L::kResOff + kb * L::kB)
                                                 : a_base + L::kA;
                     const uint64_t ad0 = umma_desc_sw128(a_base, 16, 1024);
-                    const uint64_t bd0 = umma_desc_sw128(b_base, 16, 1024);
+                    const uint64_t bd0 = umma_desc_sw128(b_base, kPlain && g.b_mn ? 8192 : 16, 1024);
                     if (!(g.debug & 1))
-                        mma4_bf16(d_tmem, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + 2, bd0 + 4,
-                                  bd0 + 6, idesc, kb != 0);
+                        mma4_bf16(d_tmem, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + bks, bd0 + 2 * bks,
+                                  bd0 + 3 * bks, idesc, kb != 0);
                     mma_commit_elect(&empty[stage]);
                     if (kb == ti.nkb - 1) mma_commit_elect(&tmem_full[a]);
                 }
@@ -762,10 +780,15 @@ cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const 
                                    void* workspace, const pk_tc_config* cfg, cudaStream_t st,
                                    const pk_epilogue* stats_epi) {
     if (!pk_tc_dgrad_supported(g) || !aligned16(dy) || !aligned16(dx)) return cudaErrorNotSupported;
-    // B operand: Wt[c][r][s][k] = W[k][r][s][c]
-    cudaError_t err = pk_cuda_filter_to_dgrad(g, PK_BF16, f, workspace, st);
-    if (err != cudaSuccess) return err;
     const int kp = pk_pitch(g->k);
+    const bool plain1x1 = g->r == 1 && g->s == 1 && g->str_h == 1 && g->str_w == 1 &&
+                          g->pad_h == 0 && g->pad_w == 0;
+    static const bool no_mn = std::getenv("PK_DGRAD_TRANSPOSE") != nullptr;  // A/B experiments
+    // 1x1: the filter W[K][C] is the MN-major B operand as is (no transpose launch);
+    // others: B operand Wt[c][r][s][k] = W[k][r][s][c]
+    const bool b_mn = plain1x1 && !no_mn && g->f_pitch % 64 == 0 && g->k == kp;
+    cudaError_t err = b_mn ? cudaSuccess : pk_cuda_filter_to_dgrad(g, PK_BF16, f, workspace, st);
+    if (err != cudaSuccess) return err;
     ConvTcArgs t{};
     t.M = g->n * g->h * g->w;
     t.Ho = g->h;
@@ -801,15 +824,19 @@ cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const 
         e.bnb_relu = stats_epi->bnb_relu;
     }
     CUtensorMap amap{}, bmap{};
-    if (!tc::make_map_2d(&bmap, workspace, g->c, t.kred, t.kred, bn)) return cudaErrorInvalidValue;
-    const bool plain = g->r == 1 && g->s == 1 && g->str_h == 1 && g->str_w == 1 &&
-                       g->pad_h == 0 && g->pad_w == 0;
+    if (b_mn) {
+        t.b_mn = 1;
+        if (!tc::make_map_2d(&bmap, f, g->k, g->f_pitch, g->f_pitch, 64)) return cudaErrorInvalidValue;
+    } else if (!tc::make_map_2d(&bmap, workspace, g->c, t.kred, t.kred, bn)) {
+        return cudaErrorInvalidValue;
+    }
+    const bool plain = plain1x1;
     if (plain) {
         static const bool pair_all = std::getenv("PK_TC2_ALL") != nullptr;
         if (bn == 256 && (t.kred > 256 || pair_all) && !e.stats && !t.debug_nores &&
             pk_gemm_pair_eligible(t.M, t.kred, g->c, g->x_pitch))
-            return pk_gemm_pair(dy, workspace, dx, t.M, t.kred, g->c, g->x_pitch, g->h, g->w, nullptr,
-                                st);
+            return pk_gemm_pair(dy, b_mn ? f : workspace, dx, t.M, t.kred, g->c, g->x_pitch, g->h, g->w,
+                                nullptr, st, b_mn ? g->f_pitch : 0);
         if (!tc::make_map_2d(&amap, dy, t.M, g->y_pitch, g->y_pitch, BM)) return cudaErrorInvalidValue;
         return dispatch_bn<PLAIN>(bn, amap, bmap, dy, dx, t, e, st);
     }

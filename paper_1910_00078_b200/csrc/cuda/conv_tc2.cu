@@ -46,6 +46,7 @@ struct Gemm2Args {
     int n_out, out_pitch;
     int m_pairs, n_tiles, total;  // pair tiles: (M / 256) x (N / 256)
     int P, Q;       // output image extent (per-activation epilogues)
+    int b_mn;       // B MN-major: two 64-wide atoms (8 KB apart) per CTA half
 };
 
 __device__ __forceinline__ void commit_pair(uint64_t* bar) {
@@ -130,7 +131,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     const uint32_t fb = smem_u32(&full[stage]) & 0xFEFFFFFFu;  // leader's barrier
                     if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * kStage2);
                     tma_load_2d_pair(smem_u32(sa), &amap, fb, kb * 64, arow);
-                    tma_load_2d_pair(smem_u32(sa + kHalfA), &bmap, fb, kb * 64, brow);
+                    if (g.b_mn) {
+                        tma_load_2d_pair(smem_u32(sa + kHalfA), &bmap, fb, brow, kb * 64);
+                        tma_load_2d_pair(smem_u32(sa + kHalfA + 8192), &bmap, fb, brow + 64, kb * 64);
+                    } else {
+                        tma_load_2d_pair(smem_u32(sa + kHalfA), &bmap, fb, kb * 64, brow);
+                    }
                     if (++stage == kStages2) {
                         stage = 0;
                         phase ^= 1;
@@ -140,7 +146,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         }
     } else if (warp == 1) {
         if (rank == 0) {
-            constexpr uint32_t idesc = idesc_bf16_f32(256, 256, false, false);
+            const uint32_t idesc = idesc_bf16_f32(256, 256, false, g.b_mn != 0);
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
@@ -153,8 +159,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem + stage * kStage2);
-                    mma4_pair(d, umma_desc_sw128(sa, 16, 1024), umma_desc_sw128(sa + kHalfA, 16, 1024),
-                              idesc, kb != 0);
+                    if (g.b_mn) {
+                        const uint64_t ad = umma_desc_sw128(sa, 16, 1024);
+                        const uint64_t bd = umma_desc_sw128(sa + kHalfA, 8192, 1024);
+                        mma4_bf16_pair(d, ad, ad + 2, ad + 4, ad + 6, bd, bd + 128, bd + 256, bd + 384,
+                                       idesc, kb != 0);
+                    } else {
+                        mma4_pair(d, umma_desc_sw128(sa, 16, 1024), umma_desc_sw128(sa + kHalfA, 16, 1024),
+                                  idesc, kb != 0);
+                    }
                     commit_pair(&empty[stage]);
                     if (kb == g.num_kb - 1) commit_pair(&tmem_full[a]);
                     if (++stage == kStages2) {
@@ -255,10 +268,12 @@ int pk_gemm_pair_eligible(int M, int kdim, int n_out, int out_pitch) {
 }
 
 cudaError_t pk_gemm_pair(const void* a, const void* b, void* y, int M, int kdim, int n_out,
-                         int out_pitch, int P, int Q, const pk_epilogue* epi, cudaStream_t st) {
+                         int out_pitch, int P, int Q, const pk_epilogue* epi, cudaStream_t st,
+                         int b_mn_pitch) {
     CUtensorMap amap{}, bmap{}, ymap{};
-    if (!tc::make_map_2d(&amap, a, M, kdim, kdim, 128) ||
-        !tc::make_map_2d(&bmap, b, n_out, kdim, kdim, 128) ||
+    const bool bmap_ok = b_mn_pitch > 0 ? tc::make_map_2d(&bmap, b, kdim, b_mn_pitch, b_mn_pitch, 64)
+                                        : tc::make_map_2d(&bmap, b, n_out, kdim, kdim, 128);
+    if (!tc::make_map_2d(&amap, a, M, kdim, kdim, 128) || !bmap_ok ||
         !tc::make_map_2d(&ymap, y, M, out_pitch, out_pitch, 32))
         return cudaErrorInvalidValue;
     Gemm2Args g{};
@@ -271,6 +286,7 @@ cudaError_t pk_gemm_pair(const void* a, const void* b, void* y, int M, int kdim,
     g.total = g.m_pairs * g.n_tiles;
     g.P = P;
     g.Q = Q;
+    g.b_mn = b_mn_pitch > 0;
     pk_epilogue e{};
     e.act = -1;
     if (epi) e = *epi;

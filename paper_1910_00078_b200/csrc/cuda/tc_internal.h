@@ -24,8 +24,11 @@ cudaError_t pk_halo_conv(const pk_conv_geom* g, bool dgrad, const void* src, con
 // CTA-pair (cta_group::2) plain GEMM for 1x1 layers whose filter slice cannot
 // stay resident (conv_tc2.cu): y[M][out_pitch] = a[M][kdim] . b[n_out][kdim]^T.
 int pk_gemm_pair_eligible(int M, int kdim, int n_out, int out_pitch);
+// b_mn_pitch > 0: b is MN-major ([kdim rows][b_mn_pitch], e.g. the filter itself for
+// backward data) instead of K-major [n_out][kdim].
 cudaError_t pk_gemm_pair(const void* a, const void* b, void* y, int M, int kdim, int n_out,
-                         int out_pitch, int P, int Q, const pk_epilogue* epi, cudaStream_t st);
+                         int out_pitch, int P, int Q, const pk_epilogue* epi, cudaStream_t st,
+                         int b_mn_pitch = 0);
 
 // Padded-grid halo backward weights for stride-1 spatial filters on 64-channel
 // tensors (wgrad_halo.cu): fp32 partials [splits][K][R*S*64]; splits = 0 when
