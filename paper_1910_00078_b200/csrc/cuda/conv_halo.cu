@@ -44,6 +44,7 @@ struct HaloArgs {
     int NR;                      // halo rows per tile (box height)
     int flip;                    // dgrad: tap (r,s) uses filter tap (R-1-r, S-1-s)
     int debug;                   // PK_HALO_DEBUG (timing experiments only): 1 = 8-row-aligned tap views
+    int b_mn;                    // dgrad: B = the filter itself (MN-major 64 x 64 atoms)
 };
 
 // RESB: the whole filter slice of the tile's output channels is resident in
@@ -144,8 +145,14 @@ __global__ void __launch_bounds__(kHThreads, 1)
                 for (int ck = 0; ck < g.cpt; ++ck)
                     for (int tap = 0; tap < taps; ++tap) {
                         const int ft = g.flip ? taps - 1 - tap : tap;
-                        tma_load_2d(smem_u32(smem + L::kBOff + (ck * taps + tap) * L::kB), &bmap,
-                                    &b_full[0], ft * g.red_ch + ck * 64, 0);
+                        if (g.b_mn) {
+                            for (int j = 0; j < BN / 64; ++j)
+                                tma_load_3d(smem_u32(smem + L::kBOff + (ck * taps + tap) * L::kB + j * 8192),
+                                            &bmap, &b_full[0], 64 * j, ft, ck * 64);
+                        } else {
+                            tma_load_2d(smem_u32(smem + L::kBOff + (ck * taps + tap) * L::kB), &bmap,
+                                        &b_full[0], ft * g.red_ch + ck * 64, 0);
+                        }
                     }
             }
             for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
@@ -167,8 +174,14 @@ __global__ void __launch_bounds__(kHThreads, 1)
                         const int ft = g.flip ? taps - 1 - tap : tap;
                         mbar_wait(&b_empty[bs], bph ^ 1);
                         mbar_arrive_expect_tx(&b_full[bs], L::kB);
-                        tma_load_2d(smem_u32(smem + L::kBOff + bs * L::kB), &bmap, &b_full[bs],
-                                    ft * g.red_ch + ck * 64, ht.nt * BN);
+                        if (g.b_mn) {
+                            for (int j = 0; j < BN / 64; ++j)
+                                tma_load_3d(smem_u32(smem + L::kBOff + bs * L::kB + j * 8192), &bmap,
+                                            &b_full[bs], ht.nt * BN + 64 * j, ft, ck * 64);
+                        } else {
+                            tma_load_2d(smem_u32(smem + L::kBOff + bs * L::kB), &bmap, &b_full[bs],
+                                        ft * g.red_ch + ck * 64, ht.nt * BN);
+                        }
                         if (++bs == BSTAGES) {
                             bs = 0;
                             bph ^= 1;
@@ -179,7 +192,9 @@ __global__ void __launch_bounds__(kHThreads, 1)
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer: A = shifted halo view per tap --------------
-        constexpr uint32_t idesc = idesc_bf16_f32(kM, BN, false, false);
+        const uint32_t idesc = idesc_bf16_f32(kM, BN, false, g.b_mn != 0);
+        const uint64_t bks = g.b_mn ? 128 : 2;  // B k-step (MN-major: 16 rows)
+        const uint32_t blbo = g.b_mn ? 8192 : 16;
         int hs = 0, bs = 0;
         uint32_t hph = 0, bph = 0;
         int it = 0;
@@ -202,7 +217,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
                     const uint64_t at = umma_desc_sw128(
                         halo_u + ((g.debug & 16) ? 0 : base_row * 128), 16, 1024);
                     const uint64_t bt = umma_desc_sw128(
-                        smem_u32(smem + L::kBOff + ck * taps * L::kB), 16, 1024);
+                        smem_u32(smem + L::kBOff + ck * taps * L::kB), blbo, 1024);
                     int r0 = 0, s0 = 0;
                     int tap = 0;
                     for (; tap + 2 <= taps; tap += 2) {
@@ -212,13 +227,13 @@ __global__ void __launch_bounds__(kHThreads, 1)
                         const uint64_t a1 = at + (uint64_t)(((r0 * g.Wg + s0) * 8) & al);
                         if (++s0 == g.S) { s0 = 0; ++r0; }
                         const uint64_t b0 = bt + (uint64_t)(tap * (L::kB >> 4));
-                        mma8_bf16(d_tmem, a0, b0, a1, b0 + (L::kB >> 4), idesc, (ck | tap) != 0);
+                        mma8_bf16_bs(d_tmem, a0, b0, a1, b0 + (L::kB >> 4), bks, idesc, (ck | tap) != 0);
                     }
                     if (tap < taps) {
                         const uint64_t a0 = at + (uint64_t)((r0 * g.Wg + s0) * 8);
                         const uint64_t b0 = bt + (uint64_t)(tap * (L::kB >> 4));
-                        mma4_bf16(d_tmem, a0, a0 + 2, a0 + 4, a0 + 6, b0, b0 + 2, b0 + 4, b0 + 6, idesc,
-                                  (ck | tap) != 0);
+                        mma4_bf16(d_tmem, a0, a0 + 2, a0 + 4, a0 + 6, b0, b0 + bks, b0 + 2 * bks,
+                                  b0 + 3 * bks, idesc, (ck | tap) != 0);
                     }
                 }
                 for (int tap = 0; tap < ((RESB && !(g.debug & ~24)) ? 0 : taps); ++tap) {
@@ -231,10 +246,10 @@ __global__ void __launch_bounds__(kHThreads, 1)
                     const uint64_t ad0 =
                         umma_desc_sw128(halo_u + ((g.debug & 1) ? (arow & ~7) : arow) * 128, 16, 1024);
                     const uint64_t bd0 = umma_desc_sw128(
-                        smem_u32(smem + L::kBOff + (RESB ? ck * taps + tap : bs) * L::kB), 16, 1024);
+                        smem_u32(smem + L::kBOff + (RESB ? ck * taps + tap : bs) * L::kB), blbo, 1024);
                     if (!(g.debug & 4))
-                        mma4_bf16(d_tmem, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + 2, bd0 + 4,
-                                  bd0 + 6, idesc, (ck | tap) != 0);
+                        mma4_bf16(d_tmem, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + bks, bd0 + 2 * bks,
+                                  bd0 + 3 * bks, idesc, (ck | tap) != 0);
                     if (!RESB) {
                         mma_commit_elect(&b_empty[bs]);
                         if (++bs == BSTAGES) {
@@ -379,7 +394,7 @@ using namespace pk;
 // geometry does not fit: stride/dilation 1, filters > 1x1, channel pitches
 // multiples of 64, padded grid width <= 256, halo <= 448 rows, N <= 256.
 cudaError_t pk_halo_conv(const pk_conv_geom* g, bool dgrad, const void* src, const void* filt,
-                         void* out, const pk_epilogue* epi, cudaStream_t st) {
+                         void* out, const pk_epilogue* epi, cudaStream_t st, bool filt_mn) {
     static const bool enabled = [] {
         const char* v = std::getenv("PK_HALO");
         return !(v && v[0] == '0');
@@ -427,7 +442,14 @@ cudaError_t pk_halo_conv(const pk_conv_geom* g, bool dgrad, const void* src, con
     if (!tc::make_map_nhwc(&amap, src, g->n, Hs, Ws, src_pitch, (a.debug & 2) ? Ws : a.Wg, a.NR, 1))
         return cudaErrorNotSupported;
     const long long kred = (long long)g->r * g->s * src_pitch;
-    if (!tc::make_map_2d(&bmap, filt, n_out, kred, kred, bn)) return cudaErrorNotSupported;
+    if (filt_mn) {
+        if (!dgrad || g->f_pitch % 64 || bn % 64) return cudaErrorNotSupported;
+        a.b_mn = 1;
+        if (!tc::make_map_filter_mn(&bmap, filt, g->k, g->r * g->s, g->f_pitch))
+            return cudaErrorNotSupported;
+    } else if (!tc::make_map_2d(&bmap, filt, n_out, kred, kred, bn)) {
+        return cudaErrorNotSupported;
+    }
     pk_epilogue e{};
     e.act = -1;
     if (epi) e = *epi;

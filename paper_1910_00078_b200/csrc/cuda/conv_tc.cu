@@ -786,7 +786,27 @@ cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const 
     static const bool no_mn = std::getenv("PK_DGRAD_TRANSPOSE") != nullptr;  // A/B experiments
     // 1x1: the filter W[K][C] is the MN-major B operand as is (no transpose launch);
     // others: B operand Wt[c][r][s][k] = W[k][r][s][c]
-    const bool b_mn = plain1x1 && !no_mn && g->f_pitch % 64 == 0 && g->k == kp;
+    const bool mn_ok = !no_mn && g->f_pitch % 64 == 0 && g->k == kp;
+    const bool b_mn = plain1x1 && mn_ok;
+    if (!plain1x1 && mn_ok) {
+        // spatial / strided: halo or rectangle kernels reading W directly
+        pk_epilogue se{};
+        se.act = -1;
+        if (stats_epi) {
+            se.stats = stats_epi->stats;
+            se.bnb_y = stats_epi->bnb_y;
+            se.bnb_gamma = stats_epi->bnb_gamma;
+            se.bnb_beta = stats_epi->bnb_beta;
+            se.bnb_mean = stats_epi->bnb_mean;
+            se.bnb_invstd = stats_epi->bnb_invstd;
+            se.bnb_relu = stats_epi->bnb_relu;
+        }
+        const cudaError_t he = pk_halo_conv(g, true, dy, f, dx, stats_epi ? &se : nullptr, st, true);
+        if (he != cudaErrorNotSupported) return he;
+        const cudaError_t te = pk_tma_conv(g, true, dy, f, dx, stats_epi ? &se : nullptr,
+                                           cfg ? cfg->block_n : 256, st, true);
+        if (te != cudaErrorNotSupported) return te;
+    }
     cudaError_t err = b_mn ? cudaSuccess : pk_cuda_filter_to_dgrad(g, PK_BF16, f, workspace, st);
     if (err != cudaSuccess) return err;
     ConvTcArgs t{};

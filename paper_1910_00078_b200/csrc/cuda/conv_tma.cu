@@ -54,6 +54,7 @@ struct TmaConvArgs {
     int num_phases;
     int mt;                   // 128-pixel M tiles per rectangle (1 or 2)
     int m_tiles, total_pairs; // PAIR: rectangle tiles (M) and pair tiles ceil(m/2) x n
+    int b_mn;                 // dgrad: B = the filter itself, MN-major 64 x 64 atoms
     int phase_tma;            // PHASED: 1 = per-phase TMA store maps (num_phases <= kStoreMaps)
     int ph_tw[kMaxPhases], ph_th[kMaxPhases], ph_tn[kMaxPhases];
     int ph_tile_start[kMaxPhases + 1];
@@ -208,9 +209,16 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                         if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (L::kA + L::kB));
                         tma_load_4d_pair(smem_u32(sa), &amap, fb, chunk * BK, xs + g.off_w[ti],
                                          ys + g.off_h[ti], ri.n0);
-                        tma_load_2d_pair(smem_u32(sa + L::kA), &bmap, fb,
-                                         ((rs >> 8) * g.S + (rs & 0xff)) * g.red_ch + chunk * BK,
-                                         ri.nt * BN + (int)rank * (BN / 2));
+                        if (g.b_mn) {
+                            for (int j = 0; j < BN / 128; ++j)
+                                tma_load_3d_pair(smem_u32(sa + L::kA + j * 8192), &bmap, fb,
+                                                 ri.nt * BN + (int)rank * (BN / 2) + 64 * j,
+                                                 (rs >> 8) * g.S + (rs & 0xff), chunk * BK);
+                        } else {
+                            tma_load_2d_pair(smem_u32(sa + L::kA), &bmap, fb,
+                                             ((rs >> 8) * g.S + (rs & 0xff)) * g.red_ch + chunk * BK,
+                                             ri.nt * BN + (int)rank * (BN / 2));
+                        }
                         if (++stage == STAGES) {
                             stage = 0;
                             phase ^= 1;
@@ -244,9 +252,16 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                         const unsigned short rs = g.taps[ti];
                         tma_load_4d(smem_u32(sa), &amap, &full[stage], chunk * BK,
                                     xs + g.off_w[ti], ys + g.off_h[ti], ri.n0);
-                        tma_load_2d(smem_u32(sa + L::kA), &bmap, &full[stage],
-                                    ((rs >> 8) * g.S + (rs & 0xff)) * g.red_ch + chunk * BK,
-                                    ri.nt * BN);
+                        if (g.b_mn) {
+                            for (int j = 0; j < BN / 64; ++j)
+                                tma_load_3d(smem_u32(sa + L::kA + j * 8192), &bmap, &full[stage],
+                                            ri.nt * BN + 64 * j, (rs >> 8) * g.S + (rs & 0xff),
+                                            chunk * BK);
+                        } else {
+                            tma_load_2d(smem_u32(sa + L::kA), &bmap, &full[stage],
+                                        ((rs >> 8) * g.S + (rs & 0xff)) * g.red_ch + chunk * BK,
+                                        ri.nt * BN);
+                        }
                     }
                     if (++stage == STAGES) {
                         stage = 0;
@@ -258,7 +273,8 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------------------------------
       if (!PAIR || rank == 0) {
-        constexpr uint32_t idesc = idesc_bf16_f32(PAIR ? 2 * BM : BM, BN, false, false);
+        const uint32_t idesc = idesc_bf16_f32(PAIR ? 2 * BM : BM, BN, false, g.b_mn != 0);
+        const uint64_t bks = g.b_mn ? 128 : 2;  // B k-step: MN-major 16 rows, K-major 32 B
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
@@ -280,11 +296,11 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                     // start fields advance by byte offset >> 4
                     const uint32_t a_base = smem_u32(smem + stage * L::kStage);
                     const uint32_t b_base = a_base + L::kA;
-                    const uint64_t bd0 = umma_desc_sw128(b_base, 16, 1024);
+                    const uint64_t bd0 = umma_desc_sw128(b_base, g.b_mn ? 8192 : 16, 1024);
                     if constexpr (PAIR) {
                         const uint64_t ad0 = umma_desc_sw128(a_base, 16, 1024);
-                        mma4_bf16_pair(d_tmem, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + 2, bd0 + 4,
-                                       bd0 + 6, idesc, kb != 0);
+                        mma4_bf16_pair(d_tmem, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + bks,
+                                       bd0 + 2 * bks, bd0 + 3 * bks, idesc, kb != 0);
                         mma_commit_pair(&empty[stage]);
                         if (kb == nkb - 1) mma_commit_pair(&tmem_full[a]);
                         if (++stage == STAGES) {
@@ -301,7 +317,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                                                     : umma_desc_sw128(a_base + mt * BM * 128, 16, 1024);
                         constexpr uint64_t as = NARROW ? (2 * (L::kA / 8)) >> 4 : 2;
                         mma4_bf16(d_tmem + mt * BN, ad0, ad0 + as, ad0 + 2 * as, ad0 + 3 * as, bd0,
-                                  bd0 + 2, bd0 + 4, bd0 + 6, idesc, kb != 0);
+                                  bd0 + bks, bd0 + 2 * bks, bd0 + 3 * bks, idesc, kb != 0);
                     }
                     mma_commit_elect(&empty[stage]);
                     if (kb == nkb - 1) mma_commit_elect(&tmem_full[a]);
@@ -887,7 +903,8 @@ using namespace pk;
 // Forward / backward-data through the TMA rectangle path. Returns
 // cudaErrorNotSupported (without launching) when the geometry does not fit.
 cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, const void* filt,
-                        void* out, const pk_epilogue* epi, int bn_want, cudaStream_t st) {
+                        void* out, const pk_epilogue* epi, int bn_want, cudaStream_t st,
+                        bool filt_mn) {
     if (g->groups != 1 || g->transpose || g->r > 255 || g->s > 255) return cudaErrorNotSupported;
     const int src_pitch = dgrad ? g->y_pitch : g->x_pitch;
     const int out_pitch = dgrad ? g->x_pitch : g->y_pitch;
@@ -948,8 +965,16 @@ cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, cons
     if (!pair_off && !narrow && sh == 1 && sw == 1 && bn == 256 && t.mt == 1 && g->r * g->s > 1 &&
         (!epi || !epi->stats) && (long long)((t.m_tiles + 1) / 2) * t.n_tiles_n >= 74)
         t.total_pairs = (t.m_tiles + 1) / 2 * t.n_tiles_n;
-    if (!tc::make_map_2d(&bmap, filt, t.n_out, kred, kred, t.total_pairs ? bn / 2 : bn))
+    if (filt_mn) {
+        // narrow sources use the dense tap order (not supported here); the filter
+        // rows (output channels of the forward conv) must cover whole 64-k chunks
+        if (!dgrad || narrow || g->f_pitch % 64 || (bn == 64 && t.total_pairs)) return cudaErrorNotSupported;
+        t.b_mn = 1;
+        if (!tc::make_map_filter_mn(&bmap, filt, g->k, g->r * g->s, g->f_pitch))
+            return cudaErrorInvalidValue;
+    } else if (!tc::make_map_2d(&bmap, filt, t.n_out, kred, kred, t.total_pairs ? bn / 2 : bn)) {
         return cudaErrorInvalidValue;
+    }
     const bool phased = sh > 1 || sw > 1;
     if (!phased &&
         !tc::make_map_nhwc(&ymap.m[0], out, g->n, t.Ho, t.Wo, out_pitch, t.qbw, t.qbh, t.qbn))

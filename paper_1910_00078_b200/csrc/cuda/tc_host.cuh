@@ -88,6 +88,21 @@ inline bool make_map_nhwc_strided(CUtensorMap* map, const void* base, int n, int
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The filter W[K][taps][pitch] as an MN-major B operand for backward data:
+// 3-D view (channel, tap, output channel), box {64 channels, 1 tap, 64 k} = one
+// 8 KB SW128 atom (64 k rows of 64 channels).
+inline bool make_map_filter_mn(CUtensorMap* map, const void* w, int k, int taps, int pitch) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)pitch, (cuuint64_t)taps, (cuuint64_t)k};
+    cuuint64_t strides[2] = {(cuuint64_t)pitch * 2, (cuuint64_t)taps * pitch * 2};
+    cuuint32_t box[3] = {64, 1, 64};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // 3-D bf16 view of an NHWC tensor as rows of pixels: dims {w*pitch, h, n},
 // box {box_elems, box_rows, 1}, no swizzle (plain rows of box_elems*2 bytes).
 // Used for narrow-channel halos, where a per-pixel (16-byte) inner box

@@ -9,8 +9,11 @@
 
 // TMA rectangle-tile path (conv_tma.cu). cudaErrorNotSupported = geometry
 // not eligible (nothing launched); callers then use the cp.async gather path.
+// filt_mn (backward data): filt is the ORIGINAL filter W[K][R][S][pitch], read as an
+// MN-major B operand (no transposed copy); otherwise the transposed [C][R][S][pitch K].
 cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, const void* filt,
-                        void* out, const pk_epilogue* epi, int bn_want, cudaStream_t st);
+                        void* out, const pk_epilogue* epi, int bn_want, cudaStream_t st,
+                        bool filt_mn = false);
 bool pk_tma_wgrad_supported(const pk_conv_geom* g);
 size_t pk_tma_wgrad_workspace(const pk_conv_geom* g, int num_sms);
 cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, void* dw,
@@ -19,7 +22,7 @@ cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, v
 // Halo-reuse path for stride-1 spatial filters (conv_halo.cu): forward, or
 // backward data (filt = transposed filter [C][R][S][pitch K]) when dgrad.
 cudaError_t pk_halo_conv(const pk_conv_geom* g, bool dgrad, const void* src, const void* filt,
-                         void* out, const pk_epilogue* epi, cudaStream_t st);
+                         void* out, const pk_epilogue* epi, cudaStream_t st, bool filt_mn = false);
 
 // CTA-pair (cta_group::2) plain GEMM for 1x1 layers whose filter slice cannot
 // stay resident (conv_tc2.cu): y[M][out_pitch] = a[M][kdim] . b[n_out][kdim]^T.

@@ -255,6 +255,14 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                                 int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+        : "memory");
+}
 // Arrive on the leader CTA's copy of a barrier (this CTA's address mapped to rank 0).
 __device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
     uint32_t remote;
@@ -293,6 +301,31 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
         "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
         "[%0], %1;\n\t}" ::"r"(smem_u32(bar)),
         "h"((uint16_t)3)
+        : "memory");
+}
+
+// mma8_bf16 with an explicit B k-step (K-major: 2, MN-major: 128 in 16-byte units).
+__device__ __forceinline__ void mma8_bf16_bs(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint64_t a1,
+                                             uint64_t b1, uint64_t bs, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 x1, x2, x3, y1, y2, y3, u1, u2, u3, v1, v2, v3, s2, s3;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "add.s64 s2, %7, %7;\n\tadd.s64 s3, s2, %7;\n\t"
+        "add.s64 x1, %1, 2;\n\tadd.s64 x2, %1, 4;\n\tadd.s64 x3, %1, 6;\n\t"
+        "add.s64 y1, %2, %7;\n\tadd.s64 y2, %2, s2;\n\tadd.s64 y3, %2, s3;\n\t"
+        "add.s64 u1, %3, 2;\n\tadd.s64 u2, %3, 4;\n\tadd.s64 u3, %3, 6;\n\t"
+        "add.s64 v1, %4, %7;\n\tadd.s64 v2, %4, s2;\n\tadd.s64 v3, %4, s3;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], x1, y1, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], x2, y2, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], x3, y3, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %4, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], u1, v1, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], u2, v2, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], u3, v3, %5, 1;\n\t}" ::"r"(tmem_d),
+        "l"(a0), "l"(b0), "l"(a1), "l"(b1), "r"(idesc), "r"(accumulate), "l"(bs)
         : "memory");
 }
 
