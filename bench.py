@@ -365,9 +365,10 @@ def ncu_family_traffic(family: str):
     """DRAM bytes (read + write) per step of one direction's kernels, from the
     committed ncu launch list of one step (profiles/*launches_step.csv,
     `--metrics ...,dram__bytes_read.sum,dram__bytes_write.sum`, launch order).
-    step() runs every forward conv first, then per layer (reversed) dgrad =
-    [filter_to_dgrad, conv kernel] or stem_dgrad, and wgrad = the *wgrad*
-    kernels; launches are classified by that order. None if absent."""
+    step() runs the 53 forward convolutions first (one launch each), then per
+    layer (reversed) the backward-data and backward-weights kernels; launches
+    are classified by that order and by name (*wgrad* = backward weights, incl.
+    the split-K sums). None if absent."""
     import csv
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*launches_step.csv")))
@@ -375,24 +376,17 @@ def ncu_family_traffic(family: str):
         return None, None
     with open(files[-1]) as f:
         rows = list(csv.DictReader(f))
+    from paper_1910_00078_b200.resnet50 import resnet50_layers
+    n_fwd = len(resnet50_layers())
     tot = {"igemm_tc_fprop": 0.0, "igemm_tc_dgrad": 0.0, "igemm_tc_wgrad": 0.0}
-    backward, after_transpose = False, False
-    for row in rows:
-        name = row["kernel"]
+    for i, row in enumerate(rows):
         b = float(row["dram__bytes_read.sum"]) + float(row["dram__bytes_write.sum"])
-        if "filter_to_dgrad" in name or "stem_dgrad" in name:
-            backward = True
-        if not backward:
+        if i < n_fwd:
             tot["igemm_tc_fprop"] += b
-        elif "wgrad" in name:
+        elif "wgrad" in row["kernel"]:
             tot["igemm_tc_wgrad"] += b
-        elif "filter_to_dgrad" in name:
+        else:
             tot["igemm_tc_dgrad"] += b
-            after_transpose = True
-            continue
-        else:  # the dgrad conv launched right after its filter transpose (or stem_dgrad)
-            tot["igemm_tc_dgrad"] += b
-        after_transpose = False
     return tot[family], os.path.basename(files[-1])
 
 
