@@ -361,6 +361,33 @@ def roofline(torch, lib, handle, net, peaks):
     return res
 
 
+def hbm_kernel_roofline(torch, lib, handle, net, peaks):
+    """The kernel with the largest share of the step's launch list is the
+    resident-filter plain GEMM (conv_tc PLAIN_RES) of the HBM-bound 1x1 layers.
+    Time each of its forward launches in the step (1x1 stride-1 layers whose
+    filter slice stays resident: reduction <= 256) with CUDA events, and compare
+    the algorithmic bytes (x + w + y, bf16, read or written once) per launch
+    with the measured HBM copy bandwidth."""
+    pitch = lambda c: (c + 7) // 8 * 8  # noqa: E731
+    ms_tot, bytes_tot, n = 0.0, 0.0, 0
+    for (L, x, w, y, dy, dx, dw, probs) in net.items:
+        if not (L.r == 1 and L.stride == 1 and pitch(L.c) <= 256 and L.k >= 64):
+            continue
+        p, s = probs[0]
+        run_conv(lib, handle, p, s, x, w, y, net.ws)
+        ms_tot += time_region(torch, lambda: run_conv(lib, handle, p, s, x, w, y, net.ws), 5) / 5
+        bytes_tot += 2.0 * (net.n * L.h * L.h * pitch(L.c) + L.k * pitch(L.c) +
+                            net.n * L.out_h * L.out_h * pitch(L.k))
+        n += 1
+    if n == 0:
+        return None
+    achieved = bytes_tot / (ms_tot * 1e-3) / 1e9
+    return {"bound": "hbm", "kernel": "conv_tc_kernel PLAIN_RES (resident-filter 1x1 GEMM), "
+            "%d ResNet-50 forward launches, N=%d" % (n, net.n), "achieved": achieved,
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+            "algorithmic_bytes_per_launch": bytes_tot / n, "ms_per_launch": ms_tot / n}
+
+
 def ncu_family_traffic(family: str):
     """DRAM bytes (read + write) per step of one direction's kernels, from the
     committed ncu launch list of one step (profiles/*launches_step.csv,
@@ -569,6 +596,7 @@ def main():
                           args.batch * L.out_h * L.out_h * pitch(L.k))
             roof_ms += max(L.flops(args.batch) / (peak * 1e12),
                            byts / (peaks["hbm_gbs"] * 1e9)) * 1e3
+        extras["roofline"]["hbm_kernel"] = hbm_kernel_roofline(torch, lib, handle, net, peaks)
         extras["roofline"]["layer_roofline_ms"] = roof_ms
         extras["roofline"]["frac_of_layer_roofline"] = roof_ms / dom["ms"]
         extras["roofline"]["step_frac_of_layer_roofline"] = 3 * roof_ms / ms_step
