@@ -93,6 +93,16 @@ cudaError_t pk_cuda_direct_fwd(const pk_conv_geom* g, int dtype, const void* x, 
                                void* y, const pk_epilogue* epi, cudaStream_t st);
 cudaError_t pk_cuda_direct_bwd_data(const pk_conv_geom* g, int dtype, const void* dy,
                                     const void* f, void* dx, cudaStream_t st);
+// Depthwise (groups == C == K), depthwise.cu: channel-vector lanes, filter taps
+// in shared memory; wgrad = per-chunk partials + a fixed-order chunk sum.
+int pk_depthwise_supported(const pk_conv_geom* g);
+cudaError_t pk_cuda_depthwise_fwd(const pk_conv_geom* g, int dtype, const void* x, const void* f, void* y,
+                                  const pk_epilogue* epi, int num_sms, cudaStream_t st);
+cudaError_t pk_cuda_depthwise_bwd_data(const pk_conv_geom* g, int dtype, const void* dy, const void* f,
+                                       void* dx, int num_sms, cudaStream_t st);
+size_t pk_depthwise_wgrad_workspace(const pk_conv_geom* g, int num_sms);
+cudaError_t pk_cuda_depthwise_wgrad(const pk_conv_geom* g, int dtype, const void* dy, const void* x, void* dw,
+                                    void* ws, size_t ws_bytes, int num_sms, cudaStream_t st);
 cudaError_t pk_cuda_direct_bwd_weights(const pk_conv_geom* g, int dtype, const void* dy,
                                        const void* x, void* dw, cudaStream_t st);
 

@@ -317,6 +317,11 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
     if (dir == ConvDirection::Forward) {
         switch (algo_) {
             case ConvAlgo::Direct:
+                if (pk_depthwise_supported(&g)) {
+                    kernel = "depthwise_simt";
+                    ck(pk_cuda_depthwise_fwd(&g, dt, a, b, out, epi, h.num_sms(), st), "depthwise_fwd");
+                    break;
+                }
                 kernel = "direct_simt";
                 ck(pk_cuda_direct_fwd(&g, dt, a, b, out, epi, st), "direct_fwd");
                 break;
@@ -348,6 +353,9 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                     kernel = "igemm_tc_fwd";
                     const pk_tc_config cfg = tc_config(tiles_);
                     ck(pk_cuda_igemm_tc_fwd(&g, a, b, out, epi, &cfg, st), "igemm_tc_fwd");
+                } else if (pk_depthwise_supported(&g)) {
+                    kernel = "depthwise_simt";
+                    ck(pk_cuda_depthwise_fwd(&g, dt, a, b, out, epi, h.num_sms(), st), "depthwise_fwd");
                 } else {
                     if (g.groups == 1 && !g.transpose && g.x_pitch % 8 == 0 && g.f_pitch == g.x_pitch) {
                         // register-tiled implicit GEMM on CUDA cores (64 px x 64 k per CTA,
@@ -415,7 +423,10 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
             }
         }
     } else if (dir == ConvDirection::BackwardData) {
-        if (algo_ == ConvAlgo::Direct) {
+        if ((algo_ == ConvAlgo::Direct || algo_ == ConvAlgo::ImplicitGemm) && pk_depthwise_supported(&g)) {
+            kernel = "depthwise_simt_bwd_data";
+            ck(pk_cuda_depthwise_bwd_data(&g, dt, a, b, out, h.num_sms(), st), "depthwise_bwd_data");
+        } else if (algo_ == ConvAlgo::Direct) {
             kernel = "direct_simt_bwd_data";
             ck(pk_cuda_direct_bwd_data(&g, dt, a, b, out, st), "direct_bwd_data");
         } else if (stem_eligible(g, dt, nullptr)) {
@@ -442,7 +453,12 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                 }
         }
     } else {
-        if (algo_ == ConvAlgo::Direct) {
+        if ((algo_ == ConvAlgo::Direct || algo_ == ConvAlgo::ImplicitGemm) && pk_depthwise_supported(&g)) {
+            kernel = "depthwise_simt_bwd_weights";
+            const std::size_t wb = pk_depthwise_wgrad_workspace(&g, h.num_sms());
+            ck(pk_cuda_depthwise_wgrad(&g, dt, a, b, out, h.scratch(13, wb), wb, h.num_sms(), st),
+               "depthwise_wgrad");
+        } else if (algo_ == ConvAlgo::Direct) {
             kernel = "direct_simt_bwd_weights";
             ck(pk_cuda_direct_bwd_weights(&g, dt, a, b, out, st), "direct_bwd_weights");
         } else if (stem_eligible(g, dt, nullptr)) {
