@@ -334,6 +334,77 @@ int dw_chunks(const pk_conv_geom* g, int num_sms) {
     return (int)std::max(1LL, std::min(want, rows));  // chunks hold whole output rows
 }
 
+// Grouped backward weights (1 < C/g <= 32, C/g % 8 == 0, 64-channel K blocks
+// aligned to groups): dW[k][r][s][c] = sum_pix dY[pix][k] * x[pix(r,s)][grp*cg + c].
+// A thread owns one output channel k and 8 input channels of its group and
+// accumulates up to kTapGroup taps over its slice of output rows; lanes of a
+// warp are consecutive k (coalesced dY, broadcast x vectors within a group).
+// Each thread's partial goes to partial[slot][k][tap][c] (slot = chunk x pixel
+// lane); the fixed-order slot sum makes the result deterministic.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) grouped_wgrad_kernel(pk_conv_geom g, const T* __restrict__ dy,
+                                                                 const T* __restrict__ x,
+                                                                 float* __restrict__ partial) {
+    const int cvs = g.cg / 8, lanes_px = kThreads / (64 * cvs);
+    const int kk = threadIdx.x % 64, rest = threadIdx.x / 64, cvi = rest % cvs, pl = rest / cvs;
+    const int k = blockIdx.y * 64 + kk, grp = k / g.kg, taps = g.r * g.s;
+    const int rows = g.n * g.p;
+    const int per = (rows + gridDim.x - 1) / gridDim.x;
+    const int r0 = blockIdx.x * per, r1 = r0 + per < rows ? r0 + per : rows;
+    const int slot = blockIdx.x * lanes_px + pl;
+    for (int t0 = 0; t0 < taps; t0 += kTapGroup) {
+        float acc[kTapGroup][8];
+#pragma unroll
+        for (int t = 0; t < kTapGroup; ++t)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[t][j] = 0.0f;
+        for (int row = r0; row < r1; ++row) {
+            const int oh = row % g.p, n = row / g.p;
+            const T* xn = x + (size_t)n * g.h * g.w * g.x_pitch + grp * g.cg + cvi * 8;
+            for (int ow = pl; ow < g.q; ow += lanes_px) {
+                const float d = ld(dy + ((size_t)row * g.q + ow) * g.y_pitch + k);
+#pragma unroll
+                for (int t = 0; t < kTapGroup; ++t) {
+                    const int tap = t0 + t;
+                    if (tap >= taps) break;
+                    const int r = tap / g.s, s = tap - r * g.s;
+                    const int ih = oh * g.str_h - g.pad_h + r * g.dil_h, iw = ow * g.str_w - g.pad_w + s * g.dil_w;
+                    if (ih < 0 || ih >= g.h || iw < 0 || iw >= g.w) continue;
+                    float v[8];
+                    load8v(xn + (ih * g.w + iw) * g.x_pitch, v);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[t][j] += d * v[j];
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < kTapGroup; ++t) {
+            if (t0 + t >= taps) break;
+            float* out = partial + (((size_t)slot * g.k + k) * taps + t0 + t) * g.cg + cvi * 8;
+            reinterpret_cast<float4*>(out)[0] = make_float4(acc[t][0], acc[t][1], acc[t][2], acc[t][3]);
+            reinterpret_cast<float4*>(out)[1] = make_float4(acc[t][4], acc[t][5], acc[t][6], acc[t][7]);
+        }
+    }
+}
+
+template <typename T>
+__global__ void grouped_wgrad_sum_kernel(pk_conv_geom g, const float* __restrict__ partial, int slots,
+                                         T* __restrict__ dw) {
+    const long long total = (long long)g.k * g.r * g.s * g.cg;  // f_pitch == cg here
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        float sum = 0.0f;
+        for (int sl = 0; sl < slots; ++sl) sum += partial[(size_t)sl * total + i];
+        st(dw + i, sum);
+    }
+}
+
+int gw_chunks(const pk_conv_geom* g, int num_sms) {
+    const int kblocks = g->k / 64;
+    const long long want = (2LL * num_sms + kblocks - 1) / kblocks;
+    return (int)std::max(1LL, std::min(want, (long long)g->n * g->p));
+}
+
 }  // namespace
 }  // namespace pk
 
@@ -432,6 +503,38 @@ cudaError_t pk_cuda_depthwise_wgrad(const pk_conv_geom* g, int dtype, const void
                                                                                        (const T*)x, (float*)ws);
         depthwise_wgrad_sum_kernel<T><<<(unsigned)std::max(1LL, std::min((long long)ceil_div(total, 256), 4LL * num_sms)),
                                         256, 0, st>>>(*g, (const float*)ws, chunks, (T*)dw);
+    });
+    count_launch(2);
+    return cudaGetLastError();
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int pk_grouped_wgrad_supported(const pk_conv_geom* g) {
+    return g->groups > 1 && !g->transpose && (g->cg == 8 || g->cg == 16 || g->cg == 32) && g->k % 64 == 0 &&
+           (64 % g->kg == 0 || g->kg % 64 == 0) && g->f_pitch == g->cg && g->x_pitch == g->c &&
+           (long long)g->h * g->w * g->x_pitch < (1LL << 31) && (long long)g->n * g->p < (1LL << 31);
+}
+
+size_t pk_grouped_wgrad_workspace(const pk_conv_geom* g, int num_sms) {
+    const int lanes_px = kThreads / (64 * (g->cg / 8));
+    return (size_t)gw_chunks(g, num_sms) * lanes_px * g->k * g->r * g->s * g->cg * sizeof(float);
+}
+
+cudaError_t pk_cuda_grouped_wgrad(const pk_conv_geom* g, int dtype, const void* dy, const void* x, void* dw,
+                                  void* ws, size_t ws_bytes, int num_sms, cudaStream_t st) {
+    if (!pk_grouped_wgrad_supported(g) || ws_bytes < pk_grouped_wgrad_workspace(g, num_sms))
+        return cudaErrorInvalidValue;
+    const int chunks = gw_chunks(g, num_sms), lanes_px = kThreads / (64 * (g->cg / 8));
+    const long long total = (long long)g->k * g->r * g->s * g->cg;
+    PK_DISPATCH_DTYPE(dtype, T, {
+        grouped_wgrad_kernel<T><<<dim3(chunks, g->k / 64), kThreads, 0, st>>>(*g, (const T*)dy, (const T*)x,
+                                                                              (float*)ws);
+        grouped_wgrad_sum_kernel<T><<<(unsigned)std::max(1LL, std::min((long long)ceil_div(total, 256),
+                                                                       4LL * num_sms)),
+                                      256, 0, st>>>(*g, (const float*)ws, chunks * lanes_px, (T*)dw);
     });
     count_launch(2);
     return cudaGetLastError();

@@ -103,6 +103,11 @@ cudaError_t pk_cuda_depthwise_bwd_data(const pk_conv_geom* g, int dtype, const v
 size_t pk_depthwise_wgrad_workspace(const pk_conv_geom* g, int num_sms);
 cudaError_t pk_cuda_depthwise_wgrad(const pk_conv_geom* g, int dtype, const void* dy, const void* x, void* dw,
                                     void* ws, size_t ws_bytes, int num_sms, cudaStream_t st);
+// Grouped backward weights for C/g in {8, 16, 32} (depthwise.cu).
+int pk_grouped_wgrad_supported(const pk_conv_geom* g);
+size_t pk_grouped_wgrad_workspace(const pk_conv_geom* g, int num_sms);
+cudaError_t pk_cuda_grouped_wgrad(const pk_conv_geom* g, int dtype, const void* dy, const void* x, void* dw,
+                                  void* ws, size_t ws_bytes, int num_sms, cudaStream_t st);
 cudaError_t pk_cuda_direct_bwd_weights(const pk_conv_geom* g, int dtype, const void* dy,
                                        const void* x, void* dw, cudaStream_t st);
 

@@ -72,3 +72,33 @@ def test_depthwise_parity(lib, si, et, direction):
         assert np.array_equal(got, again), "depthwise result is not deterministic"
         ran += 1
     assert ran >= 1
+
+
+GROUPED = [
+    dict(n=2, c=32, h=9, w=9, k=64, y=3, x=3, pad=1, groups=4),                  # cg 8, kg 16
+    dict(n=1, c=32, h=11, w=10, k=128, y=5, x=5, pad=2, stride=2, groups=2),     # cg 16, kg 64, 25 taps
+    dict(n=2, c=256, h=8, w=8, k=64, y=3, x=3, pad=2, dilation=2, groups=8),     # cg 32, kg 8
+    dict(n=4, c=256, h=14, w=14, k=256, y=3, x=3, pad=1, groups=32),             # ResNeXt-like
+    dict(n=1, c=64, h=6, w=7, k=64, y=1, x=1, groups=8),                         # 1x1
+]
+
+
+@pytest.mark.parametrize("si", range(len(GROUPED)))
+@pytest.mark.parametrize("et", [abi.F32, abi.BF16])
+def test_grouped_wgrad_parity(lib, si, et):
+    rng = np.random.default_rng(800 + si)
+    p = problem(**GROUPED[si], direction=abi.BACKWARD_WEIGHTS, etype=et)
+    h = lib.handle()
+    a, b, want = _run(lib, p, rng, et == abi.BF16)
+    ran = 0
+    for s in ("Direct", "ImplicitGemm"):
+        if not h.is_applicable(s, p):
+            continue
+        got = h.conv_run(p, s, a, b)
+        assert h.last_kernel() == "grouped_simt_bwd_weights", h.last_kernel()
+        tol = 1e-2 if et == abi.BF16 else 1e-4
+        err = rel_l2(got, want)
+        assert err <= tol, f"{s} rel-L2 {err:.3e}"
+        assert np.array_equal(got, h.conv_run(p, s, a, b)), "not deterministic"
+        ran += 1
+    assert ran >= 1
