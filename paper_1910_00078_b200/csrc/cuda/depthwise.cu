@@ -334,6 +334,98 @@ int dw_chunks(const pk_conv_geom* g, int num_sms) {
     return (int)std::max(1LL, std::min(want, rows));  // chunks hold whole output rows
 }
 
+// Grouped forward / backward data (C/g and K/g multiples of 8). A thread owns
+// 8 consecutive output channels (k forward, c backward data) of one pixel;
+// the 32 lanes of a warp are 32 pixels with the same channel vector, so the
+// filter rows in shared memory ([tap][j][64 channels], j = reduction index
+// within the group) are broadcast reads, and each lane streams its pixel's
+// group channels as 8-channel vectors. Reduction in (r, s, j) order.
+template <typename T, bool BWD>
+__global__ void __launch_bounds__(kThreads) grouped_kernel(pk_conv_geom g, const T* __restrict__ src,
+                                                           const T* __restrict__ f, T* __restrict__ dst,
+                                                           pk_epilogue e) {
+    extern __shared__ float sw[];
+    const int taps = g.r * g.s;
+    const int red = BWD ? g.kg : g.cg;             // reduction channels per group
+    const int och = BWD ? g.cg : g.kg;             // output channels per group
+    const int nout = BWD ? g.c : g.k;
+    const int pitch = BWD ? g.x_pitch : g.y_pitch, src_pitch = BWD ? g.y_pitch : g.x_pitch;
+    const int o0 = blockIdx.y * 64;
+    for (int i = threadIdx.x; i < taps * red * 64; i += blockDim.x) {
+        const int oo = i % 64, j = (i / 64) % red, tap = i / (64 * red);
+        const int o = o0 + oo;
+        float v = 0.0f;
+        if (o < nout) {
+            const int grp = o / och;
+            if (!BWD)
+                v = ld(f + ((size_t)o * taps + tap) * g.f_pitch + j);
+            else
+                v = ld(f + ((size_t)(grp * g.kg + j) * taps + tap) * g.f_pitch + (o - grp * g.cg));
+        }
+        sw[i] = v;
+    }
+    __syncthreads();
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int oc = o0 + warp * 8;  // this warp's 8 output channels
+    if (oc >= nout) return;
+    const int grp = oc / och;
+    const int oh_n = BWD ? g.h : g.p, ow_n = BWD ? g.w : g.q;
+    const int ih_n = BWD ? g.p : g.h, iw_n = BWD ? g.q : g.w;
+    const long long npix = (long long)g.n * oh_n * ow_n;
+    const bool epi = !BWD && epilogue_active(&e);
+    for (long long pix = (long long)blockIdx.x * 32 + lane; pix < npix; pix += (long long)gridDim.x * 32) {
+        const int ow = (int)(pix % ow_n);
+        const long long t = pix / ow_n;
+        const int oh = (int)(t % oh_n), n = (int)(t / oh_n);
+        const T* sn = src + (size_t)n * ih_n * iw_n * src_pitch + grp * red;
+        float acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+        for (int r = 0; r < g.r; ++r) {
+            int ih;
+            if (!BWD) {
+                ih = oh * g.str_h - g.pad_h + r * g.dil_h;
+                if (ih < 0 || ih >= ih_n) continue;
+            } else {
+                const int num = oh + g.pad_h - r * g.dil_h;
+                if (num < 0 || num % g.str_h) continue;
+                ih = num / g.str_h;
+                if (ih >= ih_n) continue;
+            }
+            for (int s = 0; s < g.s; ++s) {
+                int iw;
+                if (!BWD) {
+                    iw = ow * g.str_w - g.pad_w + s * g.dil_w;
+                    if (iw < 0 || iw >= iw_n) continue;
+                } else {
+                    const int num = ow + g.pad_w - s * g.dil_w;
+                    if (num < 0 || num % g.str_w) continue;
+                    iw = num / g.str_w;
+                    if (iw >= iw_n) continue;
+                }
+                const T* xp = sn + (size_t)(ih * iw_n + iw) * src_pitch;
+                const float* wt = sw + (r * g.s + s) * red * 64 + warp * 8;
+                for (int j0 = 0; j0 < red; j0 += 8) {
+                    float v[8];
+                    load8v(xp + j0, v);
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj) {
+                        const float4 w0 = *reinterpret_cast<const float4*>(wt + (j0 + jj) * 64);
+                        const float4 w1 = *reinterpret_cast<const float4*>(wt + (j0 + jj) * 64 + 4);
+                        acc[0] += v[jj] * w0.x; acc[1] += v[jj] * w0.y; acc[2] += v[jj] * w0.z;
+                        acc[3] += v[jj] * w0.w; acc[4] += v[jj] * w1.x; acc[5] += v[jj] * w1.y;
+                        acc[6] += v[jj] * w1.z; acc[7] += v[jj] * w1.w;
+                    }
+                }
+            }
+        }
+        if (epi)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = apply_epilogue(e, acc[q], oc + q, oh, ow, g.p, g.q);
+        store8v(dst + (size_t)pix * pitch + oc, acc);
+    }
+}
+
 // Grouped backward weights (1 < C/g <= 32, C/g % 8 == 0, 64-channel K blocks
 // aligned to groups): dW[k][r][s][c] = sum_pix dY[pix][k] * x[pix(r,s)][grp*cg + c].
 // A thread owns one output channel k and 8 input channels of its group and
@@ -538,6 +630,48 @@ cudaError_t pk_cuda_grouped_wgrad(const pk_conv_geom* g, int dtype, const void* 
     });
     count_launch(2);
     return cudaGetLastError();
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int pk_grouped_supported(const pk_conv_geom* g) {
+    return g->groups > 1 && !g->transpose && g->cg % 8 == 0 && g->kg % 8 == 0 && g->x_pitch == g->c &&
+           g->y_pitch == g->k && g->f_pitch == g->cg &&
+           (long long)g->r * g->s * std::max(g->cg, g->kg) * 64 * 4 <= 160 * 1024 &&
+           (long long)std::max(g->h, g->p) * std::max(g->w, g->q) * std::max(g->x_pitch, g->y_pitch) < (1LL << 31);
+}
+
+static cudaError_t grouped_launch(const pk_conv_geom* g, int dtype, bool bwd, const void* src, const void* f,
+                                  void* dst, const pk_epilogue& e, int num_sms, cudaStream_t st) {
+    const int nout = bwd ? g->c : g->k, red = bwd ? g->kg : g->cg;
+    const long long npix = (long long)g->n * (bwd ? (long long)g->h * g->w : (long long)g->p * g->q);
+    const int oblocks = (nout + 63) / 64;
+    const long long want = (long long)num_sms * 4 / oblocks + 1;
+    dim3 grid((unsigned)std::max(1LL, std::min((long long)ceil_div(npix, 32), want)), oblocks);
+    const size_t smem = (size_t)g->r * g->s * red * 64 * sizeof(float);
+    PK_DISPATCH_DTYPE(dtype, T, {
+        auto kern = bwd ? grouped_kernel<T, true> : grouped_kernel<T, false>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, kThreads, smem, st>>>(*g, (const T*)src, (const T*)f, (T*)dst, e);
+    });
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t pk_cuda_grouped_fwd(const pk_conv_geom* g, int dtype, const void* x, const void* f, void* y,
+                                const pk_epilogue* epi, int num_sms, cudaStream_t st) {
+    pk_epilogue none{};
+    none.act = -1;
+    return grouped_launch(g, dtype, false, x, f, y, epi ? *epi : none, num_sms, st);
+}
+
+cudaError_t pk_cuda_grouped_bwd_data(const pk_conv_geom* g, int dtype, const void* dy, const void* f, void* dx,
+                                     int num_sms, cudaStream_t st) {
+    pk_epilogue none{};
+    none.act = -1;
+    return grouped_launch(g, dtype, true, dy, f, dx, none, num_sms, st);
 }
 
 }  // extern "C"

@@ -103,6 +103,12 @@ cudaError_t pk_cuda_depthwise_bwd_data(const pk_conv_geom* g, int dtype, const v
 size_t pk_depthwise_wgrad_workspace(const pk_conv_geom* g, int num_sms);
 cudaError_t pk_cuda_depthwise_wgrad(const pk_conv_geom* g, int dtype, const void* dy, const void* x, void* dw,
                                     void* ws, size_t ws_bytes, int num_sms, cudaStream_t st);
+// Grouped forward / backward data, C/g and K/g multiples of 8 (depthwise.cu).
+int pk_grouped_supported(const pk_conv_geom* g);
+cudaError_t pk_cuda_grouped_fwd(const pk_conv_geom* g, int dtype, const void* x, const void* f, void* y,
+                                const pk_epilogue* epi, int num_sms, cudaStream_t st);
+cudaError_t pk_cuda_grouped_bwd_data(const pk_conv_geom* g, int dtype, const void* dy, const void* f, void* dx,
+                                     int num_sms, cudaStream_t st);
 // Grouped backward weights for C/g in {8, 16, 32} (depthwise.cu).
 int pk_grouped_wgrad_supported(const pk_conv_geom* g);
 size_t pk_grouped_wgrad_workspace(const pk_conv_geom* g, int num_sms);

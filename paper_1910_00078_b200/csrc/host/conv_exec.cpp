@@ -322,6 +322,11 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                     ck(pk_cuda_depthwise_fwd(&g, dt, a, b, out, epi, h.num_sms(), st), "depthwise_fwd");
                     break;
                 }
+                if (pk_grouped_supported(&g)) {
+                    kernel = "grouped_simt";
+                    ck(pk_cuda_grouped_fwd(&g, dt, a, b, out, epi, h.num_sms(), st), "grouped_fwd");
+                    break;
+                }
                 kernel = "direct_simt";
                 ck(pk_cuda_direct_fwd(&g, dt, a, b, out, epi, st), "direct_fwd");
                 break;
@@ -356,6 +361,9 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                 } else if (pk_depthwise_supported(&g)) {
                     kernel = "depthwise_simt";
                     ck(pk_cuda_depthwise_fwd(&g, dt, a, b, out, epi, h.num_sms(), st), "depthwise_fwd");
+                } else if (pk_grouped_supported(&g)) {
+                    kernel = "grouped_simt";
+                    ck(pk_cuda_grouped_fwd(&g, dt, a, b, out, epi, h.num_sms(), st), "grouped_fwd");
                 } else {
                     if (g.groups == 1 && !g.transpose && g.x_pitch % 8 == 0 && g.f_pitch == g.x_pitch) {
                         // register-tiled implicit GEMM on CUDA cores (64 px x 64 k per CTA,
@@ -426,6 +434,9 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
         if ((algo_ == ConvAlgo::Direct || algo_ == ConvAlgo::ImplicitGemm) && pk_depthwise_supported(&g)) {
             kernel = "depthwise_simt_bwd_data";
             ck(pk_cuda_depthwise_bwd_data(&g, dt, a, b, out, h.num_sms(), st), "depthwise_bwd_data");
+        } else if ((algo_ == ConvAlgo::Direct || algo_ == ConvAlgo::ImplicitGemm) && pk_grouped_supported(&g)) {
+            kernel = "grouped_simt_bwd_data";
+            ck(pk_cuda_grouped_bwd_data(&g, dt, a, b, out, h.num_sms(), st), "grouped_bwd_data");
         } else if (algo_ == ConvAlgo::Direct) {
             kernel = "direct_simt_bwd_data";
             ck(pk_cuda_direct_bwd_data(&g, dt, a, b, out, st), "direct_bwd_data");

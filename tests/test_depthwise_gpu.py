@@ -83,11 +83,16 @@ GROUPED = [
 ]
 
 
+GROUPED_KERNEL = {abi.FORWARD: "grouped_simt", abi.BACKWARD_DATA: "grouped_simt_bwd_data",
+                  abi.BACKWARD_WEIGHTS: "grouped_simt_bwd_weights"}
+
+
 @pytest.mark.parametrize("si", range(len(GROUPED)))
 @pytest.mark.parametrize("et", [abi.F32, abi.BF16])
-def test_grouped_wgrad_parity(lib, si, et):
+@pytest.mark.parametrize("direction", [abi.FORWARD, abi.BACKWARD_DATA, abi.BACKWARD_WEIGHTS])
+def test_grouped_parity(lib, si, et, direction):
     rng = np.random.default_rng(800 + si)
-    p = problem(**GROUPED[si], direction=abi.BACKWARD_WEIGHTS, etype=et)
+    p = problem(**GROUPED[si], direction=direction, etype=et)
     h = lib.handle()
     a, b, want = _run(lib, p, rng, et == abi.BF16)
     ran = 0
@@ -95,10 +100,14 @@ def test_grouped_wgrad_parity(lib, si, et):
         if not h.is_applicable(s, p):
             continue
         got = h.conv_run(p, s, a, b)
-        assert h.last_kernel() == "grouped_simt_bwd_weights", h.last_kernel()
+        sh = GROUPED[si]
+        cg, kg = sh["c"] // sh["groups"], sh["k"] // sh["groups"]
+        staged = sh["y"] * sh["x"] * max(cg, kg) * 64 * 4  # filter slice in smem (fwd / bwd-data)
+        if direction == abi.BACKWARD_WEIGHTS or staged <= 160 * 1024:
+            assert h.last_kernel() == GROUPED_KERNEL[direction], h.last_kernel()
         tol = 1e-2 if et == abi.BF16 else 1e-4
         err = rel_l2(got, want)
-        assert err <= tol, f"{s} rel-L2 {err:.3e}"
+        assert err <= tol, f"{s} {h.last_kernel()} rel-L2 {err:.3e}"
         assert np.array_equal(got, h.conv_run(p, s, a, b)), "not deterministic"
         ran += 1
     assert ran >= 1
