@@ -378,6 +378,18 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                 break;
             }
             case ConvAlgo::Im2colGemm: {
+                // Depthwise / grouped: the per-(image, group) GEMMs degenerate to one
+                // or a few rows, so the channel-vector kernels compute the same sums.
+                if (pk_depthwise_supported(&g)) {
+                    kernel = "depthwise_simt";
+                    ck(pk_cuda_depthwise_fwd(&g, dt, a, b, out, epi, h.num_sms(), st), "depthwise_fwd");
+                    break;
+                }
+                if (pk_grouped_supported(&g)) {
+                    kernel = "grouped_simt";
+                    ck(pk_cuda_grouped_fwd(&g, dt, a, b, out, epi, h.num_sms(), st), "grouped_fwd");
+                    break;
+                }
                 if (g.transpose) {
                     // col[(r,s,kk)][hw] = W_g^T X_g ; then gather into the output
                     kernel = "im2col_gemm_transpose";
@@ -431,10 +443,10 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
             }
         }
     } else if (dir == ConvDirection::BackwardData) {
-        if ((algo_ == ConvAlgo::Direct || algo_ == ConvAlgo::ImplicitGemm) && pk_depthwise_supported(&g)) {
+        if (algo_ != ConvAlgo::Winograd && algo_ != ConvAlgo::FFT && pk_depthwise_supported(&g)) {
             kernel = "depthwise_simt_bwd_data";
             ck(pk_cuda_depthwise_bwd_data(&g, dt, a, b, out, h.num_sms(), st), "depthwise_bwd_data");
-        } else if ((algo_ == ConvAlgo::Direct || algo_ == ConvAlgo::ImplicitGemm) && pk_grouped_supported(&g)) {
+        } else if (algo_ != ConvAlgo::Winograd && algo_ != ConvAlgo::FFT && pk_grouped_supported(&g)) {
             kernel = "grouped_simt_bwd_data";
             ck(pk_cuda_grouped_bwd_data(&g, dt, a, b, out, h.num_sms(), st), "grouped_bwd_data");
         } else if (algo_ == ConvAlgo::Direct) {
@@ -464,13 +476,12 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                 }
         }
     } else {
-        if ((algo_ == ConvAlgo::Direct || algo_ == ConvAlgo::ImplicitGemm) && pk_depthwise_supported(&g)) {
+        if (algo_ != ConvAlgo::Winograd && algo_ != ConvAlgo::FFT && pk_depthwise_supported(&g)) {
             kernel = "depthwise_simt_bwd_weights";
             const std::size_t wb = pk_depthwise_wgrad_workspace(&g, h.num_sms());
             ck(pk_cuda_depthwise_wgrad(&g, dt, a, b, out, h.scratch(13, wb), wb, h.num_sms(), st),
                "depthwise_wgrad");
-        } else if ((algo_ == ConvAlgo::Direct || algo_ == ConvAlgo::ImplicitGemm) &&
-                   pk_grouped_wgrad_supported(&g)) {
+        } else if (algo_ != ConvAlgo::Winograd && algo_ != ConvAlgo::FFT && pk_grouped_wgrad_supported(&g)) {
             kernel = "grouped_simt_bwd_weights";
             const std::size_t wb = pk_grouped_wgrad_workspace(&g, h.num_sms());
             ck(pk_cuda_grouped_wgrad(&g, dt, a, b, out, h.scratch(13, wb), wb, h.num_sms(), st),

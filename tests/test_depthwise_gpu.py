@@ -58,7 +58,7 @@ def test_depthwise_parity(lib, si, et, direction):
     h = lib.handle()
     a, b, want = _run(lib, p, rng, et == abi.BF16)
     ran = 0
-    for s in ("Direct", "ImplicitGemm"):
+    for s in ("Direct", "ImplicitGemm", "Im2colGemm"):
         if not h.is_applicable(s, p):
             continue
         got = h.conv_run(p, s, a, b)
@@ -96,7 +96,7 @@ def test_grouped_parity(lib, si, et, direction):
     h = lib.handle()
     a, b, want = _run(lib, p, rng, et == abi.BF16)
     ran = 0
-    for s in ("Direct", "ImplicitGemm"):
+    for s in ("Direct", "ImplicitGemm", "Im2colGemm"):
         if not h.is_applicable(s, p):
             continue
         got = h.conv_run(p, s, a, b)
