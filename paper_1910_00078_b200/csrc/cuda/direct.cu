@@ -275,6 +275,89 @@ __global__ void __launch_bounds__(256) direct_bwd_weights_kernel(pk_conv_geom g,
     }
 }
 
+// Backward weights, register-tiled (groups == 1, convolution mode): the GEMM
+// dW[k][(tap, c)] = sum_pix dY[pix][k] * x[pix + tap][c]. A CTA owns 64 k x 64
+// channels of one tap over a contiguous pixel range (split z); per 16-pixel
+// step the dY slice [16 px][64 k] and the gathered input slice [16 px][64 c]
+// are staged in smem and each thread accumulates 8 k x 4 c. Splits write fp32
+// partials summed in split order by direct_wgrad_sum_kernel (deterministic).
+template <typename T>
+__global__ void __launch_bounds__(128) direct_wgrad_tiled_kernel(pk_conv_geom g, const T* __restrict__ dy,
+                                                                 const T* __restrict__ x, float* __restrict__ out,
+                                                                 int px_per_split) {
+    constexpr int TK = 64, TC = 64, PP = 16, LD = 68;
+    __shared__ __align__(16) float As[PP][LD];  // [pixel][k]
+    __shared__ __align__(16) float Bs[PP][LD];  // [pixel][c]
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int k0 = blockIdx.x * TK;
+    const int cblocks = (g.f_pitch + TC - 1) / TC;
+    const int tap = blockIdx.y / cblocks, c0 = (blockIdx.y % cblocks) * TC;
+    const int r = tap / g.s, s = tap % g.s;
+    const int npix = g.n * g.p * g.q;
+    const int p0 = blockIdx.z * px_per_split, p1 = min(npix, p0 + px_per_split);
+    const int lpx = tid >> 3, lv = (tid & 7) * 8;  // loader: pixel, 8-channel vector
+    float acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    for (int pb = p0; pb < p1; pb += PP) {
+        const int pix = pb + lpx;
+        float av[8], bv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) av[i] = bv[i] = 0.0f;
+        if (pix < p1) {
+            const int ow = pix % g.q, t = pix / g.q, oh = t % g.p, n = t / g.p;
+            if (k0 + lv < g.y_pitch) load8(dy + (size_t)pix * g.y_pitch + k0 + lv, av);
+            const int ih = oh * g.str_h - g.pad_h + r * g.dil_h, iw = ow * g.str_w - g.pad_w + s * g.dil_w;
+            if (ih >= 0 && ih < g.h && iw >= 0 && iw < g.w && c0 + lv < g.x_pitch)
+                load8(x + (((size_t)n * g.h + ih) * g.w + iw) * g.x_pitch + c0 + lv, bv);
+        }
+        __syncthreads();  // the previous step is consumed
+        *reinterpret_cast<float4*>(&As[lpx][lv]) = make_float4(av[0], av[1], av[2], av[3]);
+        *reinterpret_cast<float4*>(&As[lpx][lv + 4]) = make_float4(av[4], av[5], av[6], av[7]);
+        *reinterpret_cast<float4*>(&Bs[lpx][lv]) = make_float4(bv[0], bv[1], bv[2], bv[3]);
+        *reinterpret_cast<float4*>(&Bs[lpx][lv + 4]) = make_float4(bv[4], bv[5], bv[6], bv[7]);
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < PP; ++q) {
+            const float4 a0 = *reinterpret_cast<const float4*>(&As[q][ty * 8]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&As[q][ty * 8 + 4]);
+            const float4 b = *reinterpret_cast<const float4*>(&Bs[q][tx * 4]);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float bb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
+        }
+    }
+    const int taps = g.r * g.s;
+    const size_t total = (size_t)g.k * taps * g.f_pitch;
+    float* o = out + (size_t)blockIdx.z * total;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int k = k0 + ty * 8 + i;
+        if (k >= g.k) break;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int c = c0 + tx * 4 + j;
+            if (c < g.f_pitch) o[((size_t)k * taps + tap) * g.f_pitch + c] = acc[i][j];
+        }
+    }
+}
+
+template <typename T>
+__global__ void direct_wgrad_sum_kernel(const float* __restrict__ partial, int splits, long long total,
+                                        T* __restrict__ dw) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        float sum = 0.0f;
+        for (int sp = 0; sp < splits; ++sp) sum += partial[(size_t)sp * total + i];
+        st(dw + i, sum);
+    }
+}
+
 }  // namespace pk
 
 using namespace pk;
@@ -333,6 +416,42 @@ cudaError_t pk_cuda_direct_bwd_weights(const pk_conv_geom* g, int dtype, const v
                       direct_bwd_weights_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(
                           *g, (const T*)dy, (const T*)x, (T*)dw));
     count_launch();
+    return cudaGetLastError();
+}
+
+int pk_direct_wgrad_tiled_supported(const pk_conv_geom* g) {
+    return g->groups == 1 && !g->transpose && g->x_pitch % 8 == 0 && g->f_pitch == g->x_pitch &&
+           g->y_pitch % 8 == 0 && (long long)g->n * g->p * g->q < (1LL << 31);
+}
+
+static int direct_wgrad_splits(const pk_conv_geom* g, int num_sms) {
+    const long long tiles = (long long)ceil_div(g->k, 64) * g->r * g->s * ceil_div(g->f_pitch, 64);
+    const long long npix = (long long)g->n * g->p * g->q;
+    long long splits = (4LL * num_sms + tiles - 1) / tiles;
+    splits = std::min(splits, std::max(1LL, npix / 256));  // >= 256 pixels per split
+    return (int)std::max(1LL, std::min(splits, 1024LL));
+}
+
+size_t pk_direct_wgrad_tiled_workspace(const pk_conv_geom* g, int num_sms) {
+    return (size_t)direct_wgrad_splits(g, num_sms) * g->k * g->r * g->s * g->f_pitch * sizeof(float);
+}
+
+cudaError_t pk_cuda_direct_wgrad_tiled(const pk_conv_geom* g, int dtype, const void* dy, const void* x, void* dw,
+                                       void* ws, size_t ws_bytes, int num_sms, cudaStream_t st) {
+    if (!pk_direct_wgrad_tiled_supported(g) || ws_bytes < pk_direct_wgrad_tiled_workspace(g, num_sms))
+        return cudaErrorInvalidValue;
+    const int splits = direct_wgrad_splits(g, num_sms);
+    const long long npix = (long long)g->n * g->p * g->q;
+    const int per = (int)((ceil_div(npix, splits) + 15) / 16 * 16);
+    const long long total = (long long)g->k * g->r * g->s * g->f_pitch;
+    dim3 grid(ceil_div(g->k, 64), g->r * g->s * ceil_div(g->f_pitch, 64), ceil_div(npix, per));
+    PK_DISPATCH_DTYPE(dtype, T, {
+        direct_wgrad_tiled_kernel<T><<<grid, 128, 0, st>>>(*g, (const T*)dy, (const T*)x, (float*)ws, per);
+        direct_wgrad_sum_kernel<T><<<(unsigned)std::max(1LL, std::min((long long)ceil_div(total, 256),
+                                                                      4LL * num_sms)),
+                                     256, 0, st>>>((const float*)ws, (int)grid.z, total, (T*)dw);
+    });
+    count_launch(2);
     return cudaGetLastError();
 }
 

@@ -486,6 +486,11 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
             const std::size_t wb = pk_grouped_wgrad_workspace(&g, h.num_sms());
             ck(pk_cuda_grouped_wgrad(&g, dt, a, b, out, h.scratch(13, wb), wb, h.num_sms(), st),
                "grouped_wgrad");
+        } else if (algo_ == ConvAlgo::Direct && pk_direct_wgrad_tiled_supported(&g)) {
+            kernel = "direct_simt_tiled_bwd_weights";
+            const std::size_t wb = pk_direct_wgrad_tiled_workspace(&g, h.num_sms());
+            ck(pk_cuda_direct_wgrad_tiled(&g, dt, a, b, out, h.scratch(13, wb), wb, h.num_sms(), st),
+               "direct_wgrad_tiled");
         } else if (algo_ == ConvAlgo::Direct) {
             kernel = "direct_simt_bwd_weights";
             ck(pk_cuda_direct_bwd_weights(&g, dt, a, b, out, st), "direct_bwd_weights");
