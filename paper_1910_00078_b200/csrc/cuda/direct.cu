@@ -275,6 +275,87 @@ __global__ void __launch_bounds__(256) direct_bwd_weights_kernel(pk_conv_geom g,
     }
 }
 
+// Backward data, register-tiled (groups == 1, convolution mode): a CTA owns 64
+// input pixels x 64 input channels; per filter tap and 16-channel k chunk the
+// gathered dY slice [16 k][64 px] (zero where the tap does not land on an
+// output position) and the filter rows [16 k][64 c] are staged in smem and
+// each thread accumulates 8 px x 4 c. Taps in (r, s) order, k ascending.
+template <typename T>
+__global__ void __launch_bounds__(128) direct_dgrad_tiled_kernel(pk_conv_geom g, const T* __restrict__ dy,
+                                                                 const T* __restrict__ f, T* __restrict__ dx) {
+    constexpr int TP = 64, TC = 64, KC = 16, LD = TP + 4;
+    __shared__ __align__(16) float As[KC][LD];  // [k][pixel]
+    __shared__ __align__(16) float Bs[KC][LD];  // [k][channel]
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int npix = g.n * g.h * g.w;
+    const int px0 = blockIdx.x * TP, c0 = blockIdx.y * TC;
+    const int lp = tid & 63, lh = tid >> 6;          // dY loader: pixel, k half
+    const int bk = tid >> 3, bc = (tid & 7) * 8;     // filter loader: k row, 8-channel vector
+    const int pix = px0 + lp;
+    const bool pv = pix < npix;
+    int ln = 0, lih = 0, liw = 0;
+    if (pv) {
+        liw = pix % g.w;
+        const int t = pix / g.w;
+        lih = t % g.h;
+        ln = t / g.h;
+    }
+    float acc[8][4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    for (int r = 0; r < g.r; ++r) {
+        const int nh = lih + g.pad_h - r * g.dil_h;
+        const int oh = nh / g.str_h;
+        const bool hv = nh >= 0 && nh % g.str_h == 0 && oh < g.p;
+        for (int s = 0; s < g.s; ++s) {
+            const int nw = liw + g.pad_w - s * g.dil_w;
+            const int ow = nw / g.str_w;
+            const bool ok = pv && hv && nw >= 0 && nw % g.str_w == 0 && ow < g.q;
+            const T* dyp = dy + (((size_t)ln * g.p + (ok ? oh : 0)) * g.q + (ok ? ow : 0)) * g.y_pitch;
+            for (int kc = 0; kc < g.k; kc += KC) {
+                const int kb = kc + lh * 8;
+                float av[8], bv[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) av[i] = bv[i] = 0.0f;
+                if (ok && kb < g.y_pitch) load8(dyp + kb, av);
+                if (kc + bk < g.k && c0 + bc < g.f_pitch)
+                    load8(f + (((size_t)(kc + bk) * g.r + r) * g.s + s) * g.f_pitch + c0 + bc, bv);
+                __syncthreads();  // the previous chunk is consumed
+#pragma unroll
+                for (int i = 0; i < 8; ++i) As[lh * 8 + i][lp] = av[i];
+                *reinterpret_cast<float4*>(&Bs[bk][bc]) = make_float4(bv[0], bv[1], bv[2], bv[3]);
+                *reinterpret_cast<float4*>(&Bs[bk][bc + 4]) = make_float4(bv[4], bv[5], bv[6], bv[7]);
+                __syncthreads();
+#pragma unroll
+                for (int q = 0; q < KC; ++q) {
+                    const float4 a0 = *reinterpret_cast<const float4*>(&As[q][ty * 8]);
+                    const float4 a1 = *reinterpret_cast<const float4*>(&As[q][ty * 8 + 4]);
+                    const float4 b = *reinterpret_cast<const float4*>(&Bs[q][tx * 4]);
+                    const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+                    const float bb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int p = px0 + ty * 8 + i;
+        if (p >= npix) break;
+        T* xp = dx + (size_t)p * g.x_pitch;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int c = c0 + tx * 4 + j;
+            if (c < g.x_pitch) st(xp + c, acc[i][j]);  // pad lanes: zero filter lanes give 0
+        }
+    }
+}
+
 // Backward weights, register-tiled (groups == 1, convolution mode): the GEMM
 // dW[k][(tap, c)] = sum_pix dY[pix][k] * x[pix + tap][c]. A CTA owns 64 k x 64
 // channels of one tap over a contiguous pixel range (split z); per 16-pixel
@@ -415,6 +496,21 @@ cudaError_t pk_cuda_direct_bwd_weights(const pk_conv_geom* g, int dtype, const v
     PK_DISPATCH_DTYPE(dtype, T,
                       direct_bwd_weights_kernel<T><<<(unsigned)blocks, 256, 0, st>>>(
                           *g, (const T*)dy, (const T*)x, (T*)dw));
+    count_launch();
+    return cudaGetLastError();
+}
+
+int pk_direct_dgrad_tiled_supported(const pk_conv_geom* g) {
+    return g->groups == 1 && !g->transpose && g->x_pitch % 8 == 0 && g->f_pitch == g->x_pitch &&
+           g->y_pitch % 8 == 0 && (long long)g->n * g->h * g->w < (1LL << 31);
+}
+
+cudaError_t pk_cuda_direct_dgrad_tiled(const pk_conv_geom* g, int dtype, const void* dy, const void* f, void* dx,
+                                       cudaStream_t st) {
+    if (!pk_direct_dgrad_tiled_supported(g)) return cudaErrorInvalidValue;
+    dim3 grid(ceil_div((long long)g->n * g->h * g->w, 64), ceil_div(g->x_pitch, 64));
+    PK_DISPATCH_DTYPE(dtype, T,
+                      direct_dgrad_tiled_kernel<T><<<grid, 128, 0, st>>>(*g, (const T*)dy, (const T*)f, (T*)dx));
     count_launch();
     return cudaGetLastError();
 }

@@ -114,6 +114,10 @@ int pk_grouped_wgrad_supported(const pk_conv_geom* g);
 size_t pk_grouped_wgrad_workspace(const pk_conv_geom* g, int num_sms);
 cudaError_t pk_cuda_grouped_wgrad(const pk_conv_geom* g, int dtype, const void* dy, const void* x, void* dw,
                                   void* ws, size_t ws_bytes, int num_sms, cudaStream_t st);
+// Register-tiled SIMT backward data (groups 1), direct.cu.
+int pk_direct_dgrad_tiled_supported(const pk_conv_geom* g);
+cudaError_t pk_cuda_direct_dgrad_tiled(const pk_conv_geom* g, int dtype, const void* dy, const void* f, void* dx,
+                                       cudaStream_t st);
 // Register-tiled SIMT backward weights (groups 1), split over pixels + fixed-order sum (direct.cu).
 int pk_direct_wgrad_tiled_supported(const pk_conv_geom* g);
 size_t pk_direct_wgrad_tiled_workspace(const pk_conv_geom* g, int num_sms);

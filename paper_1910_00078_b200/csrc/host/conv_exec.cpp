@@ -449,6 +449,9 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
         } else if (algo_ != ConvAlgo::Winograd && algo_ != ConvAlgo::FFT && pk_grouped_supported(&g)) {
             kernel = "grouped_simt_bwd_data";
             ck(pk_cuda_grouped_bwd_data(&g, dt, a, b, out, h.num_sms(), st), "grouped_bwd_data");
+        } else if (algo_ == ConvAlgo::Direct && pk_direct_dgrad_tiled_supported(&g)) {
+            kernel = "direct_simt_tiled_bwd_data";
+            ck(pk_cuda_direct_dgrad_tiled(&g, dt, a, b, out, st), "direct_dgrad_tiled");
         } else if (algo_ == ConvAlgo::Direct) {
             kernel = "direct_simt_bwd_data";
             ck(pk_cuda_direct_bwd_data(&g, dt, a, b, out, st), "direct_bwd_data");
