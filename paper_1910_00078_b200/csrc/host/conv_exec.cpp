@@ -327,6 +327,22 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                     ck(pk_cuda_grouped_fwd(&g, dt, a, b, out, epi, h.num_sms(), st), "grouped_fwd");
                     break;
                 }
+                if (g.transpose && g.groups == 1 && g.dil_h == 1 && g.dil_w == 1 && !epi) {
+                    // transpose-mode forward = backward data of the convolution whose
+                    // output grid is x: swap the roles of (c, h, w) and (k, p, q); the
+                    // transpose filter [C][R][S][pitch(K)] is that convolution's filter
+                    pk_conv_geom d = g;
+                    d.c = g.k; d.h = g.p; d.w = g.q;
+                    d.k = g.c; d.p = g.h; d.q = g.w;
+                    d.cg = g.kg; d.kg = g.cg;
+                    d.x_pitch = g.y_pitch; d.y_pitch = g.x_pitch;
+                    d.transpose = 0;
+                    if (pk_direct_dgrad_tiled_supported(&d)) {
+                        kernel = "direct_simt_tiled_transpose";
+                        ck(pk_cuda_direct_dgrad_tiled(&d, dt, a, b, out, st), "direct_transpose_tiled");
+                        break;
+                    }
+                }
                 kernel = "direct_simt";
                 ck(pk_cuda_direct_fwd(&g, dt, a, b, out, epi, st), "direct_fwd");
                 break;

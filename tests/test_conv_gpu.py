@@ -96,6 +96,24 @@ def test_transpose_mode(lib):
             assert rel_l2(got, want) <= 1e-4, s
 
 
+@pytest.mark.parametrize("et", [abi.F32, abi.BF16])
+def test_transpose_mode_tiled(lib, et):
+    """Transpose-mode forward on the Direct solver runs the register-tiled
+    backward-data kernel with the roles of input and output swapped."""
+    rng = np.random.default_rng(6)
+    h = lib.handle()
+    for shp in (dict(n=2, c=32, h=9, w=8, k=24, y=3, x=3, pad=1, stride=2),
+                dict(n=1, c=16, h=6, w=7, k=72, y=4, x=4, pad=1, stride=2),
+                dict(n=2, c=8, h=5, w=5, k=8, y=3, x=3, pad=0, stride=1),
+                dict(n=1, c=70, h=4, w=4, k=3, y=3, x=3, pad=2, stride=3)):
+        p = problem(**shp, mode=abi.TRANSPOSE, etype=et)
+        a, b = _inputs(p, rng, et == abi.BF16)
+        want = oracle.conv_ref_f64(*_transpose_as_conv(p, a, b))
+        got = h.conv_run(p, "Direct", a, b)
+        assert h.last_kernel() == "direct_simt_tiled_transpose", h.last_kernel()
+        assert rel_l2(got, want) <= (1e-2 if et == abi.BF16 else 1e-4), shp
+
+
 def _transpose_as_conv(p, x, w):
     """Transpose conv == stride-1 conv of the zero-upsampled input with the
     flipped, channel-swapped filter (independent formulation)."""
