@@ -287,18 +287,23 @@ __global__ void __launch_bounds__(128) direct_dgrad_tiled_kernel(pk_conv_geom g,
     __shared__ __align__(16) float As[KC][LD];  // [k][pixel]
     __shared__ __align__(16) float Bs[KC][LD];  // [k][channel]
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    const int npix = g.n * g.h * g.w;
+    // stride phases: a CTA's pixels share (ih mod str_h, iw mod str_w), so a tap
+    // lands for all of them or for none, and missing taps are skipped whole
+    const int ph_h = blockIdx.z / g.str_w, ph_w = blockIdx.z % g.str_w;
+    const int hp = (g.h - ph_h + g.str_h - 1) / g.str_h, wp = (g.w - ph_w + g.str_w - 1) / g.str_w;
+    const int npix = g.n * hp * wp;  // pixels of this phase
     const int px0 = blockIdx.x * TP, c0 = blockIdx.y * TC;
+    if (px0 >= npix) return;
     const int lp = tid & 63, lh = tid >> 6;          // dY loader: pixel, k half
     const int bk = tid >> 3, bc = (tid & 7) * 8;     // filter loader: k row, 8-channel vector
     const int pix = px0 + lp;
     const bool pv = pix < npix;
     int ln = 0, lih = 0, liw = 0;
     if (pv) {
-        liw = pix % g.w;
-        const int t = pix / g.w;
-        lih = t % g.h;
-        ln = t / g.h;
+        liw = ph_w + (pix % wp) * g.str_w;
+        const int t = pix / wp;
+        lih = ph_h + (t % hp) * g.str_h;
+        ln = t / hp;
     }
     float acc[8][4];
 #pragma unroll
@@ -306,10 +311,13 @@ __global__ void __launch_bounds__(128) direct_dgrad_tiled_kernel(pk_conv_geom g,
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
     for (int r = 0; r < g.r; ++r) {
+        if (g.str_h > 1 && ((ph_h + g.pad_h - r * g.dil_h) % g.str_h + g.str_h) % g.str_h)
+            continue;  // tap misses the phase
         const int nh = lih + g.pad_h - r * g.dil_h;
         const int oh = nh / g.str_h;
         const bool hv = nh >= 0 && nh % g.str_h == 0 && oh < g.p;
         for (int s = 0; s < g.s; ++s) {
+            if (g.str_w > 1 && ((ph_w + g.pad_w - s * g.dil_w) % g.str_w + g.str_w) % g.str_w) continue;
             const int nw = liw + g.pad_w - s * g.dil_w;
             const int ow = nw / g.str_w;
             const bool ok = pv && hv && nw >= 0 && nw % g.str_w == 0 && ow < g.q;
@@ -345,9 +353,11 @@ __global__ void __launch_bounds__(128) direct_dgrad_tiled_kernel(pk_conv_geom g,
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int p = px0 + ty * 8 + i;
-        if (p >= npix) break;
-        T* xp = dx + (size_t)p * g.x_pitch;
+        const int pp = px0 + ty * 8 + i;
+        if (pp >= npix) break;
+        const int iw = ph_w + (pp % wp) * g.str_w, t = pp / wp;
+        const int ih = ph_h + (t % hp) * g.str_h, n = t / hp;
+        T* xp = dx + (((size_t)n * g.h + ih) * g.w + iw) * g.x_pitch;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const int c = c0 + tx * 4 + j;
@@ -508,7 +518,9 @@ int pk_direct_dgrad_tiled_supported(const pk_conv_geom* g) {
 cudaError_t pk_cuda_direct_dgrad_tiled(const pk_conv_geom* g, int dtype, const void* dy, const void* f, void* dx,
                                        cudaStream_t st) {
     if (!pk_direct_dgrad_tiled_supported(g)) return cudaErrorInvalidValue;
-    dim3 grid(ceil_div((long long)g->n * g->h * g->w, 64), ceil_div(g->x_pitch, 64));
+    // phases: grid.z = str_h * str_w; grid.x covers the largest phase (phase 0)
+    const long long most = (long long)g->n * ceil_div(g->h, g->str_h) * ceil_div(g->w, g->str_w);
+    dim3 grid(ceil_div(most, 64), ceil_div(g->x_pitch, 64), g->str_h * g->str_w);
     PK_DISPATCH_DTYPE(dtype, T,
                       direct_dgrad_tiled_kernel<T><<<grid, 128, 0, st>>>(*g, (const T*)dy, (const T*)f, (T*)dx));
     count_launch();
