@@ -161,7 +161,6 @@ __global__ void __launch_bounds__(kThreads) depthwise3_s1_kernel(pk_conv_geom g,
     const unsigned quads = (unsigned)g.n * oh_n * qpr;
     const int kmax = BWD ? g.c : g.k;
     const bool epi = !BWD && epilogue_active(&e);
-    float w[3][3][8];
     for (unsigned qi = blockIdx.x * lanes_px + pl; qi < quads; qi += gridDim.x * lanes_px) {
         const unsigned row = qi / qpr;
         const int ow0 = (int)(qi - row * qpr) * 4;
@@ -192,12 +191,13 @@ __global__ void __launch_bounds__(kThreads) depthwise3_s1_kernel(pk_conv_geom g,
                         for (int c = 0; c < 8; ++c) v[i][c] = 0.0f;
                 }
             }
+            float w[3][8];
 #pragma unroll
             for (int s = 0; s < 3; ++s) {
                 const float4* wp = reinterpret_cast<const float4*>(sw + (r * 3 + s) * cb + cvi * 8);
                 const float4 w0 = wp[0], w1 = wp[1];
-                w[r][s][0] = w0.x; w[r][s][1] = w0.y; w[r][s][2] = w0.z; w[r][s][3] = w0.w;
-                w[r][s][4] = w1.x; w[r][s][5] = w1.y; w[r][s][6] = w1.z; w[r][s][7] = w1.w;
+                w[s][0] = w0.x; w[s][1] = w0.y; w[s][2] = w0.z; w[s][3] = w0.w;
+                w[s][4] = w1.x; w[s][5] = w1.y; w[s][6] = w1.z; w[s][7] = w1.w;
             }
             // taps in (r, s) order per output, as the reference accumulates
 #pragma unroll
@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(kThreads) depthwise3_s1_kernel(pk_conv_geom g,
 #pragma unroll
                 for (int j = 0; j < 4; ++j)
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) acc[j][c] += v[BWD ? j + 2 - s : j + s][c] * w[r][s][c];
+                    for (int c = 0; c < 8; ++c) acc[j][c] += v[BWD ? j + 2 - s : j + s][c] * w[s][c];
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
