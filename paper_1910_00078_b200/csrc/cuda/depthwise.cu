@@ -455,6 +455,22 @@ __global__ void __launch_bounds__(kThreads) grouped_wgrad_kernel(pk_conv_geom g,
             const T* xn = x + (size_t)n * g.h * g.w * g.x_pitch + grp * g.cg + cvi * 8;
             for (int ow = pl; ow < g.q; ow += lanes_px) {
                 const float d = ld(dy + ((size_t)row * g.q + ow) * g.y_pitch + k);
+                if (taps == 9 && g.s == 3) {
+                    const int ih0 = oh * g.str_h - g.pad_h, iw0 = ow * g.str_w - g.pad_w;
+                    if (ih0 >= 0 && ih0 + 2 * g.dil_h < g.h && iw0 >= 0 && iw0 + 2 * g.dil_w < g.w) {
+                        // interior pixel of a 3x3 filter: 9 loads from one base, no checks
+                        const T* xb = xn + (ih0 * g.w + iw0) * g.x_pitch;
+                        const int dr = g.dil_h * g.w * g.x_pitch, ds = g.dil_w * g.x_pitch;
+                        float v[9][8];
+#pragma unroll
+                        for (int t = 0; t < 9; ++t) load8v(xb + (t / 3) * dr + (t % 3) * ds, v[t]);
+#pragma unroll
+                        for (int t = 0; t < 9; ++t)
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) acc[t][j] += d * v[t][j];
+                        continue;
+                    }
+                }
 #pragma unroll
                 for (int t = 0; t < kTapGroup; ++t) {
                     const int tap = t0 + t;
