@@ -21,14 +21,14 @@ __global__ void __launch_bounds__(256) winograd_f23_kernel(pk_conv_geom g, const
                                                            const T* __restrict__ f,
                                                            T* __restrict__ y, pk_epilogue e) {
     __shared__ float Vs[WC][16][WT + 1];
-    __shared__ float Us[WC][16][WK + 1];
+    __shared__ __align__(16) float Us[WC][16][WK + 4];  // rows 16-byte aligned for float4 reads
     const int th = (g.p + 1) / 2, tw = (g.q + 1) / 2;
     const long long ntiles = (long long)g.n * th * tw;
     const long long t0 = (long long)blockIdx.x * WT;
     const int k0 = blockIdx.y * WK;
     const int grp = k0 / g.kg;  // host guarantees kg % WK == 0 or groups == 1
     const int tid = threadIdx.x;
-    const int tx = tid % 32, ty = tid / 32;  // tile lane, k sub-row
+    const int tx = tid % 32, ty = tid / 32;  // tile lane, k group (4 consecutive k)
 
     float M[4][16];
 #pragma unroll
@@ -37,10 +37,11 @@ __global__ void __launch_bounds__(256) winograd_f23_kernel(pk_conv_geom g, const
         for (int q = 0; q < 16; ++q) M[j][q] = 0.0f;
 
     for (int c0 = 0; c0 < g.cg; c0 += WC) {
-        // Input transform: thread -> (tile tx, channel ty).
+        // Input transform: thread -> (tile tid / WC, channel tid % WC); the WC
+        // lanes of a tile read consecutive channels of each pixel (coalesced).
         {
-            const int cl = ty, c = c0 + cl;
-            const long long t = t0 + tx;
+            const int cl = tid % WC, tl = tid / WC, c = c0 + cl;
+            const long long t = t0 + tl;
             float d[4][4];
             if (c < g.cg && t < ntiles) {
                 const int tj = (int)(t % tw);
@@ -74,10 +75,10 @@ __global__ void __launch_bounds__(256) winograd_f23_kernel(pk_conv_geom g, const
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                Vs[cl][i * 4 + 0][tx] = tt[i][0] - tt[i][2];
-                Vs[cl][i * 4 + 1][tx] = tt[i][1] + tt[i][2];
-                Vs[cl][i * 4 + 2][tx] = tt[i][2] - tt[i][1];
-                Vs[cl][i * 4 + 3][tx] = tt[i][1] - tt[i][3];
+                Vs[cl][i * 4 + 0][tl] = tt[i][0] - tt[i][2];
+                Vs[cl][i * 4 + 1][tl] = tt[i][1] + tt[i][2];
+                Vs[cl][i * 4 + 2][tl] = tt[i][2] - tt[i][1];
+                Vs[cl][i * 4 + 3][tl] = tt[i][1] - tt[i][3];
             }
         }
         // Filter transform: thread -> (output channel tx, channel ty).
@@ -118,8 +119,11 @@ __global__ void __launch_bounds__(256) winograd_f23_kernel(pk_conv_geom g, const
 #pragma unroll
             for (int q = 0; q < 16; ++q) {
                 const float v = Vs[cl][q][tx];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) M[j][q] += Us[cl][q][ty + 8 * j] * v;
+                const float4 u = *reinterpret_cast<const float4*>(&Us[cl][q][ty * 4]);  // broadcast
+                M[0][q] += u.x * v;
+                M[1][q] += u.y * v;
+                M[2][q] += u.z * v;
+                M[3][q] += u.w * v;
             }
         }
         __syncthreads();
@@ -133,7 +137,7 @@ __global__ void __launch_bounds__(256) winograd_f23_kernel(pk_conv_geom g, const
     const bool epi = epilogue_active(&e);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        const int k = k0 + ty + 8 * j;
+        const int k = k0 + ty * 4 + j;
         if (k >= g.k) continue;
         const float* m = M[j];
         float rr[2][4];
