@@ -333,6 +333,12 @@ PRIMKIT_API primkit_status primkit_handle_last_device_ms(primkit_handle* handle,
  * (e.g. "igemm_tc_fwd", "direct_simt"). */
 PRIMKIT_API primkit_status primkit_handle_last_kernel(primkit_handle* handle, char* buf,
                                                      size_t buf_len);
+/* Template instances of the tensor-core kernels the last conv run launched,
+ * in launch order, joined by '+' (e.g.
+ * "conv_tma_fprop_kernel<256, 6, false, false, 1, true>"); empty for the
+ * CUDA-core families, which last_kernel names completely. */
+PRIMKIT_API primkit_status primkit_handle_last_variant(primkit_handle* handle, char* buf,
+                                                      size_t buf_len);
 
 #ifdef __cplusplus
 }

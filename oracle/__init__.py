@@ -36,7 +36,8 @@ def build(force: bool = False) -> None:
     the reference library. Building the checker is not using it."""
     src = os.path.join(_HERE, "primkit_oracle.c")
     if force or not os.path.exists(RESTATED_SO) or os.path.getmtime(src) > os.path.getmtime(RESTATED_SO):
-        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-o", RESTATED_SO, src, "-lm"])
+        subprocess.check_call(["gcc", "-O3", "-fopenmp", "-fPIC", "-shared", "-o", RESTATED_SO, src,
+                               "-lm"])
     if os.path.isdir(REF_SOURCES) and (force or not os.path.exists(REF_SO)):
         subprocess.check_call(["make", "-s", "-f", os.path.join(_HERE, "Makefile.ref"),
                                f"-j{os.cpu_count() or 4}"])
@@ -203,6 +204,71 @@ def conv_ref_f64(p, x, w):
                     ws = w[g * kg:(g + 1) * kg, :, yy, xx]                         # kg, cg
                     out[:, g * kg:(g + 1) * kg, o_h, ok] += np.einsum("ncq,kc->nkq", xs, ws)
     return out
+
+
+# ---- sampled direct formulas on the device layout (full-size parity) -------
+
+class _DevG(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("n", "c", "h", "w", "k", "r", "s", "p", "q", "pad_h",
+                                         "pad_w", "str_h", "str_w", "dil_h", "dil_w", "xp", "yp",
+                                         "fp", "bf16")]
+
+
+def dev_geom(p, bf16=True) -> _DevG:
+    """Device-layout geometry of a (groups = 1, convolution-mode) problem:
+    activations NHWC with channel pitch roundup(C, 8), filter [K][R][S][pitch(C)]."""
+    oh, ow = out_hw(p)
+    pit = lambda c: (c + 7) // 8 * 8  # noqa: E731
+    return _DevG(p.n, p.c, p.h, p.w, p.k, p.y, p.x, oh, ow, p.pad_h, p.pad_w, p.stride_h,
+                 p.stride_w, p.dilation_h, p.dilation_w, pit(p.c), pit(p.k), pit(p.c), int(bf16))
+
+
+def _vp(a):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def sample_forward(p, x, w, idx, bf16=True):
+    """f64 forward outputs at idx (ns x 4: n, k, oh, ow); x, w in the device
+    layout (uint16 bf16 bits or float32). Restates conv.cpp:99-133."""
+    idx = np.ascontiguousarray(idx, np.int64)
+    out = np.zeros(len(idx), np.float64)
+    lib = restated()
+    lib.oc_sample_fwd(C.byref(dev_geom(p, bf16)), _vp(x), _vp(w), _vp(idx), C.c_int64(len(idx)), _vp(out))
+    return out
+
+
+def sample_backward_data(p, dy, w, idx, bf16=True):
+    """f64 dX at idx (ns x 4: n, c, h, w). Restates conv.cpp:702-799."""
+    idx = np.ascontiguousarray(idx, np.int64)
+    out = np.zeros(len(idx), np.float64)
+    restated().oc_sample_dgrad(C.byref(dev_geom(p, bf16)), _vp(dy), _vp(w), _vp(idx),
+                               C.c_int64(len(idx)), _vp(out))
+    return out
+
+
+def sample_backward_weights(p, dy, x, ks, taps, bf16=True):
+    """f64 dW on the grid ks x taps (taps: nt x 3 = r, s, c) -> [len(ks), nt].
+    Restates conv.cpp:801-873."""
+    ks = np.ascontiguousarray(ks, np.int64)
+    taps = np.ascontiguousarray(taps, np.int64)
+    out = np.zeros((len(ks), len(taps)), np.float64)
+    restated().oc_sample_wgrad(C.byref(dev_geom(p, bf16)), _vp(dy), _vp(x), _vp(ks),
+                               C.c_int64(len(ks)), _vp(taps), C.c_int64(len(taps)), _vp(out))
+    return out
+
+
+def bn_stats_device(x, c, eps=1e-5, bf16=True):
+    """Spatial BN batch statistics (primitives.cpp:61-96) of a device-layout
+    tensor x (... x pitch): (mean f32, invstd f32, biased var f64) per channel."""
+    pitch = x.shape[-1]
+    rows = x.size // pitch
+    mean, inv = np.zeros(c, np.float32), np.zeros(c, np.float32)
+    var = np.zeros(c, np.float64)
+    restated().oc_bn_stats_dev(_vp(np.ascontiguousarray(x)), C.c_int64(rows), C.c_int64(c),
+                               C.c_int64(pitch), C.c_int64(int(bf16)), C.c_float(eps), _vp(mean),
+                               _vp(inv), _vp(var))
+    return mean, inv, var
 
 
 # ---- the unmodified reference library -------------------------------------

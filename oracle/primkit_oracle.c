@@ -351,3 +351,156 @@ float oc_fused_epilogue(float acc, int has_bias, float bias, int has_bn, float m
     if (act >= 0) acc = oc_activation(act, alpha, acc);
     return acc;
 }
+
+/* ---- sampled direct formulas on the DEVICE layout (full-size parity) -----
+ *
+ * At BASELINE sizes (ResNet-50 / VGG-16 at N=128-256) the full CPU oracle is
+ * minutes per layer, so the GPU result is checked on sampled coordinates
+ * (>= 4096 output coordinates with the direct formula). These
+ * evaluate the same sums as the reference's Direct kernels
+ * (src/core/conv.cpp:99-133 forward, 702-799 backward data, 801-873 backward
+ * weights; groups = 1, convolution mode) in double, reading the operands in
+ * the device layout the GPU consumed: NHWC with channel pitch, filters
+ * [K][R][S][pitch], element type bf16 (raw 16-bit) or f32. */
+typedef struct {
+    int64_t n, c, h, w, k, r, s, p, q;
+    int64_t pad_h, pad_w, str_h, str_w, dil_h, dil_w;
+    int64_t xp, yp, fp; /* channel pitches of x, y and the filter rows */
+    int64_t bf16;
+} oc_dev;
+
+static inline double oc_ld(const void* base, int64_t i, int bf16) {
+    if (!bf16) return ((const float*)base)[i];
+    uint32_t u = (uint32_t)((const uint16_t*)base)[i] << 16;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+}
+
+/* forward: idx = ns x (n, k, oh, ow) */
+void oc_sample_fwd(const oc_dev* g, const void* x, const void* w, const int64_t* idx, int64_t ns,
+                   double* ref) {
+    const int b = (int)g->bf16;
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t i = 0; i < ns; ++i) {
+        const int64_t n = idx[4 * i], k = idx[4 * i + 1], oh = idx[4 * i + 2], ow = idx[4 * i + 3];
+        double acc = 0.0;
+        for (int64_t r = 0; r < g->r; ++r) {
+            const int64_t ih = oh * g->str_h - g->pad_h + r * g->dil_h;
+            if (ih < 0 || ih >= g->h) continue;
+            for (int64_t s = 0; s < g->s; ++s) {
+                const int64_t iw = ow * g->str_w - g->pad_w + s * g->dil_w;
+                if (iw < 0 || iw >= g->w) continue;
+                const int64_t xo = ((n * g->h + ih) * g->w + iw) * g->xp;
+                const int64_t wo = ((k * g->r + r) * g->s + s) * g->fp;
+                for (int64_t c = 0; c < g->c; ++c) acc += oc_ld(x, xo + c, b) * oc_ld(w, wo + c, b);
+            }
+        }
+        ref[i] = acc;
+    }
+}
+
+/* backward data: idx = ns x (n, c, h, w); dX[n,c,h,w] = sum over (k, r, s)
+ * with oh*str = h + pad - r*dil (exact division) of dY[n,k,oh,ow] W[k,c,r,s] */
+void oc_sample_dgrad(const oc_dev* g, const void* dy, const void* w, const int64_t* idx, int64_t ns,
+                     double* ref) {
+    const int b = (int)g->bf16;
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t i = 0; i < ns; ++i) {
+        const int64_t n = idx[4 * i], c = idx[4 * i + 1], h = idx[4 * i + 2], wq = idx[4 * i + 3];
+        double acc = 0.0;
+        for (int64_t r = 0; r < g->r; ++r) {
+            const int64_t th = h + g->pad_h - r * g->dil_h;
+            if (th < 0 || th % g->str_h) continue;
+            const int64_t oh = th / g->str_h;
+            if (oh >= g->p) continue;
+            for (int64_t s = 0; s < g->s; ++s) {
+                const int64_t tw = wq + g->pad_w - s * g->dil_w;
+                if (tw < 0 || tw % g->str_w) continue;
+                const int64_t ow = tw / g->str_w;
+                if (ow >= g->q) continue;
+                const int64_t yo = ((n * g->p + oh) * g->q + ow) * g->yp;
+                for (int64_t k = 0; k < g->k; ++k)
+                    acc += oc_ld(dy, yo + k, b) * oc_ld(w, ((k * g->r + r) * g->s + s) * g->fp + c, b);
+            }
+        }
+        ref[i] = acc;
+    }
+}
+
+/* backward weights on a (ks x taps) grid: ref[a * nt + t] = dW[ks[a], tap t]
+ * with tap t = (r, s, c) = taps[3t..3t+2]; sums over every (n, oh, ow). */
+void oc_sample_wgrad(const oc_dev* g, const void* dy, const void* x, const int64_t* ks, int64_t nk,
+                     const int64_t* taps, int64_t nt, double* ref) {
+    const int b = (int)g->bf16;
+    memset(ref, 0, sizeof(double) * nk * nt);
+#pragma omp parallel
+    {
+        double* acc = (double*)calloc((size_t)(nk * nt), sizeof(double));
+        double* dv = (double*)malloc(sizeof(double) * nk);
+        double* xv = (double*)malloc(sizeof(double) * nt);
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t n = 0; n < g->n; ++n)
+            for (int64_t oh = 0; oh < g->p; ++oh)
+                for (int64_t ow = 0; ow < g->q; ++ow) {
+                    const int64_t yo = ((n * g->p + oh) * g->q + ow) * g->yp;
+                    for (int64_t a = 0; a < nk; ++a) dv[a] = oc_ld(dy, yo + ks[a], b);
+                    for (int64_t t = 0; t < nt; ++t) {
+                        const int64_t ih = oh * g->str_h - g->pad_h + taps[3 * t] * g->dil_h;
+                        const int64_t iw = ow * g->str_w - g->pad_w + taps[3 * t + 1] * g->dil_w;
+                        xv[t] = (ih < 0 || ih >= g->h || iw < 0 || iw >= g->w)
+                                    ? 0.0
+                                    : oc_ld(x, ((n * g->h + ih) * g->w + iw) * g->xp + taps[3 * t + 2], b);
+                    }
+                    for (int64_t a = 0; a < nk; ++a) {
+                        const double d = dv[a];
+                        double* row = acc + a * nt;
+                        for (int64_t t = 0; t < nt; ++t) row[t] += d * xv[t];
+                    }
+                }
+#pragma omp critical
+        for (int64_t i = 0; i < nk * nt; ++i) ref[i] += acc[i];
+        free(acc);
+        free(dv);
+        free(xv);
+    }
+}
+
+/* src/core/primitives.cpp:61-96 statistics (spatial mode) of a tensor in the
+ * device layout [rows][pitch] (rows = N*H*W): double sums per channel,
+ * mean = sum/m, biased var = max(0, E[x^2] - mean^2), invstd =
+ * float(1/sqrt(var + eps)). */
+void oc_bn_stats_dev(const void* x, int64_t rows, int64_t c, int64_t pitch, int64_t bf16, float eps,
+                     float* mean, float* invstd, double* var) {
+    double* sum = (double*)calloc((size_t)c, sizeof(double));
+    double* sq = (double*)calloc((size_t)c, sizeof(double));
+#pragma omp parallel
+    {
+        double* ls = (double*)calloc((size_t)c, sizeof(double));
+        double* lq = (double*)calloc((size_t)c, sizeof(double));
+#pragma omp for schedule(static)
+        for (int64_t r = 0; r < rows; ++r)
+            for (int64_t ch = 0; ch < c; ++ch) {
+                const double v = oc_ld(x, r * pitch + ch, (int)bf16);
+                ls[ch] += v;
+                lq[ch] += v * v;
+            }
+#pragma omp critical
+        for (int64_t ch = 0; ch < c; ++ch) {
+            sum[ch] += ls[ch];
+            sq[ch] += lq[ch];
+        }
+        free(ls);
+        free(lq);
+    }
+    for (int64_t ch = 0; ch < c; ++ch) {
+        const double mu = sum[ch] / (double)rows;
+        double v = sq[ch] / (double)rows - mu * mu;
+        if (v < 0.0) v = 0.0;
+        mean[ch] = (float)mu;
+        invstd[ch] = (float)(1.0 / sqrt(v + eps));
+        var[ch] = v;
+    }
+    free(sum);
+    free(sq);
+}

@@ -115,6 +115,7 @@ SECTION2 = {
     "primkit_handle_kernel_launches": (ST, [P, C.POINTER(C.c_uint64)]),
     "primkit_handle_last_device_ms": (ST, [P, C.POINTER(C.c_double)]),
     "primkit_handle_last_kernel": (ST, [P, C.c_char_p, C.c_size_t]),
+    "primkit_handle_last_variant": (ST, [P, C.c_char_p, C.c_size_t]),
 }
 
 

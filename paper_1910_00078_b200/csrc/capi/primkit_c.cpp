@@ -12,6 +12,7 @@
 
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <string>
 
 #include "../cuda/kernels.h"
@@ -138,7 +139,10 @@ void conv_run_chunked(primkit::Handle& hd, const primkit::ConvProblem& p,
     ck(cudaStreamWaitEvent(up, start, 0), "cudaStreamWaitEvent");
     ck(cudaStreamWaitEvent(down, start, 0), "cudaStreamWaitEvent");
     const primkit::OpCounters saved = hd.counters();
-    std::string kernel;
+    std::string kernel, variant;
+    std::unique_ptr<primkit::ConvPlan> chunk_plan;
+    cudaEvent_t t0 = hd.timing_event(0), t1 = hd.timing_event(1);
+    ck(cudaEventRecord(t0, cs), "cudaEventRecord");
     const int chunks = (int)((p.n + nc - 1) / nc);
     for (int j = 0; j < chunks; ++j) {
         const int s = j & 1;
@@ -155,13 +159,16 @@ void conv_run_chunked(primkit::Handle& hd, const primkit::ConvProblem& p,
                                 pk_pitch(ca), dt, cs),
            "nchw_to_nhwc");
         ck(cudaEventRecord(consumed, cs), "cudaEventRecord");
+        // chunk plans stay out of the plan cache: the reference makes exactly
+        // one cached_build per conv_run (below, for the whole problem)
         primkit::ConvProblem pj = p;
         pj.n = nj;
-        auto plan = hd.cached_build(pj, solver, &cfg);
-        const size_t dws = plan->device_workspace_bytes();
+        if (nj != nc || !chunk_plan) chunk_plan = std::make_unique<primkit::ConvPlan>(solver.build_plan(pj, &cfg));
+        const size_t dws = chunk_plan->device_workspace_bytes(hd.num_sms());
         void* ws = hd.scratch(0, dws);
-        plan->run(hd, dva + (size_t)n0 * img_a_dev, dvb, dvo + (size_t)n0 * img_o_dev, ws, dws);
+        chunk_plan->run(hd, dva + (size_t)n0 * img_a_dev, dvb, dvo + (size_t)n0 * img_o_dev, ws, dws);
         kernel = hd.last_kernel;
+        variant = hd.last_variant;
         if (j >= 2) ck(cudaStreamWaitEvent(cs, d2h, 0), "cudaStreamWaitEvent");
         ck(pk_cuda_nhwc_to_nchw(dvo + (size_t)n0 * img_o_dev, out_stage[s], nj, co, (int)hwo,
                                 pk_pitch(co), dt, cs),
@@ -177,10 +184,16 @@ void conv_run_chunked(primkit::Handle& hd, const primkit::ConvProblem& p,
     cudaEvent_t done = hd.event(9);
     ck(cudaEventRecord(done, down), "cudaEventRecord");
     ck(cudaStreamWaitEvent(cs, done, 0), "cudaStreamWaitEvent");
+    ck(cudaEventRecord(t1, cs), "cudaEventRecord");
     ck(cudaStreamSynchronize(down), "cudaStreamSynchronize");
+    ck(cudaEventSynchronize(t1), "cudaEventSynchronize");
+    float ms = 0.0f;  // copies + conversions + convolutions of the whole call
+    ck(cudaEventElapsedTime(&ms, t0, t1), "cudaEventElapsedTime");
+    hd.record_device_ms(ms);
     hd.counters() = saved;
     hd.counters() += hd.cached_build(p, solver, &cfg)->op_counters();
     hd.last_kernel = kernel;
+    hd.last_variant = variant;
 }
 
 void copy_name(char* buf, size_t len, const std::string& name) {
@@ -384,7 +397,7 @@ primkit_status primkit_conv_run(primkit_handle* h, const primkit_conv_problem* p
         primkit::upload_nchw(hd, da, need(a, "operand a"), dva);
         primkit::upload_nchw(hd, db, need(b, "operand b"), dvb);
         auto plan = hd.cached_build(p, solver, &cfg);
-        const size_t dws = plan->device_workspace_bytes();
+        const size_t dws = plan->device_workspace_bytes(hd.num_sms());
         void* ws = hd.scratch(0, dws);
         if (hd.device_timing())
             hd.record_device_ms(hd.time_ms([&] { plan->run(hd, dva, dvb, dvo, ws, dws); }));
@@ -583,7 +596,7 @@ primkit_status primkit_conv_device_workspace(primkit_handle* h, const primkit_co
         const primkit::ConvProblem p = to_problem(pp);
         const primkit::Solver& s = select_solver(h, p, solver_name);
         auto plan = H(h).cached_build(p, s, nullptr);
-        *need(out, "output") = plan->device_workspace_bytes();
+        *need(out, "output") = plan->device_workspace_bytes(H(h).num_sms());
     });
 }
 
@@ -612,7 +625,7 @@ primkit_status primkit_conv_bn_workspace(primkit_handle* h, const primkit_conv_p
         const primkit::ConvProblem p = to_problem(pp);
         const primkit::Solver& s = select_solver(h, p, solver_name);
         auto plan = H(h).cached_build(p, s, nullptr);
-        const std::size_t conv = (plan->device_workspace_bytes() + 255) / 256 * 256;
+        const std::size_t conv = (plan->device_workspace_bytes(H(h).num_sms()) + 255) / 256 * 256;
         *need(out, "output") = conv + conv_bn_stats_bytes(p);
     });
 }
@@ -649,7 +662,7 @@ primkit_status primkit_conv_bn_forward_train_device(
         auto plan = H(h).cached_build(p, s, nullptr);
         primkit::Handle& hd = H(h);
         hd.activate();
-        const std::size_t conv = (plan->device_workspace_bytes() + 255) / 256 * 256;
+        const std::size_t conv = (plan->device_workspace_bytes(hd.num_sms()) + 255) / 256 * 256;
         if (ws_bytes < conv + conv_bn_stats_bytes(p))
             primkit::throw_error(primkit::ErrorCode::WorkspaceTooSmall, "workspace below requested size");
         const primkit::ConvShapes sh = primkit::resolve_shapes(p.input_desc(), p.filter_desc(),
@@ -698,7 +711,7 @@ primkit_status primkit_conv_backward_data_bn_device(
         auto plan = H(h).cached_build(p, s, nullptr);
         primkit::Handle& hd = H(h);
         hd.activate();
-        const std::size_t conv = (plan->device_workspace_bytes() + 255) / 256 * 256;
+        const std::size_t conv = (plan->device_workspace_bytes(hd.num_sms()) + 255) / 256 * 256;
         if (ws_bytes < conv + conv_bn_stats_bytes(p))
             primkit::throw_error(primkit::ErrorCode::WorkspaceTooSmall, "workspace below requested size");
         const int n = (int)p.n, c = (int)p.c, hw = (int)(p.h * p.w);
@@ -1007,6 +1020,10 @@ primkit_status primkit_handle_last_device_ms(primkit_handle* h, double* out) {
 
 primkit_status primkit_handle_last_kernel(primkit_handle* h, char* buf, size_t len) {
     return guarded([&] { copy_name(buf, len, H(h).last_kernel); });
+}
+
+primkit_status primkit_handle_last_variant(primkit_handle* h, char* buf, size_t len) {
+    return guarded([&] { copy_name(buf, len, H(h).last_variant); });
 }
 
 }  // extern "C"

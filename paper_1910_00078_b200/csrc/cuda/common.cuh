@@ -13,6 +13,8 @@ namespace pk {
 
 // Process-wide count of kernels launched by this library (pk_cuda_launch_count).
 void count_launch(int n = 1);
+// Appends the kernel's template instance to the thread's variant log (pk_cuda_variant).
+void note_kernel(const void* fn);
 
 template <typename T>
 struct Elt;
@@ -405,6 +407,7 @@ cudaError_t pk_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    note_kernel(reinterpret_cast<const void*>(kern));
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 // Same with a runtime cluster size along x (CTA pairs for cta_group::2 kernels).
@@ -430,6 +433,7 @@ cudaError_t pk_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
+    note_kernel(reinterpret_cast<const void*>(kern));
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 

@@ -269,6 +269,10 @@ cudaError_t pk_cuda_bn_bwd(const void* x, const void* y, const void* dy, void* d
 
 // Launch accounting: number of kernels this library launched (process-wide).
 uint64_t pk_cuda_launch_count(void);
+// Kernel-variant log of the calling thread: the demangled template instance of
+// every kernel launched through pk_launch since the last reset, joined by '+'.
+void pk_cuda_variant_reset(void);
+const char* pk_cuda_variant(void);
 
 #ifdef __cplusplus
 }

@@ -1,7 +1,14 @@
 #include <cstdlib>
 // Layout conversion and pointwise kernels (HBM-bound; coalesced through a
 // shared-memory transpose tile, one pass over the data).
+#include <cxxabi.h>
+
+#include <cstring>
+
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
 #include <type_traits>
 
 #include "common.cuh"
@@ -10,6 +17,47 @@ namespace pk {
 
 static std::atomic<uint64_t> g_launches{0};
 void count_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+namespace {
+thread_local std::string t_variant;
+
+// "void pk::(anonymous namespace)::k<256, 6, true>(CUtensorMap, ...)" -> "k<256, 6, true>"
+std::string short_kernel_name(const void* fn) {
+    static std::mutex mu;
+    static std::map<const void*, std::string> memo;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = memo.find(fn);
+    if (it != memo.end()) return it->second;
+    const char* mangled = nullptr;
+    std::string name = "?";
+    if (cudaFuncGetName(&mangled, fn) == cudaSuccess && mangled) {
+        int status = 0;
+        char* dem = abi::__cxa_demangle(mangled, nullptr, nullptr, &status);
+        name = (status == 0 && dem) ? dem : mangled;
+        std::free(dem);
+        for (const char* drop : {"void ", "pk::", "(anonymous namespace)::"})
+            for (size_t at; (at = name.find(drop)) != std::string::npos;) name.erase(at, std::strlen(drop));
+        int depth = 0;  // cut the parameter list: the first '(' outside template brackets
+        for (size_t i = 0; i < name.size(); ++i) {
+            if (name[i] == '<') ++depth;
+            else if (name[i] == '>') --depth;
+            else if (name[i] == '(' && depth == 0) {
+                name.resize(i);
+                break;
+            }
+        }
+    } else {
+        cudaGetLastError();
+    }
+    memo.emplace(fn, name);
+    return name;
+}
+}  // namespace
+
+void note_kernel(const void* fn) {
+    if (!t_variant.empty()) t_variant += '+';
+    t_variant += short_kernel_name(fn);
+}
 
 // Split-K grid-barrier slots (zero-initialised at module load; every use
 // leaves its slot zeroed again).
@@ -214,6 +262,9 @@ inline unsigned grid_for(long long total, int threads = 256) {
 using namespace pk;
 
 extern "C" {
+
+void pk_cuda_variant_reset(void) { pk::t_variant.clear(); }
+const char* pk_cuda_variant(void) { return pk::t_variant.c_str(); }
 
 uint64_t pk_cuda_launch_count(void) { return g_launches.load(); }
 

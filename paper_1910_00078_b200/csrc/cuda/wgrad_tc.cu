@@ -281,13 +281,15 @@ cudaError_t pk_cuda_igemm_tc_wgrad(const pk_conv_geom* g, const void* dy, const 
     if (!tc::make_map_2d(&amap, dy, w.NPQ, g->y_pitch, g->y_pitch, BK)) return cudaErrorInvalidValue;
     constexpr int STAGES = 4;
     using L = WgSmem<STAGES>;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static int attr_dev = -1;  // the attribute is per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (attr_dev != dev) {
         cudaError_t err = cudaFuncSetAttribute(igemm_tc_wgrad_kernel<STAGES>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                L::kBytes);
         if (err != cudaSuccess) return err;
-        attr_set = true;
+        attr_dev = dev;
     }
     dim3 grid((w.K + BM - 1) / BM, (w.Nn + WBN - 1) / WBN, splits);
     igemm_tc_wgrad_kernel<STAGES><<<grid, kThreads, L::kBytes, st>>>(

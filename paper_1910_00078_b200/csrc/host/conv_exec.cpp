@@ -191,9 +191,9 @@ bool stem_fused(const pk_conv_geom& g, ConvDirection dir) {
                                               : pk_cuda_stem_fused_supported(&g) != 0;
 }
 
-std::size_t stem_workspace(const pk_conv_geom& g, ConvDirection dir) {
+std::size_t stem_workspace(const pk_conv_geom& g, ConvDirection dir, int num_sms) {
     if (stem_fused(g, dir))
-        return dir == ConvDirection::BackwardWeights ? pk_cuda_stem_fused_wgrad_workspace(&g, 148) : 0;
+        return dir == ConvDirection::BackwardWeights ? pk_cuda_stem_fused_wgrad_workspace(&g, num_sms) : 0;
     const std::size_t kcp = pk_stem_kc_pitch(&g);
     const std::size_t rows = (std::size_t)g.n * g.p * g.q;
     const std::size_t col = align256(rows * kcp * 2);
@@ -202,7 +202,7 @@ std::size_t stem_workspace(const pk_conv_geom& g, ConvDirection dir) {
         case ConvDirection::BackwardData: return col + align256(kcp * pk_pitch(g.k) * 2);
         default: {
             const pk_conv_geom wg = gemm_geom((long long)rows, (int)kcp, g.k);
-            return col + align256((std::size_t)g.k * kcp * 2) + pk_tc_wgrad_workspace(&wg, 148);
+            return col + align256((std::size_t)g.k * kcp * 2) + pk_tc_wgrad_workspace(&wg, num_sms);
         }
     }
 }
@@ -261,18 +261,24 @@ bool ConvPlan::fuses_stats() const {
     return false;
 }
 
-std::size_t ConvPlan::device_workspace_bytes() const {
+std::size_t ConvPlan::device_workspace_bytes(int num_sms) const {
+    // Every device buffer run() touches besides its operands comes out of the
+    // caller's workspace, so this mirrors run()'s dispatch exactly. Split-K
+    // partial counts scale with the SM count, hence the handle's num_sms.
     const pk_conv_geom g = make_geom(problem_);
     const int dt = dtype_of(problem_.etype);
     const std::size_t acc_rows = (std::size_t)g.p * g.q;
     const bool tc_algo = problem_.direction == ConvDirection::Forward
                              ? algo_ == ConvAlgo::ImplicitGemm
                              : algo_ == ConvAlgo::Im2colGemm;
-    if (tc_algo && stem_eligible(g, dt, nullptr)) return stem_workspace(g, problem_.direction);
+    if (tc_algo && stem_eligible(g, dt, nullptr)) return stem_workspace(g, problem_.direction, num_sms);
     switch (problem_.direction) {
         case ConvDirection::Forward:
             if (algo_ == ConvAlgo::FFT) return pk_cuda_fft_scratch_bytes(&g);
+            if (algo_ == ConvAlgo::Winograd && dt == PK_BF16 && pk_winograd_tc_supported(&g))
+                return winograd_ws(g, winograd_tile_m());
             if (algo_ == ConvAlgo::Im2colGemm) {
+                if (pk_depthwise_supported(&g) || pk_grouped_supported(&g)) return 0;
                 if (g.transpose)  // fp32 column matrix [(r,s,kk)][h*w]
                     return (std::size_t)g.r * g.s * g.f_pitch * g.h * g.w * 4;
                 return align256(col_bytes(g, dt)) + acc_rows * g.kg * 4;
@@ -280,13 +286,19 @@ std::size_t ConvPlan::device_workspace_bytes() const {
             return 0;
         case ConvDirection::BackwardData:
             if (algo_ == ConvAlgo::Im2colGemm) {
+                if (pk_depthwise_supported(&g) || pk_grouped_supported(&g)) return 0;
                 if (dt == PK_BF16 && pk_tc_dgrad_supported(&g)) return pk_tc_dgrad_workspace(&g);
                 return (std::size_t)g.p * g.q * g.r * g.s * g.f_pitch * 4;
             }
             return 0;
         case ConvDirection::BackwardWeights:
+            if (pk_depthwise_supported(&g)) return pk_depthwise_wgrad_workspace(&g, num_sms);
+            if (pk_grouped_wgrad_supported(&g)) return pk_grouped_wgrad_workspace(&g, num_sms);
+            if (algo_ == ConvAlgo::Direct)
+                return pk_direct_wgrad_tiled_supported(&g) ? pk_direct_wgrad_tiled_workspace(&g, num_sms)
+                                                           : 0;
             if (algo_ == ConvAlgo::Im2colGemm) {
-                if (dt == PK_BF16 && pk_tc_wgrad_supported(&g)) return pk_tc_wgrad_workspace(&g, 148);
+                if (dt == PK_BF16 && pk_tc_wgrad_supported(&g)) return pk_tc_wgrad_workspace(&g, num_sms);
                 return align256(col_bytes(g, dt)) + (std::size_t)g.k * g.r * g.s * g.f_pitch * 4;
             }
             return 0;
@@ -301,7 +313,7 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
     const int dt = dtype_of(problem_.etype);
     const std::size_t esz = dt == PK_BF16 ? 2 : 4;
     cudaStream_t st = h.stream();
-    if (ws_bytes < device_workspace_bytes())
+    if (ws_bytes < device_workspace_bytes(h.num_sms()))
         throw_error(ErrorCode::WorkspaceTooSmall, "workspace below requested size");
     auto ck = [](cudaError_t e, const char* what) { check_cuda(e, what); };
 
@@ -314,6 +326,7 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
         ck(cudaMemsetAsync(out, 0, (std::size_t)g.n * g.h * g.w * g.x_pitch * esz, st), "memset");
 
     const char* kernel = "?";
+    pk_cuda_variant_reset();
     if (dir == ConvDirection::Forward) {
         switch (algo_) {
             case ConvAlgo::Direct:
@@ -352,7 +365,7 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                     const int m = winograd_tile_m();
                     kernel = m == 4 ? "winograd_tc_f43" : "winograd_tc_f23";
                     const std::size_t wb = winograd_ws(g, m);
-                    ck(pk_cuda_winograd_tc(&g, m, a, b, out, epi, h.scratch(12, wb), wb, st),
+                    ck(pk_cuda_winograd_tc(&g, m, a, b, out, epi, ws, wb, st),
                        "winograd_tc");
                 } else {
                     kernel = "winograd_f23";
@@ -498,17 +511,17 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
         if (algo_ != ConvAlgo::Winograd && algo_ != ConvAlgo::FFT && pk_depthwise_supported(&g)) {
             kernel = "depthwise_simt_bwd_weights";
             const std::size_t wb = pk_depthwise_wgrad_workspace(&g, h.num_sms());
-            ck(pk_cuda_depthwise_wgrad(&g, dt, a, b, out, h.scratch(13, wb), wb, h.num_sms(), st),
+            ck(pk_cuda_depthwise_wgrad(&g, dt, a, b, out, ws, wb, h.num_sms(), st),
                "depthwise_wgrad");
         } else if (algo_ != ConvAlgo::Winograd && algo_ != ConvAlgo::FFT && pk_grouped_wgrad_supported(&g)) {
             kernel = "grouped_simt_bwd_weights";
             const std::size_t wb = pk_grouped_wgrad_workspace(&g, h.num_sms());
-            ck(pk_cuda_grouped_wgrad(&g, dt, a, b, out, h.scratch(13, wb), wb, h.num_sms(), st),
+            ck(pk_cuda_grouped_wgrad(&g, dt, a, b, out, ws, wb, h.num_sms(), st),
                "grouped_wgrad");
         } else if (algo_ == ConvAlgo::Direct && pk_direct_wgrad_tiled_supported(&g)) {
             kernel = "direct_simt_tiled_bwd_weights";
             const std::size_t wb = pk_direct_wgrad_tiled_workspace(&g, h.num_sms());
-            ck(pk_cuda_direct_wgrad_tiled(&g, dt, a, b, out, h.scratch(13, wb), wb, h.num_sms(), st),
+            ck(pk_cuda_direct_wgrad_tiled(&g, dt, a, b, out, ws, wb, h.num_sms(), st),
                "direct_wgrad_tiled");
         } else if (algo_ == ConvAlgo::Direct) {
             kernel = "direct_simt_bwd_weights";
@@ -539,6 +552,7 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
         }
     }
     h.last_kernel = kernel;
+    h.last_variant = pk_cuda_variant();
     h.counters() += counters_for(problem_, algo_);
 }
 

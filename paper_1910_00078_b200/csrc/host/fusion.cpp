@@ -486,7 +486,7 @@ void fusion_execute_unfused(Handle& h, FusionPlan& plan, const void* input, void
                     h.counters() += conv_counters(p, algo);
                 } else {
                     const ConvPlan cp(p, algo, {});
-                    const std::size_t dws = cp.device_workspace_bytes();
+                    const std::size_t dws = cp.device_workspace_bytes(h.num_sms());
                     cp.run(h, src, d.filter.get(), dst, h.scratch(0, dws), dws);
                 }
                 break;

@@ -101,9 +101,12 @@ void Handle::init_device(int device) {
     check_cuda(cudaSetDevice(device_), "cudaSetDevice");
     cudaDeviceProp prop{};
     check_cuda(cudaGetDeviceProperties(&prop, device_), "cudaGetDeviceProperties");
-    if (prop.major < 10)
-        throw std::runtime_error("primkit: device " + std::string(prop.name) +
-                                 " is not sm_100 (Blackwell); this build targets sm_100a only");
+    // sm_100a code (tcgen05, TMA, arch-specific PTX) runs on compute
+    // capability 10.0 only; any other device would fail at the first launch.
+    if (prop.major != 10 || prop.minor != 0)
+        throw std::runtime_error("primkit: device " + std::string(prop.name) + " is sm_" +
+                                 std::to_string(prop.major * 10 + prop.minor) +
+                                 "; this build targets sm_100a (B200) only");
     num_sms_ = prop.multiProcessorCount;
     check_cuda(cudaEventCreate(&ev0_), "cudaEventCreate");
     check_cuda(cudaEventCreate(&ev1_), "cudaEventCreate");
@@ -224,7 +227,7 @@ std::vector<ConvAlgoPerf> Handle::find_convolution(const ConvProblem& problem, c
         if (need > workspace_bytes) continue;
 
         auto plan = cached_build(problem, *solver, &config);
-        const std::size_t dws = plan->device_workspace_bytes();
+        const std::size_t dws = plan->device_workspace_bytes(num_sms());
         void* ws = scratch(0, dws);
         void* out = scratch(3, device_bytes(result_desc(problem)));
         std::vector<double> times;
@@ -287,7 +290,7 @@ TuneResult tune(Handle& handle, const Solver& solver, const ConvProblem& problem
     double best = -1.0;
     for (const auto& config : grid) {
         const ConvPlan plan = solver.build_plan(problem, &config);
-        const std::size_t dws = plan.device_workspace_bytes();
+        const std::size_t dws = plan.device_workspace_bytes(handle.num_sms());
         void* ws = handle.scratch(0, dws);
         result.evaluations += 1;
         std::vector<double> times;

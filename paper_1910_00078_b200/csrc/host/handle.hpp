@@ -107,6 +107,11 @@ public:
     // of timing-free events for the overlapped host-buffer path; lazily made.
     cudaStream_t copy_stream(int i);
     cudaEvent_t event(int i);
+    // The two timing-enabled events time_ms() uses (0: start, 1: stop).
+    cudaEvent_t timing_event(int i) {
+        activate();
+        return i ? ev1_ : ev0_;
+    }
 
     // Times `fn` (one enqueue of device work) in ms: CUDA events on the
     // handle's stream, or the injected clock.
@@ -114,6 +119,9 @@ public:
     void record_device_ms(double ms) { last_device_ms_ = ms; }
     double last_device_ms() const { return last_device_ms_; }
     std::string last_kernel;
+    // Template instances of the kernels the last conv run launched, in launch
+    // order ("conv_tma_fprop_kernel<256, 6, false, false, 1, true>+...").
+    std::string last_variant;
 
     static constexpr int kWarmupRuns = 1;
     static constexpr int kTimedRuns = 5;

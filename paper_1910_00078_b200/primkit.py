@@ -292,6 +292,11 @@ class Handle:
         self._c("primkit_handle_last_kernel", buf, 128)
         return buf.value.decode()
 
+    def last_variant(self) -> str:
+        buf = C.create_string_buffer(1024)
+        self._c("primkit_handle_last_variant", buf, 1024)
+        return buf.value.decode()
+
 
 class FusionPlan:
     def __init__(self, lib: Library, dims, etype=abi.F32):

@@ -170,3 +170,59 @@ def test_oracle_matches_live_reference(ref):
             got = {abi.FORWARD: oracle.conv_forward, abi.BACKWARD_DATA: oracle.conv_backward_data,
                    abi.BACKWARD_WEIGHTS: oracle.conv_backward_weights}[d](p, a, b)
             assert np.array_equal(got, want), (shp, d)
+
+
+def _to_dev(a, pitch):
+    """NCHW f32 -> NHWC with channel pitch (zero pad lanes)."""
+    n, c, h, w = a.shape
+    out = np.zeros((n, h, w, pitch), np.float32)
+    out[..., :c] = a.transpose(0, 2, 3, 1)
+    return out
+
+
+def _bits(a):
+    return np.ascontiguousarray((oracle.round_bf16(a).view(np.uint32) >> 16).astype(np.uint16))
+
+
+@pytest.mark.parametrize("cfg", [
+    dict(n=2, c=5, h=9, w=7, k=6, y=3, x=3, pad=1),
+    dict(n=2, c=16, h=11, w=11, k=8, y=3, x=3, pad=1, stride=2),
+    dict(n=1, c=3, h=15, w=15, k=8, y=7, x=7, pad=3, stride=2),
+    dict(n=2, c=8, h=8, w=8, k=16, y=1, x=1, stride=2),
+    dict(n=1, c=8, h=9, w=9, k=8, y=3, x=3, pad=2, dilation=2),
+])
+@pytest.mark.parametrize("bf16", [False, True])
+def test_sampled_formulas_match_full_oracle(cfg, bf16):
+    """The device-layout sampled formulas (used for full-size GPU parity) give
+    the full restated oracle's values at every coordinate."""
+    from paper_1910_00078_b200.primkit import problem
+    rng = np.random.default_rng(5)
+    p = problem(**cfg)
+    oh, ow = oracle.out_hw(p)
+    x = oracle.round_bf16(rng.uniform(-1, 1, (p.n, p.c, p.h, p.w)).astype(np.float32))
+    w = oracle.round_bf16(rng.uniform(-1, 1, (p.k, p.c, p.y, p.x)).astype(np.float32))
+    dy = oracle.round_bf16(rng.uniform(-1, 1, (p.n, p.k, oh, ow)).astype(np.float32))
+    pit = lambda c: (c + 7) // 8 * 8  # noqa: E731
+    xd, dyd = _to_dev(x, pit(p.c)), _to_dev(dy, pit(p.k))
+    wd = _to_dev(w, pit(p.c))  # [K][R][S][pitch C]
+    conv = (lambda a: _bits(a)) if bf16 else (lambda a: np.ascontiguousarray(a, np.float32))
+    xd, dyd, wd = conv(xd), conv(dyd), conv(wd)
+
+    y = oracle.conv_ref_f64(p, x, w)
+    idx = np.array([(n, k, i, j) for n in range(p.n) for k in range(p.k) for i in range(oh)
+                    for j in range(ow)], np.int64)
+    got = oracle.sample_forward(p, xd, wd, idx, bf16)
+    np.testing.assert_allclose(got, y[idx[:, 0], idx[:, 1], idx[:, 2], idx[:, 3]], rtol=1e-9, atol=1e-9)
+
+    dx = oracle.conv_backward_data(p, dy, w).astype(np.float64)
+    idx = np.array([(n, c, i, j) for n in range(p.n) for c in range(p.c) for i in range(p.h)
+                    for j in range(p.w)], np.int64)
+    got = oracle.sample_backward_data(p, dyd, wd, idx, bf16)
+    np.testing.assert_allclose(got, dx[idx[:, 0], idx[:, 1], idx[:, 2], idx[:, 3]], rtol=1e-5, atol=1e-5)
+
+    dw = oracle.conv_backward_weights(p, dy, x).astype(np.float64)
+    taps = np.array([(r, s, c) for r in range(p.y) for s in range(p.x) for c in range(p.c)], np.int64)
+    ks = np.arange(p.k)
+    got = oracle.sample_backward_weights(p, dyd, xd, ks, taps, bf16)
+    want = dw[ks][:, taps[:, 2], taps[:, 0], taps[:, 1]]
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-4)
