@@ -213,9 +213,13 @@ class Net:
                 probs[d] = (p, solver.encode())
             self.items.append((L, x, w, y, dy, dx, dw, probs))
         self.ws = torch.empty(max(max_ws, 256), dtype=torch.uint8, device=device)
-        # one flat bf16 dW bucket (23.45 M conv parameters) -> one all-reduce
-        from paper_1910_00078_b200.dist import GradBucket
-        self.bucket = GradBucket(torch, [it[6] for it in self.items])
+
+    def register_grads(self, dp):
+        """dW tensors in the order the backward pass produces them (reverse
+        layer order) -> native NCCL buckets."""
+        from paper_1910_00078_b200 import abi
+        for it in reversed(self.items):
+            dp.register(it[6], abi.BF16)
 
     def flops(self) -> float:
         return 3.0 * sum(L.flops(self.n) for L in self.layers)
@@ -236,21 +240,27 @@ def run_conv(lib, handle, p, solver, a, b, out, ws):
         lib.check(st)
 
 
-def step(lib, handle, net, directions=(0, 1, 2), dist=None, torch=None):
+def step(lib, handle, net, directions=(0, 1, 2), dp=None):
+    """One training step's convolutions. With a data-parallel context, each
+    layer's dW is handed to the native NCCL buckets (primkit_dp_*) right after
+    its backward-weights kernel is enqueued, so a bucket's all-reduce overlaps
+    the backward of the layers below it; finish() joins before the step ends."""
     ws = net.ws
     if 0 in directions:
         for (L, x, w, y, dy, dx, dw, probs) in net.items:
             p, s = probs[0]
             run_conv(lib, handle, p, s, x, w, y, ws)
-    for (L, x, w, y, dy, dx, dw, probs) in reversed(net.items):
+    for i, (L, x, w, y, dy, dx, dw, probs) in enumerate(reversed(net.items)):
         if 1 in directions:
             p, s = probs[1]
             run_conv(lib, handle, p, s, dy, w, dx, ws)
         if 2 in directions:
             p, s = probs[2]
             run_conv(lib, handle, p, s, dy, x, dw, ws)
-    if dist is not None:
-        net.bucket.allreduce(dist)  # pack -> one NCCL all-reduce -> unpack
+            if dp is not None:
+                dp.ready(i)
+    if dp is not None:
+        dp.finish()
 
 
 def time_region(torch, fn, iters):
@@ -460,6 +470,43 @@ def layer_report(torch, lib, handle, net, peaks, path):
               file=sys.stderr)
 
 
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(nproc: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-run this script under
+    torch.distributed.run with N local ranks (one process per GPU) and
+    return its exit code; rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)]
+    return subprocess.call(cmd + sys.argv[1:], env=dict(os.environ, PK_BENCH_SPAWNED="1"))
+
+
+def launch_selftest(args) -> int:
+    """--launch-selftest: the multi-rank plumbing without a GPU (gloo):
+    world size, rank-0 reduction of per-rank values (as the timing uses)."""
+    import torch
+    import torch.distributed as tdist
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"world size {world} != --gpus {args.gpus}", file=sys.stderr)
+        return 3
+    tdist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)])
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"launch_selftest": True, "n_gpus": world, "max_over_ranks": float(t.item())}),
+              flush=True)
+    tdist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--layer-report", default=None, help="write per-layer timings (JSON)")
@@ -472,8 +519,17 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="skip e2e/cpu/fusion legs")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch the step eagerly instead of as one CUDA graph")
+    ap.add_argument("--bucket-mb", type=float, default=25.0, help="fp32 MiB per dW all-reduce bucket")
+    ap.add_argument("--dp", action="store_true",
+                    help="use the NCCL dW buckets even at one GPU (overhead measurement)")
+    ap.add_argument("--launch-selftest", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
+    if args.launch_selftest:
+        return launch_selftest(args)
 
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -485,6 +541,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     dist = None
@@ -505,29 +563,38 @@ def main():
 
     layers = resnet50_layers()
     net = Net(torch, lib, handle, layers, args.batch, device)
+    dp = None
+    if world > 1 or args.dp:
+        from paper_1910_00078_b200.dist import DataParallel
+        dp = DataParallel(lib, handle.ptr, rank, world, dist=dist,
+                          bucket_bytes=int(args.bucket_mb * (1 << 20)))
+        net.register_grads(dp)
     if args.layer_report:
         layer_report(torch, lib, handle, net, load_peaks()[0], args.layer_report)
         return 0
     for _ in range(args.warmup):
-        step(lib, handle, net, dist=dist)
+        step(lib, handle, net, dp=dp)
     torch.cuda.synchronize()
+    if dp is not None:
+        dp.check()
     if dist:
         dist.barrier()
 
     launches0 = C.c_uint64()
     lib.check(lib.lib.primkit_handle_kernel_launches(handle.ptr, C.byref(launches0)))
-    run_step = lambda: step(lib, handle, net, dist=dist)  # noqa: E731
+    run_step = lambda: step(lib, handle, net, dp=dp)  # noqa: E731
     graph_note = "eager launches"
     launches_per_step = None
     if args.graph:
-        # The step's 159 conv launches (+ the dW all-reduce) replayed as one CUDA
+        # The step's 159 conv launches (+ the dW bucket all-reduces on the comm
+        # stream, forked and joined inside the capture) replayed as one CUDA
         # graph: same kernels, same work, no per-launch host overhead.
         try:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph):
                 lib.check(lib.lib.primkit_handle_set_stream(
                     handle.ptr, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
-                step(lib, handle, net)  # the 159 convolutions
+                step(lib, handle, net, dp=dp)  # the 159 convolutions (+ NCCL buckets)
             lib.check(lib.lib.primkit_handle_set_stream(handle.ptr, C.c_void_p(stream.cuda_stream)))
             lc = C.c_uint64()
             lib.check(lib.lib.primkit_handle_kernel_launches(handle.ptr, C.byref(lc)))
@@ -536,18 +603,18 @@ def main():
             graph.replay()
             torch.cuda.synchronize()
 
-            def run_step():
-                graph.replay()
-                if dist is not None:  # dW all-reduce stays an eager NCCL call
-                    net.bucket.allreduce(dist)
+            run_step = graph.replay
             graph_note = ("CUDA graph of the step's convolutions" +
-                          (" + eager NCCL dW all-reduce" if dist is not None else ""))
+                          (" + NCCL dW bucket all-reduces (comm stream, captured)"
+                           if dp is not None else ""))
         except Exception as exc:  # fall back to eager launches
             lib.check(lib.lib.primkit_handle_set_stream(handle.ptr, C.c_void_p(stream.cuda_stream)))
             graph_note = f"eager launches (graph capture failed: {exc})"
     clocks = ClockSampler(local)
     ms_total = time_region(torch, run_step, args.steps)
     clk = clocks.stop()
+    if dp is not None:
+        dp.check()
     launches1 = C.c_uint64()
     lib.check(lib.lib.primkit_handle_kernel_launches(handle.ptr, C.byref(launches1)))
     if launches_per_step is not None:
@@ -622,7 +689,9 @@ def main():
                                    "bf16, NHWC device layout",
                        "model": "ResNet-50 conv layers", "global_batch": args.batch * world,
                        "per_gpu_batch": args.batch, "parallelism": f"dp{world}",
-                       "dw_allreduce": "NCCL all_reduce, one bf16 bucket" if world > 1 else None,
+                       "dw_allreduce": (f"native NCCL fp32 sum, {dp.buckets()} buckets of <= "
+                                        f"{args.bucket_mb:g} MiB in backward order, comm stream "
+                                        "overlapped with the remaining backward") if dp else None,
                        "l2": "working set per step >> 126 MB L2 (no flush needed)",
                        "launch": graph_note},
             "gpu_launches": int(launches1.value - launches0.value),
@@ -630,6 +699,8 @@ def main():
         }
         line.update(extras)
         print(json.dumps(line), flush=True)
+    if dp is not None:
+        dp.close()
     if dist:
         dist.barrier()
         dist.destroy_process_group()

@@ -340,6 +340,38 @@ PRIMKIT_API primkit_status primkit_handle_last_kernel(primkit_handle* handle, ch
 PRIMKIT_API primkit_status primkit_handle_last_variant(primkit_handle* handle, char* buf,
                                                       size_t buf_len);
 
+/* ---- 3. data-parallel weight-gradient all-reduce (north_star) ----
+ * One process per GPU, the batch sharded over them. Backward-weights results
+ * are registered in the order the backward pass produces them (reverse layer
+ * order) and grouped into fp32 buckets; when the last gradient of a bucket is
+ * marked ready, the bucket is all-reduced with NCCL (sum, optional 1/world
+ * average) on an internal comm stream gated by an event on the handle's
+ * stream, so it overlaps the remaining backward kernels. finish() makes the
+ * handle's stream wait for all buckets. All work is stream-ordered and can be
+ * captured into a CUDA graph. While a dp context exists, grid-wide barriers
+ * inside the convolution kernels are disabled (the collective occupies SMs).
+ * NCCL is loaded at run time (libnccl.so.2). No reference counterpart: the
+ * reference is a single-process CPU library. */
+#define PRIMKIT_DP_UNIQUE_ID_BYTES 128
+typedef struct primkit_dp primkit_dp;
+
+PRIMKIT_API primkit_status primkit_dp_unique_id(uint8_t id[PRIMKIT_DP_UNIQUE_ID_BYTES]);
+PRIMKIT_API primkit_status primkit_dp_create(primkit_handle* handle,
+                                             const uint8_t id[PRIMKIT_DP_UNIQUE_ID_BYTES],
+                                             int nranks, int rank, int average, primkit_dp** out);
+PRIMKIT_API void primkit_dp_destroy(primkit_dp* dp);
+/* Target fp32 bytes per bucket (default 25 MiB); before the first grad_ready. */
+PRIMKIT_API primkit_status primkit_dp_set_bucket_bytes(primkit_dp* dp, uint64_t bytes);
+PRIMKIT_API primkit_status primkit_dp_register(primkit_dp* dp, void* grad, uint64_t elems,
+                                               primkit_element_type etype, int* out_index);
+PRIMKIT_API primkit_status primkit_dp_grad_ready(primkit_dp* dp, int index);
+PRIMKIT_API primkit_status primkit_dp_finish(primkit_dp* dp);
+/* Polls NCCL for an asynchronous error; on one, aborts the communicator and
+ * returns PRIMKIT_STATUS_INTERNAL with the NCCL message. */
+PRIMKIT_API primkit_status primkit_dp_check(primkit_dp* dp);
+PRIMKIT_API primkit_status primkit_dp_buckets(primkit_dp* dp, int* out_count);
+PRIMKIT_API primkit_status primkit_dp_bucket_of(primkit_dp* dp, int index, int* out_bucket);
+
 #ifdef __cplusplus
 }
 #endif

@@ -116,6 +116,17 @@ SECTION2 = {
     "primkit_handle_last_device_ms": (ST, [P, C.POINTER(C.c_double)]),
     "primkit_handle_last_kernel": (ST, [P, C.c_char_p, C.c_size_t]),
     "primkit_handle_last_variant": (ST, [P, C.c_char_p, C.c_size_t]),
+    # section 3: data-parallel all-reduce
+    "primkit_dp_unique_id": (ST, [C.c_char_p]),
+    "primkit_dp_create": (ST, [P, C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(P)]),
+    "primkit_dp_destroy": (None, [P]),
+    "primkit_dp_set_bucket_bytes": (ST, [P, C.c_uint64]),
+    "primkit_dp_register": (ST, [P, P, C.c_uint64, C.c_int, C.POINTER(C.c_int)]),
+    "primkit_dp_grad_ready": (ST, [P, C.c_int]),
+    "primkit_dp_finish": (ST, [P]),
+    "primkit_dp_check": (ST, [P]),
+    "primkit_dp_buckets": (ST, [P, C.POINTER(C.c_int)]),
+    "primkit_dp_bucket_of": (ST, [P, C.c_int, C.POINTER(C.c_int)]),
 }
 
 

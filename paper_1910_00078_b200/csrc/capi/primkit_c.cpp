@@ -16,6 +16,7 @@
 #include <string>
 
 #include "../cuda/kernels.h"
+#include "../host/dp.hpp"
 #include "../host/fusion.hpp"
 #include "../host/handle.hpp"
 
@@ -221,6 +222,11 @@ struct primkit_handle {
 
 struct primkit_fusion_plan {
     primkit::FusionPlan impl;
+};
+
+struct primkit_dp {
+    primkit::DataParallel* impl = nullptr;
+    ~primkit_dp() { primkit::dp_destroy(impl); }
 };
 
 namespace {
@@ -1024,6 +1030,61 @@ primkit_status primkit_handle_last_kernel(primkit_handle* h, char* buf, size_t l
 
 primkit_status primkit_handle_last_variant(primkit_handle* h, char* buf, size_t len) {
     return guarded([&] { copy_name(buf, len, H(h).last_variant); });
+}
+
+// ---- section 3: data-parallel gradient all-reduce ---------------------------
+
+static primkit::DataParallel& DP(primkit_dp* d) {
+    if (!d || !d->impl) primkit::throw_error(primkit::ErrorCode::InvalidValue, "null dp context");
+    return *d->impl;
+}
+
+primkit_status primkit_dp_unique_id(uint8_t id[PRIMKIT_DP_UNIQUE_ID_BYTES]) {
+    return guarded([&] { primkit::dp_unique_id(need(id, "id")); });
+}
+
+primkit_status primkit_dp_create(primkit_handle* h, const uint8_t id[PRIMKIT_DP_UNIQUE_ID_BYTES],
+                                 int nranks, int rank, int average, primkit_dp** out) {
+    return guarded([&] {
+        need(out, "dp output");
+        auto d = std::make_unique<primkit_dp>();
+        d->impl = primkit::dp_create(H(h), need(id, "id"), nranks, rank, average != 0);
+        *out = d.release();
+    });
+}
+
+void primkit_dp_destroy(primkit_dp* dp) { delete dp; }
+
+primkit_status primkit_dp_set_bucket_bytes(primkit_dp* dp, uint64_t bytes) {
+    return guarded([&] { primkit::dp_set_bucket_bytes(DP(dp), bytes); });
+}
+
+primkit_status primkit_dp_register(primkit_dp* dp, void* grad, uint64_t elems,
+                                   primkit_element_type etype, int* out_index) {
+    return guarded([&] {
+        const int i = primkit::dp_add(DP(dp), grad, elems, static_cast<primkit::ElementType>(etype));
+        if (out_index) *out_index = i;
+    });
+}
+
+primkit_status primkit_dp_grad_ready(primkit_dp* dp, int index) {
+    return guarded([&] { primkit::dp_ready(DP(dp), index); });
+}
+
+primkit_status primkit_dp_finish(primkit_dp* dp) {
+    return guarded([&] { primkit::dp_finish(DP(dp)); });
+}
+
+primkit_status primkit_dp_check(primkit_dp* dp) {
+    return guarded([&] { primkit::dp_check(DP(dp)); });
+}
+
+primkit_status primkit_dp_buckets(primkit_dp* dp, int* out_count) {
+    return guarded([&] { *need(out_count, "output") = primkit::dp_bucket_count(DP(dp)); });
+}
+
+primkit_status primkit_dp_bucket_of(primkit_dp* dp, int index, int* out_bucket) {
+    return guarded([&] { *need(out_bucket, "output") = primkit::dp_bucket_of(DP(dp), index); });
 }
 
 }  // extern "C"

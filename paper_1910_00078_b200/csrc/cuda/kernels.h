@@ -267,6 +267,27 @@ cudaError_t pk_cuda_bn_bwd(const void* x, const void* y, const void* dy, void* d
                            float* dbeta, int relu, int round_params_bf16, void* scratch,
                            cudaStream_t st);
 
+// ---- data-parallel gradient buckets (dp.cu) -----------------------------------
+// One gradient tensor inside an fp32 bucket: device pointer, element count,
+// element type (pk_dtype) and its element offset in the bucket.
+typedef struct pk_dp_seg {
+    void* ptr;
+    long long elems;
+    long long offset;
+    int dtype;
+    int pad_;
+} pk_dp_seg;
+// bucket[seg.offset + i] = float(seg.ptr[i]) for every segment (segs in device memory).
+cudaError_t pk_cuda_dp_pack(const pk_dp_seg* segs_dev, int nseg, long long max_elems, float* bucket,
+                            cudaStream_t st);
+// seg.ptr[i] = dtype(bucket[seg.offset + i] * scale) (RNE for bf16).
+cudaError_t pk_cuda_dp_unpack(const pk_dp_seg* segs_dev, int nseg, long long max_elems,
+                              const float* bucket, float scale, cudaStream_t st);
+// Grid-wide barriers (the in-kernel split-K finish) need every CTA of a grid
+// co-resident; with a collective running concurrently on other SMs that no
+// longer holds, so the data-parallel layer turns them off (process-wide).
+void pk_cuda_allow_grid_barriers(int on);
+
 // Launch accounting: number of kernels this library launched (process-wide).
 uint64_t pk_cuda_launch_count(void);
 // Kernel-variant log of the calling thread: the demangled template instance of

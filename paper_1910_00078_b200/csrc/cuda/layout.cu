@@ -63,7 +63,10 @@ void note_kernel(const void* fn) {
 // leaves its slot zeroed again).
 __device__ unsigned int g_splitk_sync[64][2];
 
+static std::atomic<bool> g_grid_barriers{true};
+
 unsigned int* splitk_sync_slot() {
+    if (!g_grid_barriers.load(std::memory_order_relaxed)) return nullptr;
     static unsigned int* base = [] {
         void* p = nullptr;
         if (std::getenv("PK_SPLITK_FUSE") && std::getenv("PK_SPLITK_FUSE")[0] == '0') return (unsigned int*)nullptr;
@@ -264,6 +267,7 @@ using namespace pk;
 extern "C" {
 
 void pk_cuda_variant_reset(void) { pk::t_variant.clear(); }
+void pk_cuda_allow_grid_barriers(int on) { pk::g_grid_barriers.store(on != 0); }
 const char* pk_cuda_variant(void) { return pk::t_variant.c_str(); }
 
 uint64_t pk_cuda_launch_count(void) { return g_launches.load(); }

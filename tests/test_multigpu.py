@@ -82,3 +82,36 @@ def test_sharded_dw_allreduce_matches_full_batch():
         p.join(timeout=120)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=5) <= 1e-5
+
+
+def test_bench_spawns_ranks_for_gpus_flag():
+    """`bench.py --gpus 2` without a launcher re-runs itself under
+    torch.distributed.run with 2 ranks (world size asserted == --gpus) and
+    rank 0 prints the reduced line (gloo self-test, no GPU needed)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2",
+                          "--launch-selftest"], capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(line) for line in out.stdout.splitlines() if line.startswith("{")]
+    assert lines == [{"launch_selftest": True, "n_gpus": 2, "max_over_ranks": 2.0}]
+
+
+def test_grad_bucket_reduces_in_fp32():
+    """The bucket sums bf16 gradients in fp32 (one rounding at unpack), not in
+    bf16 (error growing with world size)."""
+    import torch
+    from paper_1910_00078_b200.dist import GradBucket
+    t = [torch.tensor([1.0, 256.0], dtype=torch.bfloat16), torch.tensor([3.0], dtype=torch.float32)]
+    b = GradBucket(torch, t)
+    assert b.flat.dtype == torch.float32
+
+    class _Sum8:  # stands in for an 8-rank sum of identical shards
+        @staticmethod
+        def all_reduce(x, group=None):
+            x.mul_(8)
+    b.allreduce(_Sum8)
+    assert t[0].tolist() == [8.0, 2048.0] and t[1].tolist() == [24.0]
