@@ -333,6 +333,11 @@ PRIMKIT_API primkit_status primkit_handle_last_device_ms(primkit_handle* handle,
  * (e.g. "igemm_tc_fwd", "direct_simt"). */
 PRIMKIT_API primkit_status primkit_handle_last_kernel(primkit_handle* handle, char* buf,
                                                      size_t buf_len);
+/* Plan-cache counters of the handle (reference PlanCache::Stats,
+ * proj/src/core/plan_cache.hpp): plans built, memory hits, disk hits. */
+PRIMKIT_API primkit_status primkit_handle_plan_cache_stats(primkit_handle* handle, uint64_t* builds,
+                                                          uint64_t* memory_hits,
+                                                          uint64_t* disk_hits);
 /* Template instances of the tensor-core kernels the last conv run launched,
  * in launch order, joined by '+' (e.g.
  * "conv_tma_fprop_kernel<256, 6, false, false, 1, true>"); empty for the

@@ -116,6 +116,8 @@ SECTION2 = {
     "primkit_handle_last_device_ms": (ST, [P, C.POINTER(C.c_double)]),
     "primkit_handle_last_kernel": (ST, [P, C.c_char_p, C.c_size_t]),
     "primkit_handle_last_variant": (ST, [P, C.c_char_p, C.c_size_t]),
+    "primkit_handle_plan_cache_stats": (ST, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                             C.POINTER(C.c_uint64)]),
     # section 3: data-parallel all-reduce
     "primkit_dp_unique_id": (ST, [C.c_char_p]),
     "primkit_dp_create": (ST, [P, C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(P)]),

@@ -1032,6 +1032,16 @@ primkit_status primkit_handle_last_variant(primkit_handle* h, char* buf, size_t 
     return guarded([&] { copy_name(buf, len, H(h).last_variant); });
 }
 
+primkit_status primkit_handle_plan_cache_stats(primkit_handle* h, uint64_t* builds,
+                                              uint64_t* memory_hits, uint64_t* disk_hits) {
+    return guarded([&] {
+        const auto st = H(h).plan_cache().stats();
+        *need(builds, "output") = st.builds;
+        *need(memory_hits, "output") = st.memory_hits;
+        *need(disk_hits, "output") = st.disk_hits;
+    });
+}
+
 // ---- section 3: data-parallel gradient all-reduce ---------------------------
 
 static primkit::DataParallel& DP(primkit_dp* d) {

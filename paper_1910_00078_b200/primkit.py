@@ -292,6 +292,19 @@ class Handle:
         self._c("primkit_handle_last_kernel", buf, 128)
         return buf.value.decode()
 
+    def plan_cache_stats(self) -> tuple[int, int, int]:
+        """(builds, memory_hits, disk_hits) of the handle's plan cache."""
+        v = [C.c_uint64() for _ in range(3)]
+        self._c("primkit_handle_plan_cache_stats", *[C.byref(x) for x in v])
+        return tuple(x.value for x in v)
+
+    def device_workspace(self, p, solver: str | None) -> int:
+        """Device scratch of the plan for (p, solver); one cached_build."""
+        v = C.c_uint64()
+        self._c("primkit_conv_device_workspace", C.byref(p), None if solver is None else solver.encode(),
+                C.byref(v))
+        return v.value
+
     def last_variant(self) -> str:
         buf = C.create_string_buffer(1024)
         self._c("primkit_handle_last_variant", buf, 1024)
