@@ -314,6 +314,54 @@ PRIMKIT_API primkit_status primkit_activation_backward(primkit_handle* handle,
                                                        const float* x, const float* dy,
                                                        float* dx);
 
+/* Pooling (reference primitives.hpp:65-86, primitives.cpp:204-310). window,
+ * pad, stride are {h, w}; dims the NCHW input. Max keeps the first maximum in
+ * window scan order; indices receive its linear NCHW input offset (-1 for an
+ * empty window, and everywhere for average pooling); average divides by the
+ * number of valid (unpadded) taps. Host variants take packed NCHW floats and
+ * indices in NCHW output order; device variants take the device layout
+ * (NHWC, channel pitch) with indices [N][OH][OW][C]. Backward is computed as
+ * a deterministic gather that reproduces the reference's accumulation order. */
+typedef enum { PRIMKIT_POOL_MAX = 0, PRIMKIT_POOL_AVG = 1 } primkit_pooling_kind;
+PRIMKIT_API primkit_status primkit_pooling_output_dims(const int64_t window[2], const int64_t pad[2],
+                                                       const int64_t stride[2], const int64_t dims[4],
+                                                       int64_t out_dims[4]);
+PRIMKIT_API primkit_status primkit_pooling_forward(primkit_handle* handle, primkit_pooling_kind kind,
+                                                   const int64_t window[2], const int64_t pad[2],
+                                                   const int64_t stride[2], const int64_t dims[4],
+                                                   primkit_element_type etype, const float* x, float* y,
+                                                   int64_t* indices);
+PRIMKIT_API primkit_status primkit_pooling_backward(primkit_handle* handle, primkit_pooling_kind kind,
+                                                    const int64_t window[2], const int64_t pad[2],
+                                                    const int64_t stride[2], const int64_t dims[4],
+                                                    primkit_element_type etype, const float* dy,
+                                                    const int64_t* indices, float* dx);
+PRIMKIT_API primkit_status primkit_pooling_forward_device(
+    primkit_handle* handle, primkit_pooling_kind kind, const int64_t window[2], const int64_t pad[2],
+    const int64_t stride[2], const int64_t dims[4], primkit_element_type etype, const void* x, void* y,
+    int64_t* indices);
+PRIMKIT_API primkit_status primkit_pooling_backward_device(
+    primkit_handle* handle, primkit_pooling_kind kind, const int64_t window[2], const int64_t pad[2],
+    const int64_t stride[2], const int64_t dims[4], primkit_element_type etype, const void* dy,
+    const int64_t* indices, void* dx);
+
+/* Softmax along `axis` of a packed rank-`rank` tensor (reference
+ * primitives.hpp:88-91, primitives.cpp:312-370): max-stabilised, denominator
+ * and backward dot product in double. INVALID_AXIS for an axis out of range. */
+PRIMKIT_API primkit_status primkit_softmax_forward(primkit_handle* handle, int rank, const int64_t* dims,
+                                                   primkit_element_type etype, int64_t axis,
+                                                   const float* x, float* y);
+PRIMKIT_API primkit_status primkit_softmax_backward(primkit_handle* handle, int rank, const int64_t* dims,
+                                                    primkit_element_type etype, int64_t axis,
+                                                    const float* y, const float* dy, float* dx);
+PRIMKIT_API primkit_status primkit_softmax_forward_device(primkit_handle* handle, int rank,
+                                                          const int64_t* dims, primkit_element_type etype,
+                                                          int64_t axis, const void* x, void* y);
+PRIMKIT_API primkit_status primkit_softmax_backward_device(primkit_handle* handle, int rank,
+                                                           const int64_t* dims, primkit_element_type etype,
+                                                           int64_t axis, const void* y, const void* dy,
+                                                           void* dx);
+
 /* Layout converters used by the host ABI, exposed for device callers:
  * packed NCHW f32 (device memory) <-> device NHWC layout of `etype`. */
 PRIMKIT_API primkit_status primkit_nchw_to_device(primkit_handle* handle, const int64_t dims[4],

@@ -38,9 +38,9 @@ def build(force: bool = False) -> None:
     if force or not os.path.exists(RESTATED_SO) or os.path.getmtime(src) > os.path.getmtime(RESTATED_SO):
         subprocess.check_call(["gcc", "-O3", "-fopenmp", "-fPIC", "-shared", "-o", RESTATED_SO, src,
                                "-lm"])
-    if os.path.isdir(REF_SOURCES) and (force or not os.path.exists(REF_SO)):
+    if os.path.isdir(REF_SOURCES):  # make is incremental (shim / source timestamps)
         subprocess.check_call(["make", "-s", "-f", os.path.join(_HERE, "Makefile.ref"),
-                               f"-j{os.cpu_count() or 4}"])
+                               f"-j{os.cpu_count() or 4}"] + (["-B"] if force else []))
 
 
 class _ConvP(C.Structure):
@@ -269,6 +269,97 @@ def bn_stats_device(x, c, eps=1e-5, bf16=True):
                                C.c_int64(pitch), C.c_int64(int(bf16)), C.c_float(eps), _vp(mean),
                                _vp(inv), _vp(var))
     return mean, inv, var
+
+
+# ---- pooling / softmax (primitives.cpp:204-370) --------------------------------
+
+_I64 = C.POINTER(C.c_int64)
+
+
+def _i64(a):
+    return (C.c_int64 * len(a))(*[int(v) for v in a])
+
+
+def pool_out_hw(dims, win, pad, stride):
+    return ((dims[2] + 2 * pad[0] - win[0]) // stride[0] + 1, (dims[3] + 2 * pad[1] - win[1]) // stride[1] + 1)
+
+
+def pool_forward(kind, x, win, pad, stride, bf16=False):
+    """(y, indices) of the restated reference pooling (kind 0 max, 1 avg)."""
+    x = np.ascontiguousarray(x, np.float32)
+    oh, ow = pool_out_hw(x.shape, win, pad, stride)
+    y = np.zeros((x.shape[0], x.shape[1], oh, ow), np.float32)
+    idx = np.zeros(y.shape, np.int64)
+    restated().oc_pool_fwd(kind, _i64(x.shape), _i64(win), _i64(pad), _i64(stride), _fp(x), _fp(y),
+                           idx.ctypes.data_as(_I64), int(bf16))
+    return y, idx
+
+
+def pool_backward(kind, in_dims, dy, idx, win, pad, stride, bf16=False):
+    dy = np.ascontiguousarray(dy, np.float32)
+    idx = np.ascontiguousarray(idx, np.int64)
+    dx = np.zeros(in_dims, np.float32)
+    restated().oc_pool_bwd(kind, _i64(in_dims), _i64(win), _i64(pad), _i64(stride), _fp(dy),
+                           idx.ctypes.data_as(_I64), _fp(dx), int(bf16))
+    return dx
+
+
+def _split(shape, axis):
+    outer = int(np.prod(shape[:axis])) if axis else 1
+    inner = int(np.prod(shape[axis + 1:])) if axis + 1 < len(shape) else 1
+    return outer, shape[axis], inner
+
+
+def softmax_forward(x, axis, bf16=False):
+    x = np.ascontiguousarray(x, np.float32)
+    y = np.zeros_like(x)
+    o, a, i = _split(x.shape, axis)
+    restated().oc_softmax_fwd(C.c_int64(o), C.c_int64(a), C.c_int64(i), _fp(x), _fp(y), int(bf16))
+    return y
+
+
+def softmax_backward(y, dy, axis, bf16=False):
+    y, dy = np.ascontiguousarray(y, np.float32), np.ascontiguousarray(dy, np.float32)
+    dx = np.zeros_like(y)
+    o, a, i = _split(y.shape, axis)
+    restated().oc_softmax_bwd(C.c_int64(o), C.c_int64(a), C.c_int64(i), _fp(y), _fp(dy), _fp(dx), int(bf16))
+    return dx
+
+
+def ref_pool_forward(kind, x, win, pad, stride, bf16=False):
+    L = reference().lib
+    x = np.ascontiguousarray(x, np.float32)
+    oh, ow = pool_out_hw(x.shape, win, pad, stride)
+    y = np.zeros((x.shape[0], x.shape[1], oh, ow), np.float32)
+    idx = np.zeros(y.shape, np.int64)
+    ref_check(L.ref_pooling_forward(kind, _i64(win), _i64(pad), _i64(stride), _i64(x.shape), int(bf16), _fp(x),
+                                    _fp(y), idx.ctypes.data_as(_I64)))
+    return y, idx
+
+
+def ref_pool_backward(kind, in_dims, dy, idx, win, pad, stride, bf16=False):
+    L = reference().lib
+    dx = np.zeros(in_dims, np.float32)
+    ref_check(L.ref_pooling_backward(kind, _i64(win), _i64(pad), _i64(stride), _i64(in_dims), int(bf16),
+                                     _fp(np.ascontiguousarray(dy, np.float32)),
+                                     np.ascontiguousarray(idx, np.int64).ctypes.data_as(_I64), _fp(dx)))
+    return dx
+
+
+def ref_softmax_forward(x, axis, bf16=False):
+    L = reference().lib
+    x = np.ascontiguousarray(x, np.float32)
+    y = np.zeros_like(x)
+    ref_check(L.ref_softmax_forward(x.ndim, _i64(x.shape), int(bf16), C.c_int64(axis), _fp(x), _fp(y)))
+    return y
+
+
+def ref_softmax_backward(y, dy, axis, bf16=False):
+    L = reference().lib
+    y, dy = np.ascontiguousarray(y, np.float32), np.ascontiguousarray(dy, np.float32)
+    dx = np.zeros_like(y)
+    ref_check(L.ref_softmax_backward(y.ndim, _i64(y.shape), int(bf16), C.c_int64(axis), _fp(y), _fp(dy), _fp(dx)))
+    return dx
 
 
 # ---- the unmodified reference library -------------------------------------

@@ -504,3 +504,120 @@ void oc_bn_stats_dev(const void* x, int64_t rows, int64_t c, int64_t pitch, int6
     free(sum);
     free(sq);
 }
+
+/* src/core/primitives.cpp:204-260 — pooling forward, NCHW. kind 0 = max
+ * (first maximum in window scan order, strict >; linear input index), 1 =
+ * average (double sum of the valid taps / their count). Empty windows give 0
+ * and index -1. win/pad/str = {h, w}. */
+void oc_pool_fwd(int kind, const int64_t d[4], const int64_t win[2], const int64_t pad[2],
+                 const int64_t str[2], const float* x, float* y, int64_t* idx, int bf16) {
+    const int64_t N = d[0], Cc = d[1], H = d[2], W = d[3];
+    const int64_t OH = (H + 2 * pad[0] - win[0]) / str[0] + 1, OW = (W + 2 * pad[1] - win[1]) / str[1] + 1;
+    for (int64_t n = 0; n < N; ++n)
+        for (int64_t c = 0; c < Cc; ++c)
+            for (int64_t i = 0; i < OH; ++i)
+                for (int64_t j = 0; j < OW; ++j) {
+                    float best = -INFINITY;
+                    int64_t bi = -1, count = 0;
+                    double sum = 0.0;
+                    for (int64_t p = 0; p < win[0]; ++p) {
+                        const int64_t ih = i * str[0] - pad[0] + p;
+                        if (ih < 0 || ih >= H) continue;
+                        for (int64_t q = 0; q < win[1]; ++q) {
+                            const int64_t iw = j * str[1] - pad[1] + q;
+                            if (iw < 0 || iw >= W) continue;
+                            const int64_t lin = ((n * Cc + c) * H + ih) * W + iw;
+                            const float v = x[lin];
+                            sum += v;
+                            ++count;
+                            if (v > best) {
+                                best = v;
+                                bi = lin;
+                            }
+                        }
+                    }
+                    const int64_t o = ((n * Cc + c) * OH + i) * OW + j;
+                    if (kind == 0) {
+                        y[o] = count ? best : 0.0f;
+                        idx[o] = bi;
+                    } else {
+                        y[o] = count ? (float)(sum / (double)count) : 0.0f;
+                        idx[o] = -1;
+                    }
+                    if (bf16) y[o] = oc_round_bf16(y[o]);
+                }
+}
+
+/* src/core/primitives.cpp:262-310 — pooling backward (scatter in output
+ * order, one rounding store per addition). dx must be zeroed by the caller. */
+void oc_pool_bwd(int kind, const int64_t d[4], const int64_t win[2], const int64_t pad[2],
+                 const int64_t str[2], const float* dy, const int64_t* idx, float* dx, int bf16) {
+    const int64_t N = d[0], Cc = d[1], H = d[2], W = d[3];
+    const int64_t OH = (H + 2 * pad[0] - win[0]) / str[0] + 1, OW = (W + 2 * pad[1] - win[1]) / str[1] + 1;
+    if (kind == 0) {
+        for (int64_t o = 0; o < N * Cc * OH * OW; ++o)
+            if (idx[o] >= 0) {
+                dx[idx[o]] += dy[o];
+                if (bf16) dx[idx[o]] = oc_round_bf16(dx[idx[o]]);
+            }
+        return;
+    }
+    for (int64_t n = 0; n < N; ++n)
+        for (int64_t c = 0; c < Cc; ++c)
+            for (int64_t i = 0; i < OH; ++i)
+                for (int64_t j = 0; j < OW; ++j) {
+                    int64_t count = 0;
+                    for (int64_t p = 0; p < win[0]; ++p) {
+                        const int64_t ih = i * str[0] - pad[0] + p;
+                        if (ih < 0 || ih >= H) continue;
+                        for (int64_t q = 0; q < win[1]; ++q) {
+                            const int64_t iw = j * str[1] - pad[1] + q;
+                            if (iw >= 0 && iw < W) ++count;
+                        }
+                    }
+                    if (!count) continue;
+                    const float g = dy[((n * Cc + c) * OH + i) * OW + j] / (float)count;
+                    for (int64_t p = 0; p < win[0]; ++p) {
+                        const int64_t ih = i * str[0] - pad[0] + p;
+                        if (ih < 0 || ih >= H) continue;
+                        for (int64_t q = 0; q < win[1]; ++q) {
+                            const int64_t iw = j * str[1] - pad[1] + q;
+                            if (iw < 0 || iw >= W) continue;
+                            const int64_t lin = ((n * Cc + c) * H + ih) * W + iw;
+                            dx[lin] += g;
+                            if (bf16) dx[lin] = oc_round_bf16(dx[lin]);
+                        }
+                    }
+                }
+}
+
+/* src/core/primitives.cpp:329-351 — softmax forward over [outer][axis][inner]. */
+void oc_softmax_fwd(int64_t outer, int64_t axis, int64_t inner, const float* x, float* y, int bf16) {
+    for (int64_t o = 0; o < outer; ++o)
+        for (int64_t i = 0; i < inner; ++i) {
+            const float* xc = x + o * axis * inner + i;
+            float mx = xc[0];
+            for (int64_t a = 1; a < axis; ++a) mx = xc[a * inner] > mx ? xc[a * inner] : mx;
+            double den = 0.0;
+            for (int64_t a = 0; a < axis; ++a) den += exp((double)(xc[a * inner] - mx));
+            for (int64_t a = 0; a < axis; ++a) {
+                float v = (float)(exp((double)(xc[a * inner] - mx)) / den);
+                y[o * axis * inner + i + a * inner] = bf16 ? oc_round_bf16(v) : v;
+            }
+        }
+}
+
+/* src/core/primitives.cpp:353-370 — softmax backward. */
+void oc_softmax_bwd(int64_t outer, int64_t axis, int64_t inner, const float* y, const float* dy, float* dx,
+                    int bf16) {
+    for (int64_t o = 0; o < outer; ++o)
+        for (int64_t i = 0; i < inner; ++i) {
+            const int64_t b = o * axis * inner + i;
+            double dot = 0.0;
+            for (int64_t a = 0; a < axis; ++a) dot += (double)dy[b + a * inner] * y[b + a * inner];
+            for (int64_t a = 0; a < axis; ++a) {
+                float v = (float)(y[b + a * inner] * ((double)dy[b + a * inner] - dot));
+                dx[b + a * inner] = bf16 ? oc_round_bf16(v) : v;
+            }
+        }
+}

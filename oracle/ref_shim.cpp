@@ -164,3 +164,69 @@ int ref_activation_backward(int kind, float alpha, const std::int64_t dims[4],
 float ref_round_bf16(float v) { return round_bf16(v); }
 
 }  // extern "C"
+
+// ---- pooling / softmax (C++-only in the reference: primitives.hpp:65-91) ----
+extern "C" {
+
+int ref_pooling_forward(int kind, const std::int64_t win[2], const std::int64_t pad[2],
+                        const std::int64_t str[2], const std::int64_t dims[4], int etype,
+                        const float* x, float* y, std::int64_t* indices) {
+    return guard([&] {
+        PoolingDescriptor pd;
+        pd.window_h = win[0];
+        pd.window_w = win[1];
+        pd.pad_h = pad[0];
+        pd.pad_w = pad[1];
+        pd.stride_h = str[0];
+        pd.stride_w = str[1];
+        const std::vector<std::int64_t> d(dims, dims + 4);
+        PoolingForwardResult r = pooling_forward(static_cast<PoolingKind>(kind), pd,
+                                                 make(d, static_cast<ElementType>(etype), x));
+        std::memcpy(y, r.y.data(), sizeof(float) * r.y.size());
+        std::memcpy(indices, r.indices.data(), sizeof(std::int64_t) * r.indices.size());
+    });
+}
+
+int ref_pooling_backward(int kind, const std::int64_t win[2], const std::int64_t pad[2],
+                         const std::int64_t str[2], const std::int64_t dims[4], int etype,
+                         const float* dy, const std::int64_t* indices, float* dx) {
+    return guard([&] {
+        PoolingDescriptor pd;
+        pd.window_h = win[0];
+        pd.window_w = win[1];
+        pd.pad_h = pad[0];
+        pd.pad_w = pad[1];
+        pd.stride_h = str[0];
+        pd.stride_w = str[1];
+        const auto et = static_cast<ElementType>(etype);
+        const std::int64_t oh = (dims[2] + 2 * pad[0] - win[0]) / str[0] + 1;
+        const std::int64_t ow = (dims[3] + 2 * pad[1] - win[1]) / str[1] + 1;
+        const Tensor tdy = make({dims[0], dims[1], oh, ow}, et, dy);
+        std::vector<std::int64_t> idx(indices, indices + tdy.size());
+        const Tensor r = pooling_backward(static_cast<PoolingKind>(kind), pd,
+                                          TensorDescriptor::packed({dims[0], dims[1], dims[2], dims[3]}, et),
+                                          tdy, idx);
+        std::memcpy(dx, r.data(), sizeof(float) * r.size());
+    });
+}
+
+int ref_softmax_forward(int rank, const std::int64_t* dims, int etype, std::int64_t axis, const float* x,
+                        float* y) {
+    return guard([&] {
+        const std::vector<std::int64_t> d(dims, dims + rank);
+        const Tensor r = softmax_forward(make(d, static_cast<ElementType>(etype), x), axis);
+        std::memcpy(y, r.data(), sizeof(float) * r.size());
+    });
+}
+
+int ref_softmax_backward(int rank, const std::int64_t* dims, int etype, std::int64_t axis, const float* y,
+                         const float* dy, float* dx) {
+    return guard([&] {
+        const std::vector<std::int64_t> d(dims, dims + rank);
+        const auto et = static_cast<ElementType>(etype);
+        const Tensor r = softmax_backward(make(d, et, y), make(d, et, dy), axis);
+        std::memcpy(dx, r.data(), sizeof(float) * r.size());
+    });
+}
+
+}  // extern "C"

@@ -85,6 +85,8 @@ SECTION1 = {
     "primkit_fusion_execute": (ST, [P, P, FP, FP, C.c_int]),
 }
 
+POOL_MAX, POOL_AVG = 0, 1
+
 # section 2 (B200 additions)
 SECTION2 = {
     "primkit_handle_create_with_stream": (ST, [P, C.c_int, C.POINTER(P)]),
@@ -118,6 +120,15 @@ SECTION2 = {
     "primkit_handle_last_variant": (ST, [P, C.c_char_p, C.c_size_t]),
     "primkit_handle_plan_cache_stats": (ST, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                              C.POINTER(C.c_uint64)]),
+    "primkit_pooling_output_dims": (ST, [I64P, I64P, I64P, I64P, I64P]),
+    "primkit_pooling_forward": (ST, [P, C.c_int, I64P, I64P, I64P, I64P, C.c_int, FP, FP, I64P]),
+    "primkit_pooling_backward": (ST, [P, C.c_int, I64P, I64P, I64P, I64P, C.c_int, FP, I64P, FP]),
+    "primkit_pooling_forward_device": (ST, [P, C.c_int, I64P, I64P, I64P, I64P, C.c_int, P, P, P]),
+    "primkit_pooling_backward_device": (ST, [P, C.c_int, I64P, I64P, I64P, I64P, C.c_int, P, P, P]),
+    "primkit_softmax_forward": (ST, [P, C.c_int, I64P, C.c_int, C.c_int64, FP, FP]),
+    "primkit_softmax_backward": (ST, [P, C.c_int, I64P, C.c_int, C.c_int64, FP, FP, FP]),
+    "primkit_softmax_forward_device": (ST, [P, C.c_int, I64P, C.c_int, C.c_int64, P, P]),
+    "primkit_softmax_backward_device": (ST, [P, C.c_int, I64P, C.c_int, C.c_int64, P, P, P]),
     # section 3: data-parallel all-reduce
     "primkit_dp_unique_id": (ST, [C.c_char_p]),
     "primkit_dp_create": (ST, [P, C.c_char_p, C.c_int, C.c_int, C.c_int, C.POINTER(P)]),

@@ -11,7 +11,9 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <algorithm>
 #include <exception>
+#include <vector>
 #include <memory>
 #include <string>
 
@@ -1030,6 +1032,267 @@ primkit_status primkit_handle_last_kernel(primkit_handle* h, char* buf, size_t l
 
 primkit_status primkit_handle_last_variant(primkit_handle* h, char* buf, size_t len) {
     return guarded([&] { copy_name(buf, len, H(h).last_variant); });
+}
+
+// ---- pooling / softmax (reference primitives.cpp:204-370) -------------------
+
+namespace {
+
+pk_pool_geom pool_geom(const int64_t win[2], const int64_t pad[2], const int64_t str[2],
+                       const int64_t d[4]) {
+    need(win, "window");
+    need(pad, "pad");
+    need(str, "stride");
+    need(d, "dims");
+    // primitives.cpp:207-220: validation order and messages
+    if (win[0] < 1 || win[1] < 1 || str[0] < 1 || str[1] < 1 || pad[0] < 0 || pad[1] < 0)
+        primkit::throw_error(primkit::ErrorCode::InvalidValue, "bad pooling descriptor");
+    for (int i = 0; i < 4; ++i)
+        if (d[i] < 0) primkit::throw_error(primkit::ErrorCode::InvalidShape, "negative dimension");
+    const int64_t oh = (d[2] + 2 * pad[0] - win[0]) / str[0] + 1;
+    const int64_t ow = (d[3] + 2 * pad[1] - win[1]) / str[1] + 1;
+    if (oh < 1 || ow < 1)
+        primkit::throw_error(primkit::ErrorCode::InvalidShape, "pooling output extent below 1");
+    pk_pool_geom g{};
+    g.n = (int)d[0]; g.c = (int)d[1]; g.h = (int)d[2]; g.w = (int)d[3];
+    g.oh = (int)oh; g.ow = (int)ow;
+    g.win_h = (int)win[0]; g.win_w = (int)win[1];
+    g.str_h = (int)str[0]; g.str_w = (int)str[1];
+    g.pad_h = (int)pad[0]; g.pad_w = (int)pad[1];
+    g.pitch = pk_pitch(g.c);
+    return g;
+}
+
+struct AxisSplit {
+    long long outer = 1, axis = 1, inner = 1;
+};
+
+// primitives.cpp:312-324
+AxisSplit split_axis(int rank, const int64_t* dims, int64_t axis) {
+    if (rank < 1 || !dims) primkit::throw_error(primkit::ErrorCode::InvalidShape, "softmax needs a tensor");
+    if (axis < 0 || axis >= rank) primkit::throw_error(primkit::ErrorCode::InvalidAxis, "softmax axis out of range");
+    AxisSplit s;
+    s.axis = dims[axis];
+    for (int64_t i = 0; i < axis; ++i) s.outer *= dims[i];
+    for (int64_t i = axis + 1; i < rank; ++i) s.inner *= dims[i];
+    return s;
+}
+
+int dtype_of(primkit_element_type et) { return et == PRIMKIT_BF16 ? PK_BF16 : PK_F32; }
+
+// Packed host floats <-> device elements of `et` (bf16: RNE, the reference's quantize-on-entry).
+void* upload_packed(primkit::Handle& hd, int slot, const float* src, size_t count, primkit_element_type et) {
+    void* dev = hd.scratch(slot, count * (et == PRIMKIT_BF16 ? 2 : 4));
+    if (et == PRIMKIT_BF16) {
+        std::vector<uint16_t> bits(count);
+        for (size_t i = 0; i < count; ++i) {
+            const float v = primkit::round_bf16(src[i]);
+            uint32_t u;
+            std::memcpy(&u, &v, 4);
+            bits[i] = (uint16_t)(u >> 16);
+        }
+        primkit::check_cuda(cudaMemcpyAsync(dev, bits.data(), count * 2, cudaMemcpyHostToDevice, hd.stream()),
+                            "cudaMemcpyAsync");
+        hd.sync();  // bits is a stack vector
+    } else {
+        primkit::check_cuda(cudaMemcpyAsync(dev, src, count * 4, cudaMemcpyHostToDevice, hd.stream()),
+                            "cudaMemcpyAsync");
+    }
+    return dev;
+}
+
+void download_packed(primkit::Handle& hd, const void* dev, float* dst, size_t count, primkit_element_type et) {
+    if (et == PRIMKIT_BF16) {
+        std::vector<uint16_t> bits(count);
+        primkit::check_cuda(cudaMemcpyAsync(bits.data(), dev, count * 2, cudaMemcpyDeviceToHost, hd.stream()),
+                            "cudaMemcpyAsync");
+        hd.sync();
+        for (size_t i = 0; i < count; ++i) {
+            const uint32_t u = (uint32_t)bits[i] << 16;
+            std::memcpy(dst + i, &u, 4);
+        }
+    } else {
+        primkit::check_cuda(cudaMemcpyAsync(dst, dev, count * 4, cudaMemcpyDeviceToHost, hd.stream()),
+                            "cudaMemcpyAsync");
+        hd.sync();
+    }
+}
+
+}  // namespace
+
+primkit_status primkit_pooling_output_dims(const int64_t window[2], const int64_t pad[2],
+                                           const int64_t stride[2], const int64_t dims[4],
+                                           int64_t out_dims[4]) {
+    return guarded([&] {
+        const pk_pool_geom g = pool_geom(window, pad, stride, dims);
+        need(out_dims, "output");
+        out_dims[0] = g.n; out_dims[1] = g.c; out_dims[2] = g.oh; out_dims[3] = g.ow;
+    });
+}
+
+primkit_status primkit_pooling_forward_device(primkit_handle* h, primkit_pooling_kind kind,
+                                              const int64_t window[2], const int64_t pad[2],
+                                              const int64_t stride[2], const int64_t dims[4],
+                                              primkit_element_type et, const void* x, void* y,
+                                              int64_t* indices) {
+    return guarded([&] {
+        const pk_pool_geom g = pool_geom(window, pad, stride, dims);
+        primkit::Handle& hd = H(h);
+        hd.activate();
+        primkit::check_cuda(pk_cuda_pool_fwd(&g, dtype_of(et), kind == PRIMKIT_POOL_MAX, need(x, "x"),
+                                             need(y, "y"), reinterpret_cast<long long*>(indices), hd.stream()),
+                            "pool_fwd");
+        hd.last_kernel = kind == PRIMKIT_POOL_MAX ? "pool_max_fwd" : "pool_avg_fwd";
+    });
+}
+
+primkit_status primkit_pooling_backward_device(primkit_handle* h, primkit_pooling_kind kind,
+                                               const int64_t window[2], const int64_t pad[2],
+                                               const int64_t stride[2], const int64_t dims[4],
+                                               primkit_element_type et, const void* dy,
+                                               const int64_t* indices, void* dx) {
+    return guarded([&] {
+        const pk_pool_geom g = pool_geom(window, pad, stride, dims);
+        if (kind == PRIMKIT_POOL_MAX) need(indices, "indices");
+        primkit::Handle& hd = H(h);
+        hd.activate();
+        primkit::check_cuda(pk_cuda_pool_bwd(&g, dtype_of(et), kind == PRIMKIT_POOL_MAX, need(dy, "dy"),
+                                             reinterpret_cast<const long long*>(indices), need(dx, "dx"),
+                                             hd.stream()),
+                            "pool_bwd");
+        hd.last_kernel = kind == PRIMKIT_POOL_MAX ? "pool_max_bwd" : "pool_avg_bwd";
+    });
+}
+
+primkit_status primkit_pooling_forward(primkit_handle* h, primkit_pooling_kind kind,
+                                       const int64_t window[2], const int64_t pad[2],
+                                       const int64_t stride[2], const int64_t dims[4],
+                                       primkit_element_type et, const float* x, float* y,
+                                       int64_t* indices) {
+    return guarded([&] {
+        const pk_pool_geom g = pool_geom(window, pad, stride, dims);
+        primkit::Handle& hd = H(h);
+        const primkit::TensorDescriptor din = dims4(dims, et);
+        const int64_t od[4] = {g.n, g.c, g.oh, g.ow};
+        const primkit::TensorDescriptor dout = dims4(od, et);
+        void* dvx = hd.scratch(1, primkit::device_bytes(din));
+        void* dvy = hd.scratch(2, primkit::device_bytes(dout));
+        const size_t nidx = (size_t)g.n * g.c * g.oh * g.ow;
+        long long* dvi = kind == PRIMKIT_POOL_MAX ? static_cast<long long*>(hd.scratch(4, nidx * 8)) : nullptr;
+        primkit::upload_nchw(hd, din, need(x, "x"), dvx);
+        primkit::check_cuda(pk_cuda_pool_fwd(&g, dtype_of(et), kind == PRIMKIT_POOL_MAX, dvx, dvy, dvi,
+                                             hd.stream()),
+                            "pool_fwd");
+        primkit::download_nchw(hd, dout, dvy, need(y, "y"));
+        if (dvi && indices) {  // device order [n][oh][ow][c] -> reference order [n][c][oh][ow]
+            std::vector<int64_t> tmp(nidx);
+            primkit::check_cuda(cudaMemcpyAsync(tmp.data(), dvi, nidx * 8, cudaMemcpyDeviceToHost, hd.stream()),
+                                "cudaMemcpyAsync");
+            hd.sync();
+            const size_t hw = (size_t)g.oh * g.ow;
+            for (size_t n = 0; n < (size_t)g.n; ++n)
+                for (size_t p = 0; p < hw; ++p)
+                    for (size_t c = 0; c < (size_t)g.c; ++c)
+                        indices[(n * g.c + c) * hw + p] = tmp[(n * hw + p) * g.c + c];
+        } else if (indices) {
+            std::fill(indices, indices + nidx, (int64_t)-1);  // average pooling: no argmax (reference: -1)
+        }
+    });
+}
+
+primkit_status primkit_pooling_backward(primkit_handle* h, primkit_pooling_kind kind,
+                                        const int64_t window[2], const int64_t pad[2],
+                                        const int64_t stride[2], const int64_t dims[4],
+                                        primkit_element_type et, const float* dy,
+                                        const int64_t* indices, float* dx) {
+    return guarded([&] {
+        const pk_pool_geom g = pool_geom(window, pad, stride, dims);
+        if (kind == PRIMKIT_POOL_MAX) need(indices, "indices");
+        primkit::Handle& hd = H(h);
+        const primkit::TensorDescriptor din = dims4(dims, et);
+        const int64_t od[4] = {g.n, g.c, g.oh, g.ow};
+        const primkit::TensorDescriptor dout = dims4(od, et);
+        void* dvdy = hd.scratch(1, primkit::device_bytes(dout));
+        void* dvdx = hd.scratch(2, primkit::device_bytes(din));
+        const size_t nidx = (size_t)g.n * g.c * g.oh * g.ow;
+        long long* dvi = nullptr;
+        primkit::upload_nchw(hd, dout, need(dy, "dy"), dvdy);
+        if (kind == PRIMKIT_POOL_MAX) {
+            const size_t hw = (size_t)g.oh * g.ow;
+            std::vector<int64_t> tmp(nidx);
+            for (size_t n = 0; n < (size_t)g.n; ++n)
+                for (size_t p = 0; p < hw; ++p)
+                    for (size_t c = 0; c < (size_t)g.c; ++c)
+                        tmp[(n * hw + p) * g.c + c] = indices[(n * g.c + c) * hw + p];
+            dvi = static_cast<long long*>(hd.scratch(4, nidx * 8));
+            primkit::check_cuda(cudaMemcpyAsync(dvi, tmp.data(), nidx * 8, cudaMemcpyHostToDevice, hd.stream()),
+                                "cudaMemcpyAsync");
+            hd.sync();
+        }
+        primkit::check_cuda(pk_cuda_pool_bwd(&g, dtype_of(et), kind == PRIMKIT_POOL_MAX, dvdy, dvi, dvdx,
+                                             hd.stream()),
+                            "pool_bwd");
+        primkit::download_nchw(hd, din, dvdx, need(dx, "dx"));
+    });
+}
+
+primkit_status primkit_softmax_forward_device(primkit_handle* h, int rank, const int64_t* dims,
+                                              primkit_element_type et, int64_t axis, const void* x,
+                                              void* y) {
+    return guarded([&] {
+        const AxisSplit s = split_axis(rank, dims, axis);
+        primkit::Handle& hd = H(h);
+        hd.activate();
+        primkit::check_cuda(pk_cuda_softmax_fwd(dtype_of(et), need(x, "x"), need(y, "y"), s.outer, (int)s.axis,
+                                                s.inner, hd.stream()),
+                            "softmax_fwd");
+    });
+}
+
+primkit_status primkit_softmax_backward_device(primkit_handle* h, int rank, const int64_t* dims,
+                                               primkit_element_type et, int64_t axis, const void* y,
+                                               const void* dy, void* dx) {
+    return guarded([&] {
+        const AxisSplit s = split_axis(rank, dims, axis);
+        primkit::Handle& hd = H(h);
+        hd.activate();
+        primkit::check_cuda(pk_cuda_softmax_bwd(dtype_of(et), need(y, "y"), need(dy, "dy"), need(dx, "dx"),
+                                                s.outer, (int)s.axis, s.inner, hd.stream()),
+                            "softmax_bwd");
+    });
+}
+
+primkit_status primkit_softmax_forward(primkit_handle* h, int rank, const int64_t* dims,
+                                       primkit_element_type et, int64_t axis, const float* x, float* y) {
+    return guarded([&] {
+        const AxisSplit s = split_axis(rank, dims, axis);
+        primkit::Handle& hd = H(h);
+        hd.activate();
+        const size_t count = (size_t)(s.outer * s.axis * s.inner);
+        void* dx = upload_packed(hd, 1, need(x, "x"), count, et);
+        void* dy = hd.scratch(2, count * (et == PRIMKIT_BF16 ? 2 : 4));
+        primkit::check_cuda(pk_cuda_softmax_fwd(dtype_of(et), dx, dy, s.outer, (int)s.axis, s.inner, hd.stream()),
+                            "softmax_fwd");
+        download_packed(hd, dy, need(y, "y"), count, et);
+    });
+}
+
+primkit_status primkit_softmax_backward(primkit_handle* h, int rank, const int64_t* dims,
+                                        primkit_element_type et, int64_t axis, const float* y,
+                                        const float* dy, float* dx) {
+    return guarded([&] {
+        const AxisSplit s = split_axis(rank, dims, axis);
+        primkit::Handle& hd = H(h);
+        hd.activate();
+        const size_t count = (size_t)(s.outer * s.axis * s.inner);
+        void* dvy = upload_packed(hd, 1, need(y, "y"), count, et);
+        void* dvdy = upload_packed(hd, 2, need(dy, "dy"), count, et);
+        void* dvdx = hd.scratch(3, count * (et == PRIMKIT_BF16 ? 2 : 4));
+        primkit::check_cuda(pk_cuda_softmax_bwd(dtype_of(et), dvy, dvdy, dvdx, s.outer, (int)s.axis, s.inner,
+                                                hd.stream()),
+                            "softmax_bwd");
+        download_packed(hd, dvdx, need(dx, "dx"), count, et);
+    });
 }
 
 primkit_status primkit_handle_plan_cache_stats(primkit_handle* h, uint64_t* builds,

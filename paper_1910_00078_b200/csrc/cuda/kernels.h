@@ -267,6 +267,25 @@ cudaError_t pk_cuda_bn_bwd(const void* x, const void* y, const void* dy, void* d
                            float* dbeta, int relu, int round_params_bf16, void* scratch,
                            cudaStream_t st);
 
+// ---- pooling / softmax (pool.cu; reference primitives.cpp:204-370) -------------
+typedef struct pk_pool_geom {
+    int n, c, h, w, oh, ow;
+    int win_h, win_w, str_h, str_w, pad_h, pad_w;
+    int pitch;  // channel pitch of x / y / dx / dy (NHWC device layout)
+} pk_pool_geom;
+int pk_pool_supported(const pk_pool_geom* g);
+// y [n][oh][ow][pitch]; indices (max only, nullable) [n][oh][ow][c] int64 =
+// linear NCHW input offset of the first maximum (-1 for an empty window).
+cudaError_t pk_cuda_pool_fwd(const pk_pool_geom* g, int dtype, int is_max, const void* x, void* y,
+                             long long* indices, cudaStream_t st);
+cudaError_t pk_cuda_pool_bwd(const pk_pool_geom* g, int dtype, int is_max, const void* dy,
+                             const long long* indices, void* dx, cudaStream_t st);
+// packed tensor viewed as [outer][axis][inner]
+cudaError_t pk_cuda_softmax_fwd(int dtype, const void* x, void* y, long long outer, int axis,
+                                long long inner, cudaStream_t st);
+cudaError_t pk_cuda_softmax_bwd(int dtype, const void* y, const void* dy, void* dx, long long outer,
+                                int axis, long long inner, cudaStream_t st);
+
 // ---- data-parallel gradient buckets (dp.cu) -----------------------------------
 // One gradient tensor inside an fp32 bucket: device pointer, element count,
 // element type (pk_dtype) and its element offset in the bucket.

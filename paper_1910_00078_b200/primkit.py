@@ -292,6 +292,43 @@ class Handle:
         self._c("primkit_handle_last_kernel", buf, 128)
         return buf.value.decode()
 
+    def pooling_forward(self, kind, x, window, pad=(0, 0), stride=None, etype=abi.F32):
+        """(y, indices) — reference pooling_forward (primitives.cpp:204-260)."""
+        x = _f32(x)
+        stride = window if stride is None else stride
+        od = (C.c_int64 * 4)()
+        i64 = lambda v: (C.c_int64 * len(v))(*v)  # noqa: E731
+        self.L.check(self.L.lib.primkit_pooling_output_dims(i64(window), i64(pad), i64(stride),
+                                                            _dims(x.shape), od))
+        y = np.zeros(list(od), np.float32)
+        idx = np.zeros(list(od), np.int64)
+        self._c("primkit_pooling_forward", kind, i64(window), i64(pad), i64(stride), _dims(x.shape), etype,
+                _fp(x), _fp(y), idx.ctypes.data_as(C.POINTER(C.c_int64)))
+        return y, idx
+
+    def pooling_backward(self, kind, in_dims, dy, indices, window, pad=(0, 0), stride=None, etype=abi.F32):
+        dy = _f32(dy)
+        stride = window if stride is None else stride
+        i64 = lambda v: (C.c_int64 * len(v))(*v)  # noqa: E731
+        dx = np.zeros(in_dims, np.float32)
+        idx = None if indices is None else np.ascontiguousarray(indices, np.int64)
+        self._c("primkit_pooling_backward", kind, i64(window), i64(pad), i64(stride), _dims(in_dims), etype,
+                _fp(dy), None if idx is None else idx.ctypes.data_as(C.POINTER(C.c_int64)), _fp(dx))
+        return dx
+
+    def softmax_forward(self, x, axis, etype=abi.F32):
+        x = _f32(x)
+        y = np.zeros_like(x)
+        self._c("primkit_softmax_forward", x.ndim, (C.c_int64 * x.ndim)(*x.shape), etype, axis, _fp(x), _fp(y))
+        return y
+
+    def softmax_backward(self, y, dy, axis, etype=abi.F32):
+        y, dy = _f32(y), _f32(dy)
+        dx = np.zeros_like(y)
+        self._c("primkit_softmax_backward", y.ndim, (C.c_int64 * y.ndim)(*y.shape), etype, axis, _fp(y),
+                _fp(dy), _fp(dx))
+        return dx
+
     def plan_cache_stats(self) -> tuple[int, int, int]:
         """(builds, memory_hits, disk_hits) of the handle's plan cache."""
         v = [C.c_uint64() for _ in range(3)]

@@ -226,3 +226,49 @@ def test_sampled_formulas_match_full_oracle(cfg, bf16):
     got = oracle.sample_backward_weights(p, dyd, xd, ks, taps, bf16)
     want = dw[ks][:, taps[:, 2], taps[:, 0], taps[:, 1]]
     np.testing.assert_allclose(got, want, rtol=1e-5, atol=1e-4)
+
+
+POOL_CASES = [
+    ((2, 3, 7, 7), (3, 3), (1, 1), (2, 2)),      # ResNet stem max-pool shape, padded
+    ((1, 2, 6, 5), (2, 2), (0, 0), (2, 2)),
+    ((2, 2, 5, 5), (3, 2), (1, 0), (1, 2)),       # overlapping windows
+    ((1, 1, 3, 3), (5, 5), (2, 2), (3, 3)),       # windows larger than the image
+    ((1, 4, 7, 7), (7, 7), (0, 0), (1, 1)),       # global average pool
+]
+
+
+@pytest.mark.parametrize("case", POOL_CASES)
+@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("bf16", [False, True])
+def test_pooling_restatement_matches_reference(ref, case, kind, bf16):
+    dims, win, pad, stride = case
+    rng = np.random.default_rng(8)
+    x = rng.uniform(-1, 1, dims).astype(np.float32)
+    x[0, 0, 0, :2] = 0.5  # ties: the first maximum wins
+    if bf16:
+        x = oracle.round_bf16(x)
+    y, idx = oracle.pool_forward(kind, x, win, pad, stride, bf16)
+    yr, idxr = oracle.ref_pool_forward(kind, x, win, pad, stride, bf16)
+    assert np.array_equal(y, yr) and np.array_equal(idx, idxr)
+    dy = rng.uniform(-1, 1, y.shape).astype(np.float32)
+    if bf16:
+        dy = oracle.round_bf16(dy)
+    dx = oracle.pool_backward(kind, dims, dy, idx, win, pad, stride, bf16)
+    dxr = oracle.ref_pool_backward(kind, dims, dy, idxr, win, pad, stride, bf16)
+    assert np.array_equal(dx, dxr)
+
+
+@pytest.mark.parametrize("shape,axis", [((4, 10), 1), ((2, 5, 3, 3), 1), ((3, 7), 0), ((2, 3, 4), 2)])
+@pytest.mark.parametrize("bf16", [False, True])
+def test_softmax_restatement_matches_reference(ref, shape, axis, bf16):
+    rng = np.random.default_rng(9)
+    x = rng.uniform(-4, 4, shape).astype(np.float32)
+    if bf16:
+        x = oracle.round_bf16(x)
+    y = oracle.softmax_forward(x, axis, bf16)
+    assert np.array_equal(y, oracle.ref_softmax_forward(x, axis, bf16))
+    dy = rng.uniform(-1, 1, shape).astype(np.float32)
+    if bf16:
+        dy = oracle.round_bf16(dy)
+    assert np.array_equal(oracle.softmax_backward(y, dy, axis, bf16),
+                          oracle.ref_softmax_backward(y, dy, axis, bf16))
