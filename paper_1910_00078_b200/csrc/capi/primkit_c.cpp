@@ -621,10 +621,19 @@ primkit_status primkit_conv_run_device(primkit_handle* h, const primkit_conv_pro
 }
 
 // Per-CTA fp32 partials (+ 2 x C finalize scratch) over the channels of the
-// convolution OUTPUT (K forward, C backward data).
-static std::size_t conv_bn_stats_bytes(const primkit::ConvProblem& p) {
+// convolution OUTPUT (K forward, C backward data), then the standalone BN's
+// scratch (its per-CTA double partials): all of it from the caller's workspace.
+static std::size_t conv_bn_part_bytes(const primkit::ConvProblem& p) {
     const std::size_t ch = p.direction == primkit::ConvDirection::BackwardData ? p.c : p.k;
-    return ((std::size_t)pk_stats_slots() + 1) * ch * 2 * sizeof(float);
+    return (((std::size_t)pk_stats_slots() + 1) * ch * 2 * sizeof(float) + 255) / 256 * 256;
+}
+
+static std::size_t conv_bn_stats_bytes(const primkit::ConvProblem& p) {
+    const primkit::ConvShapes sh = primkit::resolve_shapes(p.input_desc(), p.filter_desc(),
+                                                            p.conv_desc());
+    const bool bwd = p.direction == primkit::ConvDirection::BackwardData;
+    const int ch = (int)(bwd ? sh.c : sh.k), hw = (int)(bwd ? sh.h * sh.w : sh.oh * sh.ow);
+    return conv_bn_part_bytes(p) + pk_bn_scratch_bytes((int)sh.n, ch, hw, 0);
 }
 
 primkit_status primkit_conv_bn_workspace(primkit_handle* h, const primkit_conv_problem* pp,
@@ -681,7 +690,7 @@ primkit_status primkit_conv_bn_forward_train_device(
         const bool fused = dt == PK_BF16 && plan->fuses_stats() && stats_epilogue_pays(p, sh);
         cudaStream_t st = hd.stream();
         if (fused) {
-            primkit::check_cuda(cudaMemsetAsync(part, 0, conv_bn_stats_bytes(p), st), "memset");
+            primkit::check_cuda(cudaMemsetAsync(part, 0, conv_bn_part_bytes(p), st), "memset");
             pk_epilogue e{};
             e.act = -1;
             e.stats = part;
@@ -694,7 +703,7 @@ primkit_status primkit_conv_bn_forward_train_device(
             hd.last_kernel = hd.last_kernel + "+bn_stats_epilogue";
         } else {
             plan->run(hd, need(x, "x"), need(w, "w"), need(conv_out, "conv_out"), workspace, conv);
-            void* scratch = hd.scratch(7, pk_bn_scratch_bytes(n, k, hw, 0));
+            void* scratch = static_cast<char*>(workspace) + conv + conv_bn_part_bytes(p);
             primkit::check_cuda(pk_cuda_bn_fwd_train(conv_out, need(y, "y"), n, k, hw, pk_pitch(k), dt,
                                                      0, gamma, beta, running_mean, running_var, eps,
                                                      momentum, saved_mean, saved_invstd, relu,
@@ -727,7 +736,15 @@ primkit_status primkit_conv_backward_data_bn_device(
         float* part = reinterpret_cast<float*>(static_cast<char*>(workspace) + conv);
         float* tot = part + (std::size_t)pk_stats_slots() * c * 2;
         cudaStream_t st = hd.stream();
-        if (dt == PK_BF16 && plan->fuses_stats()) {
+        void* scratch = static_cast<char*>(workspace) + conv + conv_bn_part_bytes(p);
+        // BN statistics in the dgrad epilogue (PK_CBN_BWD_EPI=1) re-read the BN
+        // input inside the epilogue on the MMA pipeline's critical path; measured
+        // slower (ResNet-50 N=256: 13.5 ms vs 10.2 ms for all layers) than the
+        // plain dgrad + ONE persistent BN-backward launch that recomputes the ReLU
+        // mask from the BN input (no BN output read, no y rebuild).
+        const char* epi_env = std::getenv("PK_CBN_BWD_EPI");
+        const bool epi_stats = epi_env && epi_env[0] == '1';
+        if (dt == PK_BF16 && epi_stats && plan->fuses_stats()) {
             primkit::check_cuda(cudaMemsetAsync(part, 0, (std::size_t)pk_stats_slots() * c * 2 * 4, st),
                                 "memset");
             pk_epilogue e{};
@@ -747,20 +764,28 @@ primkit_status primkit_conv_backward_data_bn_device(
                                                               dgamma, dbeta, tot, st),
                                 "bn_bwd_finalize_apply");
             hd.last_kernel = hd.last_kernel + "+bn_bwd_stats_epilogue";
-        } else {
-            plan->run(hd, need(dy, "dy"), need(w, "w"), need(dz, "dz"), workspace, conv);
-            // standalone BN backward needs the BN output for the ReLU mask:
-            // rebuild it into bn_dx first (same shape), then run in place
-            void* scratch = hd.scratch(7, pk_bn_scratch_bytes(n, c, hw, 0));
-            void* ybuf = hd.scratch(8, (std::size_t)n * hw * pk_pitch(c) * (dt == PK_BF16 ? 2 : 4));
-            primkit::check_cuda(pk_cuda_bn_apply_stats(bn_x, ybuf, n, c, hw, pk_pitch(c), dt, gamma,
-                                                       beta, saved_mean, saved_invstd, relu, st),
-                                "bn_apply");
-            primkit::check_cuda(pk_cuda_bn_bwd(bn_x, ybuf, dz, need(bn_dx, "bn_dx"), n, c, hw,
-                                               pk_pitch(c), dt, 0, gamma, saved_mean, saved_invstd,
-                                               dgamma, dbeta, relu, dt == PK_BF16, scratch, st),
-                                "bn_bwd");
+            return;
         }
+        plan->run(hd, need(dy, "dy"), need(w, "w"), need(dz, "dz"), workspace, conv);
+        const cudaError_t fe = pk_cuda_bn_bwd_fold(need(bn_x, "bn_x"), dz, need(bn_dx, "bn_dx"), n, c, hw,
+                                                   pk_pitch(c), dt, gamma, beta, saved_mean,
+                                                   saved_invstd, relu, dgamma, dbeta, scratch, st);
+        if (fe == cudaSuccess) {
+            hd.last_kernel = hd.last_kernel + "+bn_bwd_fold";
+            return;
+        }
+        if (fe != cudaErrorNotSupported) primkit::check_cuda(fe, "bn_bwd_fold");
+        cudaGetLastError();
+        // other layouts (f32): rebuild the BN output for the ReLU mask, then the
+        // standalone backward
+        void* ybuf = hd.scratch(8, (std::size_t)n * hw * pk_pitch(c) * (dt == PK_BF16 ? 2 : 4));
+        primkit::check_cuda(pk_cuda_bn_apply_stats(bn_x, ybuf, n, c, hw, pk_pitch(c), dt, gamma,
+                                                   beta, saved_mean, saved_invstd, relu, st),
+                            "bn_apply");
+        primkit::check_cuda(pk_cuda_bn_bwd(bn_x, ybuf, dz, bn_dx, n, c, hw, pk_pitch(c), dt, 0, gamma,
+                                           saved_mean, saved_invstd, dgamma, dbeta, relu,
+                                           dt == PK_BF16, scratch, st),
+                            "bn_bwd");
     });
 }
 

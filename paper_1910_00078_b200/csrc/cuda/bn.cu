@@ -468,6 +468,20 @@ inline unsigned bn_vec_blocks(long long rows, int vpr) {
     return (unsigned)(b < 1 ? 1 : b);
 }
 
+// Single-launch persistent forms (bn_coop.cu); cudaErrorNotSupported when the
+// layout does not qualify (then the multi-kernel path below runs).
+size_t bn_coop_scratch_bytes(int c);
+cudaError_t bn_coop_fwd(const void* x, void* y, long long rows, int c, int pitch, int dtype,
+                        const float* gamma, const float* beta, float* running_mean,
+                        float* running_var, float eps, float momentum, float* saved_mean,
+                        float* saved_invstd, int relu, const float* ext, int ext_slots,
+                        void* scratch, cudaStream_t st);
+cudaError_t bn_coop_bwd(const void* x, const void* y, const void* dy, void* dx, long long rows,
+                        int c, int pitch, int dtype, const float* gamma, const float* beta,
+                        const float* mean, const float* invstd, float* dgamma, float* dbeta,
+                        int relu, int round_bf16, const float* ext, int ext_slots, float* tot,
+                        void* scratch, cudaStream_t st);
+
 inline unsigned gsz(long long total) {
     long long b = (total + 255) / 256;
     if (b > 148LL * 32) b = 148LL * 32;
@@ -486,6 +500,11 @@ cudaError_t pk_cuda_bn_finalize_apply(const float* part, int slots, const void* 
                                       float eps, float momentum, float* saved_mean,
                                       float* saved_invstd, int relu, cudaStream_t st) {
     const long long rows = (long long)n * hw;
+    if (bn_coop_fwd(x, y, rows, c, pitch, dtype, gamma, beta, running_mean, running_var, eps,
+                    momentum, saved_mean, saved_invstd, relu, part, slots, nullptr,
+                    st) == cudaSuccess)
+        return cudaSuccess;
+    cudaGetLastError();
     bn_finalize_partials_kernel<<<(c + 7) / 8, 256, 0, st>>>(
         part, slots, c, (double)rows, eps, momentum, running_mean, running_var, saved_mean,
         saved_invstd);
@@ -511,6 +530,10 @@ cudaError_t pk_cuda_bn_bwd_finalize_apply(const float* part, int slots, const vo
                                           cudaStream_t st) {
     if (!bn_vec_ok(dtype, pitch)) return cudaErrorNotSupported;
     const long long rows = (long long)n * hw;
+    if (bn_coop_bwd(y, nullptr, dz, dx, rows, c, pitch, dtype, gamma, beta, mean, invstd, dgamma,
+                    dbeta, relu, 1, part, slots, tot_scratch, nullptr, st) == cudaSuccess)
+        return cudaSuccess;
+    cudaGetLastError();
     bn_bwd_finalize_partials_kernel<<<(c + 7) / 8, 256, 0, st>>>(part, slots, c, 1, dgamma,
                                                                       dbeta, tot_scratch);
     bn_bwd_apply_bf16x8_kernel<<<bn_vec_blocks(rows, pitch / 8), 256, 0, st>>>(
@@ -538,10 +561,22 @@ cudaError_t pk_cuda_bn_apply_stats(const void* x, void* y, int n, int c, int hw,
     return cudaGetLastError();
 }
 
+cudaError_t pk_cuda_bn_bwd_fold(const void* x, const void* dz, void* dx, int n, int c, int hw,
+                                int pitch, int dtype, const float* gamma, const float* beta,
+                                const float* mean, const float* invstd, int relu, float* dgamma,
+                                float* dbeta, void* scratch, cudaStream_t st) {
+    const long long rows = (long long)n * hw;
+    float* tot = (float*)((char*)scratch + bn_coop_scratch_bytes(c) - (size_t)c * 2 * sizeof(float) - 256);
+    return bn_coop_bwd(x, nullptr, dz, dx, rows, c, pitch, dtype, gamma, beta, mean, invstd,
+                       dgamma, dbeta, relu, dtype == PK_BF16, nullptr, 0, tot, scratch, st);
+}
+
 size_t pk_bn_scratch_bytes(int n, int c, int hw, int per_act) {
     if (per_act) return (size_t)c * hw * 2 * sizeof(double);
     const int a = bn_chunks((long long)n * hw, c), b = bn_vec_chunks((long long)n * hw);
-    return (size_t)(a > b ? a : b) * c * 2 * sizeof(double);
+    const size_t legacy = (size_t)(a > b ? a : b) * c * 2 * sizeof(double);
+    const size_t coop = bn_coop_scratch_bytes(c);
+    return legacy > coop ? legacy : coop;
 }
 
 cudaError_t pk_cuda_bn_fwd_train(const void* x, void* y, int n, int c, int hw, int pitch,
@@ -550,6 +585,11 @@ cudaError_t pk_cuda_bn_fwd_train(const void* x, void* y, int n, int c, int hw, i
                                  float momentum, float* saved_mean, float* saved_invstd,
                                  int relu, void* scratch, cudaStream_t st) {
     const long long rows = (long long)n * hw;
+    if (!per_act && bn_coop_fwd(x, y, rows, c, pitch, dtype, gamma, beta, running_mean,
+                                running_var, eps, momentum, saved_mean, saved_invstd, relu,
+                                nullptr, 0, scratch, st) == cudaSuccess)
+        return cudaSuccess;
+    cudaGetLastError();
     double* part = (double*)scratch;
     int chunks = 1, nstat = c;
     double m = (double)rows;
@@ -594,6 +634,15 @@ cudaError_t pk_cuda_bn_bwd(const void* x, const void* y, const void* dy, void* d
                            float* dbeta, int relu, int round_params_bf16, void* scratch,
                            cudaStream_t st) {
     const long long rows = (long long)n * hw;
+    if (!per_act) {
+        // totals live behind the CTA partials in the scratch
+        float* tot = (float*)((char*)scratch + bn_coop_scratch_bytes(c) - (size_t)c * 2 * sizeof(float) - 256);
+        if (bn_coop_bwd(x, y, dy, dx, rows, c, pitch, dtype, gamma, nullptr, saved_mean,
+                        saved_invstd, dgamma, dbeta, relu, round_params_bf16, nullptr, 0, tot,
+                        scratch, st) == cudaSuccess)
+            return cudaSuccess;
+        cudaGetLastError();
+    }
     double* part = (double*)scratch;
     int chunks = 1, nstat = c;
     double m = (double)rows;

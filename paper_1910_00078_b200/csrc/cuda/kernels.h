@@ -261,6 +261,13 @@ cudaError_t pk_cuda_bn_bwd_finalize_apply(const float* part, int slots, const vo
                                           const float* mean, const float* invstd, int relu,
                                           float* dgamma, float* dbeta, float* tot_scratch,
                                           cudaStream_t st);
+// BN backward (+ReLU with the mask recomputed from the BN input x through the
+// folded affine, so the BN output is not needed) in one launch: statistics of
+// d = dz * mask, then dx; bf16 NHWC only (cudaErrorNotSupported otherwise).
+cudaError_t pk_cuda_bn_bwd_fold(const void* x, const void* dz, void* dx, int n, int c, int hw,
+                                int pitch, int dtype, const float* gamma, const float* beta,
+                                const float* mean, const float* invstd, int relu, float* dgamma,
+                                float* dbeta, void* scratch, cudaStream_t st);
 cudaError_t pk_cuda_bn_bwd(const void* x, const void* y, const void* dy, void* dx, int n, int c,
                            int hw, int pitch, int dtype, int per_act, const float* gamma,
                            const float* saved_mean, const float* saved_invstd, float* dgamma,

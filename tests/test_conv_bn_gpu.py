@@ -132,7 +132,7 @@ BWD_SHAPES = [  # the BackwardData convolution of the NEXT layer; its dX feeds t
 
 @pytest.mark.parametrize("si", range(len(BWD_SHAPES)))
 @pytest.mark.parametrize("relu", [0, 1])
-def test_dgrad_bn_backward(lib, si, relu):
+def test_dgrad_bn_backward(lib, si, relu, monkeypatch):
     rng = np.random.default_rng(700 + si)
     p = problem(**BWD_SHAPES[si], direction=abi.BACKWARD_DATA, etype=abi.BF16)
     ho = (p.h + 2 * p.pad_h - p.y) // p.stride_h + 1
@@ -151,7 +151,11 @@ def test_dgrad_bn_backward(lib, si, relu):
     g, b, sm, si_ = dev(gamma), dev(beta), dev(smean), dev(sinv)
     h = lib.handle()
     out = []
-    for fused in (True, False):
+    # fold: dgrad + one-launch BN backward, mask from the BN input (default);
+    # epi: statistics in the dgrad epilogue (PK_CBN_BWD_EPI=1); Direct: unfused
+    for mode in ("fold", "epi", "unfused"):
+        fused = mode != "unfused"
+        monkeypatch.setenv("PK_CBN_BWD_EPI", "1" if mode == "epi" else "0")
         dz = torch.zeros((p.n, p.h, p.w, cp), dtype=torch.bfloat16, device="cuda")
         bdx = torch.zeros_like(dz)
         dg, db = torch.zeros(p.c, device="cuda"), torch.zeros(p.c, device="cuda")
@@ -166,10 +170,13 @@ def test_dgrad_bn_backward(lib, si, relu):
             h.ptr, C.byref(p), solver, _vp(dy), _vp(w), _vp(dz), _vp(bx), _vp(g), _vp(b), _vp(sm),
             _vp(si_), int(relu), _vp(bdx), _vp(dg), _vp(db), _vp(wsb), C.c_size_t(wsb.numel())))
         torch.cuda.synchronize()
-        if fused:
+        if mode == "epi":
             assert "bn_bwd_stats_epilogue" in h.last_kernel(), h.last_kernel()
+        if mode == "fold":
+            assert "bn_bwd_fold" in h.last_kernel(), h.last_kernel()
         out.append((_nchw(dz, p.c), _nchw(bdx, p.c), dg.cpu().numpy(), db.cpu().numpy()))
-    (dz_f, bdx_f, dg_f, db_f), (dz_u, bdx_u, dg_u, db_u) = out
+    (dz_f, bdx_f, dg_f, db_f), (dz_e, bdx_e, dg_e, db_e), (dz_u, bdx_u, dg_u, db_u) = out
+    assert rel_l2(bdx_e, bdx_f) <= 2e-2 and rel_l2(dg_e, dg_f) <= 2e-2
     assert rel_l2(dz_f, oracle.conv_backward_data(p, dyn, wn)) <= 1e-2
     # reference BN backward on the stored dz, ReLU mask of the forward output
     mask = 1.0
