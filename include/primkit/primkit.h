@@ -393,6 +393,34 @@ PRIMKIT_API primkit_status primkit_handle_plan_cache_stats(primkit_handle* handl
 PRIMKIT_API primkit_status primkit_handle_last_variant(primkit_handle* handle, char* buf,
                                                       size_t buf_len);
 
+/* ---- auto-tuning of the B200 kernel choice (handle.cpp tune_kernels) ----
+ * The reference tunes only the ImplicitGemm forward grid (primkit_tune,
+ * handle.cpp:167-226 of the reference). Here every solver whose plan runs the
+ * tcgen05 families, in every direction, has a kernel choice
+ * "<block_n>,<family>,<pair>,<mt>,<split>" (0 = heuristic; see pk_tc_config):
+ * primkit_tune_kernels times the candidates on device tensors (U(-1,1), the
+ * handle's seed), drops any whose output differs from the heuristic choice's
+ * beyond the dtype tolerance, stores the fastest in the perf-db under
+ * "<solver>#sm100" and returns its values plus the heuristic and best medians. */
+PRIMKIT_API primkit_status primkit_tune_kernels(primkit_handle* handle,
+                                               const primkit_conv_problem* problem,
+                                               const char* solver_name, int64_t budget,
+                                               char* best_values, size_t buf_len,
+                                               double* default_ms, double* best_ms);
+/* The kernel choice a plan for (problem, solver) would run with after the
+ * perf-db lookups (user db, then the shipped system db). */
+PRIMKIT_API primkit_status primkit_plan_kernel_config(primkit_handle* handle,
+                                                     const primkit_conv_problem* problem,
+                                                     const char* solver_name, char* buf,
+                                                     size_t buf_len);
+/* Replace the handle's shipped ("system") perf-db, consulted after the user
+ * perf-db: NULL or "" disables it. At creation it is loaded from
+ * $PRIMKIT_SYSTEM_DB, else <libprimkit dir>/../db/sm100_b200.pkdb. */
+PRIMKIT_API primkit_status primkit_handle_load_system_db(primkit_handle* handle, const char* path);
+/* Path of the loaded system perf-db ("" when none) and its record count. */
+PRIMKIT_API primkit_status primkit_handle_system_db(primkit_handle* handle, char* buf,
+                                                   size_t buf_len, uint64_t* records);
+
 /* ---- 3. data-parallel weight-gradient all-reduce (north_star) ----
  * One process per GPU, the batch sharded over them. Backward-weights results
  * are registered in the order the backward pass produces them (reverse layer

@@ -118,6 +118,12 @@ SECTION2 = {
     "primkit_handle_last_device_ms": (ST, [P, C.POINTER(C.c_double)]),
     "primkit_handle_last_kernel": (ST, [P, C.c_char_p, C.c_size_t]),
     "primkit_handle_last_variant": (ST, [P, C.c_char_p, C.c_size_t]),
+    "primkit_tune_kernels": (ST, [P, C.POINTER(ConvProblem), C.c_char_p, C.c_int64, C.c_char_p,
+                                  C.c_size_t, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "primkit_plan_kernel_config": (ST, [P, C.POINTER(ConvProblem), C.c_char_p, C.c_char_p,
+                                        C.c_size_t]),
+    "primkit_handle_load_system_db": (ST, [P, C.c_char_p]),
+    "primkit_handle_system_db": (ST, [P, C.c_char_p, C.c_size_t, C.POINTER(C.c_uint64)]),
     "primkit_handle_plan_cache_stats": (ST, [P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                              C.POINTER(C.c_uint64)]),
     "primkit_pooling_output_dims": (ST, [I64P, I64P, I64P, I64P, I64P]),

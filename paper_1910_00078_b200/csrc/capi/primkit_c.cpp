@@ -1059,6 +1059,42 @@ primkit_status primkit_handle_last_variant(primkit_handle* h, char* buf, size_t 
     return guarded([&] { copy_name(buf, len, H(h).last_variant); });
 }
 
+primkit_status primkit_tune_kernels(primkit_handle* h, const primkit_conv_problem* pp,
+                                    const char* solver_name, int64_t budget, char* best_values,
+                                    size_t buf_len, double* default_ms, double* best_ms) {
+    return guarded([&] {
+        const primkit::ConvProblem p = to_problem(pp);
+        const primkit::Solver& s = solver_named(h, solver_name);
+        if (budget <= 0) budget = 256;
+        const primkit::KernelTuneResult r = primkit::tune_kernels(H(h), s, p, budget);
+        if (best_values) copy_name(best_values, buf_len, primkit::serialize_kernel_config(r.best));
+        if (default_ms) *default_ms = r.default_ms;
+        if (best_ms) *best_ms = r.best_ms;
+    });
+}
+
+primkit_status primkit_plan_kernel_config(primkit_handle* h, const primkit_conv_problem* pp,
+                                          const char* solver_name, char* buf, size_t buf_len) {
+    return guarded([&] {
+        const primkit::ConvProblem p = to_problem(pp);
+        const primkit::Solver& s = solver_named(h, solver_name);
+        auto plan = H(h).cached_build(p, s, nullptr);
+        copy_name(buf, buf_len, primkit::serialize_kernel_config(plan->kernel_config()));
+    });
+}
+
+primkit_status primkit_handle_load_system_db(primkit_handle* h, const char* path) {
+    return guarded([&] { H(h).load_system_db(path ? path : ""); });
+}
+
+primkit_status primkit_handle_system_db(primkit_handle* h, char* buf, size_t buf_len,
+                                        uint64_t* records) {
+    return guarded([&] {
+        if (buf) copy_name(buf, buf_len, H(h).system_db_path());
+        if (records) *records = H(h).system_db().size();
+    });
+}
+
 // ---- pooling / softmax (reference primitives.cpp:204-370) -------------------
 
 namespace {

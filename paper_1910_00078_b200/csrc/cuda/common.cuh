@@ -15,6 +15,19 @@ namespace pk {
 void count_launch(int n = 1);
 // Appends the kernel's template instance to the thread's variant log (pk_cuda_variant).
 void note_kernel(const void* fn);
+// Kernel choice in force for the calling thread's current top-level launcher
+// (set by pk_cuda_igemm_tc_fwd / _dgrad / _wgrad from their config argument,
+// read by the family dispatchers below them); nullptr = heuristics only.
+const pk_tc_config* active_tc_config();
+struct ActiveTcConfig {
+    explicit ActiveTcConfig(const pk_tc_config* c);
+    ~ActiveTcConfig();
+    const pk_tc_config* prev;
+};
+inline int cfg_field(int pk_tc_config::*f) {
+    const pk_tc_config* c = active_tc_config();
+    return c ? c->*f : 0;
+}
 
 template <typename T>
 struct Elt;

@@ -688,6 +688,9 @@ cudaError_t pk_cuda_igemm_tc_fwd(const pk_conv_geom* g, const void* x, const voi
                                  cudaStream_t st) {
     if (!pk_tc_fwd_supported(g) || !aligned16(x) || !aligned16(f) || !aligned16(y))
         return cudaErrorNotSupported;
+    const ActiveTcConfig active(cfg);
+    const int want_bn = cfg && cfg->block_n ? cfg->block_n : 256;
+    const int family = cfg ? cfg->family : 0, pair = cfg ? cfg->pair : 0;
     // narrow-channel stems: halo-staged fused kernel (stem_fused.cu)
     static const bool stem_on = [] {
         const char* v = std::getenv("PK_STEM_FUSED");
@@ -714,7 +717,7 @@ cudaError_t pk_cuda_igemm_tc_fwd(const pk_conv_geom* g, const void* x, const voi
     t.num_kb = (t.kred + BK - 1) / BK;
     t.n_out = g->k;
     t.out_pitch = g->y_pitch;
-    const int bn = pick_bn(cfg ? cfg->block_n : 256, g->y_pitch);
+    const int bn = pick_bn(want_bn, g->y_pitch);
     base_args(t, bn);
     t.total_tiles = ((t.M + BM - 1) / BM) * t.n_tiles_n;
     pk_epilogue e{};
@@ -727,18 +730,22 @@ cudaError_t pk_cuda_igemm_tc_fwd(const pk_conv_geom* g, const void* x, const voi
     if (plain) {
         // filter slice too large to stay resident: CTA-pair kernel (half the B bytes)
         static const bool pair_all = std::getenv("PK_TC2_ALL") != nullptr;  // A/B experiments
-        if (bn == 256 && (t.kred > 256 || pair_all) && !e.stats && !t.debug_nores &&
-            pk_gemm_pair_eligible(t.M, t.kred, g->k, g->y_pitch))
+        if (bn == 256 && pair != 1 && (t.kred > 256 || pair_all || pair == 2) && !e.stats &&
+            !t.debug_nores && pk_gemm_pair_eligible(t.M, t.kred, g->k, g->y_pitch))
             return pk_gemm_pair(x, f, y, t.M, t.kred, g->k, g->y_pitch, g->p, g->q, &e, st);
         if (!tc::make_map_2d(&amap, x, t.M, g->x_pitch, g->x_pitch, BM)) return cudaErrorInvalidValue;
         return dispatch_bn<PLAIN>(bn, amap, bmap, x, y, t, e, st);
     }
     // stride-1 spatial filters: halo-reuse tiles (input loaded once per tile)
-    const cudaError_t he = pk_halo_conv(g, false, x, f, y, &e, st);
-    if (he != cudaErrorNotSupported) return he;
+    if (family < 1) {
+        const cudaError_t he = pk_halo_conv(g, false, x, f, y, &e, st);
+        if (he != cudaErrorNotSupported) return he;
+    }
     // TMA rectangle tiles when the channel pitch is a multiple of 64
-    const cudaError_t te = pk_tma_conv(g, false, x, f, y, &e, cfg ? cfg->block_n : 256, st);
-    if (te != cudaErrorNotSupported) return te;
+    if (family < 2) {
+        const cudaError_t te = pk_tma_conv(g, false, x, f, y, &e, want_bn, st);
+        if (te != cudaErrorNotSupported) return te;
+    }
     return dispatch_bn<GATHER_FWD>(bn, amap, bmap, x, y, t, e, st);
 }
 
@@ -780,6 +787,9 @@ cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const 
                                    void* workspace, const pk_tc_config* cfg, cudaStream_t st,
                                    const pk_epilogue* stats_epi) {
     if (!pk_tc_dgrad_supported(g) || !aligned16(dy) || !aligned16(dx)) return cudaErrorNotSupported;
+    const ActiveTcConfig active(cfg);
+    const int want_bn = cfg && cfg->block_n ? cfg->block_n : 256;
+    const int family = cfg ? cfg->family : 0, pair = cfg ? cfg->pair : 0;
     const int kp = pk_pitch(g->k);
     const bool plain1x1 = g->r == 1 && g->s == 1 && g->str_h == 1 && g->str_w == 1 &&
                           g->pad_h == 0 && g->pad_w == 0;
@@ -801,11 +811,15 @@ cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const 
             se.bnb_invstd = stats_epi->bnb_invstd;
             se.bnb_relu = stats_epi->bnb_relu;
         }
-        const cudaError_t he = pk_halo_conv(g, true, dy, f, dx, stats_epi ? &se : nullptr, st, true);
-        if (he != cudaErrorNotSupported) return he;
-        const cudaError_t te = pk_tma_conv(g, true, dy, f, dx, stats_epi ? &se : nullptr,
-                                           cfg ? cfg->block_n : 256, st, true);
-        if (te != cudaErrorNotSupported) return te;
+        if (family < 1) {
+            const cudaError_t he = pk_halo_conv(g, true, dy, f, dx, stats_epi ? &se : nullptr, st, true);
+            if (he != cudaErrorNotSupported) return he;
+        }
+        if (family < 2) {
+            const cudaError_t te = pk_tma_conv(g, true, dy, f, dx, stats_epi ? &se : nullptr, want_bn,
+                                               st, true);
+            if (te != cudaErrorNotSupported) return te;
+        }
     }
     cudaError_t err = b_mn ? cudaSuccess : pk_cuda_filter_to_dgrad(g, PK_BF16, f, workspace, st);
     if (err != cudaSuccess) return err;
@@ -829,7 +843,7 @@ cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const 
     t.num_kb = (t.kred + BK - 1) / BK;
     t.n_out = g->c;
     t.out_pitch = g->x_pitch;
-    const int bn = pick_bn(cfg ? cfg->block_n : 256, g->x_pitch);
+    const int bn = pick_bn(want_bn, g->x_pitch);
     base_args(t, bn);
     t.total_tiles = ((t.M + BM - 1) / BM) * t.n_tiles_n;
     pk_epilogue e{};
@@ -853,18 +867,22 @@ cudaError_t pk_cuda_igemm_tc_dgrad(const pk_conv_geom* g, const void* dy, const 
     const bool plain = plain1x1;
     if (plain) {
         static const bool pair_all = std::getenv("PK_TC2_ALL") != nullptr;
-        if (bn == 256 && (t.kred > 256 || pair_all) && !e.stats && !t.debug_nores &&
-            pk_gemm_pair_eligible(t.M, t.kred, g->c, g->x_pitch))
+        if (bn == 256 && pair != 1 && (t.kred > 256 || pair_all || pair == 2) && !e.stats &&
+            !t.debug_nores && pk_gemm_pair_eligible(t.M, t.kred, g->c, g->x_pitch))
             return pk_gemm_pair(dy, b_mn ? f : workspace, dx, t.M, t.kred, g->c, g->x_pitch, g->h, g->w,
                                 nullptr, st, b_mn ? g->f_pitch : 0);
         if (!tc::make_map_2d(&amap, dy, t.M, g->y_pitch, g->y_pitch, BM)) return cudaErrorInvalidValue;
         return dispatch_bn<PLAIN>(bn, amap, bmap, dy, dx, t, e, st);
     }
-    const cudaError_t he = pk_halo_conv(g, true, dy, workspace, dx, stats_epi ? &e : nullptr, st);
-    if (he != cudaErrorNotSupported) return he;
-    const cudaError_t te = pk_tma_conv(g, true, dy, workspace, dx, stats_epi ? &e : nullptr,
-                                       cfg ? cfg->block_n : 256, st);
-    if (te != cudaErrorNotSupported) return te;
+    if (family < 1) {
+        const cudaError_t he = pk_halo_conv(g, true, dy, workspace, dx, stats_epi ? &e : nullptr, st);
+        if (he != cudaErrorNotSupported) return he;
+    }
+    if (family < 2) {
+        const cudaError_t te = pk_tma_conv(g, true, dy, workspace, dx, stats_epi ? &e : nullptr,
+                                           want_bn, st);
+        if (te != cudaErrorNotSupported) return te;
+    }
     if ((g->str_h > 1 || g->str_w > 1) && build_phases(t, g->n, g->h, g->w))
         return dispatch_bn<PHASE_DGRAD>(bn, amap, bmap, dy, dx, t, e, st);
     return dispatch_bn<GATHER_DGRAD>(bn, amap, bmap, dy, dx, t, e, st);

@@ -938,7 +938,8 @@ cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, cons
     // 256-pixel rectangles (two M=128 MMAs per filter stage) when the tile
     // width leaves TMEM room for two double-buffered accumulators
     static const bool mt_off = std::getenv("PK_TMA_MT1") != nullptr;
-    t.mt = (!mt_off && !narrow && sh == 1 && sw == 1 && bn <= 128) ? 2 : 1;
+    const int cfg_mt = cfg_field(&pk_tc_config::mt), cfg_pair = cfg_field(&pk_tc_config::pair);
+    t.mt = (!mt_off && cfg_mt != 1 && !narrow && sh == 1 && sw == 1 && bn <= 128) ? 2 : 1;
     const RectTile rt = tc::best_rect(g->n, hp0, wp0, BM * t.mt);
     t.bw = rt.bw;
     t.bh = rt.bh;
@@ -962,8 +963,9 @@ cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, cons
     }();
     t.m_tiles = t.n_tiles_n ? t.total_tiles / t.n_tiles_n : 0;
     t.total_pairs = 0;
-    if (!pair_off && !narrow && sh == 1 && sw == 1 && bn == 256 && t.mt == 1 && g->r * g->s > 1 &&
-        (!epi || !epi->stats) && (long long)((t.m_tiles + 1) / 2) * t.n_tiles_n >= 74)
+    if (!pair_off && cfg_pair != 1 && !narrow && sh == 1 && sw == 1 && bn == 256 && t.mt == 1 &&
+        g->r * g->s > 1 && (!epi || !epi->stats) &&
+        (cfg_pair == 2 || (long long)((t.m_tiles + 1) / 2) * t.n_tiles_n >= 74))
         t.total_pairs = (t.m_tiles + 1) / 2 * t.n_tiles_n;
     if (filt_mn) {
         // narrow sources use the dense tap order (not supported here); the filter
@@ -1011,7 +1013,15 @@ static int tma_wgrad_splits(int tiles_mn, int num_kb, int num_sms) {
     int splits = num_sms / tiles_mn;
     const int max_splits = num_kb / 4 > 1 ? num_kb / 4 : 1;
     if (splits > max_splits) splits = max_splits;
-    return splits < 1 ? 1 : splits;
+    if (splits < 1) splits = 1;
+    // tuned split-K: scale the one-wave count by split/4 (at least 2 k-blocks per split)
+    if (const int k = cfg_field(&pk_tc_config::split)) {
+        splits = splits * k / 4;
+        const int cap = num_kb / 2 > 1 ? num_kb / 2 : 1;
+        if (splits > cap) splits = cap;
+        if (splits < 1) splits = 1;
+    }
+    return splits;
 }
 
 // Filter-position tile width 256 and two output-channel tiles per CTA
@@ -1036,6 +1046,10 @@ static WgTile wgrad_tile(const pk_conv_geom* g) {
     if (t.nb == 128 && t.mt == 2 && g->r == 1 && g->s == 1 && (long long)g->n * g->p * g->q <= 16384 &&
         nn >= 512)
         t.nb = 256;
+    // tuned choices (pk_tc_config): tile width, one or two M tiles, CTA pairs
+    if (const int bn = cfg_field(&pk_tc_config::block_n); bn == 128 || bn == 256) t.nb = bn;
+    if (const int mt = cfg_field(&pk_tc_config::mt); mt == 1 || (mt == 2 && g->k >= 256)) t.mt = mt;
+    if (t.nb == 192 && t.mt == 2) t.nb = 256;
     if (env) {
         int nb = 0, mt = 0;
         if (std::sscanf(env, "%dx%d", &nb, &mt) == 2 && (nb == 128 || nb == 256 || (nb == 192 && mt == 1)) &&
@@ -1049,7 +1063,10 @@ static WgTile wgrad_tile(const pk_conv_geom* g) {
     }();
     // measured (ResNet-50 N=256): 1x1 layers gain 3-15% (conv3_1ds 71 -> 61 us), 3x3 lose
     const bool pair_ok = g->k % 256 == 0 && nn % 256 == 0;
-    if (pair_ok && (pair_env == 1 || (pair_env != 0 && g->r * g->s == 1))) t = {256, 1, true};
+    const int cfg_pair = cfg_field(&pk_tc_config::pair);
+    if (pair_ok && cfg_pair != 1 &&
+        (pair_env == 1 || cfg_pair == 2 || (pair_env != 0 && g->r * g->s == 1)))
+        t = {256, 1, true};
     return t;
 }
 

@@ -179,17 +179,29 @@ cudaError_t pk_cuda_fft_fwd(const pk_conv_geom* g, int dtype, const void* x, con
                             void* y, void* scratch, cudaStream_t st);
 
 // ---- tcgen05 implicit GEMM (bf16 in, fp32 TMEM accumulate) -------------------
+// Kernel choice of the tcgen05 convolution families (the auto-tuner's design
+// space, solver.cpp / handle.cpp tune). Every field: 0 = the built-in
+// heuristic; a value the geometry cannot honour falls back to the heuristic.
 typedef struct pk_tc_config {
-    int block_n;     // output-channel tile: 32..256 (multiple of 16)
-    int stages;      // smem pipeline depth
-    int raster;      // M-tile group width for L2-friendly rasterisation
+    int block_n;  // output-channel (fwd/dgrad) or filter-position (wgrad) tile: 64/128/256
+    int family;   // 1: no halo-reuse kernels; 2: no halo, no TMA rectangles (cp.async gather)
+    int pair;     // 1: never CTA pairs (cta_group::2); 2: CTA pairs wherever supported
+    int mt;       // 1: one M=128 tile per CTA; 2: two (256-pixel rectangles, M=256 wgrad)
+    int split;    // wgrad split-K: splits = max(1, one_wave_splits * split / 4)
 } pk_tc_config;
 // 1 if the tensor-core path supports this geometry (groups == 1, bf16, ...).
 int pk_tc_fwd_supported(const pk_conv_geom* g);
 int pk_tc_dgrad_supported(const pk_conv_geom* g);
 int pk_tc_wgrad_supported(const pk_conv_geom* g);
 size_t pk_tc_dgrad_workspace(const pk_conv_geom* g);
-size_t pk_tc_wgrad_workspace(const pk_conv_geom* g, int num_sms);
+// Streams `bytes` of `buf` through L2 (reads only): evicts the previous working
+// set before a timed run (Find / tune device timing).
+cudaError_t pk_cuda_l2_flush(const void* buf, size_t bytes, cudaStream_t st);
+// sums[0] = sum (a-b)^2, sums[1] = sum b^2 (device doubles) over n elements
+cudaError_t pk_cuda_sq_diff(const void* a, const void* b, long long n, int dtype, double* sums,
+                            cudaStream_t st);
+// split-K partials of pk_cuda_igemm_tc_wgrad under the same config
+size_t pk_tc_wgrad_workspace(const pk_conv_geom* g, int num_sms, const pk_tc_config* cfg);
 cudaError_t pk_cuda_igemm_tc_fwd(const pk_conv_geom* g, const void* x, const void* f, void* y,
                                  const pk_epilogue* epi, const pk_tc_config* cfg,
                                  cudaStream_t st);

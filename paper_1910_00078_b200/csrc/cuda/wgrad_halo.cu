@@ -224,6 +224,7 @@ bool halo_args(const pk_conv_geom* g, HwArgs& a) {
 using namespace pk;
 
 int pk_halo_wgrad_splits(const pk_conv_geom* g, int num_sms) {
+    if (cfg_field(&pk_tc_config::family) >= 1) return 0;  // tuned: no halo kernels
     HwArgs a;
     if (!halo_args(g, a)) return 0;
     return a.total_kb < num_sms ? a.total_kb : num_sms;

@@ -245,7 +245,8 @@ static int wgrad_splits(const pk_conv_geom* g, int num_sms) {
     return splits;
 }
 
-size_t pk_tc_wgrad_workspace(const pk_conv_geom* g, int num_sms) {
+size_t pk_tc_wgrad_workspace(const pk_conv_geom* g, int num_sms, const pk_tc_config* cfg) {
+    const ActiveTcConfig active(cfg);
     if (pk_tma_wgrad_supported(g)) return pk_tma_wgrad_workspace(g, num_sms);
     return (size_t)wgrad_splits(g, num_sms) * g->k * g->r * g->s * pk_pitch(g->cg) * 4;
 }
@@ -253,8 +254,8 @@ size_t pk_tc_wgrad_workspace(const pk_conv_geom* g, int num_sms) {
 cudaError_t pk_cuda_igemm_tc_wgrad(const pk_conv_geom* g, const void* dy, const void* x, void* dw,
                                    void* workspace, int num_sms, const pk_tc_config* cfg,
                                    cudaStream_t st) {
-    (void)cfg;
     if (!pk_tc_wgrad_supported(g)) return cudaErrorNotSupported;
+    const ActiveTcConfig active(cfg);
     if (pk_tma_wgrad_supported(g)) return pk_tma_wgrad(g, dy, x, dw, workspace, num_sms, st);
     WgGeom w{};
     w.K = g->k;

@@ -99,16 +99,7 @@ OpCounters counters_for(const ConvProblem& p, ConvAlgo algo) {
     return c;
 }
 
-// tcgen05 tiling selected by the ImplicitGemm perf config (solver.cpp).
-pk_tc_config tc_config(const ImplicitGemmTiles& t) {
-    pk_tc_config cfg{};
-    cfg.block_n = static_cast<int>(256 / std::max<std::int64_t>(1, t.tile_m));
-    cfg.raster = static_cast<int>(t.tile_n);
-    cfg.stages = t.tile_k == 1 ? 4 : t.tile_k == 2 ? 3 : 2;
-    return cfg;
-}
-
-const pk_tc_config kDefaultTc{256, 4, 1};
+const pk_tc_config kDefaultTc{};  // heuristics throughout
 
 // Output tile of the bf16 tensor-core Winograd: F(2x2,3x3) as the reference
 // (conv.cpp:269-365); PK_WINOGRAD_M=4 selects F(4x4,3x3).
@@ -202,7 +193,7 @@ std::size_t stem_workspace(const pk_conv_geom& g, ConvDirection dir, int num_sms
         case ConvDirection::BackwardData: return col + align256(kcp * pk_pitch(g.k) * 2);
         default: {
             const pk_conv_geom wg = gemm_geom((long long)rows, (int)kcp, g.k);
-            return col + align256((std::size_t)g.k * kcp * 2) + pk_tc_wgrad_workspace(&wg, num_sms);
+            return col + align256((std::size_t)g.k * kcp * 2) + pk_tc_wgrad_workspace(&wg, num_sms, &kDefaultTc);
         }
     }
 }
@@ -298,7 +289,8 @@ std::size_t ConvPlan::device_workspace_bytes(int num_sms) const {
                 return pk_direct_wgrad_tiled_supported(&g) ? pk_direct_wgrad_tiled_workspace(&g, num_sms)
                                                            : 0;
             if (algo_ == ConvAlgo::Im2colGemm) {
-                if (dt == PK_BF16 && pk_tc_wgrad_supported(&g)) return pk_tc_wgrad_workspace(&g, num_sms);
+                if (dt == PK_BF16 && pk_tc_wgrad_supported(&g))
+                    return pk_tc_wgrad_workspace(&g, num_sms, &kcfg_);
                 return align256(col_bytes(g, dt)) + (std::size_t)g.k * g.r * g.s * g.f_pitch * 4;
             }
             return 0;
@@ -385,8 +377,7 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                     run_stem(g, dir, a, b, out, ws, epi, h.num_sms(), st);
                 } else if (dt == PK_BF16 && pk_tc_fwd_supported(&g)) {
                     kernel = "igemm_tc_fwd";
-                    const pk_tc_config cfg = tc_config(tiles_);
-                    ck(pk_cuda_igemm_tc_fwd(&g, a, b, out, epi, &cfg, st), "igemm_tc_fwd");
+                    ck(pk_cuda_igemm_tc_fwd(&g, a, b, out, epi, &kcfg_, st), "igemm_tc_fwd");
                 } else if (pk_depthwise_supported(&g)) {
                     kernel = "depthwise_simt";
                     ck(pk_cuda_depthwise_fwd(&g, dt, a, b, out, epi, h.num_sms(), st), "depthwise_fwd");
@@ -489,7 +480,7 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
             run_stem(g, dir, a, b, out, ws, nullptr, h.num_sms(), st);
         } else if (dt == PK_BF16 && pk_tc_dgrad_supported(&g)) {
             kernel = "igemm_tc_dgrad";
-            ck(pk_cuda_igemm_tc_dgrad(&g, a, b, out, ws, &kDefaultTc, st,
+            ck(pk_cuda_igemm_tc_dgrad(&g, a, b, out, ws, &kcfg_, st,
                                       (epi && epi->stats) ? epi : nullptr),
                "igemm_tc_dgrad");
         } else {
@@ -531,7 +522,7 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
             run_stem(g, dir, a, b, out, ws, nullptr, h.num_sms(), st);
         } else if (dt == PK_BF16 && pk_tc_wgrad_supported(&g)) {
             kernel = "igemm_tc_wgrad";
-            ck(pk_cuda_igemm_tc_wgrad(&g, a, b, out, ws, h.num_sms(), &kDefaultTc, st),
+            ck(pk_cuda_igemm_tc_wgrad(&g, a, b, out, ws, h.num_sms(), &kcfg_, st),
                "igemm_tc_wgrad");
         } else {
             kernel = "im2col+gemm_simt_wgrad";

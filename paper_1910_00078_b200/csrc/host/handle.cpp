@@ -1,6 +1,9 @@
 #include "handle.hpp"
 
+#include <dlfcn.h>
+
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdlib>
 #include <random>
@@ -21,6 +24,17 @@ double steady_ms() {
 std::filesystem::path default_cache_dir() {
     if (const char* env = std::getenv("PRIMKIT_CACHE_DIR"); env && *env) return env;
     return std::filesystem::temp_directory_path() / "primkit-cache";
+}
+
+// $PRIMKIT_SYSTEM_DB (empty: none), else the db shipped next to the library.
+std::string default_system_db() {
+    if (const char* env = std::getenv("PRIMKIT_SYSTEM_DB")) return env;
+    Dl_info info{};
+    if (dladdr(reinterpret_cast<void*>(&default_system_db), &info) && info.dli_fname) {
+        const std::filesystem::path lib = std::filesystem::absolute(info.dli_fname);
+        return (lib.parent_path().parent_path() / "db" / "sm100_b200.pkdb").string();
+    }
+    return "";
 }
 
 FindEnforce env_find_enforce() {
@@ -70,6 +84,30 @@ Handle::Handle()
       clock_(steady_ms),
       find_enforce_(env_find_enforce()) {
     device_ = -1;  // resolved lazily: host-only queries never touch the GPU
+    try {
+        load_system_db(default_system_db());
+    } catch (const Error&) {
+        system_db_ = PerfDb{};  // unreadable / corrupt shipped db: run untuned
+        system_db_path_.clear();
+    }
+}
+
+void Handle::load_system_db(const std::string& path) {
+    system_db_ = PerfDb{};
+    system_db_path_.clear();
+    if (path.empty()) return;
+    std::error_code ec;
+    if (!std::filesystem::is_regular_file(path, ec)) return;
+    system_db_ = PerfDb::load(path);
+    system_db_path_ = path;
+}
+
+bool Handle::kernel_record(const ConvProblem& problem, const Solver& solver, pk_tc_config* out) const {
+    const std::string name = solver.name() + kKernelRecordSuffix;
+    for (const PerfDb* db : {&perfdb_, &system_db_})
+        if (auto values = db->get(problem.key(), name))
+            if (parse_kernel_config(*values, out)) return true;
+    return false;
 }
 
 Handle::Handle(cudaStream_t stream, int device) : Handle() {
@@ -168,12 +206,15 @@ const Solver* Handle::find_solver(const std::string& name) const {
 }
 
 PerfConfig Handle::resolve_config(const ConvProblem& problem, const Solver& solver) const {
-    if (auto values = perfdb_.get(problem.key(), solver.name())) {
-        try {
-            PerfConfig c = solver.config_from_values(problem, *values);
-            if (solver.config_valid(problem, c)) return c;
-        } catch (const Error&) {
-            // stale / foreign record -> default
+    // user perf-db first, then the shipped one (a tuned user record wins)
+    for (const PerfDb* db : {&perfdb_, &system_db_}) {
+        if (auto values = db->get(problem.key(), solver.name())) {
+            try {
+                PerfConfig c = solver.config_from_values(problem, *values);
+                if (solver.config_valid(problem, c)) return c;
+            } catch (const Error&) {
+                // stale / foreign record -> next db / default
+            }
         }
     }
     return solver.default_config(problem);
@@ -183,12 +224,21 @@ std::shared_ptr<const ConvPlan> Handle::cached_build(const ConvProblem& problem,
                                                      const Solver& solver,
                                                      const PerfConfig* config) {
     const PerfConfig resolved = config ? *config : resolve_config(problem, solver);
-    const std::string key =
-        PlanCache::hash_key(problem.key(), solver.name(), resolved.serialize_values());
+    pk_tc_config kc{};
+    const bool has_kc = kernel_record(problem, solver, &kc);
+    std::string values = resolved.serialize_values();
+    std::string descriptor = plan_descriptor(problem, solver, resolved);
+    if (has_kc) {  // a kernel record makes it a different plan
+        values += '|' + serialize_kernel_config(kc);
+        descriptor += "kernel " + serialize_kernel_config(kc) + '\n';
+    }
+    const std::string key = PlanCache::hash_key(problem.key(), solver.name(), values);
     auto make = [&]() -> std::shared_ptr<void> {
-        return std::make_shared<ConvPlan>(solver.build_plan(problem, &resolved));
+        auto p = std::make_shared<ConvPlan>(solver.build_plan(problem, &resolved));
+        if (has_kc) p->set_kernel_config(kc);
+        return p;
     };
-    auto plan = plan_cache_->get_or_build(key, plan_descriptor(problem, solver, resolved), make,
+    auto plan = plan_cache_->get_or_build(key, descriptor, make,
                                           [&](const std::string&) { return make(); });
     return std::static_pointer_cast<const ConvPlan>(plan);
 }
@@ -196,6 +246,16 @@ std::shared_ptr<const ConvPlan> Handle::cached_build(const ConvProblem& problem,
 double Handle::time_ms(const std::function<void()>& fn) {
     activate();
     if (device_timing_) {
+        // cold L2, as inside a training step where each layer's operands were
+        // evicted by the layers in between: tuning against warm-L2 repeats
+        // measured choices that lose in the step (ResNet-50 conv5 fits L2)
+        constexpr std::size_t kFlush = 192ull << 20;  // > 126 MB L2
+        void* flush = scratch(14, kFlush);
+        if (!flush_init_) {
+            check_cuda(cudaMemsetAsync(flush, 0, kFlush, stream_), "cudaMemsetAsync");
+            flush_init_ = true;
+        }
+        check_cuda(pk_cuda_l2_flush(flush, kFlush, stream_), "l2_flush");
         check_cuda(cudaEventRecord(ev0_, stream_), "cudaEventRecord");
         fn();
         check_cuda(cudaEventRecord(ev1_, stream_), "cudaEventRecord");
@@ -315,6 +375,113 @@ TuneResult tune(Handle& handle, const Solver& solver, const ConvProblem& problem
     }
     if (best < 0.0) throw_error(ErrorCode::NoValidConfig, "all configs pruned");
     handle.perfdb().set(problem.key(), solver.name(), result.best.serialize_values());
+    return result;
+}
+
+// ---- kernel-choice tuning (B200 design space) --------------------------------
+
+namespace {
+
+std::vector<pk_tc_config> kernel_candidates(ConvDirection dir) {
+    std::vector<pk_tc_config> out;
+    out.push_back(pk_tc_config{});  // heuristics: the reference point
+    if (dir == ConvDirection::BackwardWeights) {
+        const int pm[4][2] = {{0, 0}, {1, 1}, {1, 2}, {2, 0}};
+        for (int bn : {0, 128, 256})
+            for (int fam : {0, 1})
+                for (const auto& q : pm)
+                    for (int split : {0, 2, 8}) {
+                        pk_tc_config c{bn, fam, q[0], q[1], split};
+                        if (bn || fam || q[0] || q[1] || split) out.push_back(c);
+                    }
+    } else {
+        const int pm[5][2] = {{0, 0}, {1, 1}, {2, 2}, {1, 0}, {0, 1}};
+        for (int bn : {0, 128, 64})
+            for (int fam : {0, 1, 2})
+                for (const auto& q : pm) {
+                    pk_tc_config c{bn, fam, q[0], q[1], 0};
+                    if (bn || fam || q[0] || q[1]) out.push_back(c);
+                }
+    }
+    return out;
+}
+
+}  // namespace
+
+KernelTuneResult tune_kernels(Handle& handle, const Solver& solver, const ConvProblem& problem,
+                              std::int64_t budget) {
+    if (budget < 1) throw_error(ErrorCode::InvalidValue, "tuning budget must be >= 1");
+    if (!solver.is_applicable(problem))
+        throw_error(ErrorCode::NoApplicableSolver, solver.name() + " is not applicable to " + problem.key());
+    const TensorDescriptor da =
+        problem.direction == ConvDirection::Forward ? problem.input_desc() : problem.output_desc();
+    const TensorDescriptor db = problem.direction == ConvDirection::BackwardWeights
+                                    ? problem.input_desc()
+                                    : problem.filter_desc();
+    void* a = handle.scratch(4, device_bytes(da));
+    void* b = handle.scratch(5, device_bytes(db));
+    random_device_tensor(handle, da, handle.rng_seed, a);
+    random_device_tensor(handle, db, handle.rng_seed + 1, b);
+    const TensorDescriptor dr = result_desc(problem);
+    const std::size_t out_bytes = device_bytes(dr);
+    void* out = handle.scratch(3, out_bytes);
+    void* ref = handle.scratch(6, out_bytes);
+    auto* sums = static_cast<double*>(handle.scratch(9, 2 * sizeof(double)));
+    const int dt = problem.etype == ElementType::BF16 ? PK_BF16 : PK_F32;
+    const long long elems = static_cast<long long>(out_bytes / etype_bytes(problem.etype));
+    const double tol = problem.etype == ElementType::BF16 ? 1e-2 : 1e-4;
+
+    const PerfConfig base_cfg = handle.resolve_config(problem, solver);
+    const ConvPlan base = solver.build_plan(problem, &base_cfg);
+    auto candidates = kernel_candidates(problem.direction);
+    if (static_cast<std::int64_t>(candidates.size()) > budget)
+        candidates.resize(static_cast<std::size_t>(budget));
+
+    KernelTuneResult result;
+    std::map<std::string, double> seen;  // kernel instances (+ split) -> median ms
+    double best = -1.0;
+    for (std::size_t i = 0; i < candidates.size(); ++i) {
+        ConvPlan plan = base;
+        plan.set_kernel_config(candidates[i]);
+        const std::size_t dws = plan.device_workspace_bytes(handle.num_sms());
+        void* ws = handle.scratch(0, dws);
+        result.evaluations += 1;
+        plan.run(handle, a, b, i == 0 ? ref : out, ws, dws);  // warm-up + variant
+        std::string variant = handle.last_variant;
+        if (problem.direction == ConvDirection::BackwardWeights)
+            variant += "/split" + std::to_string(candidates[i].split);
+        if (i > 0) {
+            if (seen.count(variant)) continue;  // same kernels as an earlier candidate
+            // a candidate must compute the same convolution as the heuristic choice
+            check_cuda(pk_cuda_sq_diff(out, ref, elems, dt, sums, handle.stream()), "sq_diff");
+            double hs[2] = {0.0, 0.0};
+            check_cuda(cudaMemcpyAsync(hs, sums, sizeof(hs), cudaMemcpyDeviceToHost, handle.stream()),
+                       "cudaMemcpyAsync");
+            handle.sync();
+            const double rel = hs[1] > 0.0 ? std::sqrt(hs[0] / hs[1]) : std::sqrt(hs[0]);
+            if (!(rel <= tol)) continue;
+        }
+        std::vector<double> times;
+        for (int run = 0; run < Handle::kTimedRuns; ++run)
+            times.push_back(handle.time_ms([&] { plan.run(handle, a, b, out, ws, dws); }));
+        const double med = median_of(std::move(times));
+        seen[variant] = med;
+        if (i == 0) result.default_ms = med;
+        if (best < 0.0 || med < best) {
+            best = med;
+            result.best = candidates[i];
+            result.best_variant = variant;
+        }
+    }
+    // keep the heuristic choice unless a candidate beats it by more than the
+    // run-to-run spread (2%): a record is a claim that the choice pays
+    if (result.best_variant != "" && best > 0.98 * result.default_ms) {
+        result.best = pk_tc_config{};
+        best = result.default_ms;
+    }
+    result.best_ms = best;
+    handle.perfdb().set(problem.key(), solver.name() + kKernelRecordSuffix,
+                        serialize_kernel_config(result.best));
     return result;
 }
 

@@ -93,6 +93,18 @@ public:
                                                  const PerfConfig* config);
     PerfConfig resolve_config(const ConvProblem& problem, const Solver& solver) const;
 
+    // Shipped ("system") perf-db, consulted after the user perf-db by
+    // resolve_config and kernel_record: tuned configs and kernel records for
+    // the ResNet-50 / VGG-16 benchmark shapes (MIOpen ships tuned parameters,
+    // PAPER.md:69). Loaded at handle creation from $PRIMKIT_SYSTEM_DB, else
+    // <library dir>/../db/sm100_b200.pkdb; an empty path disables it.
+    void load_system_db(const std::string& path);
+    const PerfDb& system_db() const { return system_db_; }
+    const std::string& system_db_path() const { return system_db_path_; }
+    // The "<solver>#sm100" kernel record for the problem (user db, then system
+    // db), if any.
+    bool kernel_record(const ConvProblem& problem, const Solver& solver, pk_tc_config* out) const;
+
     // Device context.
     int device() const { return device_; }
     cudaStream_t stream() const { return stream_; }
@@ -131,6 +143,8 @@ private:
 
     OpCounters counters_;
     PerfDb perfdb_;
+    PerfDb system_db_;
+    std::string system_db_path_;
     std::shared_ptr<PlanCache> plan_cache_;
     std::vector<std::shared_ptr<const Solver>> solvers_;
     std::function<double()> clock_;
@@ -146,6 +160,7 @@ private:
     std::vector<cudaEvent_t> events_;
     std::map<int, DeviceBuffer> scratch_;
     double last_device_ms_ = 0.0;
+    bool flush_init_ = false;
 };
 
 struct TuneResult {
@@ -155,6 +170,21 @@ struct TuneResult {
 
 TuneResult tune(Handle& handle, const Solver& solver, const ConvProblem& problem,
                 std::int64_t budget, bool exhaustive = false);
+
+// Device-timed search over the tcgen05 kernel choices (pk_tc_config) for a
+// problem under any solver whose plan runs the tensor-core families, every
+// direction (the reference's tune covers only the ImplicitGemm forward grid).
+// Candidates that launch the same kernel instances are timed once. The best
+// is recorded in the perf-db as "<solver>#sm100" and used by later builds.
+struct KernelTuneResult {
+    pk_tc_config best{};
+    double best_ms = 0.0;
+    double default_ms = 0.0;
+    std::int64_t evaluations = 0;
+    std::string best_variant;
+};
+KernelTuneResult tune_kernels(Handle& handle, const Solver& solver, const ConvProblem& problem,
+                              std::int64_t budget);
 std::int64_t default_tune_budget(const Solver& solver, const ConvProblem& problem);
 
 // ---- host <-> device operand staging (the host-buffer ABI) ----

@@ -347,6 +347,29 @@ class Handle:
         self._c("primkit_handle_last_variant", buf, 1024)
         return buf.value.decode()
 
+    def tune_kernels(self, p, solver: str, budget: int = 0) -> tuple[str, float, float]:
+        """B200 kernel-choice search (primkit_tune_kernels): (best values,
+        heuristic median ms, best median ms); the best is stored in the perf-db."""
+        buf = C.create_string_buffer(64)
+        d, b = C.c_double(), C.c_double()
+        self._c("primkit_tune_kernels", C.byref(p), solver.encode(), budget, buf, 64, C.byref(d),
+                C.byref(b))
+        return buf.value.decode(), d.value, b.value
+
+    def kernel_config(self, p, solver: str) -> str:
+        buf = C.create_string_buffer(64)
+        self._c("primkit_plan_kernel_config", C.byref(p), solver.encode(), buf, 64)
+        return buf.value.decode()
+
+    def load_system_db(self, path: str | None):
+        self._c("primkit_handle_load_system_db", (path or "").encode())
+
+    def system_db(self) -> tuple[str, int]:
+        buf = C.create_string_buffer(4096)
+        n = C.c_uint64()
+        self._c("primkit_handle_system_db", buf, 4096, C.byref(n))
+        return buf.value.decode(), n.value
+
 
 class FusionPlan:
     def __init__(self, lib: Library, dims, etype=abi.F32):
