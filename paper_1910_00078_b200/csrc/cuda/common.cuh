@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -155,8 +156,35 @@ __device__ __forceinline__ void epilogue_chunk64(const pk_epilogue& e, float (&x
 // (16-byte chunks XOR-swizzled by lane & 7) for a TMA / coalesced store.
 // Channels at or beyond `valid` are written as zero; the common full chunk
 // takes the mask-free path (the per-element selects cost 3x the packing).
+__device__ __forceinline__ uint32_t pack2(float a, float b, bool f16) {
+    if (f16) {
+        __half2 h2 = __floats2half2_rn(a, b);
+        return *reinterpret_cast<uint32_t*>(&h2);
+    }
+    __nv_bfloat162 b2 = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&b2);
+}
+
+// f16: stage IEEE fp16 instead of bf16 (the fp16 transform domain of the
+// tensor-core Winograd, winograd_tc.cu).
 __device__ __forceinline__ void pack_stage64(const float (&xf)[64], uint32_t stg_u, int lane,
-                                             int valid) {
+                                             int valid, bool f16 = false) {
+    if (f16) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            uint32_t w[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int c = jj * 8 + 2 * e;
+                w[e] = pack2(c < valid ? xf[c] : 0.0f, c + 1 < valid ? xf[c + 1] : 0.0f, true);
+            }
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                             stg_u + lane * 128 + ((jj ^ (lane & 7)) << 4)),
+                         "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                         : "memory");
+        }
+        return;
+    }
     if (valid >= 64) {
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {

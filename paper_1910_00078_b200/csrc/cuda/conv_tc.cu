@@ -65,6 +65,9 @@ struct ConvTcArgs {
     // rows_per_batch = b_batch_mtiles * BM; B rows of batch b start at
     // b * b_batch_rows. 0 = not batched.
     int b_batch_mtiles, b_batch_rows;
+    // batched plain GEMM only: A, B and the output are IEEE fp16 (Winograd
+    // transform domain), the accumulator fp32 as always
+    int f16;
     // plain modes: B given MN-major (the filter W[K][C] itself for backward data,
     // no transpose launch): BN/64 atoms of 64 output channels x 64 k per k-block
     int b_mn;
@@ -332,7 +335,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     } else if (warp == 4) {
         // ======================= MMA issuer ==================================
-        const uint32_t idesc = idesc_bf16_f32(BM, BN, false, kPlain && g.b_mn);
+        const uint32_t idesc = (kPlain && g.f16) ? idesc_f16_f32(BM, BN, false, false)
+                                                 : idesc_bf16_f32(BM, BN, false, kPlain && g.b_mn);
         // B k-step (16 k): K-major +32 B, MN-major +16 rows (2048 B); atoms 8 KB apart
         const uint64_t bks = kPlain && g.b_mn ? 128 : 2;
         int stage = 0;
@@ -466,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int e = 0; e < 64; ++e) xf[e] = __uint_as_float(v[e]);
                 if (has_epi) epilogue_chunk64(epi, xf, n0 + c0, g.n_out, my_oy, my_ox, g.Ho, g.Wo);
-                pack_stage64(xf, stg_u, lane, min(g.n_out - (n0 + c0), BN - c0));
+                pack_stage64(xf, stg_u, lane, min(g.n_out - (n0 + c0), BN - c0), kPlain && g.f16);
                 if (kTmaStore) {
                     fence_proxy_async_smem();
                     __syncwarp();
@@ -751,7 +755,7 @@ cudaError_t pk_cuda_igemm_tc_fwd(const pk_conv_geom* g, const void* x, const voi
 
 cudaError_t pk_cuda_gemm_tc_batched(const void* a, const void* b, void* y, int batch,
                                     int rows_per_batch, int kdim, int n_out, int b_rows_per_batch,
-                                    int out_pitch, cudaStream_t st) {
+                                    int out_pitch, cudaStream_t st, int f16) {
     if (rows_per_batch % BM || kdim % 8 || out_pitch % 8 || !aligned16(a) || !aligned16(b) ||
         !aligned16(y) || tc::encode_fn() == nullptr)
         return cudaErrorNotSupported;
@@ -774,6 +778,7 @@ cudaError_t pk_cuda_gemm_tc_batched(const void* a, const void* b, void* y, int b
     t.total_tiles = (t.M / BM) * t.n_tiles_n;
     t.b_batch_mtiles = rows_per_batch / BM;
     t.b_batch_rows = b_rows_per_batch;
+    t.f16 = f16;
     pk_epilogue e{};
     e.act = -1;
     CUtensorMap amap{}, bmap{};

@@ -171,7 +171,7 @@ cudaError_t pk_cuda_winograd_tc(const pk_conv_geom* g, int m, const void* x, con
 // fp32 accumulate, bf16 out). A/Y rows per batch must be a multiple of 128.
 cudaError_t pk_cuda_gemm_tc_batched(const void* a, const void* b, void* y, int batch,
                                     int rows_per_batch, int kdim, int n_out, int b_rows_per_batch,
-                                    int out_pitch, cudaStream_t st);
+                                    int out_pitch, cudaStream_t st, int f16);
 
 // ---- FFT convolution (complex<double>, radix-2, pow2 planes) -----------------
 size_t pk_cuda_fft_scratch_bytes(const pk_conv_geom* g);

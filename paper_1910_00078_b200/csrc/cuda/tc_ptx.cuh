@@ -176,6 +176,12 @@ __device__ __forceinline__ uint64_t umma_desc_noswz(uint32_t saddr, uint32_t lbo
     return d;
 }
 
+// Instruction descriptor: kind::f16, A/B = fp16, D = f32 (bf16 bits 7/10 clear).
+__host__ __device__ constexpr uint32_t idesc_f16_f32(int m, int n, bool a_mn_major, bool b_mn_major) {
+    return (1u << 4) | ((a_mn_major ? 1u : 0u) << 15) | ((b_mn_major ? 1u : 0u) << 16) |
+           (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
+}
+
 // Instruction descriptor: kind::f16, A/B = bf16, D = f32.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int m, int n, bool a_mn_major,
                                                       bool b_mn_major) {

@@ -13,8 +13,17 @@
 // 128 contiguous bytes of one pixel row, so every patch load is coalesced),
 // applies the separable transform in fp32 and rounds once to bf16. Edge tiles
 // are zero padded on input and cropped on output exactly as the reference.
-// V and M live in a handle-owned workspace; large problems are processed in
+// V and M live in the caller's workspace; large problems are processed in
 // chunks of tiles so the workspace stays bounded (pk_winograd_tc_workspace).
+//
+// Transform-domain precision: F(2,3) stores U, V, M in bf16 (the reference's
+// round-on-store element type). F(4,3) amplifies every rounding through its
+// 6x6 transforms (B^T entries up to 5, A^T up to 8): in bf16 the U, V and M
+// roundings alone each cost ~1.8e-2 relative L2, so F(4,3) runs its transform
+// domain in IEEE fp16 (8x finer mantissa, kind::f16 MMAs with fp32
+// accumulation at the same rate), valid while |V| and |M| stay below 65504.
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -71,9 +80,19 @@ __device__ __forceinline__ float2 ld_bf2(const __nv_bfloat16* p) {
     const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(p);
     return __bfloat1622float2(v);
 }
+__device__ __forceinline__ float2 ld_bf2(const __half* p) {
+    return __half22float2(*reinterpret_cast<const __half2*>(p));
+}
 __device__ __forceinline__ void st_bf2(__nv_bfloat16* p, float a, float b) {
     *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(a, b);
 }
+__device__ __forceinline__ void st_bf2(__half* p, float a, float b) {
+    *reinterpret_cast<__half2*>(p) = __floats2half2_rn(a, b);
+}
+
+// element type of U, V, M for F(m x m, 3 x 3)
+template <int M_>
+using TDom = typename std::conditional<M_ == 4, __half, __nv_bfloat16>::type;
 
 struct WinoArgs {
     int n, h, w, p, q, pad_h, pad_w;
@@ -87,7 +106,7 @@ struct WinoArgs {
 template <int M_>
 __global__ void __launch_bounds__(256) winograd_input_kernel(WinoArgs a,
                                                              const __nv_bfloat16* __restrict__ x,
-                                                             __nv_bfloat16* __restrict__ v) {
+                                                             TDom<M_>* __restrict__ v) {
     using W = Wino<M_>;
     constexpr int AL = W::A;
     const int c2n = a.cp / 2;
@@ -96,7 +115,7 @@ __global__ void __launch_bounds__(256) winograd_input_kernel(WinoArgs a,
     const int c = (int)(idx - lt * c2n) * 2;
     if (lt >= a.rows) return;
     const size_t plane = (size_t)a.rows * a.cp;
-    __nv_bfloat16* vo = v + (size_t)lt * a.cp + c;
+    TDom<M_>* vo = v + (size_t)lt * a.cp + c;
     if (lt >= a.tc) {
 #pragma unroll
         for (int xi = 0; xi < AL * AL; ++xi) st_bf2(vo + xi * plane, 0.f, 0.f);
@@ -163,7 +182,7 @@ __global__ void __launch_bounds__(256) winograd_input_kernel(WinoArgs a,
 template <int M_>
 __global__ void __launch_bounds__(256) winograd_filter_kernel(int K, int cp,
                                                               const __nv_bfloat16* __restrict__ f,
-                                                              __nv_bfloat16* __restrict__ u) {
+                                                              TDom<M_>* __restrict__ u) {
     using W = Wino<M_>;
     constexpr int AL = W::A;
     const int c2n = cp / 2;
@@ -211,7 +230,7 @@ __global__ void __launch_bounds__(256) winograd_filter_kernel(int K, int cp,
 // y[n][m*ti + i][m*tj + j][k] = epilogue((A^T M A)[i][j]), cropped at the edges.
 template <int M_>
 __global__ void __launch_bounds__(256) winograd_output_kernel(WinoArgs a,
-                                                              const __nv_bfloat16* __restrict__ mm,
+                                                              const TDom<M_>* __restrict__ mm,
                                                               __nv_bfloat16* __restrict__ y,
                                                               pk_epilogue e) {
     using W = Wino<M_>;
@@ -222,7 +241,7 @@ __global__ void __launch_bounds__(256) winograd_output_kernel(WinoArgs a,
     const int k = (int)(idx - lt * k2n) * 2;
     if (lt >= a.tc || k >= a.k) return;
     const size_t plane = (size_t)a.rows * a.kp;
-    const __nv_bfloat16* mp = mm + (size_t)lt * a.kp + k;
+    const TDom<M_>* mp = mm + (size_t)lt * a.kp + k;
     float m0[AL][AL], m1[AL][AL];
 #pragma unroll
     for (int xi = 0; xi < AL * AL; ++xi) {
@@ -304,8 +323,8 @@ cudaError_t run(const pk_conv_geom* g, const void* x, const void* f, void* y,
     constexpr int AL = M_ + 2;
     const size_t ub = u_bytes(g, M_);
     if (ws_bytes < ub + 128 * bytes_per_tile(g, M_)) return cudaErrorNotSupported;
-    auto* u = static_cast<__nv_bfloat16*>(ws);
-    auto* v = reinterpret_cast<__nv_bfloat16*>(static_cast<char*>(ws) + ub);
+    auto* u = static_cast<TDom<M_>*>(ws);
+    auto* v = reinterpret_cast<TDom<M_>*>(static_cast<char*>(ws) + ub);
     {
         const int total = g->k * (g->x_pitch / 2);
         winograd_filter_kernel<M_><<<ceil_div(total, 256), 256, 0, st>>>(
@@ -335,13 +354,13 @@ cudaError_t run(const pk_conv_geom* g, const void* x, const void* f, void* y,
         a.t0 = t0;
         a.tc = T - t0 < chunk ? T - t0 : chunk;
         a.rows = (int)((a.tc + 127) / 128 * 128);
-        __nv_bfloat16* mm = v + (size_t)AL * AL * a.rows * a.cp;
+        TDom<M_>* mm = v + (size_t)AL * AL * a.rows * a.cp;
         const long long nin = (long long)a.rows * (a.cp / 2);
         winograd_input_kernel<M_><<<ceil_div(nin, 256), 256, 0, st>>>(
             a, static_cast<const __nv_bfloat16*>(x), v);
         count_launch();
         cudaError_t err = pk_cuda_gemm_tc_batched(v, u, mm, AL * AL, a.rows, a.cp, g->k, g->k,
-                                                  a.kp, st);
+                                                  a.kp, st, M_ == 4);
         if (err != cudaSuccess) return err;
         const long long nout = a.tc * (a.kp / 2);
         winograd_output_kernel<M_><<<ceil_div(nout, 256), 256, 0, st>>>(
