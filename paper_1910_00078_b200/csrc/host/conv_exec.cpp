@@ -300,6 +300,9 @@ std::size_t ConvPlan::device_workspace_bytes(int num_sms) const {
 
 void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                    std::size_t ws_bytes, const pk_epilogue* epi) const {
+    static const char* const kRange[3] = {"primkit conv forward", "primkit conv backward-data",
+                                          "primkit conv backward-weights"};
+    const NvtxRange range(kRange[static_cast<int>(problem_.direction)]);
     h.activate();
     const pk_conv_geom g = make_geom(problem_);
     const int dt = dtype_of(problem_.etype);

@@ -16,7 +16,18 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace primkit {
+
+// NVTX range for profilers (nsys / ncu --nvtx): header-only NVTX3, a no-op
+// unless a tool is attached (SURVEY §5 tracing).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 enum class ErrorCode {
     Ok = 0,

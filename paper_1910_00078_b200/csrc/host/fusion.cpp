@@ -379,6 +379,7 @@ FusionPlan::DeviceArgs& FusionPlan::device_args(Handle& h) {
 }
 
 void fusion_execute(Handle& h, FusionPlan& plan, const void* input, void* output) {
+    const NvtxRange range("primkit fusion execute");
     if (!plan.compiled()) throw_error(ErrorCode::NotCompiled, "fusion plan is not compiled");
     require_args(plan);
     auto& d = plan.device_args(h);
@@ -442,6 +443,7 @@ void fusion_execute(Handle& h, FusionPlan& plan, const void* input, void* output
 }
 
 void fusion_execute_unfused(Handle& h, FusionPlan& plan, const void* input, void* output) {
+    const NvtxRange range("primkit fusion execute (unfused)");
     if (!plan.compiled()) throw_error(ErrorCode::NotCompiled, "fusion plan is not compiled");
     require_args(plan);
     auto& d = plan.device_args(h);
