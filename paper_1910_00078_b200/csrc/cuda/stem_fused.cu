@@ -834,6 +834,7 @@ struct DgArgs {
     int npad;                   // MMA N = roundup(taps*4, 16)
     int cstride;                // colg row stride (words, odd)
     int v2;                     // 1: pipelined kernel (halo <= one M tile)
+    int v3;                     // 1: row-strip kernel (ResNet conv1 geometry)
     int debug;                  // PK_STEM_DEBUG (v2, profiling only): 1 no MMA, 2 no drain, 4 no gather
     unsigned long long* trace;  // PK_STEM_TRACE (profiling only)
 };
@@ -1330,6 +1331,267 @@ __global__ void __launch_bounds__(kDg2Threads, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// backward data v3 ("row strips"), ResNet conv1 geometry: 7x7, stride 2, pad 3,
+// H = 2P, W = 2Q, Q <= 128.
+//
+// dX[y][x] = sum over dY rows i, columns j' of dY[i][j'] . W[r][s] with
+// y = 2i + r - 3, x = 2j' + s - 3. For the dX pixel pair x = 2j + xp (xp = 0, 1)
+// the tap columns s reaching it come from the four dY columns j' = j + d - 1
+// (d = 0..3) with s = xp + 5 - 2d. So ONE GEMM per dY row gives, per dY column j
+// (= TMEM lane), the row's whole contribution to dX pixels 2j and 2j+1 for all
+// seven tap rows r:
+//   D[j][(xp, r, c)] = sum_d sum_k dY[i][j + d - 1][k] . B_d[k][(xp, r, c)],
+//   B_d = W[k][r][xp + 5 - 2d][c] (zero where s is outside 0..6)
+// K = 4 x 64 (the four shifted copies of the row are the same shared-memory tile
+// read from 128-byte row d: SWIZZLE_128B descriptors may start at any row), N = 48
+// (2 x 7 x 3 = 42 used). The dY row lands as one in-bounds TMA box of the flat pixel
+// array, pixels -1 .. 134 of the row; the three that belong to the neighbouring rows
+// but are read (-1, Q, Q+1) are zeroed in shared memory by the MMA warp (partly
+// out-of-bounds boxes stream at ~4 TB/s, in-bounds ones at the HBM rate). Rows
+// outside the image are skipped by the gather. No cross-lane traffic: thread j adds
+// its 42 columns into a window of the 7 dX rows the dY row reaches; rows 2i-3, 2i-2
+// are then complete and leave as two 16-byte pixels each.
+//
+// A CTA owns a band of kDg3Band dX rows of one image and walks the dY rows reaching
+// it two at a time (one TMA box, 8 MMA groups, one handshake per pair: per-row
+// handshakes cost more than the row's MMAs). Rows outside the image are zero fill,
+// so every band is the same 16 pairs (dY read once + ~4 rows per band, dX once).
+//   warps 0-3: gather (lane quarter q = warp), warp 4: TMA producer, warp 5: MMA
+constexpr int kDg3Threads = 32 * 6;
+constexpr int kDg3Stages = 4;     // dY row pairs in flight (4 x 34 KB)
+constexpr int kDg3Bufs = 3;       // TMEM accumulator pairs (2 x 64 columns each)
+constexpr int kDg3Band = 56;      // dX rows per work unit (224 = 4 bands: 1024 units at N=256)
+constexpr int kDg3N = 48;         // MMA N: (xp, r, c) columns, xp-major, 24 per xp
+constexpr int kDg3BoxPx = 136;    // pixels -1 .. 134 of a dY row
+constexpr int kDg3Steps = 16;     // dY row pairs per band: rows i_lo .. i_lo + 31 (band/2 + 3 used)
+static_assert(2 * kDg3Steps >= kDg3Band / 2 + 3, "band rows");
+
+struct Dg3Layout {
+    int a_stage, b_off, bar_off, bytes;
+    __host__ __device__ Dg3Layout() {
+        a_stage = 2 * kDg3BoxPx * 128;               // two rows of 17 KB, 1024-aligned
+        b_off = kDg3Stages * a_stage;
+        bar_off = b_off + 4 * kDg3N * 128;           // four K blocks of N rows x 64 k
+        bytes = bar_off + 256 + 1024;
+    }
+};
+
+// Work unit u = (image, band): dY rows i_lo .. i_lo + 2 * kDg3Steps - 1.
+struct Dg3Walk {
+    int n, i_lo, Y0;
+    __device__ Dg3Walk(const DgArgs& g, int u) {
+        const int nb = (g.H + kDg3Band - 1) / kDg3Band;
+        n = u / nb;
+        Y0 = (u - n * nb) * kDg3Band;
+        i_lo = Y0 / 2 - 1;
+    }
+};
+
+template <int C>
+__global__ void __launch_bounds__(kDg3Threads, 1)
+    stem_dgrad3_kernel(const __grid_constant__ CUtensorMap dymap, const __nv_bfloat16* __restrict__ w,
+                       __nv_bfloat16* __restrict__ dx, const __grid_constant__ DgArgs g) {
+    pdl_wait();
+    pdl_trigger();
+    const Dg3Layout L;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* a_full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+    uint64_t* a_empty = a_full + kDg3Stages;
+    uint64_t* tmem_full = a_empty + kDg3Stages;
+    uint64_t* tmem_empty = tmem_full + kDg3Bufs;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + kDg3Bufs);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int units = g.N * ((g.H + kDg3Band - 1) / kDg3Band);
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kDg3Stages; ++i) {
+            mbar_init(&a_full[i], 1);
+            mbar_init(&a_empty[i], 1);
+        }
+        for (int i = 0; i < kDg3Bufs; ++i) {
+            mbar_init(&tmem_full[i], 1);
+            mbar_init(&tmem_empty[i], 4);
+        }
+        fence_barrier_init();
+        tma_prefetch(&dymap);
+    }
+    if (warp == 5) tmem_alloc(tmem_slot, 512);
+    // B_d[n][k], n = xp * 24 + r * C + c (K-major SWIZZLE_128B, 64 k = one atom)
+    for (int i = threadIdx.x; i < 4 * kDg3N * 8; i += blockDim.x) {
+        const int jj = i & 7, row = i >> 3, d = row / kDg3N, n = row - d * kDg3N;
+        const int xp = n / 24, rc = n - xp * 24, r = rc / C, c = rc - r * C;
+        const int s = xp + 5 - 2 * d;
+        const bool ok = rc < 7 * C && s >= 0 && s < 7;
+        __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int k = jj * 8 + e;
+            v[e] = (ok && k < g.K) ? w[((size_t)k * 49 + r * 7 + s) * g.x_pitch + c] : __float2bfloat16_rn(0.0f);
+        }
+        st_shared_v4(smem_u32(smem + L.b_off) + row * 128 + ((jj ^ (row & 7)) << 4),
+                     *reinterpret_cast<const uint4*>(v));
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 4) {
+        // ---------------- TMA producer: one box of two dY rows per step ----------------
+        int n = 0;
+        for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
+            const Dg3Walk wk(g, unit);
+            for (int st = 0; st < kDg3Steps; ++st, ++n) {
+                const int s = n % kDg3Stages;
+                if (n >= kDg3Stages) mbar_wait(&a_empty[s], ((n / kDg3Stages) - 1) & 1);
+                dstamp(g, n, 12);
+                if (lane == 0 && (g.debug & 32)) {
+                    mbar_arrive(&a_full[s]);
+                } else if (lane == 0) {
+                    // two in-bounds boxes of the flat pixel array: pixels -1 .. 134 of rows i, i+1
+                    // (the MMA warp zeroes the neighbours' pixels -1, Q, Q+1 before use)
+                    mbar_arrive_expect_tx(&a_full[s], 2 * kDg3BoxPx * 128);
+                    const int base = (wk.n * g.P + wk.i_lo + 2 * st) * g.Q - 1;
+                    tma_load_2d(smem_u32(smem + s * L.a_stage), &dymap, &a_full[s], 0, base);
+                    tma_load_2d(smem_u32(smem + s * L.a_stage + kDg3BoxPx * 128), &dymap, &a_full[s], 0, base + g.Q);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer: 2 rows x 4 shifted copies x 4 K steps ---------------
+        const uint32_t idesc = idesc_bf16_f32(128, kDg3N, false, false);
+        const uint32_t b0 = smem_u32(smem + L.b_off);
+        const int steps = ((units - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x) * kDg3Steps;
+        for (int n = 0; n < steps; ++n) {
+            const int s = n % kDg3Stages, buf = n % kDg3Bufs;
+            dstamp(g, n, 0);
+            mbar_wait(&a_full[s], (n / kDg3Stages) & 1);
+            dstamp(g, n, 1);
+            // pixels -1, Q, Q+1 of each row are the neighbouring rows' data: zero them
+            // (generic stores, then a proxy fence so the tensor core sees them)
+            if (lane < 6 * 8) {
+                const int rr = lane >> 3, row = rr / 3, e = rr % 3, q16 = lane & 7;
+                const int prow = e == 0 ? 0 : g.Q + e;
+                st_shared_v4(smem_u32(smem + s * L.a_stage + row * kDg3BoxPx * 128 + prow * 128 + q16 * 16),
+                             make_uint4(0u, 0u, 0u, 0u));
+            }
+            if (lane < 16) {
+                const int rr = 4 + (lane >> 3), row = rr / 3, e = rr % 3, q16 = lane & 7;
+                const int prow = e == 0 ? 0 : g.Q + e;
+                st_shared_v4(smem_u32(smem + s * L.a_stage + row * kDg3BoxPx * 128 + prow * 128 + q16 * 16),
+                             make_uint4(0u, 0u, 0u, 0u));
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            dstamp(g, n, 2);
+            mbar_wait(&tmem_empty[buf], ((n / kDg3Bufs) & 1) ^ 1);
+            dstamp(g, n, 3);
+            tc_fence_after();
+            if (!(g.debug & 1)) {
+#pragma unroll
+                for (int row = 0; row < 2; ++row) {
+                    const uint32_t a0 = smem_u32(smem + s * L.a_stage + row * kDg3BoxPx * 128);
+#pragma unroll
+                    for (int d = 0; d < 4; ++d) {
+                        // shifted copy d: box rows d .. d+127 (pixels j + d - 1), B block d
+                        const uint64_t ad = umma_desc_sw128(a0 + d * 128, 16, 1024);
+                        const uint64_t bd = umma_desc_sw128(b0 + d * kDg3N * 128, 16, 1024);
+                        mma4_bf16(tmem_base + buf * 128 + row * 64, ad, ad + 2, ad + 4, ad + 6, bd, bd + 2,
+                                  bd + 4, bd + 6, idesc, d > 0);
+                    }
+                }
+            }
+            dstamp(g, n, 4);
+            mma_commit_elect(&a_empty[s]);
+            mma_commit_elect(&tmem_full[buf]);
+            __syncwarp();
+            dstamp(g, n, 5);
+        }
+    } else {
+        // ---------------- gather: lane j owns dX pixels 2j, 2j+1 ---------------------
+        const int j = 32 * warp + lane;
+        const bool owned = j < g.Q;
+        const uint32_t ta_q = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
+        int n = 0;
+        for (int unit = blockIdx.x; unit < units; unit += gridDim.x) {
+            const Dg3Walk wk(g, unit);
+            // window of the 7 dX rows dY row i reaches: slot r <-> y = 2i + r - 3
+            float acc[7][2][C];
+#pragma unroll
+            for (int r = 0; r < 7; ++r)
+#pragma unroll
+                for (int xp = 0; xp < 2; ++xp)
+#pragma unroll
+                    for (int c = 0; c < C; ++c) acc[r][xp][c] = 0.0f;
+#pragma unroll 1
+            for (int st = 0; st < kDg3Steps; ++st, ++n) {
+                const int buf = n % kDg3Bufs;
+                if (warp == 0) dstamp(g, n, 6);
+                mbar_wait(&tmem_full[buf], (n / kDg3Bufs) & 1);
+                if (warp == 0) dstamp(g, n, 7);
+                tc_fence_after();
+                uint32_t v[96];
+#pragma unroll
+                for (int k = 0; k < 6; ++k)
+                    tmem_ld16(ta_q + buf * 128 + (k / 3) * 64 + (k % 3) * 16,
+                              *reinterpret_cast<uint32_t(*)[16]>(&v[k * 16]));
+                tmem_ld_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tmem_empty[buf]);
+                dstamp(g, n, 8 + warp);
+#pragma unroll
+                for (int row = 0; row < 2; ++row) {
+                    const int i = wk.i_lo + 2 * st + row;
+                    if (!(g.debug & 2) && i >= 0 && i < g.P) {  // other rows are another image's
+#pragma unroll
+                        for (int r = 0; r < 7; ++r)
+#pragma unroll
+                            for (int xp = 0; xp < 2; ++xp)
+#pragma unroll
+                                for (int c = 0; c < C; ++c)
+                                    acc[r][xp][c] += __uint_as_float(v[row * 48 + xp * 24 + r * C + c]);
+                    }
+                    // dX rows 2i-3 and 2i-2 (slots 0, 1) are complete: store (inside the band)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int y = 2 * i - 3 + e;
+                        if (owned && y >= wk.Y0 && y < wk.Y0 + kDg3Band && y < g.H && !(g.debug & 4)) {
+                            __align__(16) __nv_bfloat16 ob[16];
+#pragma unroll
+                            for (int xp = 0; xp < 2; ++xp)
+#pragma unroll
+                                for (int c = 0; c < 8; ++c)
+                                    ob[xp * 8 + c] = __float2bfloat16_rn(c < C ? acc[e][xp][c < C ? c : 0] : 0.0f);
+                            uint4* dst = reinterpret_cast<uint4*>(dx + (((size_t)wk.n * g.H + y) * g.W + 2 * j) * g.x_pitch);
+                            dst[0] = reinterpret_cast<const uint4*>(ob)[0];
+                            dst[1] = reinterpret_cast<const uint4*>(ob)[1];
+                        }
+                    }
+                    // shift the window by two dX rows
+#pragma unroll
+                    for (int r = 0; r < 7; ++r)
+#pragma unroll
+                        for (int xp = 0; xp < 2; ++xp)
+#pragma unroll
+                            for (int c = 0; c < C; ++c) acc[r][xp][c] = r < 5 ? acc[r + 2 < 7 ? r + 2 : 0][xp][c] : 0.0f;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 512);
+    }
+}
+
 __host__ __device__ inline int floor_div(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
 bool dg_args(const pk_conv_geom* g, DgArgs& a) {
@@ -1343,9 +1605,20 @@ bool dg_args(const pk_conv_geom* g, DgArgs& a) {
     a.npad = (a.taps * 4 + 15) / 16 * 16;
     if (2 * a.npad > 512) return false;
     a.cstride = ((a.npad / 4) * a.C) | 1;  // all padded taps stored; odd: conflict-free
+    // v3 row strips: 7x7 stride 2 pad 3 with H = 2P, W = 2Q and a dY row within the 128 lanes
+    static const int dg_ver = [] {
+        const char* v = std::getenv("PK_STEM_DG");
+        return v ? std::atoi(v) : 3;
+    }();
+    if (dg_ver >= 3 && a.R == 7 && a.S == 7 && a.sh == 2 && a.sw == 2 && a.ph == 3 && a.pw == 3 &&
+        a.H == 2 * a.P && a.W == 2 * a.Q && a.Q <= 128 && a.C <= 3 &&
+        Dg3Layout().bytes <= 227 * 1024) {
+        a.v3 = 1;
+        return true;
+    }
     static const int cand[][2] = {{16, 32}, {8, 32}, {16, 16}, {8, 16}, {8, 8}, {4, 8}};
     // pipelined v2 first: the largest tile whose halo fits one 128-row MMA
-    static const bool v2_off = std::getenv("PK_STEM_DG_V1") != nullptr;
+    static const bool v2_off = std::getenv("PK_STEM_DG_V1") != nullptr || dg_ver == 1;
     for (const auto& c : cand) {
         if (v2_off || (a.taps * a.C + 15) / 16 * 16 > 256) break;
         const int TY = c[0], TX = c[1];
@@ -1549,9 +1822,48 @@ cudaError_t pk_cuda_stem_fused_dgrad(const pk_conv_geom* g, const void* dy, cons
     DgArgs a;
     if (!dg_args(g, a)) return cudaErrorNotSupported;
     CUtensorMap dymap{};
+    int grid = tc::num_sms_of_current_device();
+    if (const char* v = std::getenv("PK_STEM_DEBUG")) a.debug = std::atoi(v);
+    if (a.v3) {
+        // flat pixel rows [N*P*Q][64]: boxes of pixels -1 .. 134 of a dY row
+        if (!tc::make_map_2d(&dymap, dy, (long long)g->n * g->p * g->q, 64, g->y_pitch, kDg3BoxPx))
+            return cudaErrorNotSupported;
+        const int units = g->n * ((g->h + kDg3Band - 1) / kDg3Band);
+        if (units < grid) grid = units;
+        static int attr3[4] = {-1, -1, -1, -1};
+        static unsigned long long* trace3 = [] {
+            unsigned long long* p = nullptr;
+            if (std::getenv("PK_STEM_TRACE")) cudaMalloc(&p, 32 * 32 * 8);
+            return p;
+        }();
+        a.trace = trace3;
+        auto go3 = [&](auto kern, int* attr_dev) {
+            cudaError_t err = set_smem(kern, Dg3Layout().bytes, attr_dev);
+            if (err != cudaSuccess) return err;
+            err = pk_launch(kern, dim3(grid), dim3(kDg3Threads), Dg3Layout().bytes, st, dymap,
+                            (const __nv_bfloat16*)w, (__nv_bfloat16*)dx, a);
+            if (err != cudaSuccess) return err;
+            count_launch();
+            if (a.trace) {  // profiling only (PK_STEM_TRACE): per-step clock stamps of CTA 0
+                unsigned long long h[32 * 32];
+                cudaStreamSynchronize(st);
+                cudaMemcpy(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost);
+                for (int i = 0; i < 32; ++i) {
+                    fprintf(stderr, "dg3 step %2d:", i);
+                    for (int e = 0; e < 13; ++e) fprintf(stderr, " %6lld", (long long)(h[i * 32 + e] - h[0]));
+                    fprintf(stderr, "\n");
+                }
+            }
+            return cudaGetLastError();
+        };
+        switch (a.C) {
+            case 1: return go3(stem_dgrad3_kernel<1>, &attr3[1]);
+            case 2: return go3(stem_dgrad3_kernel<2>, &attr3[2]);
+            default: return go3(stem_dgrad3_kernel<3>, &attr3[3]);
+        }
+    }
     if (!tc::make_map_nhwc(&dymap, dy, g->n, g->p, g->q, g->y_pitch, a.WX, a.HY, 1))
         return cudaErrorNotSupported;
-    int grid = tc::num_sms_of_current_device();
     if (a.total_tiles < grid) grid = a.total_tiles;
     static unsigned long long* trace = [] {
         unsigned long long* p = nullptr;
@@ -1559,7 +1871,6 @@ cudaError_t pk_cuda_stem_fused_dgrad(const pk_conv_geom* g, const void* dy, cons
         return p;
     }();
     a.trace = trace;
-    if (const char* v = std::getenv("PK_STEM_DEBUG")) a.debug = std::atoi(v);
     auto go = [&](auto kern, int* attr_dev) {
         cudaError_t err = set_smem(kern, 227 * 1024, attr_dev);
         if (err != cudaSuccess) return err;
