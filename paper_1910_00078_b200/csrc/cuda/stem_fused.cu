@@ -1332,6 +1332,250 @@ __global__ void __launch_bounds__(kDg2Threads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// forward v2 ("row strips"), ResNet conv1 geometry: 7x7, stride 2, pad 3,
+// K = 64, Q <= 128. One output row p is ONE GEMM over the seven input rows
+// 2p-3 .. 2p+3 it reads: TMEM lane = output column q, and with the input row
+// stored as 8-byte pixels (4 channels) the 16-byte unit t of lane q — input
+// pixels 2q-3+2t, 2q-2+2t — sits at byte 16q + 16t of the row. So the A operand of
+// (input row, K step m) is the row itself read as a K-major no-swizzle matrix:
+// start 32m, rows 16 B apart (SBO 128 per 8 lanes), the second K unit 16 B on
+// (LBO 16). No im2col and no per-tile halo: each input row is staged once per
+// band (8-byte cp.async, zero fill outside the image) and read by the MMAs of the
+// four output rows that use it. B = packed filter [r][t][k][8] (t = tap-column
+// pair, s = 2t + e/4, c = e%4; s = 7 and c >= C are zero), resident.
+// Per output row: 7 rows x 2 K steps = 14 MMAs M=128 N=64 into one of four TMEM
+// accumulators; the epilogue (bias/BN/activation/statistics as the tile kernels)
+// stages each warp's 32 pixels and TMA-stores them.
+//   warps 0-3: epilogue (lane quarter q), warp 4: input-row loader, warp 5: MMA
+constexpr int kF2Threads = 32 * 6;
+constexpr int kF2Band = 28;        // output rows per work unit (112 = 4 bands: 1024 units at N=256)
+constexpr int kF2Ring = 24;        // staged input rows (8-byte pixels, 2 KB each)
+constexpr int kF2RowBytes = 2048;  // input columns -3 .. 252
+constexpr int kF2Bufs = 4;         // TMEM accumulator pairs (2 output rows x 64 columns)
+
+struct F2Layout {
+    int b_off, bp_off, ring_off, stg_off, bar_off, bytes;
+    __host__ __device__ F2Layout() {
+        b_off = 0;                                   // [r][t][64 k][16 B]: 7 x 4 x 1 KB
+        bp_off = 28 * 1024;                          // [r' = 2..6][t][128 rows][16 B]: 5 x 4 x 2 KB
+        ring_off = bp_off + 40 * 1024;
+        stg_off = ring_off + kF2Ring * kF2RowBytes;
+        bar_off = stg_off + 4 * 2 * 4096;            // 4 epilogue warps x 2 staging buffers
+        bytes = bar_off + 512 + 1024;
+    }
+};
+
+__global__ void __launch_bounds__(kF2Threads, 1)
+    stem_fprop2_kernel(const __grid_constant__ CUtensorMap ymap, const __nv_bfloat16* __restrict__ x,
+                       const __nv_bfloat16* __restrict__ w, const __grid_constant__ StemArgs g,
+                       const pk_epilogue epi) {
+    pdl_wait();
+    pdl_trigger();
+    const F2Layout L;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    uint64_t* row_full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
+    uint64_t* row_empty = row_full + kF2Ring;
+    uint64_t* tmem_full = row_empty + kF2Ring;
+    uint64_t* tmem_empty = tmem_full + kF2Bufs;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + kF2Bufs);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nb = (g.P + kF2Band - 1) / kF2Band;
+    const int units = g.N * nb;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kF2Ring; ++i) {
+            mbar_init(&row_full[i], 32);  // one cp.async arrive per loader lane
+            mbar_init(&row_empty[i], 1);
+        }
+        for (int i = 0; i < kF2Bufs; ++i) {
+            mbar_init(&tmem_full[i], 1);
+            mbar_init(&tmem_empty[i], 4);
+        }
+        fence_barrier_init();
+        tma_prefetch(&ymap);
+    }
+    if (warp == 5) tmem_alloc(tmem_slot, 512);
+    // B[r][t][k][8]: unit t of filter row r = taps (r, 2t), (r, 2t+1) x 4 channels;
+    // Bpair[r'][t][128]: rows 0..63 = B[r'][t], rows 64..127 = B[r'-2][t] (one N=128
+    // MMA feeds output rows p (tap row r') and p+1 (tap row r'-2) from the same input row)
+    for (int i = threadIdx.x; i < 7 * 4 * 64 + 5 * 4 * 128; i += blockDim.x) {
+        int r, t, k, dst;
+        if (i < 7 * 4 * 64) {
+            k = i & 63;
+            r = (i >> 6) >> 2;
+            t = (i >> 6) & 3;
+            dst = L.b_off + i * 16;
+        } else {
+            const int j = i - 7 * 4 * 64, row = j & 127, rt = j >> 7, rp = 2 + (rt >> 2);
+            t = rt & 3;
+            k = row & 63;
+            r = row < 64 ? rp : rp - 2;
+            dst = L.bp_off + j * 16;
+        }
+        __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int s = 2 * t + (e >> 2), c = e & 3;
+            v[e] = (s < 7 && c < g.C && k < g.K) ? w[((size_t)k * 49 + r * 7 + s) * g.x_pitch + c]
+                                                 : __float2bfloat16_rn(0.0f);
+        }
+        st_shared_v4(smem_u32(smem + dst), *reinterpret_cast<const uint4*>(v));
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t ring0 = smem_u32(smem + L.ring_off);
+
+    if (warp == 4) {
+        // ---------------- loader: input rows 2p0-3 .. 2(p0+band-1)+3 per unit ---------
+        int rc = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            const int n = u / nb, p0 = (u - n * nb) * kF2Band;
+            const int p1 = min(p0 + kF2Band, g.P);
+            for (int rho = 2 * p0 - 3; rho <= 2 * (p1 - 1) + 3; ++rho, ++rc) {
+                const int s = rc % kF2Ring;
+                if (rc >= kF2Ring) mbar_wait(&row_empty[s], ((rc / kF2Ring) - 1) & 1);
+                const bool row_in = rho >= 0 && rho < g.H;
+                const __nv_bfloat16* src_row = x + ((size_t)n * g.H + (row_in ? rho : 0)) * g.W * g.x_pitch;
+                if (g.debug & 2) {  // timing only: no input loads
+                    mbar_arrive(&row_full[s]);
+                    continue;
+                }
+#pragma unroll
+                for (int e = 0; e < kF2RowBytes / 8 / 32; ++e) {
+                    const int col = e * 32 + lane - 3;
+                    const bool in = row_in && col >= 0 && col < g.W;
+                    cp_async_8(ring0 + s * kF2RowBytes + (col + 3) * 8, in ? src_row + (size_t)col * g.x_pitch : x,
+                               in ? 8u : 0u);
+                }
+                cp_async_arrive_noinc(&row_full[s]);
+            }
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer: output rows in pairs (p, p+1) --------------------
+        // input rows 2p-3+k, k = 0..8: k = 7, 8 -> p+1 only (N=64, first: they start its
+        // accumulator), k = 0, 1 -> p only (N=64, k = 0 starts it), k = 2..6 -> both
+        // (N=128 over the adjacent accumulators, B = Bpair)
+        const uint32_t id64 = idesc_bf16_f32(128, 64, false, false);
+        const uint32_t id128 = idesc_bf16_f32(128, 128, false, false);
+        const uint32_t b0 = smem_u32(smem + L.b_off), bp0 = smem_u32(smem + L.bp_off);
+        int rc = 0, ready = 0, pc = 0;  // rc: ring index of this unit's first input row
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            const int n = u / nb, p0 = (u - n * nb) * kF2Band;
+            const int p1 = min(p0 + kF2Band, g.P);
+            const int rows = 2 * (p1 - p0) + 5;
+            for (int p = p0; p < p1; p += 2, ++pc) {
+                const int first = rc + 2 * (p - p0);  // ring index of input row 2p-3
+                while (ready < first + 9) {
+                    mbar_wait(&row_full[ready % kF2Ring], (ready / kF2Ring) & 1);
+                    ++ready;
+                }
+                const int buf = pc % kF2Bufs;
+                mbar_wait(&tmem_empty[buf], ((pc / kF2Bufs) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d0 = tmem_base + buf * 128;
+                auto arow = [&](int k) {
+                    return umma_desc_noswz(ring0 + ((first + k) % kF2Ring) * kF2RowBytes, 16, 128);
+                };
+                if (!(g.debug & 1)) {
+                    {   // rows 7, 8: output row p+1, tap rows 5, 6 (k = 7 starts the accumulator)
+                        const uint64_t a7 = arow(7), a8 = arow(8);
+                        const uint64_t c5 = umma_desc_noswz(b0 + 5 * 4096, 1024, 128),
+                                       c6 = umma_desc_noswz(b0 + 6 * 4096, 1024, 128);
+                        mma4_bf16(d0 + 64, a7, a7 + 2, a8, a8 + 2, c5, c5 + 128, c6, c6 + 128, id64, 0);
+                    }
+                    {   // rows 0, 1: output row p, tap rows 0, 1 (k = 0 starts the accumulator)
+                        const uint64_t a0 = arow(0), a1 = arow(1);
+                        const uint64_t c0 = umma_desc_noswz(b0, 1024, 128), c1 = umma_desc_noswz(b0 + 4096, 1024, 128);
+                        mma4_bf16(d0, a0, a0 + 2, a1, a1 + 2, c0, c0 + 128, c1, c1 + 128, id64, 0);
+                    }
+#pragma unroll
+                    for (int k = 2; k < 7; k += 2) {  // rows 2..6: both output rows
+                        const uint64_t ak = arow(k), bk = umma_desc_noswz(bp0 + (k - 2) * 8192, 2048, 128);
+                        if (k + 1 < 7) {
+                            const uint64_t ak1 = arow(k + 1), bk1 = umma_desc_noswz(bp0 + (k - 1) * 8192, 2048, 128);
+                            mma4_bf16(d0, ak, ak + 2, ak1, ak1 + 2, bk, bk + 256, bk1, bk1 + 256, id128, 1);
+                        } else {
+                            mma2_bf16(d0, ak, ak + 2, bk, bk + 256, id128);
+                        }
+                    }
+                }
+                mma_commit_elect(&tmem_full[buf]);
+                // input rows no later pair of this unit reads: 2p-3 .. 2p (or all at the end)
+                const int done = p + 2 < p1 ? 4 : rows - 2 * (p - p0);
+                for (int k = 0; k < done; ++k) mma_commit_elect(&row_empty[(first + k) % kF2Ring]);
+                __syncwarp();
+            }
+            rc += rows;
+        }
+    } else {
+        // ---------------- epilogue (4 warps, one TMEM lane quarter each) ---------
+        const int q = warp;
+        uint8_t* stg_base = smem + L.stg_off + warp * 2 * 4096;
+        int sbuf = 0;
+        const bool has_epi = epilogue_active(&epi);
+        const int ox = q * 32 + lane;
+        BnStatAcc bacc;
+        bacc.init();
+        int pc = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            const int n = u / nb, p0 = (u - n * nb) * kF2Band;
+            const int p1 = min(p0 + kF2Band, g.P);
+            for (int pp = p0; pp < p1; pp += 2, ++pc) {
+                const int buf = pc % kF2Bufs;
+                mbar_wait(&tmem_full[buf], (pc / kF2Bufs) & 1);
+                tc_fence_after();
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {
+                    const int p = pp + h;
+                    uint32_t v[64];
+                    const uint32_t ta = tmem_base + buf * 128 + h * 64 + (static_cast<uint32_t>(q * 32) << 16);
+                    tmem_ld16(ta + 0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+                    tmem_ld16(ta + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+                    tmem_ld16(ta + 32, *reinterpret_cast<uint32_t(*)[16]>(&v[32]));
+                    tmem_ld16(ta + 48, *reinterpret_cast<uint32_t(*)[16]>(&v[48]));
+                    tmem_ld_wait();
+                    if (h == 1) {
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&tmem_empty[buf]);
+                    }
+                    if (q * 32 >= g.Q) continue;  // no output column in this lane quarter
+                    const uint32_t stg_u = smem_u32(stg_base + sbuf * 4096);
+                    if (lane == 0) bulk_wait_read<1>();
+                    __syncwarp();
+                    float xf[64];
+#pragma unroll
+                    for (int e = 0; e < 64; ++e) xf[e] = __uint_as_float(v[e]);
+                    if (has_epi) epilogue_chunk64(epi, xf, 0, g.K, p, ox, g.P, g.Q);
+                    pack_stage64(xf, stg_u, lane, 64);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0 && !(g.debug & 4)) {
+                        tma_store_4d(&ymap, stg_u, 0, q * 32, p, n);  // columns >= Q are clipped
+                        bulk_commit();
+                    }
+                    if (epi.stats) bacc.add(epi, stg_u, lane, ox < g.Q, 0, 0, 0, g.K, g.K);
+                    sbuf ^= 1;
+                }
+            }
+        }
+        if (epi.stats) bacc.finish(epi, lane, g.K);
+        if (lane == 0) bulk_wait_all();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, 512);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // backward data v3 ("row strips"), ResNet conv1 geometry: 7x7, stride 2, pad 3,
 // H = 2P, W = 2Q, Q <= 128.
 //
@@ -1805,6 +2049,28 @@ cudaError_t pk_cuda_stem_fused_fprop(const pk_conv_geom* g, const void* x, const
     pk_epilogue e{};
     e.act = -1;
     if (epi) e = *epi;
+    static const bool f2_off = [] {
+        const char* v = std::getenv("PK_STEM_FWD");
+        return v && std::atoi(v) == 1;
+    }();
+    if (!f2_off && g->k == 64 && a.R == 7 && a.S == 7 && a.sh == 2 && a.sw == 2 && a.ph == 3 && a.pw == 3 &&
+        a.Q <= 128 && a.W <= 2 * 128 && a.C <= 4 && a.dh == 1 && a.dw == 1 && a.P % 2 == 0) {
+        // row strips: one TMA store box = one warp's 32 output columns of a row
+        CUtensorMap ymap2{};
+        if (!tc::make_map_nhwc(&ymap2, y, g->n, g->p, g->q, g->y_pitch, 32, 1, 1))
+            return cudaErrorNotSupported;
+        static int attr_f2 = -1;
+        cudaError_t err = set_smem(stem_fprop2_kernel, F2Layout().bytes, &attr_f2);
+        if (err != cudaSuccess) return err;
+        int grid = num_sms_of_current_device();
+        const int units = g->n * ((g->p + kF2Band - 1) / kF2Band);
+        if (units < grid) grid = units;
+        err = pk_launch(stem_fprop2_kernel, dim3(grid), dim3(kF2Threads), F2Layout().bytes, st, ymap2,
+                        (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, a, e);
+        if (err != cudaSuccess) return err;
+        count_launch();
+        return cudaGetLastError();
+    }
     switch (g->k) {
         case 64: return launch_stem_fprop<64>(ymap, x, w, a, e, st);
         case 128: return launch_stem_fprop<128>(ymap, x, w, a, e, st);

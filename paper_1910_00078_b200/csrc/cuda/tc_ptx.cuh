@@ -335,6 +335,18 @@ __device__ __forceinline__ void mma8_bf16_bs(uint32_t tmem_d, uint64_t a0, uint6
         : "memory");
 }
 
+// Two SS MMAs from one elected thread (accumulate).
+__device__ __forceinline__ void mma2_bf16(uint32_t tmem_d, uint64_t a0, uint64_t a1, uint64_t b0,
+                                          uint64_t b1, uint32_t idesc) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %3, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %4, %5, 1;\n\t}" ::"r"(tmem_d),
+        "l"(a0), "l"(a1), "l"(b0), "l"(b1), "r"(idesc)
+        : "memory");
+}
+
 __device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
