@@ -18,6 +18,7 @@
 //
 // Backward data at stride 1 is the same convolution of dY with the
 // transposed filter, taps flipped (grid pad R-1-pad).
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -45,7 +46,11 @@ struct HaloArgs {
     int flip;                    // dgrad: tap (r,s) uses filter tap (R-1-r, S-1-s)
     int debug;                   // PK_HALO_DEBUG (timing experiments only): 1 = 8-row-aligned tap views
     int b_mn;                    // dgrad: B = the filter itself (MN-major 64 x 64 atoms)
+    unsigned long long* trace;   // PK_HALO_TRACE (profiling only): clock stamps of CTA 0 per tile
 };
+__device__ __forceinline__ void hstamp(const HaloArgs& g, int it, int ev) {
+    if (g.trace && blockIdx.x == 0 && it < 32 && (threadIdx.x & 31) == 0) g.trace[it * 32 + ev] = clock64();
+}
 
 // RESB: the whole filter slice of the tile's output channels is resident in
 // smem (loaded once per CTA) — used when it fits (taps x chunks x BN x 128 B
@@ -158,7 +163,9 @@ __global__ void __launch_bounds__(kHThreads, 1)
             for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
                 const HTile ht = htile(g, t);
                 for (int ck = 0; ck < g.cpt; ++ck) {
+                    hstamp(g, (t - blockIdx.x) / gridDim.x, 8);
                     mbar_wait(&h_empty[hs], hph ^ 1);
+                    hstamp(g, (t - blockIdx.x) / gridDim.x, 9);
                     mbar_arrive_expect_tx(&h_full[hs], halo_bytes);
                     if (inb)
                         tma_load_4d(smem_u32(smem + hs * L::kHalo), &amap, &h_full[hs], ck * 64, 0,
@@ -202,12 +209,15 @@ __global__ void __launch_bounds__(kHThreads, 1)
         for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++it) {
             const HTile ht = htile(g, t);
             const int a = it & 1;
+            hstamp(g, it, 0);
             mbar_wait(&tmem_empty[a], ((it >> 1) & 1) ^ 1);
+            hstamp(g, it, 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + a * BN;
             const int base_row = ht.p0 - ht.row0 * g.Wg;
             for (int ck = 0; ck < g.cpt; ++ck) {
                 mbar_wait(&h_full[hs], hph);
+                hstamp(g, it, 2);
                 tc_fence_after();
                 const uint32_t halo_u = smem_u32(smem + hs * L::kHalo);
                 if (RESB && !(g.debug & ~24)) {
@@ -258,6 +268,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
                         }
                     }
                 }
+                hstamp(g, it, 3);
                 mma_commit_elect(&h_empty[hs]);
                 if (++hs == HB) {
                     hs = 0;
@@ -285,7 +296,9 @@ __global__ void __launch_bounds__(kHThreads, 1)
             const bool row_ok = oy < g.Ho && ox < g.Wo;
             const long long pix = ((long long)ht.n * g.Ho + oy) * g.Wo + ox;
             const int a = it & 1;
+            if (warp == 2) hstamp(g, it, 4);
             mbar_wait(&tmem_full[a], (it >> 1) & 1);
+            if (warp == 2) hstamp(g, it, 5);
             tc_fence_after();
             const int span = min(BN, g.out_pitch - n0c);
             const int nchunks = (span + 63) / 64;
@@ -348,6 +361,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
                     bacc.add(epi, stg_u, lane, row_ok, pix, (ci >> 1) & 1, n0c + c0, g.n_out,
                              g.out_pitch);
                 __syncwarp();  // staging reused by the next chunk
+                if (warp == 2) hstamp(g, it, 6);
             }
         }
         if (epi.stats) bacc.finish(epi, lane, g.n_out);
@@ -381,6 +395,16 @@ cudaError_t launch_halo(const CUtensorMap& amap, const CUtensorMap& bmap, void* 
                                (__nv_bfloat16*)out, g, e);
     if (le != cudaSuccess) return le;
     count_launch();
+    if (g.trace) {  // profiling only (PK_HALO_TRACE)
+        unsigned long long h[32 * 32];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, g.trace, sizeof(h), cudaMemcpyDeviceToHost);
+        for (int i = 0; i < 32; ++i) {
+            fprintf(stderr, "halo tile %2d:", i);
+            for (int ev = 0; ev < 10; ++ev) fprintf(stderr, " %7lld", (long long)(h[i * 32 + ev] - h[0]));
+            fprintf(stderr, "\n");
+        }
+    }
     return cudaGetLastError();
 }
 
@@ -428,6 +452,12 @@ cudaError_t pk_halo_conv(const pk_conv_geom* g, bool dgrad, const void* src, con
     a.out_pitch = out_pitch;
     a.flip = dgrad ? 1 : 0;
     if (const char* v = std::getenv("PK_HALO_DEBUG")) a.debug = std::atoi(v);
+    static unsigned long long* trace = [] {
+        unsigned long long* p = nullptr;
+        if (std::getenv("PK_HALO_TRACE")) cudaMalloc(&p, 32 * 32 * 8);
+        return p;
+    }();
+    a.trace = trace;
     // halo of 128 positions: rows touched by [p0, p0 + 127 + (R-1)Wg + S-1]
     a.NR = (127 + (g->r - 1) * a.Wg + g->s - 1 + a.Wg - 1) / a.Wg + 1;
     if (a.Wg > 256 || a.NR > 256 || a.NR * a.Wg > 448) return cudaErrorNotSupported;
