@@ -653,14 +653,18 @@ primkit_status primkit_conv_bn_workspace(primkit_handle* h, const primkit_conv_p
 // per-channel reductions there cost more than the separate statistics read
 // they save (measured, ResNet-50 N=256: conv2_1c 0.388 ms fused vs 0.348 ms
 // conv + standalone BN; conv4_2a 0.080 vs 0.090). PK_CBN_FUSE=1 / 0 forces.
-bool stats_epilogue_pays(const primkit::ConvProblem& p, const primkit::ConvShapes& sh) {
+// Statistics in the conv epilogue save the BN statistics pass's read of the conv
+// output. Measured per layer on all 53 ResNet-50 convs at N=256 (tools/bench_configs.py
+// cfg4, profiles/r02_cfg4_layers.json) against conv + the single-launch BN
+// (bn_coop.cu), whose two passes over the output are L2 hits for every layer whose
+// output fits the 126 MB L2: the epilogue form was slower or equal on 51 of 53
+// layers (its atomics and the partial-buffer reset cost more than an L2 re-read), so
+// it is opt-in (PK_CBN_FUSE=1). The saving that remains is the normalised output's
+// HBM round trip, which needs the NEXT convolution to apply BN + ReLU while loading
+// its A operand.
+bool stats_epilogue_pays(const primkit::ConvProblem&, const primkit::ConvShapes&) {
     if (const char* v = std::getenv("PK_CBN_FUSE")) return v[0] != '0';
-    if (sh.y * sh.x > 1) return true;
-    const double flops = 2.0 * sh.n * sh.k * sh.cg * sh.y * sh.x * sh.oh * sh.ow;
-    const double bytes = 2.0 * ((double)sh.n * sh.h * sh.w * pk_pitch((int)sh.c) +
-                                (double)sh.k * sh.y * sh.x * pk_pitch((int)sh.cg) +
-                                (double)sh.n * sh.oh * sh.ow * pk_pitch((int)sh.k));
-    return flops / bytes >= 180.0;
+    return false;
 }
 
 primkit_status primkit_conv_bn_forward_train_device(

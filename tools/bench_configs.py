@@ -229,8 +229,14 @@ def cfg4(d, iters, n=256):
             lib.check(lib.lib.primkit_batchnorm_forward_train_device(
                 d.h, dims, abi.BF16, vp(conv), vp(g), vp(b), vp(rm), vp(rv), C.c_float(1e-5),
                 C.c_float(0.1), vp(z), vp(sm), vp(si), 1))
-        out["fwd"]["fused_ms"] += timed(fused, iters)
-        out["fwd"]["unfused_ms"] += timed(unfused, iters)
+        tf, tu = timed(fused, iters), timed(unfused, iters)
+        out["fwd"]["fused_ms"] += tf
+        out["fwd"]["unfused_ms"] += tu
+        kname = C.create_string_buffer(96)
+        fused()
+        lib.lib.primkit_handle_last_kernel(d.h, kname, 96)
+        out.setdefault("layers", []).append({"layer": L.name, "fwd_fused_ms": tf, "fwd_unfused_ms": tu,
+                                             "fwd_kernel": kname.value.decode()})
         # backward: this layer's dgrad produces dz of the preceding BN (C channels)
         if L.c % 8 == 0 and L.c >= 64:
             pb = problem(n=n, c=L.c, h=L.h, w=L.h, k=L.k, y=L.r, x=L.r, pad=L.pad, stride=L.stride,
@@ -253,8 +259,10 @@ def cfg4(d, iters, n=256):
                 lib.check(lib.lib.primkit_batchnorm_backward_device(
                     d.h, dimc, abi.BF16, vp(bnx), vp(bny), vp(dz), vp(gc), vp(bc), vp(mc), vp(ic),
                     vp(bdx), vp(dg), vp(db), 1))
-            out["bwd"]["fused_ms"] += timed(bfused, iters)
-            out["bwd"]["unfused_ms"] += timed(bunfused, iters)
+            tbf, tbu = timed(bfused, iters), timed(bunfused, iters)
+            out["bwd"]["fused_ms"] += tbf
+            out["bwd"]["unfused_ms"] += tbu
+            out["layers"][-1].update({"bwd_fused_ms": tbf, "bwd_unfused_ms": tbu})
     for k in ("fwd", "bwd"):
         out[k]["speedup"] = out[k]["unfused_ms"] / out[k]["fused_ms"]
     out["batch"] = n
