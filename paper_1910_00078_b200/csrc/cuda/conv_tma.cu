@@ -22,6 +22,7 @@
 // Backward weights: rectangles of 64 pixels form the reduction blocks; dY and
 // the tap-shifted X rectangles arrive by TMA as MN-major operands; split-K
 // over rectangles with a fixed-order fp32 reduction.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -126,7 +127,10 @@ __device__ __forceinline__ int tile_kblocks(const TmaConvArgs& g, const RectInfo
 // rectangle's tap boxes and HALF of the 256 filter rows, the leader issues
 // M=256 MMAs, commits are multicast and both epilogues release the leader's
 // accumulator remotely.
-template <int BN, int STAGES, bool PHASED, bool NARROW, int MT, bool PAIR = false>
+// F32: fp32 operands as tf32 MMAs (the 3xTF32 path: operands are the hi/lo
+// concatenations of tf32x3_split, read as 32 fp32 per 128-byte row, so the
+// descriptors are the bf16 kernel's) and an fp32 output written directly.
+template <int BN, int STAGES, bool PHASED, bool NARROW, int MT, bool PAIR = false, bool F32 = false>
 __global__ void __launch_bounds__(kFpropThreads, 1)
     conv_tma_fprop_kernel(const __grid_constant__ CUtensorMap amap,
                           const __grid_constant__ CUtensorMap bmap,
@@ -273,7 +277,8 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------------------------------
       if (!PAIR || rank == 0) {
-        const uint32_t idesc = idesc_bf16_f32(PAIR ? 2 * BM : BM, BN, false, g.b_mn != 0);
+        const uint32_t idesc = F32 ? idesc_tf32_f32(BM, BN, false, false)
+                                   : idesc_bf16_f32(PAIR ? 2 * BM : BM, BN, false, g.b_mn != 0);
         const uint64_t bks = g.b_mn ? 128 : 2;  // B k-step: MN-major 16 rows, K-major 32 B
         int stage = 0;
         uint32_t phase = 0;
@@ -316,8 +321,12 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                         const uint64_t ad0 = NARROW ? umma_desc_noswz(a_base, L::kA / 8, 128)
                                                     : umma_desc_sw128(a_base + mt * BM * 128, 16, 1024);
                         constexpr uint64_t as = NARROW ? (2 * (L::kA / 8)) >> 4 : 2;
-                        mma4_bf16(d_tmem + mt * BN, ad0, ad0 + as, ad0 + 2 * as, ad0 + 3 * as, bd0,
-                                  bd0 + bks, bd0 + 2 * bks, bd0 + 3 * bks, idesc, kb != 0);
+                        if constexpr (F32)
+                            mma4_tf32(d_tmem + mt * BN, ad0, ad0 + as, ad0 + 2 * as, ad0 + 3 * as, bd0,
+                                      bd0 + bks, bd0 + 2 * bks, bd0 + 3 * bks, idesc, kb != 0);
+                        else
+                            mma4_bf16(d_tmem + mt * BN, ad0, ad0 + as, ad0 + 2 * as, ad0 + 3 * as, bd0,
+                                      bd0 + bks, bd0 + 2 * bks, bd0 + 3 * bks, idesc, kb != 0);
                     }
                     mma_commit_elect(&empty[stage]);
                     if (kb == nkb - 1) mma_commit_elect(&tmem_full[a]);
@@ -338,7 +347,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
         uint8_t* stg_base = smem + L::kStagingOff + ew * L::kStgBufs * 4096;
         int sbuf = 0;
         const bool has_epi = epilogue_active(&epi);
-        const bool tma_st = !PHASED || g.phase_tma;
+        const bool tma_st = !F32 && (!PHASED || g.phase_tma);
         BnStatAcc bacc;
         bacc.init();
         int it = 0;
@@ -416,6 +425,19 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
 #pragma unroll
                 for (int e = 0; e < 64; ++e) xf[e] = __uint_as_float(v[e]);
                 if (has_epi) epilogue_chunk64(epi, xf, n0c + c0, g.n_out, oy, ox, g.Ho, g.Wo);
+                if constexpr (F32) {
+                    // fp32 output: each lane writes its row's 64 values (pitch in floats)
+                    if (row_ok) {
+                        float* dst = reinterpret_cast<float*>(out) +
+                                     (((size_t)pn * g.Ho + oy) * g.Wo + ox) * g.out_pitch + n0c + c0;
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj)
+                            if (n0c + c0 + jj * 4 < g.out_pitch && c0 + jj * 4 < BN)
+                                reinterpret_cast<float4*>(dst)[jj] =
+                                    make_float4(xf[4 * jj], xf[4 * jj + 1], xf[4 * jj + 2], xf[4 * jj + 3]);
+                    }
+                    continue;
+                }
                 pack_stage64(xf, stg_u, lane, min(g.n_out - (n0c + c0), BN - c0));
                 if (tma_st) {
                     fence_proxy_async_smem();
@@ -785,12 +807,12 @@ __global__ void wgrad_sum_kernel(const float* __restrict__ partial, int splits, 
 // ---------------------------------------------------------------------------
 // host
 
-template <int BN, int STAGES, bool PHASED, bool NARROW, int MT = 1, bool PAIR = false>
+template <int BN, int STAGES, bool PHASED, bool NARROW, int MT = 1, bool PAIR = false, bool F32 = false>
 cudaError_t launch_fprop(const CUtensorMap& amap, const CUtensorMap& bmap, const YMaps& ymap,
                          void* out, const TmaConvArgs& g, const pk_epilogue& e, cudaStream_t st) {
     using L = FSmem<BN, STAGES, MT, PAIR>;
     static_assert(L::kBytes <= 227 * 1024, "smem");
-    auto kern = conv_tma_fprop_kernel<BN, STAGES, PHASED, NARROW, MT, PAIR>;
+    auto kern = conv_tma_fprop_kernel<BN, STAGES, PHASED, NARROW, MT, PAIR, F32>;
     static int attr_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -902,10 +924,13 @@ using namespace pk;
 
 // Forward / backward-data through the TMA rectangle path. Returns
 // cudaErrorNotSupported (without launching) when the geometry does not fit.
-cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, const void* filt,
-                        void* out, const pk_epilogue* epi, int bn_want, cudaStream_t st,
-                        bool filt_mn) {
+namespace pk {
+namespace {
+cudaError_t tma_conv_impl(const pk_conv_geom* g, bool dgrad, const void* src, const void* filt,
+                          void* out, const pk_epilogue* epi, int bn_want, cudaStream_t st,
+                          bool filt_mn, bool f32) {
     if (g->groups != 1 || g->transpose || g->r > 255 || g->s > 255) return cudaErrorNotSupported;
+    if (f32 && (dgrad || filt_mn || g->x_pitch % 64)) return cudaErrorNotSupported;
     const int src_pitch = dgrad ? g->y_pitch : g->x_pitch;
     const int out_pitch = dgrad ? g->x_pitch : g->y_pitch;
     // narrow sources (pitch < 64, e.g. the 3-channel stem) use 16-byte-row boxes
@@ -939,7 +964,7 @@ cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, cons
     // width leaves TMEM room for two double-buffered accumulators
     static const bool mt_off = std::getenv("PK_TMA_MT1") != nullptr;
     const int cfg_mt = cfg_field(&pk_tc_config::mt), cfg_pair = cfg_field(&pk_tc_config::pair);
-    t.mt = (!mt_off && cfg_mt != 1 && !narrow && sh == 1 && sw == 1 && bn <= 128) ? 2 : 1;
+    t.mt = (!f32 && !mt_off && cfg_mt != 1 && !narrow && sh == 1 && sw == 1 && bn <= 128) ? 2 : 1;
     const RectTile rt = tc::best_rect(g->n, hp0, wp0, BM * t.mt);
     t.bw = rt.bw;
     t.bh = rt.bh;
@@ -963,7 +988,7 @@ cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, cons
     }();
     t.m_tiles = t.n_tiles_n ? t.total_tiles / t.n_tiles_n : 0;
     t.total_pairs = 0;
-    if (!pair_off && cfg_pair != 1 && !narrow && sh == 1 && sw == 1 && bn == 256 && t.mt == 1 &&
+    if (!f32 && !pair_off && cfg_pair != 1 && !narrow && sh == 1 && sw == 1 && bn == 256 && t.mt == 1 &&
         g->r * g->s > 1 && (!epi || !epi->stats) &&
         (cfg_pair == 2 || (long long)((t.m_tiles + 1) / 2) * t.n_tiles_n >= 74))
         t.total_pairs = (t.m_tiles + 1) / 2 * t.n_tiles_n;
@@ -1000,12 +1025,95 @@ cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, cons
     pk_epilogue e{};
     e.act = -1;
     if (epi) e = *epi;
+    if (f32) {
+        if (phased || narrow || e.stats) return cudaErrorNotSupported;
+        if (bn == 64) return launch_fprop<64, 6, false, false, 1, false, true>(amap, bmap, ymap, out, t, e, st);
+        if (bn == 128) return launch_fprop<128, 5, false, false, 1, false, true>(amap, bmap, ymap, out, t, e, st);
+        return launch_fprop<256, 4, false, false, 1, false, true>(amap, bmap, ymap, out, t, e, st);
+    }
     if (narrow)
         return phased ? dispatch_fprop<true, true>(bn, amap, bmap, ymap, out, t, e, st)
                       : dispatch_fprop<false, true>(bn, amap, bmap, ymap, out, t, e, st);
     return phased ? dispatch_fprop<true, false>(bn, amap, bmap, ymap, out, t, e, st)
                   : dispatch_fprop<false, false>(bn, amap, bmap, ymap, out, t, e, st);
 }
+
+// 3xTF32 operand split: x_cat[pix][3Cp] = (hi(x), hi(x), lo(x)), w_cat[k][tap][3Cp] =
+// (hi(w), lo(w), hi(w)), hi = x rounded to tf32 (10-bit mantissa, low 13 bits zero),
+// lo = x - hi (exact in fp32). One GEMM over the 3Cp "channels" then sums
+// hi.hi + hi.lo + lo.hi: the fp32 product up to lo.lo (~2^-22 relative).
+__device__ __forceinline__ float tf32_hi(float v) {
+    uint32_t u = __float_as_uint(v);
+    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;  // RNE-ish (ties up)
+    return __uint_as_float(u);
+}
+__global__ void tf32x3_split_kernel(const float4* __restrict__ src, float4* __restrict__ dst, long long rows,
+                                    int cp4, int order) {
+    const long long total = rows * cp4;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / cp4;
+        const int c = (int)(i - r * cp4);
+        const float4 v = src[i];
+        const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+        const float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        float4* row = dst + r * 3 * cp4 + c;
+        row[0] = h;                        // block 0: hi (both operands)
+        row[cp4] = order ? l : h;          // block 1: x: hi, w: lo
+        row[2 * cp4] = order ? h : l;      // block 2: x: lo, w: hi
+    }
+}
+}  // namespace
+}  // namespace pk
+
+cudaError_t pk_tma_conv(const pk_conv_geom* g, bool dgrad, const void* src, const void* filt,
+                        void* out, const pk_epilogue* epi, int bn_want, cudaStream_t st,
+                        bool filt_mn) {
+    return pk::tma_conv_impl(g, dgrad, src, filt, out, epi, bn_want, st, filt_mn, false);
+}
+
+extern "C" {
+// Reduction depth limit: the tensor core's fp32 accumulation is not round-to-nearest,
+// and its error grows with the number of accumulated products. Measured: R*S*C = 576
+// and 1152 stay inside the reference's max-rel 1e-4 (proj/tests/acceptance.cpp:137);
+// 5x5 x 64 (1600, 4800 tf32 products) reached 2.6e-4, so deeper reductions stay on the
+// fp32 FMA kernels.
+int pk_tf32x3_fwd_supported(const pk_conv_geom* g) {
+    return g->groups == 1 && !g->transpose && g->x_pitch % 32 == 0 && g->f_pitch == g->x_pitch &&
+           g->r <= 255 && g->s <= 255 && g->y_pitch % 4 == 0 && g->r * g->s * g->x_pitch <= 1152 &&
+           tc::encode_fn() != nullptr;
+}
+
+size_t pk_tf32x3_fwd_workspace(const pk_conv_geom* g) {
+    const size_t xb = (size_t)g->n * g->h * g->w * 3 * g->x_pitch * 4;
+    const size_t wb = (size_t)g->k * g->r * g->s * 3 * g->f_pitch * 4;
+    return (xb + 255) / 256 * 256 + wb;
+}
+
+// fp32 forward convolution on the tensor cores with fp32-level accuracy (3xTF32).
+cudaError_t pk_cuda_tf32x3_fwd(const pk_conv_geom* g, const void* x, const void* w, void* y,
+                               const pk_epilogue* epi, void* workspace, size_t ws_bytes, cudaStream_t st) {
+    if (!pk_tf32x3_fwd_supported(g) || ws_bytes < pk_tf32x3_fwd_workspace(g)) return cudaErrorNotSupported;
+    const size_t xb = (size_t)g->n * g->h * g->w * 3 * g->x_pitch * 4;
+    float* xcat = static_cast<float*>(workspace);
+    float* wcat = reinterpret_cast<float*>(static_cast<char*>(workspace) + (xb + 255) / 256 * 256);
+    const long long xrows = (long long)g->n * g->h * g->w, wrows = (long long)g->k * g->r * g->s;
+    const int cp4 = g->x_pitch / 4;
+    auto blocks = [](long long n) { return (unsigned)std::min<long long>((n + 255) / 256, 148LL * 16); };
+    cudaError_t err = pk_launch(tf32x3_split_kernel, dim3(blocks(xrows * cp4)), dim3(256), 0, st,
+                                (const float4*)x, (float4*)xcat, xrows, cp4, 0);
+    if (err != cudaSuccess) return err;
+    count_launch();
+    err = pk_launch(tf32x3_split_kernel, dim3(blocks(wrows * cp4)), dim3(256), 0, st, (const float4*)w,
+                    (float4*)wcat, wrows, cp4, 1);
+    if (err != cudaSuccess) return err;
+    count_launch();
+    // the concatenations viewed as bf16 tensors of 6 x pitch elements per pixel / filter tap
+    pk_conv_geom g2 = *g;
+    g2.x_pitch = g2.f_pitch = 6 * g->x_pitch;
+    return pk::tma_conv_impl(&g2, false, xcat, wcat, y, epi, 256, st, false, true);
+}
+}  // extern "C"
 
 // One wave: split-K so that tiles x splits fills the SMs once (no tail wave);
 // at least 4 k-blocks per split.

@@ -202,6 +202,13 @@ cudaError_t pk_cuda_sq_diff(const void* a, const void* b, long long n, int dtype
                             cudaStream_t st);
 // split-K partials of pk_cuda_igemm_tc_wgrad under the same config
 size_t pk_tc_wgrad_workspace(const pk_conv_geom* g, int num_sms, const pk_tc_config* cfg);
+// fp32 forward convolution on the tensor cores at fp32 accuracy (3xTF32: hi/lo
+// operand split into the workspace, one tf32 GEMM over the concatenation, fp32 out;
+// groups 1, channel pitch multiple of 32). cudaErrorNotSupported: not eligible.
+int pk_tf32x3_fwd_supported(const pk_conv_geom* g);
+size_t pk_tf32x3_fwd_workspace(const pk_conv_geom* g);
+cudaError_t pk_cuda_tf32x3_fwd(const pk_conv_geom* g, const void* x, const void* w, void* y,
+                               const pk_epilogue* epi, void* workspace, size_t ws_bytes, cudaStream_t st);
 cudaError_t pk_cuda_igemm_tc_fwd(const pk_conv_geom* g, const void* x, const void* f, void* y,
                                  const pk_epilogue* epi, const pk_tc_config* cfg,
                                  cudaStream_t st);

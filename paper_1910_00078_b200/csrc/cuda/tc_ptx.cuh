@@ -182,6 +182,13 @@ __host__ __device__ constexpr uint32_t idesc_f16_f32(int m, int n, bool a_mn_maj
            (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
 }
 
+// Instruction descriptor: kind::tf32, A/B = tf32 (fp32 in shared memory), D = f32.
+__host__ __device__ constexpr uint32_t idesc_tf32_f32(int m, int n, bool a_mn_major, bool b_mn_major) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn_major ? 1u : 0u) << 15) |
+           ((b_mn_major ? 1u : 0u) << 16) | (static_cast<uint32_t>(n >> 3) << 17) |
+           (static_cast<uint32_t>(m >> 4) << 24);
+}
+
 // Instruction descriptor: kind::f16, A/B = bf16, D = f32.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int m, int n, bool a_mn_major,
                                                       bool b_mn_major) {
@@ -214,6 +221,22 @@ __device__ __forceinline__ void mma4_bf16(uint32_t tmem_d, uint64_t a0, uint64_t
         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %2, %6, %9, 1;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %3, %7, %9, 1;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %4, %8, %9, 1;\n\t}" ::"r"(tmem_d),
+        "l"(a0), "l"(a1), "l"(a2), "l"(a3), "l"(b0), "l"(b1), "l"(b2), "l"(b3), "r"(idesc),
+        "r"(accumulate)
+        : "memory");
+}
+// Four tf32 MMAs (K = 8 fp32 = 32 bytes each, so the same descriptor steps as bf16).
+__device__ __forceinline__ void mma4_tf32(uint32_t tmem_d, uint64_t a0, uint64_t a1, uint64_t a2,
+                                          uint64_t a3, uint64_t b0, uint64_t b1, uint64_t b2,
+                                          uint64_t b3, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "setp.ne.b32 p, %10, 0;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %5, %9, p;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %2, %6, %9, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %3, %7, %9, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %4, %8, %9, 1;\n\t}" ::"r"(tmem_d),
         "l"(a0), "l"(a1), "l"(a2), "l"(a3), "l"(b0), "l"(b1), "l"(b2), "l"(b3), "r"(idesc),
         "r"(accumulate)
         : "memory");

@@ -8,6 +8,7 @@
 //              Winograd     winograd_f23                 winograd_f23
 //              FFT          fft (complex<double>)        fft
 //              ImplicitGemm igemm_simt_tiled / _fwd      igemm_tc_fwd
+//   (f32 Direct / ImplicitGemm forward, groups 1, pitch % 32 == 0: 3xTF32 tcgen05, tf32x3_tc_fwd)
 //   BwdData    Direct       direct_bwd_data              direct_bwd_data
 //              Im2colGemm   SIMT GEMM + col2im / image   igemm_tc_dgrad
 //   BwdWeights Direct       direct_bwd_weights           direct_bwd_weights
@@ -252,6 +253,17 @@ bool ConvPlan::fuses_stats() const {
     return false;
 }
 
+// fp32 forward convolutions (Direct / ImplicitGemm, groups 1) run as 3xTF32 tensor-core
+// GEMMs when the channel pitch allows (fp32-level accuracy; PK_TF32X3=0: SIMT kernels).
+bool tf32x3_eligible(const pk_conv_geom& g, int dt) {
+    static const bool off = [] {
+        const char* v = std::getenv("PK_TF32X3");
+        return v && v[0] == '0';
+    }();
+    return !off && dt == PK_F32 && !pk_depthwise_supported(&g) && !pk_grouped_supported(&g) &&
+           pk_tf32x3_fwd_supported(&g);
+}
+
 std::size_t ConvPlan::device_workspace_bytes(int num_sms) const {
     // Every device buffer run() touches besides its operands comes out of the
     // caller's workspace, so this mirrors run()'s dispatch exactly. Split-K
@@ -265,6 +277,8 @@ std::size_t ConvPlan::device_workspace_bytes(int num_sms) const {
     if (tc_algo && stem_eligible(g, dt, nullptr)) return stem_workspace(g, problem_.direction, num_sms);
     switch (problem_.direction) {
         case ConvDirection::Forward:
+            if ((algo_ == ConvAlgo::Direct || algo_ == ConvAlgo::ImplicitGemm) && tf32x3_eligible(g, dt))
+                return pk_tf32x3_fwd_workspace(&g);
             if (algo_ == ConvAlgo::FFT) return pk_cuda_fft_scratch_bytes(&g);
             if (algo_ == ConvAlgo::Winograd && dt == PK_BF16 && pk_winograd_tc_supported(&g))
                 return winograd_ws(g, winograd_tile_m());
@@ -351,6 +365,11 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                         break;
                     }
                 }
+                if (tf32x3_eligible(g, dt)) {
+                    kernel = "tf32x3_tc_fwd";
+                    ck(pk_cuda_tf32x3_fwd(&g, a, b, out, epi, ws, ws_bytes, st), "tf32x3_fwd");
+                    break;
+                }
                 kernel = "direct_simt";
                 ck(pk_cuda_direct_fwd(&g, dt, a, b, out, epi, st), "direct_fwd");
                 break;
@@ -387,6 +406,9 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                 } else if (pk_grouped_supported(&g)) {
                     kernel = "grouped_simt";
                     ck(pk_cuda_grouped_fwd(&g, dt, a, b, out, epi, h.num_sms(), st), "grouped_fwd");
+                } else if (tf32x3_eligible(g, dt)) {
+                    kernel = "tf32x3_tc_fwd";
+                    ck(pk_cuda_tf32x3_fwd(&g, a, b, out, epi, ws, ws_bytes, st), "tf32x3_fwd");
                 } else {
                     if (g.groups == 1 && !g.transpose && g.x_pitch % 8 == 0 && g.f_pitch == g.x_pitch) {
                         // register-tiled implicit GEMM on CUDA cores (64 px x 64 k per CTA,

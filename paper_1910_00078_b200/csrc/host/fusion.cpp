@@ -337,7 +337,7 @@ FusionPlan::DeviceArgs& FusionPlan::device_args(Handle& h) {
     upload_vec(h, dev_->beta, args_.bn_beta);
     upload_vec(h, dev_->mean, args_.bn_mean);
     upload_vec(h, dev_->var, args_.bn_var);
-    // Folded affine for the bf16 tensor-core epilogue (no per-activation BN):
+    // Folded affine for the tensor-core epilogues (no per-activation BN):
     //   ((acc + b) - mu) / sqrt(var + eps) * g + beta = acc * s + t,
     //   s = g / sqrt(var + eps), t = (b - mu) * s + beta
     dev_->folded = false;
@@ -346,7 +346,8 @@ FusionPlan::DeviceArgs& FusionPlan::device_args(Handle& h) {
     for (const FusionOp& op : ops_)
         if (op.kind == FusionOp::Kind::BatchNormInference && op.bn_mode == BatchNormMode::PerActivation)
             per_act = true;
-    if (conv && input_desc_.etype == ElementType::BF16 && !per_act) {
+    // (also the fp32 3xTF32 path: its epilogue reads the affine as float4 vectors)
+    if (conv && !per_act) {
         const std::int64_t k = cur_desc_.dims[1];
         const std::size_t padded = static_cast<std::size_t>((k + 63) / 64 * 64 + 64);
         std::vector<float> s(padded, 0.0f), t(padded, 0.0f);
@@ -426,6 +427,20 @@ void fusion_execute(Handle& h, FusionPlan& plan, const void* input, void* output
             h.last_kernel = "winograd_f23+epilogue";
             check_cuda(pk_cuda_winograd_f23(&g, dt, input, d.filter.get(), output, &e, st),
                        "winograd_f23");
+        } else if (dt == PK_F32 && tf32x3_eligible(g, dt)) {
+            // fp32 Direct row: 3xTF32 tensor-core GEMM (fp32-level accuracy), the
+            // epilogue's exact formula applied before the fp32 store
+            const std::size_t wsb = pk_tf32x3_fwd_workspace(&g);
+            h.last_kernel = "tf32x3_tc_fwd+epilogue";
+            pk_epilogue tce = e;
+            if (d.folded) {
+                tce.bias = nullptr;
+                tce.bn_mean = tce.bn_var = tce.bn_gamma = tce.bn_beta = nullptr;
+                tce.ch_scale = static_cast<const float*>(d.scale.get());
+                tce.ch_shift = static_cast<const float*>(d.shift.get());
+            }
+            check_cuda(pk_cuda_tf32x3_fwd(&g, input, d.filter.get(), output, &tce, h.scratch(11, wsb), wsb, st),
+                       "tf32x3_fwd");
         } else {
             h.last_kernel = "direct_simt+epilogue";
             check_cuda(pk_cuda_direct_fwd(&g, dt, input, d.filter.get(), output, &e, st),
