@@ -843,9 +843,9 @@ cudaError_t dispatch_fprop(int bn, const CUtensorMap& amap, const CUtensorMap& b
                            const pk_epilogue& e, cudaStream_t st) {
     if (g.total_pairs > 0 && !PHASED && !NARROW && bn == 256)
         return launch_fprop<256, 6, false, false, 1, true>(amap, bmap, ymap, out, g, e, st);
-    if (g.mt == 2 && !PHASED && !NARROW) {
-        if (bn == 64) return launch_fprop<64, 4, false, false, 2>(amap, bmap, ymap, out, g, e, st);
-        if (bn == 128) return launch_fprop<128, 3, false, false, 2>(amap, bmap, ymap, out, g, e, st);
+    if (g.mt == 2 && !NARROW) {
+        if (bn == 64) return launch_fprop<64, 4, PHASED, false, 2>(amap, bmap, ymap, out, g, e, st);
+        if (bn == 128) return launch_fprop<128, 3, PHASED, false, 2>(amap, bmap, ymap, out, g, e, st);
     }
     if (bn == 64) return launch_fprop<64, 6, PHASED, NARROW>(amap, bmap, ymap, out, g, e, st);
     if (bn == 128) return launch_fprop<128, 5, PHASED, NARROW>(amap, bmap, ymap, out, g, e, st);
@@ -964,7 +964,14 @@ cudaError_t tma_conv_impl(const pk_conv_geom* g, bool dgrad, const void* src, co
     // width leaves TMEM room for two double-buffered accumulators
     static const bool mt_off = std::getenv("PK_TMA_MT1") != nullptr;
     const int cfg_mt = cfg_field(&pk_tc_config::mt), cfg_pair = cfg_field(&pk_tc_config::pair);
-    t.mt = (!f32 && !mt_off && cfg_mt != 1 && !narrow && sh == 1 && sw == 1 && bn <= 128) ? 2 : 1;
+    // phased (strided dgrad) tiles too: their few k-blocks (1-4 taps x chunks) leave the
+    // per-tile handshakes dominant, and 256-pixel tiles halve them (PK_TMA_MT2_PHASED=0: off)
+    static const bool mt_phased_off = [] {
+        const char* v = std::getenv("PK_TMA_MT2_PHASED");
+        return v && v[0] == '0';
+    }();
+    t.mt = (!f32 && !mt_off && cfg_mt != 1 && !narrow && ((sh == 1 && sw == 1) || !mt_phased_off) &&
+            bn <= 128) ? 2 : 1;
     const RectTile rt = tc::best_rect(g->n, hp0, wp0, BM * t.mt);
     t.bw = rt.bw;
     t.bh = rt.bh;
