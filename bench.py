@@ -9,8 +9,9 @@ tcgen05), BackwardData (Im2colGemm -> tcgen05 dgrad), BackwardWeights
 followed (N>1) by the dW all-reduce. value = algorithmic FLOPs
 (2*N*K*C*R*S*P*Q per direction, summed) of all ranks / max-over-ranks time.
 
-Also reported on the same JSON line: the roofline of the dominant kernel
-family, the fused conv+bias+ReLU speedup (cfg2), an end-to-end number through
+Also reported on the same JSON line: the roofline of the dominant kernel (by
+launch share of the step: the HBM-bound resident-filter 1x1 GEMM; the tcgen05
+family's tensor roofline rides along), the fused conv+bias+ReLU speedup (cfg2), an end-to-end number through
 the host-buffer C ABI, the reference CPU path timed on this host, clocks.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -378,6 +379,22 @@ def roofline(torch, lib, handle, net, peaks):
     return res
 
 
+def ncu_fwd_launch_traffic(layer_indices):
+    """Average DRAM bytes (read + write) per launch of the given forward layers,
+    from the committed ncu launch list of one step (forward launches first, in
+    layer order). None if absent."""
+    import csv
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*launches_step.csv")))
+    if not files or not layer_indices:
+        return None, None
+    with open(files[-1]) as f:
+        rows = list(csv.DictReader(f))
+    b = [float(rows[i]["dram__bytes_read.sum"]) + float(rows[i]["dram__bytes_write.sum"])
+         for i in layer_indices if i < len(rows)]
+    return (sum(b) / len(b) if b else None), os.path.basename(files[-1])
+
+
 def hbm_kernel_roofline(torch, lib, handle, net, peaks):
     """The kernel with the largest share of the step's launch list is the
     resident-filter plain GEMM (conv_tc PLAIN_RES) of the HBM-bound 1x1 layers.
@@ -387,9 +404,11 @@ def hbm_kernel_roofline(torch, lib, handle, net, peaks):
     with the measured HBM copy bandwidth."""
     pitch = lambda c: (c + 7) // 8 * 8  # noqa: E731
     ms_tot, bytes_tot, n = 0.0, 0.0, 0
-    for (L, x, w, y, dy, dx, dw, probs) in net.items:
+    idx = []
+    for li, (L, x, w, y, dy, dx, dw, probs) in enumerate(net.items):
         if not (L.r == 1 and L.stride == 1 and pitch(L.c) <= 256 and L.k >= 64):
             continue
+        idx.append(li)
         p, s = probs[0]
         run_conv(lib, handle, p, s, x, w, y, net.ws)
         ms_tot += time_region(torch, lambda: run_conv(lib, handle, p, s, x, w, y, net.ws), 5) / 5
@@ -399,10 +418,13 @@ def hbm_kernel_roofline(torch, lib, handle, net, peaks):
     if n == 0:
         return None
     achieved = bytes_tot / (ms_tot * 1e-3) / 1e9
+    traffic, src = ncu_fwd_launch_traffic(idx)
     return {"bound": "hbm", "kernel": "conv_tc_kernel PLAIN_RES (resident-filter 1x1 GEMM), "
             "%d ResNet-50 forward launches, N=%d" % (n, net.n), "achieved": achieved,
             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-            "algorithmic_bytes_per_launch": bytes_tot / n, "ms_per_launch": ms_tot / n}
+            "traffic": traffic, "traffic_unit": "bytes per launch (ncu DRAM read + write, average)",
+            "traffic_source": src, "algorithmic_bytes_per_launch": bytes_tot / n,
+            "ms_per_launch": ms_tot / n}
 
 
 def ncu_family_traffic(family: str):
@@ -650,7 +672,7 @@ def main():
         peak = peaks["bf16_tflops_sustained"]
         dom_name = max(rf, key=lambda k: rf[k]["ms"])  # largest share of the step
         dom = rf[dom_name]
-        extras["roofline"] = {
+        family = {
             "bound": "tensor",
             "kernel": "%s family (all 53 ResNet-50 convs of that direction, N=%d; largest share "
                       "of the step)" % (dom_name, args.batch),
@@ -670,9 +692,17 @@ def main():
                           args.batch * L.out_h * L.out_h * pitch(L.k))
             roof_ms += max(L.flops(args.batch) / (peak * 1e12),
                            byts / (peaks["hbm_gbs"] * 1e9)) * 1e3
-        extras["roofline"]["hbm_kernel"] = hbm_kernel_roofline(torch, lib, handle, net, peaks)
-        extras["roofline"]["layer_roofline_ms"] = roof_ms
-        extras["roofline"]["frac_of_layer_roofline"] = roof_ms / dom["ms"]
+        family["layer_roofline_ms"] = roof_ms
+        family["frac_of_layer_roofline"] = roof_ms / dom["ms"]
+        # The dominant single kernel by launch share of the step's ncu launch list
+        # (profiles/*launches_step.md) is the HBM-bound resident-filter 1x1 GEMM:
+        # it is the line's roofline; the tensor family and the whole-step position
+        # against the per-layer roofline ride along.
+        hk = hbm_kernel_roofline(torch, lib, handle, net, peaks)
+        extras["roofline"] = dict(hk) if hk else family
+        if hk:
+            extras["roofline"]["peak_source"] = f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json)"
+            extras["roofline"]["tensor_family"] = family
         extras["roofline"]["step_frac_of_layer_roofline"] = 3 * roof_ms / ms_step
         if rank == 0:
             extras["fusion"] = fusion_speedup(torch, lib, handle, device)
