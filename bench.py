@@ -221,6 +221,7 @@ class Net:
                 probs[d] = (p, solver.encode())
             self.items.append((L, x, w, y, dy, dx, dw, probs))
         self.ws = torch.empty(max(max_ws, 256), dtype=torch.uint8, device=device)
+        self.ws2 = None  # backward-weights stream's workspace (two-stream backward)
 
     def register_grads(self, dp):
         """dW tensors in the order the backward pass produces them (reverse
@@ -248,27 +249,51 @@ def run_conv(lib, handle, p, solver, a, b, out, ws):
         lib.check(st)
 
 
-def step(lib, handle, net, directions=(0, 1, 2), dp=None):
+def step(lib, handle, net, directions=(0, 1, 2), dp=None, wside=None):
     """One training step's convolutions. With a data-parallel context, each
     layer's dW is handed to the native NCCL buckets (primkit_dp_*) right after
     its backward-weights kernel is enqueued, so a bucket's all-reduce overlaps
-    the backward of the layers below it; finish() joins before the step ends."""
+    the backward of the layers below it; finish() joins before the step ends.
+
+    wside = (torch, handle, stream, events): backward weights on a second
+    stream with its own handle and workspace. A layer's dW needs only its dY
+    (produced by the previous layer's backward data) and its forward input, so
+    it runs beside the next backward-data kernel and fills the SMs that kernel's
+    tail and ramp leave idle (the graph keeps the true dependencies as events)."""
     ws = net.ws
     if 0 in directions:
         for (L, x, w, y, dy, dx, dw, probs) in net.items:
             p, s = probs[0]
             run_conv(lib, handle, p, s, x, w, y, ws)
+    if wside is not None and 2 in directions:
+        torch, wh, wstream, ev = wside
+        main = torch.cuda.current_stream()
+        ev[0].record(main)               # forward done: inputs of every dW ready
+        wstream.wait_event(ev[0])
     for i, (L, x, w, y, dy, dx, dw, probs) in enumerate(reversed(net.items)):
+        if wside is not None and 2 in directions:
+            p, s = probs[2]
+            # dY of this layer came from the previous iteration's backward data
+            if i > 0 and 1 in directions:
+                wstream.wait_event(ev[i])
+            run_conv(lib, wh, p, s, dy, x, dw, net.ws2)
+            if dp is not None:
+                dp.ready(i)
         if 1 in directions:
             p, s = probs[1]
             run_conv(lib, handle, p, s, dy, w, dx, ws)
-        if 2 in directions:
+            if wside is not None and 2 in directions:
+                ev[i + 1].record(main)
+        if wside is None and 2 in directions:
             p, s = probs[2]
             run_conv(lib, handle, p, s, dy, x, dw, ws)
             if dp is not None:
                 dp.ready(i)
     if dp is not None:
         dp.finish()
+    if wside is not None and 2 in directions:
+        ev[len(net.items) + 1].record(wstream)
+        main.wait_event(ev[len(net.items) + 1])
 
 
 def time_region(torch, fn, iters):
@@ -546,6 +571,8 @@ def main():
     ap.add_argument("--batch", type=int, default=256, help="images per GPU")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-extras", action="store_true", help="skip e2e/cpu/fusion legs")
+    ap.add_argument("--streams", type=int, default=2, choices=(1, 2),
+                    help="2: backward weights on a second stream beside backward data")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch the step eagerly instead of as one CUDA graph")
     ap.add_argument("--bucket-mb", type=float, default=25.0, help="fp32 MiB per dW all-reduce bucket")
@@ -592,17 +619,29 @@ def main():
 
     layers = resnet50_layers()
     net = Net(torch, lib, handle, layers, args.batch, device)
+    wside = None
+    if args.streams == 2:
+        wstream = torch.cuda.Stream(device=device)
+        wh_ptr = C.c_void_p()
+        lib.check(lib.lib.primkit_handle_create_with_stream(C.c_void_p(wstream.cuda_stream), local,
+                                                            C.byref(wh_ptr)))
+
+        class _WH:
+            ptr = wh_ptr
+        net.ws2 = torch.empty_like(net.ws)
+        wside = (torch, _WH(), wstream,
+                 [torch.cuda.Event() for _ in range(len(layers) + 2)])
     dp = None
     if world > 1 or args.dp:
         from paper_1910_00078_b200.dist import DataParallel
-        dp = DataParallel(lib, handle.ptr, rank, world, dist=dist,
+        dp = DataParallel(lib, (wside[1].ptr if wside else handle.ptr), rank, world, dist=dist,
                           bucket_bytes=int(args.bucket_mb * (1 << 20)))
         net.register_grads(dp)
     if args.layer_report:
         layer_report(torch, lib, handle, net, load_peaks()[0], args.layer_report)
         return 0
     for _ in range(args.warmup):
-        step(lib, handle, net, dp=dp)
+        step(lib, handle, net, dp=dp, wside=wside)
     torch.cuda.synchronize()
     if dp is not None:
         dp.check()
@@ -611,7 +650,7 @@ def main():
 
     launches0 = C.c_uint64()
     lib.check(lib.lib.primkit_handle_kernel_launches(handle.ptr, C.byref(launches0)))
-    run_step = lambda: step(lib, handle, net, dp=dp)  # noqa: E731
+    run_step = lambda: step(lib, handle, net, dp=dp, wside=wside)  # noqa: E731
     graph_note = "eager launches"
     launches_per_step = None
     if args.graph:
@@ -623,7 +662,7 @@ def main():
             with torch.cuda.graph(graph):
                 lib.check(lib.lib.primkit_handle_set_stream(
                     handle.ptr, C.c_void_p(torch.cuda.current_stream().cuda_stream)))
-                step(lib, handle, net, dp=dp)  # the 159 convolutions (+ NCCL buckets)
+                step(lib, handle, net, dp=dp, wside=wside)  # the 159 convolutions (+ NCCL buckets)
             lib.check(lib.lib.primkit_handle_set_stream(handle.ptr, C.c_void_p(stream.cuda_stream)))
             lc = C.c_uint64()
             lib.check(lib.lib.primkit_handle_kernel_launches(handle.ptr, C.byref(lc)))
