@@ -6,7 +6,7 @@
 //   Forward    Direct       direct_fwd                   direct_fwd
 //              Im2colGemm   im2col + SIMT GEMM / image   im2col + tcgen05 GEMM / image
 //              Winograd     winograd_f23                 winograd_f23
-//              FFT          fft (complex<double>)        fft
+//              FFT          fft (complex<float>, batched) fft
 //              ImplicitGemm igemm_simt_tiled / _fwd      igemm_tc_fwd
 //   (f32 Direct / ImplicitGemm forward, groups 1, pitch % 32 == 0: 3xTF32 tcgen05, tf32x3_tc_fwd)
 //   BwdData    Direct       direct_bwd_data              direct_bwd_data
