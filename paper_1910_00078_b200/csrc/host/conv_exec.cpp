@@ -277,7 +277,9 @@ std::size_t ConvPlan::device_workspace_bytes(int num_sms) const {
     if (tc_algo && stem_eligible(g, dt, nullptr)) return stem_workspace(g, problem_.direction, num_sms);
     switch (problem_.direction) {
         case ConvDirection::Forward:
-            if ((algo_ == ConvAlgo::Direct || algo_ == ConvAlgo::ImplicitGemm) && tf32x3_eligible(g, dt))
+            if ((algo_ == ConvAlgo::Direct || algo_ == ConvAlgo::ImplicitGemm ||
+                 (algo_ == ConvAlgo::Im2colGemm && !g.transpose)) &&
+                tf32x3_eligible(g, dt))
                 return pk_tf32x3_fwd_workspace(&g);
             if (algo_ == ConvAlgo::FFT) return pk_cuda_fft_scratch_bytes(&g);
             if (algo_ == ConvAlgo::Winograd && dt == PK_BF16 && pk_winograd_tc_supported(&g))
@@ -450,6 +452,13 @@ void ConvPlan::run(Handle& h, const void* a, const void* b, void* out, void* ws,
                                "gemm_simt");
                             ck(pk_cuda_col2im_transpose(&g, dt, col, n, grp, out, st), "col2im_t");
                         }
+                    break;
+                }
+                if (tf32x3_eligible(g, dt)) {
+                    // fp32: the column matrix formed on the fly by TMA (implicit im2col)
+                    // and one 3xTF32 tensor-core GEMM instead of the per-image SIMT GEMMs
+                    kernel = "tf32x3_tc_fwd";
+                    ck(pk_cuda_tf32x3_fwd(&g, a, b, out, epi, ws, ws_bytes, st), "tf32x3_fwd");
                     break;
                 }
                 const bool tc = dt == PK_BF16 && pk_tc_fwd_supported(&g);

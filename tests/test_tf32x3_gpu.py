@@ -1,6 +1,6 @@
 """fp32 forward convolutions on the tensor cores at fp32 accuracy (3xTF32).
 
-Direct / ImplicitGemm fp32 forward problems with groups 1 and a channel pitch
+Direct / ImplicitGemm / Im2colGemm fp32 forward problems with groups 1 and a channel pitch
 that is a multiple of 32 run `tf32x3_tc_fwd`: the operands are split into a
 tf32 "hi" part and an fp32 remainder "lo" (conv_tma.cu tf32x3_split_kernel) and
 one tcgen05 kind::tf32 GEMM over the concatenation sums hi.hi + hi.lo + lo.hi.
@@ -30,7 +30,7 @@ SHAPES = [
 
 
 @pytest.mark.parametrize("si", range(len(SHAPES)))
-@pytest.mark.parametrize("solver", ["ImplicitGemm", "Direct"])
+@pytest.mark.parametrize("solver", ["ImplicitGemm", "Direct", "Im2colGemm"])
 def test_tf32x3_forward_matches_fp32_oracle(lib, si, solver):
     rng = np.random.default_rng(500 + si)
     sh = SHAPES[si]
