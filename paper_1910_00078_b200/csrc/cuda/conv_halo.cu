@@ -67,13 +67,20 @@ constexpr int kResMax = 80 * 1024;
 // when BN = 64.
 constexpr int kHaloRows3 = 352;
 constexpr int kResMax3 = 74 * 1024;
-template <int BN, int BSTAGES, bool RESB, int HB = kHaloBufs>
+// MT = 2: 256-position tiles (two M=128 MMAs per tap on views 128 rows apart in
+// the same halo): a 3x3 halo over a 58-wide grid is 8 rows for 256 positions
+// instead of 6 rows for 128, so the L2 -> SM halo bytes per output drop by a
+// third (the 64-channel layers are bound by that stream, not by the MMAs:
+// with the MMAs disabled the 128-position kernel still took 55.6 of 80 us on
+// ResNet conv2_x). Two halo buffers, direct epilogue stores (no staging).
+constexpr int kHaloRowsMT2 = 480;
+template <int BN, int BSTAGES, bool RESB, int HB = kHaloBufs, int MT = 1>
 struct HSmem {
-    static constexpr int kHalo = (HB == 3 ? kHaloRows3 : 448) * 128;  // grid rows x 128 B
+    static constexpr int kHalo = (MT == 2 ? kHaloRowsMT2 : HB == 3 ? kHaloRows3 : 448) * 128;  // grid rows x 128 B
     static constexpr int kB = BN * 128;                // one (tap, chunk) filter slice
     static constexpr int kBOff = HB * kHalo;
     static constexpr int kStgOff = kBOff + (RESB ? (HB == 3 ? kResMax3 : kResMax) : BSTAGES * kB);
-    static constexpr int kStaging = (HB == 3 ? 4 : 8) * 4096;
+    static constexpr int kStaging = MT == 2 ? 0 : (HB == 3 ? 4 : 8) * 4096;
     static constexpr int kBarOff = kStgOff + kStaging;
     static constexpr int kBytes = kBarOff + (2 * HB + 2 * BSTAGES + 4) * 8 + 16 + 1024;
 };
@@ -81,23 +88,25 @@ struct HSmem {
 struct HTile {
     int n, p0, nt, row0;
 };
+template <int MT = 1>
 __device__ __forceinline__ HTile htile(const HaloArgs& g, int t) {
     HTile h;
     h.nt = t % g.n_tiles_n;
     const int mt = t / g.n_tiles_n;
     h.n = mt / g.tiles_img;
-    h.p0 = (mt - h.n * g.tiles_img) * kM;
+    h.p0 = (mt - h.n * g.tiles_img) * (kM * MT);
     h.row0 = h.p0 / g.Wg;
     return h;
 }
 
-template <int BN, int BSTAGES, bool RESB, int HB>
+template <int BN, int BSTAGES, bool RESB, int HB, int MT = 1>
 __global__ void __launch_bounds__(kHThreads, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap amap,
                      const __grid_constant__ CUtensorMap bmap, __nv_bfloat16* __restrict__ out,
                      const __grid_constant__ HaloArgs g, const pk_epilogue epi) {
-    using L = HSmem<BN, BSTAGES, RESB, HB>;
+    using L = HSmem<BN, BSTAGES, RESB, HB, MT>;
     static_assert(HB == 2 || BN == 64, "3 halo buffers: BN = 64 only");
+    static_assert(MT == 1 || (BN == 64 && RESB && HB == 2), "256-position tiles: BN = 64");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -109,7 +118,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
     uint64_t* tmem_empty = tmem_full + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr uint32_t kCols = 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+    constexpr uint32_t kCols = 2 * MT * BN <= 128 ? 128 : 2 * MT * BN <= 256 ? 256 : 512;
     const int taps = g.R * g.S;
 
     if (threadIdx.x == 0) {
@@ -161,7 +170,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
                     }
             }
             for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
-                const HTile ht = htile(g, t);
+                const HTile ht = htile<MT>(g, t);
                 for (int ck = 0; ck < g.cpt; ++ck) {
                     hstamp(g, (t - blockIdx.x) / gridDim.x, 8);
                     mbar_wait(&h_empty[hs], hph ^ 1);
@@ -207,20 +216,20 @@ __global__ void __launch_bounds__(kHThreads, 1)
         int it = 0;
         if (RESB) mbar_wait(&b_full[0], 0);
         for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++it) {
-            const HTile ht = htile(g, t);
+            const HTile ht = htile<MT>(g, t);
             const int a = it & 1;
             hstamp(g, it, 0);
             mbar_wait(&tmem_empty[a], ((it >> 1) & 1) ^ 1);
             hstamp(g, it, 1);
             tc_fence_after();
-            const uint32_t d_tmem = tmem_base + a * BN;
+            const uint32_t d_tmem = tmem_base + a * (MT * BN);
             const int base_row = ht.p0 - ht.row0 * g.Wg;
             for (int ck = 0; ck < g.cpt; ++ck) {
                 mbar_wait(&h_full[hs], hph);
                 hstamp(g, it, 2);
                 tc_fence_after();
                 const uint32_t halo_u = smem_u32(smem + hs * L::kHalo);
-                if (RESB && !(g.debug & ~24)) {
+                if (RESB && !(g.debug & ~56)) {
                     // resident filter: descriptors are the tile base plus a per-tap
                     // offset (start field in 16-byte units), two taps per issue block;
                     // keeps the issuing thread ahead of N=64 MMAs (48 clk each)
@@ -228,25 +237,31 @@ __global__ void __launch_bounds__(kHThreads, 1)
                         halo_u + ((g.debug & 16) ? 0 : base_row * 128), 16, 1024);
                     const uint64_t bt = umma_desc_sw128(
                         smem_u32(smem + L::kBOff + ck * taps * L::kB), blbo, 1024);
+#pragma unroll
+                  for (int mt = 0; mt < MT; ++mt) {
+                    // M tile mt: positions p0 + 128 mt, i.e. the halo view 128 rows further
+                    const uint64_t atm = at + (uint64_t)(mt * 128 * 8);
+                    const uint32_t dm = d_tmem + mt * BN;
                     int r0 = 0, s0 = 0;
                     int tap = 0;
                     for (; tap + 2 <= taps; tap += 2) {
                         const int al = (g.debug & 16) ? ~63 : ~0;  // timing: 8-row-aligned views
-                        const uint64_t a0 = at + (uint64_t)(((r0 * g.Wg + s0) * 8) & al);
+                        const uint64_t a0 = atm + (uint64_t)(((r0 * g.Wg + s0) * 8) & al);
                         if (++s0 == g.S) { s0 = 0; ++r0; }
-                        const uint64_t a1 = at + (uint64_t)(((r0 * g.Wg + s0) * 8) & al);
+                        const uint64_t a1 = atm + (uint64_t)(((r0 * g.Wg + s0) * 8) & al);
                         if (++s0 == g.S) { s0 = 0; ++r0; }
                         const uint64_t b0 = bt + (uint64_t)(tap * (L::kB >> 4));
-                        mma8_bf16_bs(d_tmem, a0, b0, a1, b0 + (L::kB >> 4), bks, idesc, (ck | tap) != 0);
+                        mma8_bf16_bs(dm, a0, b0, a1, b0 + (L::kB >> 4), bks, idesc, (ck | tap) != 0);
                     }
                     if (tap < taps) {
-                        const uint64_t a0 = at + (uint64_t)((r0 * g.Wg + s0) * 8);
+                        const uint64_t a0 = atm + (uint64_t)((r0 * g.Wg + s0) * 8);
                         const uint64_t b0 = bt + (uint64_t)(tap * (L::kB >> 4));
-                        mma4_bf16(d_tmem, a0, a0 + 2, a0 + 4, a0 + 6, b0, b0 + bks, b0 + 2 * bks,
+                        mma4_bf16(dm, a0, a0 + 2, a0 + 4, a0 + 6, b0, b0 + bks, b0 + 2 * bks,
                                   b0 + 3 * bks, idesc, (ck | tap) != 0);
                     }
+                  }
                 }
-                for (int tap = 0; tap < ((RESB && !(g.debug & ~24)) ? 0 : taps); ++tap) {
+                for (int tap = 0; tap < ((RESB && !(g.debug & ~56)) ? 0 : taps); ++tap) {
                     const int r = tap / g.S, s = tap - r * g.S;
                     if (!RESB) {
                         mbar_wait(&b_full[bs], bph);
@@ -285,16 +300,13 @@ __global__ void __launch_bounds__(kHThreads, 1)
         uint8_t* stg = smem + L::kStgOff + (HB == 3 ? q : ew) * 4096;
         const uint32_t stg_u = smem_u32(stg);
         const bool has_epi = epilogue_active(&epi);
+        const bool direct = MT == 2 || (!epi.stats && !(g.debug & 32));  // PK_HALO_DEBUG=32: staged
         BnStatAcc bacc;
         bacc.init();
         int it = 0;
         for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++it) {
-            const HTile ht = htile(g, t);
+            const HTile ht = htile<MT>(g, t);
             const int n0c = ht.nt * BN;
-            const int p = ht.p0 + q * 32 + lane;  // this lane's grid position
-            const int oy = p / g.Wg, ox = p - oy * g.Wg;
-            const bool row_ok = oy < g.Ho && ox < g.Wo;
-            const long long pix = ((long long)ht.n * g.Ho + oy) * g.Wo + ox;
             const int a = it & 1;
             if (warp == 2) hstamp(g, it, 4);
             mbar_wait(&tmem_full[a], (it >> 1) & 1);
@@ -302,8 +314,10 @@ __global__ void __launch_bounds__(kHThreads, 1)
             tc_fence_after();
             const int span = min(BN, g.out_pitch - n0c);
             const int nchunks = (span + 63) / 64;
+            // work units j = (M tile, 64-column chunk), alternating between the warp halves
+            const int units = MT * nchunks;
             int my_last = -1;
-            for (int ci = half; ci < nchunks; ci += 2) my_last = ci;
+            for (int j = half; j < units; j += 2) my_last = j;
             if (my_last < 0) {
                 tc_fence_before();
                 __syncwarp();
@@ -318,16 +332,22 @@ __global__ void __launch_bounds__(kHThreads, 1)
                 continue;
             }
 #pragma unroll 1
-            for (int ci = half; ci < nchunks; ci += 2) {
+            for (int j = half; j < units; j += 2) {
+                const int mt = j / nchunks, ci = j - mt * nchunks;
                 const int c0 = ci * 64;
+                const int p = ht.p0 + mt * kM + q * 32 + lane;  // this lane's grid position
+                const int oy = p / g.Wg, ox = p - oy * g.Wg;
+                const bool row_ok = oy < g.Ho && ox < g.Wo;
+                const long long pix = ((long long)ht.n * g.Ho + oy) * g.Wo + ox;
                 uint32_t v[64];
-                const uint32_t ta = tmem_base + a * BN + c0 + (static_cast<uint32_t>(q * 32) << 16);
+                const uint32_t ta = tmem_base + a * (MT * BN) + mt * BN + c0 +
+                                    (static_cast<uint32_t>(q * 32) << 16);
                 tmem_ld16(ta + 0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
                 tmem_ld16(ta + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
                 tmem_ld16(ta + 32, *reinterpret_cast<uint32_t(*)[16]>(&v[32]));
                 tmem_ld16(ta + 48, *reinterpret_cast<uint32_t(*)[16]>(&v[48]));
                 tmem_ld_wait();
-                if (ci == my_last) {
+                if (j == my_last) {
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tmem_empty[a]);
@@ -336,6 +356,27 @@ __global__ void __launch_bounds__(kHThreads, 1)
 #pragma unroll
                 for (int e = 0; e < 64; ++e) xf[e] = __uint_as_float(v[e]);
                 if (has_epi) epilogue_chunk64(epi, xf, n0c + c0, g.n_out, oy, ox, g.Ho, g.Wo);
+                if (direct) {
+                    // each lane stores its own position's 64 channels (8 x 16 B): no
+                    // staging round trip through shared memory, whose bandwidth the
+                    // N=64 SS MMAs and the halo TMA writes already saturate
+                    const int valid = g.n_out - (n0c + c0);
+                    __nv_bfloat16* dst = out + pix * g.out_pitch + n0c + c0;
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj) {
+                        uint32_t w[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int c = jj * 8 + 2 * e;
+                            const __nv_bfloat162 b2 = __floats2bfloat162_rn(c < valid ? xf[c] : 0.0f,
+                                                                            c + 1 < valid ? xf[c + 1] : 0.0f);
+                            w[e] = *reinterpret_cast<const uint32_t*>(&b2);
+                        }
+                        if (row_ok && n0c + c0 + jj * 8 < g.out_pitch)
+                            *reinterpret_cast<uint4*>(dst + jj * 8) = make_uint4(w[0], w[1], w[2], w[3]);
+                    }
+                    continue;
+                }
                 // stage the rounded 32 x 64 tile (128-byte rows, swizzled), then
                 // store 4 full rows per instruction (8 lanes x 16 B per row)
                 pack_stage64(xf, stg_u, lane, g.n_out - (n0c + c0));
@@ -346,7 +387,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const int row = (lane >> 3) + 4 * i;
-                        const int pr = ht.p0 + q * 32 + row;
+                        const int pr = ht.p0 + mt * kM + q * 32 + row;
                         const int ry = pr / g.Wg, rx = pr - ry * g.Wg;
                         uint4 val;
                         asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
@@ -374,12 +415,12 @@ __global__ void __launch_bounds__(kHThreads, 1)
     }
 }
 
-template <int BN, int BSTAGES, bool RESB, int HB = kHaloBufs>
+template <int BN, int BSTAGES, bool RESB, int HB = kHaloBufs, int MT = 1>
 cudaError_t launch_halo(const CUtensorMap& amap, const CUtensorMap& bmap, void* out,
                         const HaloArgs& g, const pk_epilogue& e, cudaStream_t st) {
-    using L = HSmem<BN, BSTAGES, RESB, HB>;
+    using L = HSmem<BN, BSTAGES, RESB, HB, MT>;
     static_assert(L::kBytes <= 227 * 1024, "smem");
-    auto kern = conv_halo_kernel<BN, BSTAGES, RESB, HB>;
+    auto kern = conv_halo_kernel<BN, BSTAGES, RESB, HB, MT>;
     static int attr_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -458,13 +499,27 @@ cudaError_t pk_halo_conv(const pk_conv_geom* g, bool dgrad, const void* src, con
         return p;
     }();
     a.trace = trace;
-    // halo of 128 positions: rows touched by [p0, p0 + 127 + (R-1)Wg + S-1]
-    a.NR = (127 + (g->r - 1) * a.Wg + g->s - 1 + a.Wg - 1) / a.Wg + 1;
-    if (a.Wg > 256 || a.NR > 256 || a.NR * a.Wg > 448) return cudaErrorNotSupported;
-    a.tiles_img = (a.Ho * a.Wg + kM - 1) / kM;
+    // 256-position tiles (MT = 2) for 64-wide outputs without a statistics epilogue
+    // (PK_HALO_MT2=0: 128-position tiles)
+    static const bool mt2_off = [] {
+        const char* v = std::getenv("PK_HALO_MT2");
+        return v && v[0] == '0';
+    }();
+    const int bn0 = out_pitch <= 64 ? 64 : out_pitch <= 128 ? 128 : 256;
+    int mt = 1;
+    if (!mt2_off && bn0 == 64 && !(epi && epi->stats)) {
+        const int nr2 = (2 * kM - 1 + (g->r - 1) * a.Wg + g->s - 1 + a.Wg - 1) / a.Wg + 1;
+        if (a.Wg <= 256 && nr2 * a.Wg <= kHaloRowsMT2 &&
+            (long long)src_pitch / 64 * g->r * g->s * 64 * 128 <= kResMax)
+            mt = 2;
+    }
+    // halo of 128 MT positions: rows touched by [p0, p0 + 128 MT - 1 + (R-1)Wg + S-1]
+    a.NR = (kM * mt - 1 + (g->r - 1) * a.Wg + g->s - 1 + a.Wg - 1) / a.Wg + 1;
+    if (a.Wg > 256 || a.NR > 256 || a.NR * a.Wg > (mt == 2 ? kHaloRowsMT2 : 448)) return cudaErrorNotSupported;
+    a.tiles_img = (a.Ho * a.Wg + kM * mt - 1) / (kM * mt);
     // small images waste most of a tile on padding columns: leave them to the
     // rectangle kernel (valid fraction below ~80%)
-    if ((long long)a.Ho * a.Wo * 10 < (long long)a.tiles_img * kM * 8) return cudaErrorNotSupported;
+    if ((long long)a.Ho * a.Wo * 10 < (long long)a.tiles_img * kM * mt * 8) return cudaErrorNotSupported;
     const int bn = out_pitch <= 64 ? 64 : out_pitch <= 128 ? 128 : 256;
     a.n_tiles_n = (out_pitch + bn - 1) / bn;
     a.total_tiles = a.tiles_img * g->n * a.n_tiles_n;
@@ -487,6 +542,7 @@ cudaError_t pk_halo_conv(const pk_conv_geom* g, bool dgrad, const void* src, con
     // streamed per-tap filter slices leave the MMA waiting on TMA latency)
     const bool resb = a.n_tiles_n == 1 && (long long)a.cpt * g->r * g->s * bn * 128 <= kResMax;
     if (!resb) return cudaErrorNotSupported;
+    if (mt == 2) return launch_halo<64, 8, true, 2, 2>(amap, bmap, out, a, e, st);
     static const bool hb2 = std::getenv("PK_HALO_HB2") != nullptr;
     if (bn == 64 && !hb2 && a.NR * a.Wg <= kHaloRows3 &&
         (long long)a.cpt * g->r * g->s * bn * 128 <= kResMax3)
