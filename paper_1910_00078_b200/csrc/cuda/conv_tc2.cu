@@ -17,6 +17,7 @@
 // drains its own 128 TMEM lanes, fused per-channel affine / activation, TMA
 // stores, then arrives remotely on the leader's TMEM-empty barrier).
 // Validated first in tools/probes/cta2_probe.cu.
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -47,6 +48,7 @@ struct Gemm2Args {
     int m_pairs, n_tiles, total;  // pair tiles: (M / 256) x (N / 256)
     int P, Q;       // output image extent (per-activation epilogues)
     int b_mn;       // B MN-major: two 64-wide atoms (8 KB apart) per CTA half
+    unsigned long long* trace;  // PK_TC2_TRACE: summed wait clocks per role (profiling only)
 };
 
 __device__ __forceinline__ void commit_pair(uint64_t* bar) {
@@ -122,11 +124,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            long long tw = 0;
+            const long long t0 = clock64();
             for (int t = pair_id; t < g.total; t += num_pairs) {
                 const int mp = t / g.n_tiles, nt = t - mp * g.n_tiles;
                 const int arow = mp * 256 + (int)rank * 128, brow = nt * 256 + (int)rank * 128;
                 for (int kb = 0; kb < g.num_kb; ++kb) {
+                    const long long w0 = clock64();
                     mbar_wait(&empty[stage], phase ^ 1);
+                    tw += clock64() - w0;
                     uint8_t* sa = smem + stage * kStage2;
                     const uint32_t fb = smem_u32(&full[stage]) & 0xFEFFFFFFu;  // leader's barrier
                     if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * kStage2);
@@ -143,6 +149,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                     }
                 }
             }
+            if (g.trace) {
+                atomicAdd(&g.trace[4], (unsigned long long)tw);
+                atomicAdd(&g.trace[5], (unsigned long long)(clock64() - t0));
+            }
         }
     } else if (warp == 1) {
         if (rank == 0) {
@@ -150,13 +160,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
+            long long tf = 0, te = 0;
+            const long long t0 = clock64();
             for (int t = pair_id; t < g.total; t += num_pairs, ++it) {
                 const int a = it & 1;
+                long long w0 = clock64();
                 mbar_wait(&tmem_empty[a], ((it >> 1) & 1) ^ 1);
+                te += clock64() - w0;
                 tc_fence_after();
                 const uint32_t d = tmem_base + a * 256;
                 for (int kb = 0; kb < g.num_kb; ++kb) {
+                    w0 = clock64();
                     mbar_wait(&full[stage], phase);
+                    tf += clock64() - w0;
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem + stage * kStage2);
                     if (g.b_mn) {
@@ -175,6 +191,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                         phase ^= 1;
                     }
                 }
+            }
+            if (g.trace && lane == 0) {
+                atomicAdd(&g.trace[0], (unsigned long long)tf);
+                atomicAdd(&g.trace[1], (unsigned long long)te);
+                atomicAdd(&g.trace[2], (unsigned long long)(clock64() - t0));
+                atomicAdd(&g.trace[3], 1ull);
             }
         }
     } else {
@@ -287,6 +309,13 @@ cudaError_t pk_gemm_pair(const void* a, const void* b, void* y, int M, int kdim,
     g.P = P;
     g.Q = Q;
     g.b_mn = b_mn_pitch > 0;
+    static unsigned long long* trace = [] {
+        unsigned long long* p = nullptr;
+        if (std::getenv("PK_TC2_TRACE")) cudaMalloc(&p, 8 * 8);
+        return p;
+    }();
+    g.trace = trace;
+    if (trace) cudaMemsetAsync(trace, 0, 8 * 8, st);
     pk_epilogue e{};
     e.act = -1;
     if (epi) e = *epi;
@@ -304,5 +333,15 @@ cudaError_t pk_gemm_pair(const void* a, const void* b, void* y, int M, int kdim,
     const cudaError_t le = pk_launch(gemm_pair_kernel, dim3(grid), dim3(kThreads2), kBytes2, st, amap,
                                      bmap, ymap, g, e);
     count_launch();
+    if (trace) {  // profiling only (PK_TC2_TRACE; not inside graph capture)
+        unsigned long long h[8];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+        const double n = h[3] ? (double)h[3] : 1.0;
+        fprintf(stderr,
+                "tc2: pairs %llu, per pair: mma loop %.0f clk, wait full %.0f, wait tmem_empty %.0f | "
+                "producer loop %.0f, wait empty %.0f (per CTA)\n",
+                h[3], h[2] / n, h[0] / n, h[1] / n, h[5] / (2 * n), h[4] / (2 * n));
+    }
     return le != cudaSuccess ? le : cudaGetLastError();
 }
