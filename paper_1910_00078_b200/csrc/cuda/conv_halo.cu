@@ -74,12 +74,18 @@ constexpr int kResMax3 = 74 * 1024;
 // with the MMAs disabled the 128-position kernel still took 55.6 of 80 us on
 // ResNet conv2_x). Two halo buffers, direct epilogue stores (no staging).
 constexpr int kHaloRowsMT2 = 480;
-template <int BN, int BSTAGES, bool RESB, int HB = kHaloBufs, int MT = 1>
+// PAIR (MT = 2, BN = 64, K-major filter): a CTA pair (cta_group::2) runs the same
+// 256-position tile of two images with M = 256 MMAs; each CTA keeps HALF of the
+// filter resident (32 output channels), so the SS MMAs read 5 KB of operands per
+// K step per SM instead of 6 KB and the freed 36 KB hold a third halo buffer.
+constexpr int kResPair = 40 * 1024;
+template <int BN, int BSTAGES, bool RESB, int HB = kHaloBufs, int MT = 1, bool PAIR = false>
 struct HSmem {
     static constexpr int kHalo = (MT == 2 ? kHaloRowsMT2 : HB == 3 ? kHaloRows3 : 448) * 128;  // grid rows x 128 B
-    static constexpr int kB = BN * 128;                // one (tap, chunk) filter slice
+    static constexpr int kB = (PAIR ? BN / 2 : BN) * 128;  // one (tap, chunk) filter slice (this CTA's)
     static constexpr int kBOff = HB * kHalo;
-    static constexpr int kStgOff = kBOff + (RESB ? (HB == 3 ? kResMax3 : kResMax) : BSTAGES * kB);
+    static constexpr int kStgOff =
+        kBOff + (RESB ? (PAIR ? kResPair : HB == 3 ? kResMax3 : kResMax) : BSTAGES * kB);
     static constexpr int kStaging = MT == 2 ? 0 : (HB == 3 ? 4 : 8) * 4096;
     static constexpr int kBarOff = kStgOff + kStaging;
     static constexpr int kBytes = kBarOff + (2 * HB + 2 * BSTAGES + 4) * 8 + 16 + 1024;
@@ -99,14 +105,23 @@ __device__ __forceinline__ HTile htile(const HaloArgs& g, int t) {
     return h;
 }
 
-template <int BN, int BSTAGES, bool RESB, int HB, int MT = 1>
+template <int BN, int BSTAGES, bool RESB, int HB, int MT = 1, bool PAIR = false>
 __global__ void __launch_bounds__(kHThreads, 1)
     conv_halo_kernel(const __grid_constant__ CUtensorMap amap,
                      const __grid_constant__ CUtensorMap bmap, __nv_bfloat16* __restrict__ out,
                      const __grid_constant__ HaloArgs g, const pk_epilogue epi) {
-    using L = HSmem<BN, BSTAGES, RESB, HB, MT>;
+    using L = HSmem<BN, BSTAGES, RESB, HB, MT, PAIR>;
     static_assert(HB == 2 || BN == 64, "3 halo buffers: BN = 64 only");
-    static_assert(MT == 1 || (BN == 64 && RESB && HB == 2), "256-position tiles: BN = 64");
+    static_assert(MT == 1 || (BN == 64 && RESB && (HB == 2 || PAIR)), "256-position tiles: BN = 64");
+    static_assert(!PAIR || (MT == 2 && BN == 64), "pairs: 256-position tiles, BN = 64");
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    // tile loop: PAIR CTAs run pair tile pt = (image pair, tile in image) on image 2j + rank
+    const int t_first = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int t_step = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    const int t_end = PAIR ? g.total_tiles / 2 : g.total_tiles;
+    auto my_tile = [&](int pt) {
+        return PAIR ? (2 * (pt / g.tiles_img) + (int)rank) * g.tiles_img + pt % g.tiles_img : pt;
+    };
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -132,15 +147,25 @@ __global__ void __launch_bounds__(kHThreads, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tmem_full[i], 1);
-            mbar_init(&tmem_empty[i], 8);
+            mbar_init(&tmem_empty[i], PAIR ? 16 : 8);
         }
         fence_barrier_init();
         tma_prefetch(&amap);
         tma_prefetch(&bmap);
     }
-    if (warp == 1) tmem_alloc(tmem_slot, kCols);
+    if (warp == 1) {
+        if (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(kCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            tmem_alloc(tmem_slot, kCols);
+        }
+    }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();  // the peer's barriers exist before any cross-CTA signal
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_wait();  // predecessor complete: inputs ready, outputs free
@@ -154,7 +179,18 @@ __global__ void __launch_bounds__(kHThreads, 1)
             // PK_HALO_DEBUG=2 (timing only): in-bounds boxes of the unpadded width
             const bool inb = g.debug & 2;
             const uint32_t halo_bytes = g.NR * (inb ? g.Wg - 2 * g.pad_w : g.Wg) * 128;
-            if (RESB) {  // whole filter slice once: (chunk, tap) blocks of BN x 128 B
+            if (PAIR) {
+                // this CTA's 32 filter rows of every (chunk, tap) slice; both CTAs'
+                // loads complete on the leader's barrier
+                const uint32_t fb = smem_u32(&b_full[0]) & 0xFEFFFFFFu;
+                if (rank == 0) mbar_arrive_expect_tx(&b_full[0], 2 * g.cpt * taps * L::kB);
+                for (int ck = 0; ck < g.cpt; ++ck)
+                    for (int tap = 0; tap < taps; ++tap) {
+                        const int ft = g.flip ? taps - 1 - tap : tap;
+                        tma_load_2d_pair(smem_u32(smem + L::kBOff + (ck * taps + tap) * L::kB), &bmap, fb,
+                                         ft * g.red_ch + ck * 64, (int)rank * (BN / 2));
+                    }
+            } else if (RESB) {  // whole filter slice once: (chunk, tap) blocks of BN x 128 B
                 mbar_arrive_expect_tx(&b_full[0], g.cpt * taps * L::kB);
                 for (int ck = 0; ck < g.cpt; ++ck)
                     for (int tap = 0; tap < taps; ++tap) {
@@ -169,12 +205,24 @@ __global__ void __launch_bounds__(kHThreads, 1)
                         }
                     }
             }
-            for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
-                const HTile ht = htile<MT>(g, t);
+            int pit = 0;
+            for (int pt = t_first; pt < t_end; pt += t_step, ++pit) {
+                const HTile ht = htile<MT>(g, my_tile(pt));
                 for (int ck = 0; ck < g.cpt; ++ck) {
-                    hstamp(g, (t - blockIdx.x) / gridDim.x, 8);
+                    hstamp(g, pit, 8);
                     mbar_wait(&h_empty[hs], hph ^ 1);
-                    hstamp(g, (t - blockIdx.x) / gridDim.x, 9);
+                    hstamp(g, pit, 9);
+                    if (PAIR) {
+                        const uint32_t fb = smem_u32(&h_full[hs]) & 0xFEFFFFFFu;
+                        if (rank == 0) mbar_arrive_expect_tx(&h_full[hs], 2 * halo_bytes);
+                        tma_load_4d_pair(smem_u32(smem + hs * L::kHalo), &amap, fb, ck * 64, -g.pad_w,
+                                         ht.row0 - g.pad_h, ht.n);
+                        if (++hs == HB) {
+                            hs = 0;
+                            hph ^= 1;
+                        }
+                        continue;
+                    }
                     mbar_arrive_expect_tx(&h_full[hs], halo_bytes);
                     if (inb)
                         tma_load_4d(smem_u32(smem + hs * L::kHalo), &amap, &h_full[hs], ck * 64, 0,
@@ -207,16 +255,17 @@ __global__ void __launch_bounds__(kHThreads, 1)
             }
         }
     } else if (warp == 1) {
+      if (!PAIR || rank == 0) {
         // ---------------- MMA issuer: A = shifted halo view per tap --------------
-        const uint32_t idesc = idesc_bf16_f32(kM, BN, false, g.b_mn != 0);
+        const uint32_t idesc = idesc_bf16_f32(PAIR ? 2 * kM : kM, BN, false, g.b_mn != 0);
         const uint64_t bks = g.b_mn ? 128 : 2;  // B k-step (MN-major: 16 rows)
         const uint32_t blbo = g.b_mn ? 8192 : 16;
         int hs = 0, bs = 0;
         uint32_t hph = 0, bph = 0;
         int it = 0;
         if (RESB) mbar_wait(&b_full[0], 0);
-        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++it) {
-            const HTile ht = htile<MT>(g, t);
+        for (int pt = t_first; pt < t_end; pt += t_step, ++it) {
+            const HTile ht = htile<MT>(g, my_tile(pt));
             const int a = it & 1;
             hstamp(g, it, 0);
             mbar_wait(&tmem_empty[a], ((it >> 1) & 1) ^ 1);
@@ -229,7 +278,7 @@ __global__ void __launch_bounds__(kHThreads, 1)
                 hstamp(g, it, 2);
                 tc_fence_after();
                 const uint32_t halo_u = smem_u32(smem + hs * L::kHalo);
-                if (RESB && !(g.debug & ~56)) {
+                if (PAIR || (RESB && !(g.debug & ~56))) {
                     // resident filter: descriptors are the tile base plus a per-tap
                     // offset (start field in 16-byte units), two taps per issue block;
                     // keeps the issuing thread ahead of N=64 MMAs (48 clk each)
@@ -251,17 +300,24 @@ __global__ void __launch_bounds__(kHThreads, 1)
                         const uint64_t a1 = atm + (uint64_t)(((r0 * g.Wg + s0) * 8) & al);
                         if (++s0 == g.S) { s0 = 0; ++r0; }
                         const uint64_t b0 = bt + (uint64_t)(tap * (L::kB >> 4));
-                        mma8_bf16_bs(dm, a0, b0, a1, b0 + (L::kB >> 4), bks, idesc, (ck | tap) != 0);
+                        if constexpr (PAIR)
+                            mma8_bf16_bs_pair(dm, a0, b0, a1, b0 + (L::kB >> 4), bks, idesc, (ck | tap) != 0);
+                        else
+                            mma8_bf16_bs(dm, a0, b0, a1, b0 + (L::kB >> 4), bks, idesc, (ck | tap) != 0);
                     }
                     if (tap < taps) {
                         const uint64_t a0 = atm + (uint64_t)((r0 * g.Wg + s0) * 8);
                         const uint64_t b0 = bt + (uint64_t)(tap * (L::kB >> 4));
-                        mma4_bf16(dm, a0, a0 + 2, a0 + 4, a0 + 6, b0, b0 + bks, b0 + 2 * bks,
-                                  b0 + 3 * bks, idesc, (ck | tap) != 0);
+                        if constexpr (PAIR)
+                            mma4_bf16_pair(dm, a0, a0 + 2, a0 + 4, a0 + 6, b0, b0 + bks, b0 + 2 * bks,
+                                           b0 + 3 * bks, idesc, (ck | tap) != 0);
+                        else
+                            mma4_bf16(dm, a0, a0 + 2, a0 + 4, a0 + 6, b0, b0 + bks, b0 + 2 * bks,
+                                      b0 + 3 * bks, idesc, (ck | tap) != 0);
                     }
                   }
                 }
-                for (int tap = 0; tap < ((RESB && !(g.debug & ~56)) ? 0 : taps); ++tap) {
+                for (int tap = 0; tap < ((PAIR || (RESB && !(g.debug & ~56))) ? 0 : taps); ++tap) {
                     const int r = tap / g.S, s = tap - r * g.S;
                     if (!RESB) {
                         mbar_wait(&b_full[bs], bph);
@@ -284,14 +340,21 @@ __global__ void __launch_bounds__(kHThreads, 1)
                     }
                 }
                 hstamp(g, it, 3);
-                mma_commit_elect(&h_empty[hs]);
+                if (PAIR)
+                    mma_commit_pair(&h_empty[hs]);
+                else
+                    mma_commit_elect(&h_empty[hs]);
                 if (++hs == HB) {
                     hs = 0;
                     hph ^= 1;
                 }
             }
-            mma_commit_elect(&tmem_full[a]);
+            if (PAIR)
+                mma_commit_pair(&tmem_full[a]);
+            else
+                mma_commit_elect(&tmem_full[a]);
         }
+      }
     } else {
         // ---------------- epilogue (8 warps): direct 16-byte stores ---------------
         const int ew = warp - 2;
@@ -304,8 +367,8 @@ __global__ void __launch_bounds__(kHThreads, 1)
         BnStatAcc bacc;
         bacc.init();
         int it = 0;
-        for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x, ++it) {
-            const HTile ht = htile<MT>(g, t);
+        for (int pt = t_first; pt < t_end; pt += t_step, ++it) {
+            const HTile ht = htile<MT>(g, my_tile(pt));
             const int n0c = ht.nt * BN;
             const int a = it & 1;
             if (warp == 2) hstamp(g, it, 4);
@@ -321,13 +384,23 @@ __global__ void __launch_bounds__(kHThreads, 1)
             if (my_last < 0) {
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tmem_empty[a]);
+                if (lane == 0) {
+                    if (PAIR)
+                        mbar_arrive_leader(&tmem_empty[a]);
+                    else
+                        mbar_arrive(&tmem_empty[a]);
+                }
             }
             if (g.debug & 8) {  // timing experiments: no epilogue work
                 if (my_last >= 0) {
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&tmem_empty[a]);
+                    if (lane == 0) {
+                    if (PAIR)
+                        mbar_arrive_leader(&tmem_empty[a]);
+                    else
+                        mbar_arrive(&tmem_empty[a]);
+                }
                 }
                 continue;
             }
@@ -350,7 +423,12 @@ __global__ void __launch_bounds__(kHThreads, 1)
                 if (j == my_last) {
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&tmem_empty[a]);
+                    if (lane == 0) {
+                    if (PAIR)
+                        mbar_arrive_leader(&tmem_empty[a]);
+                    else
+                        mbar_arrive(&tmem_empty[a]);
+                }
                 }
                 float xf[64];
 #pragma unroll
@@ -409,18 +487,23 @@ __global__ void __launch_bounds__(kHThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync_all();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem_base, kCols);
+        if (PAIR)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(kCols));
+        else
+            tmem_dealloc(tmem_base, kCols);
     }
 }
 
-template <int BN, int BSTAGES, bool RESB, int HB = kHaloBufs, int MT = 1>
+template <int BN, int BSTAGES, bool RESB, int HB = kHaloBufs, int MT = 1, bool PAIR = false>
 cudaError_t launch_halo(const CUtensorMap& amap, const CUtensorMap& bmap, void* out,
                         const HaloArgs& g, const pk_epilogue& e, cudaStream_t st) {
-    using L = HSmem<BN, BSTAGES, RESB, HB, MT>;
+    using L = HSmem<BN, BSTAGES, RESB, HB, MT, PAIR>;
     static_assert(L::kBytes <= 227 * 1024, "smem");
-    auto kern = conv_halo_kernel<BN, BSTAGES, RESB, HB, MT>;
+    auto kern = conv_halo_kernel<BN, BSTAGES, RESB, HB, MT, PAIR>;
     static int attr_dev = -1;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -431,8 +514,9 @@ cudaError_t launch_halo(const CUtensorMap& amap, const CUtensorMap& bmap, void* 
         attr_dev = dev;
     }
     int grid = num_sms_of_current_device();
+    if (PAIR) grid = grid / 2 * 2;
     if (g.total_tiles < grid) grid = g.total_tiles;
-    cudaError_t le = pk_launch(kern, dim3(grid), dim3(kHThreads), L::kBytes, st, amap, bmap,
+    cudaError_t le = pk_launch(kern, dim3(grid), dim3(kHThreads), L::kBytes, st, PAIR ? 2 : 1, amap, bmap,
                                (__nv_bfloat16*)out, g, e);
     if (le != cudaSuccess) return le;
     count_launch();
@@ -527,6 +611,17 @@ cudaError_t pk_halo_conv(const pk_conv_geom* g, bool dgrad, const void* src, con
     if (!tc::make_map_nhwc(&amap, src, g->n, Hs, Ws, src_pitch, (a.debug & 2) ? Ws : a.Wg, a.NR, 1))
         return cudaErrorNotSupported;
     const long long kred = (long long)g->r * g->s * src_pitch;
+    // CTA pairs over image pairs (K-major filter only; PK_HALO_PAIR=1)
+    static const bool pair_on = std::getenv("PK_HALO_PAIR") && std::getenv("PK_HALO_PAIR")[0] == '1';
+    const bool pair = pair_on && mt == 2 && !filt_mn && g->n % 2 == 0 && a.n_tiles_n == 1 &&
+                      (long long)a.cpt * g->r * g->s * 32 * 128 <= kResPair && a.debug == 0;
+    if (pair) {
+        if (!tc::make_map_2d(&bmap, filt, n_out, kred, kred, bn / 2)) return cudaErrorNotSupported;
+        pk_epilogue e{};
+        e.act = -1;
+        if (epi) e = *epi;
+        return launch_halo<64, 8, true, 3, 2, true>(amap, bmap, out, a, e, st);
+    }
     if (filt_mn) {
         if (!dgrad || g->f_pitch % 64 || bn % 64) return cudaErrorNotSupported;
         a.b_mn = 1;

@@ -358,6 +358,31 @@ __device__ __forceinline__ void mma8_bf16_bs(uint32_t tmem_d, uint64_t a0, uint6
         : "memory");
 }
 
+// mma8_bf16_bs for a CTA pair (leader CTA, cta_group::2, M = 256).
+__device__ __forceinline__ void mma8_bf16_bs_pair(uint32_t tmem_d, uint64_t a0, uint64_t b0, uint64_t a1,
+                                                  uint64_t b1, uint64_t bs, uint32_t idesc,
+                                                  uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 x1, x2, x3, y1, y2, y3, u1, u2, u3, v1, v2, v3, s2, s3;\n\t"
+        "setp.ne.b32 p, %6, 0;\n\t"
+        "add.s64 s2, %7, %7;\n\tadd.s64 s3, s2, %7;\n\t"
+        "add.s64 x1, %1, 2;\n\tadd.s64 x2, %1, 4;\n\tadd.s64 x3, %1, 6;\n\t"
+        "add.s64 y1, %2, %7;\n\tadd.s64 y2, %2, s2;\n\tadd.s64 y3, %2, s3;\n\t"
+        "add.s64 u1, %3, 2;\n\tadd.s64 u2, %3, 4;\n\tadd.s64 u3, %3, 6;\n\t"
+        "add.s64 v1, %4, %7;\n\tadd.s64 v2, %4, s2;\n\tadd.s64 v3, %4, s3;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %5, p;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], x1, y1, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], x2, y2, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], x3, y3, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %3, %4, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], u1, v1, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], u2, v2, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], u3, v3, %5, 1;\n\t}" ::"r"(tmem_d),
+        "l"(a0), "l"(b0), "l"(a1), "l"(b1), "r"(idesc), "r"(accumulate), "l"(bs)
+        : "memory");
+}
+
 // Two SS MMAs from one elected thread (accumulate).
 __device__ __forceinline__ void mma2_bf16(uint32_t tmem_d, uint64_t a0, uint64_t a1, uint64_t b0,
                                           uint64_t b1, uint32_t idesc) {
