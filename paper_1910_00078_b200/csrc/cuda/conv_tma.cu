@@ -1312,7 +1312,11 @@ cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, v
     w.total = (long long)w.K * w.Nn;
     // in-kernel finish pays for small outputs (launch saved); large ones want the
     // full-GPU sum kernel (measured: conv2 wgrads -7 us each, conv4/5 3x3 +8 us)
-    if (!wt.pair && (long long)tiles_mn * splits <= num_sms && w.total <= 65536)
+    static const long long fuse_max = [] {  // PK_SPLITK_FUSE_MAX: output-size cap (A/B only)
+        const char* v = std::getenv("PK_SPLITK_FUSE_MAX");
+        return v ? std::atoll(v) : 65536LL;
+    }();
+    if (!wt.pair && (long long)tiles_mn * splits <= num_sms && w.total <= fuse_max)
         w.sync = splitk_sync_slot();
     cudaError_t le;
     if (wt.mt == 2)
