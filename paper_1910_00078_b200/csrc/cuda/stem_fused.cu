@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 const uint32_t b_base = a_base + L::kA;
                 constexpr uint64_t ks = 2048 >> 4;  // 16 MN-major K rows (pixels)
                 const uint64_t bd0 = umma_desc_sw128(b_base, L::kAtom, 1024);
-                for (int mt = 0; mt < mtiles; ++mt) {
+                for (int mt = 0; mt < ((g.debug & 1) ? 0 : mtiles); ++mt) {  // PK_STEM_DEBUG=1: no MMA
                     const uint64_t ad0 = umma_desc_sw128(a_base + mt * 2 * L::kAtom, L::kAtom, 1024);
 #pragma unroll
                     for (int k = 0; k < kTile / 16; k += 4)
@@ -772,7 +772,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     tma_load_4d(smem_u32(sbase + L::kA + a * L::kAtom), &dymap, &full[stage], a * 64,
                                 ox0, oy0, n);
             }
-            build_tile(bp, smem_u32(sbase), halo0 + (i % kHaloStages) * kHaloStageBytes);
+            if (!(g.debug & 2))  // PK_STEM_DEBUG=2 (timing only): no operand build
+                build_tile(bp, smem_u32(sbase), halo0 + (i % kHaloStages) * kHaloStageBytes);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[stage]);
