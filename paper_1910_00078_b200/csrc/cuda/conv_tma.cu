@@ -137,7 +137,8 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                           const __grid_constant__ YMaps ymaps, __nv_bfloat16* __restrict__ out,
                           const __grid_constant__ TmaConvArgs g, const pk_epilogue epi) {
     using L = FSmem<BN, STAGES, MT, PAIR>;
-    static_assert(!PAIR || (MT == 1 && !PHASED && !NARROW && BN == 256), "pair variant");
+    static_assert(!PAIR || (!PHASED && !NARROW && ((MT == 1 && BN == 256) || (MT == 2 && BN == 128))),
+                  "pair variant");
     const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
     // tile loop: this CTA's rectangle tile of pair tile pt (PAIR) or tile pt
     const int t_first = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
@@ -303,9 +304,14 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                     const uint32_t b_base = a_base + L::kA;
                     const uint64_t bd0 = umma_desc_sw128(b_base, g.b_mn ? 8192 : 16, 1024);
                     if constexpr (PAIR) {
-                        const uint64_t ad0 = umma_desc_sw128(a_base, 16, 1024);
-                        mma4_bf16_pair(d_tmem, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + bks,
-                                       bd0 + 2 * bks, bd0 + 3 * bks, idesc, kb != 0);
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
+                            // MT = 2: each CTA's 256-pixel rectangle is two M=128 halves; the
+                            // pair's M=256 MMA for half mt takes half mt of both CTAs
+                            const uint64_t ad0 = umma_desc_sw128(a_base + mt * BM * 128, 16, 1024);
+                            mma4_bf16_pair(d_tmem + mt * BN, ad0, ad0 + 2, ad0 + 4, ad0 + 6, bd0, bd0 + bks,
+                                           bd0 + 2 * bks, bd0 + 3 * bks, idesc, kb != 0);
+                        }
                         mma_commit_pair(&empty[stage]);
                         if (kb == nkb - 1) mma_commit_pair(&tmem_full[a]);
                         if (++stage == STAGES) {
@@ -843,6 +849,8 @@ cudaError_t dispatch_fprop(int bn, const CUtensorMap& amap, const CUtensorMap& b
                            const pk_epilogue& e, cudaStream_t st) {
     if (g.total_pairs > 0 && !PHASED && !NARROW && bn == 256)
         return launch_fprop<256, 6, false, false, 1, true>(amap, bmap, ymap, out, g, e, st);
+    if (g.total_pairs > 0 && !PHASED && !NARROW && bn == 128 && g.mt == 2)
+        return launch_fprop<128, 4, false, false, 2, true>(amap, bmap, ymap, out, g, e, st);
     if (g.mt == 2 && !NARROW) {
         if (bn == 64) return launch_fprop<64, 4, PHASED, false, 2>(amap, bmap, ymap, out, g, e, st);
         if (bn == 128) return launch_fprop<128, 3, PHASED, false, 2>(amap, bmap, ymap, out, g, e, st);
@@ -995,7 +1003,14 @@ cudaError_t tma_conv_impl(const pk_conv_geom* g, bool dgrad, const void* src, co
     }();
     t.m_tiles = t.n_tiles_n ? t.total_tiles / t.n_tiles_n : 0;
     t.total_pairs = 0;
-    if (!f32 && !pair_off && cfg_pair != 1 && !narrow && sh == 1 && sw == 1 && bn == 256 && t.mt == 1 &&
+    // 128-wide tiles with 256-pixel rectangles as CTA pairs: per SM the MMAs read A + B/2
+    // instead of A + B from shared memory, which bounds the single-CTA form (measured ResNet
+    // conv3_x 3x3 fwd and dgrad 57.3 -> 53.6 us; PK_TMA_PAIR_MT2=0 disables)
+    static const bool pair_mt2 = !(std::getenv("PK_TMA_PAIR_MT2") && std::getenv("PK_TMA_PAIR_MT2")[0] == '0');
+    if (pair_mt2 && !f32 && !pair_off && cfg_pair != 1 && !narrow && sh == 1 && sw == 1 && bn == 128 &&
+        t.mt == 2 && g->r * g->s > 1 && (!epi || !epi->stats))
+        t.total_pairs = (t.m_tiles + 1) / 2 * t.n_tiles_n;
+    else if (!f32 && !pair_off && cfg_pair != 1 && !narrow && sh == 1 && sw == 1 && bn == 256 && t.mt == 1 &&
         g->r * g->s > 1 && (!epi || !epi->stats) &&
         (cfg_pair == 2 || (long long)((t.m_tiles + 1) / 2) * t.n_tiles_n >= 74))
         t.total_pairs = (t.m_tiles + 1) / 2 * t.n_tiles_n;
