@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
                           const __grid_constant__ YMaps ymaps, __nv_bfloat16* __restrict__ out,
                           const __grid_constant__ TmaConvArgs g, const pk_epilogue epi) {
     using L = FSmem<BN, STAGES, MT, PAIR>;
-    static_assert(!PAIR || (!PHASED && !NARROW && ((MT == 1 && BN == 256) || (MT == 2 && BN == 128))),
+    static_assert(!PAIR || (!NARROW && ((MT == 1 && BN == 256) || (MT == 2 && BN == 128))),
                   "pair variant");
     const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
     // tile loop: this CTA's rectangle tile of pair tile pt (PAIR) or tile pt
@@ -851,6 +851,8 @@ cudaError_t dispatch_fprop(int bn, const CUtensorMap& amap, const CUtensorMap& b
         return launch_fprop<256, 6, false, false, 1, true>(amap, bmap, ymap, out, g, e, st);
     if (g.total_pairs > 0 && !PHASED && !NARROW && bn == 128 && g.mt == 2)
         return launch_fprop<128, 4, false, false, 2, true>(amap, bmap, ymap, out, g, e, st);
+    if (g.total_pairs > 0 && PHASED && !NARROW && bn == 256 && g.mt == 1)
+        return launch_fprop<256, 6, true, false, 1, true>(amap, bmap, ymap, out, g, e, st);
     if (g.mt == 2 && !NARROW) {
         if (bn == 64) return launch_fprop<64, 4, PHASED, false, 2>(amap, bmap, ymap, out, g, e, st);
         if (bn == 128) return launch_fprop<128, 3, PHASED, false, 2>(amap, bmap, ymap, out, g, e, st);
@@ -867,8 +869,11 @@ int choose_bn(int want, int out_pitch) {
 }
 
 // Fill tile grid / tap tables. Phases: ph in [0, sh) x [0, sw) (1 x 1 for fprop).
+// even_tiles (CTA pairs over phased grids): every phase gets an even tile count, the
+// extra tile sitting past the batch (n0 >= N: zero loads, clipped stores), so no pair
+// straddles two phases with different tap lists.
 bool fill_phases(TmaConvArgs& t, int n_img, int Ho, int Wo, int sh, int sw, int R, int S,
-                 int pad_h, int pad_w, int dil_h, int dil_w, bool dgrad) {
+                 int pad_h, int pad_w, int dil_h, int dil_w, bool dgrad, bool even_tiles = false) {
     if (sh * sw > kMaxPhases || R * S > kMaxTaps) return false;
     t.num_phases = sh * sw;
     int tiles = 0, taps = 0;
@@ -885,7 +890,10 @@ bool fill_phases(TmaConvArgs& t, int n_img, int Ho, int Wo, int sh, int sw, int 
             t.ph_th[i] = (hp + t.bh - 1) / t.bh;
             t.ph_tn[i] = (n_img + t.bn - 1) / t.bn;
             t.ph_tile_start[i] = tiles;
-            if (hp > 0 && wp > 0) tiles += t.ph_tw[i] * t.ph_th[i] * t.ph_tn[i];
+            if (hp > 0 && wp > 0) {
+                const int c = t.ph_tw[i] * t.ph_th[i] * t.ph_tn[i];
+                tiles += even_tiles ? c + (c & 1) : c;
+            }
             t.ph_tap_start[i] = taps;
             for (int r = 0; r < R; ++r) {
                 int oh;
@@ -986,8 +994,19 @@ cudaError_t tma_conv_impl(const pk_conv_geom* g, bool dgrad, const void* src, co
     t.bn = rt.bn;
     quarter_box(t);
     t.n_tiles_n = (out_pitch + bn - 1) / bn;
+    // CTA pairs over the sub-pixel phases of strided backward data, 256-wide tiles (measured
+    // conv4_1b 60.6 -> 55.9, conv5_1b 58.9 -> 51.3, conv4_1ds 83.7 -> 78.0 us; PK_TMA_PAIR_PHASED=0: off)
+    static const bool pair_phased_off = [] {
+        const char* v = std::getenv("PK_TMA_PAIR_PHASED");
+        return v && v[0] == '0';
+    }();
+    const int cfg_pair0 = cfg_field(&pk_tc_config::pair);
+    const bool pair_phased = (sh > 1 || sw > 1) && !pair_phased_off && !f32 && !narrow && cfg_pair0 != 1 &&
+                             !(std::getenv("PK_TMA_PAIR") && std::getenv("PK_TMA_PAIR")[0] == '0') &&
+                             bn == 256 && t.mt == 1 &&  // 128-wide phased pairs measured slower (conv3_1b 86 -> 95 us)
+                             (!epi || !epi->stats) && !(filt_mn && bn == 64);
     if (!fill_phases(t, g->n, t.Ho, t.Wo, sh, sw, g->r, g->s, g->pad_h, g->pad_w, g->dil_h,
-                     g->dil_w, dgrad))
+                     g->dil_w, dgrad, pair_phased))
         return cudaErrorNotSupported;
     CUtensorMap amap{}, bmap{};
     YMaps ymap{};
@@ -1007,7 +1026,9 @@ cudaError_t tma_conv_impl(const pk_conv_geom* g, bool dgrad, const void* src, co
     // instead of A + B from shared memory, which bounds the single-CTA form (measured ResNet
     // conv3_x 3x3 fwd and dgrad 57.3 -> 53.6 us; PK_TMA_PAIR_MT2=0 disables)
     static const bool pair_mt2 = !(std::getenv("PK_TMA_PAIR_MT2") && std::getenv("PK_TMA_PAIR_MT2")[0] == '0');
-    if (pair_mt2 && !f32 && !pair_off && cfg_pair != 1 && !narrow && sh == 1 && sw == 1 && bn == 128 &&
+    if (pair_phased) {
+        t.total_pairs = t.m_tiles / 2 * t.n_tiles_n;
+    } else if (pair_mt2 && !f32 && !pair_off && cfg_pair != 1 && !narrow && sh == 1 && sw == 1 && bn == 128 &&
         t.mt == 2 && g->r * g->s > 1 && (!epi || !epi->stats))
         t.total_pairs = (t.m_tiles + 1) / 2 * t.n_tiles_n;
     else if (!f32 && !pair_off && cfg_pair != 1 && !narrow && sh == 1 && sw == 1 && bn == 256 && t.mt == 1 &&
