@@ -58,17 +58,33 @@ class ClockSampler:
                  "-lms", "50"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+        self.mark = 0
+        if self.proc:
+            # nvidia-smi can take a second or more to start on a fresh box: wait for its
+            # first sample so the (short) timed region is actually sampled
+            t0 = time.time()
+            while time.time() - t0 < 10.0 and not self._rows():
+                time.sleep(0.02)
+            self.mark = len(self._rows())
+
+    def _rows(self):
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) == 7:
+                    rows.append(parts)
+        return rows
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)  # the sample that covers the end of the region
         self.proc.terminate()
         self.proc.wait()
-        rows = []
-        for line in open(self.path):
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 7:
-                rows.append(parts)
+        rows = self._rows()
+        # samples taken while the region ran (the ones before it only prove the sampler is up)
+        rows = rows[self.mark:] or rows[-1:]
         os.unlink(self.path)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}

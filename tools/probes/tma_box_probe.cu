@@ -145,10 +145,16 @@ int main() {
     // box {64, bw, bh, 1} at tile origins on a (bw-2) x (bh-2) grid (overlapping
     // halos), with and without out-of-bounds borders.
     {
-        const int n = 256, H = 112, W = 112;
-        struct H4 { int bw, bh, oob, inflight; };
-        std::vector<H4> hc = {{11, 11, 1, 3}, {11, 11, 0, 3}, {11, 11, 1, 6}, {19, 11, 1, 3}, {34, 6, 1, 3}, {58, 6, 0, 3}};
+        const int n = 256;
+        struct H4 { int bw, bh, oob, inflight, H, W; };
+        // the last six: ResNet conv2_x (56x56x64) halo rows as the halo kernel loads them
+        // (58-wide boxes at x = -1, i.e. OOB left/right borders) vs in-bounds boxes of the same bytes on a 58-wide tensor
+        std::vector<H4> hc = {{11, 11, 1, 3, 112, 112}, {11, 11, 0, 3, 112, 112}, {11, 11, 1, 6, 112, 112},
+                              {19, 11, 1, 3, 112, 112}, {34, 6, 1, 3, 112, 112}, {58, 6, 0, 3, 112, 112},
+                              {58, 8, 1, 2, 56, 56},     {58, 8, 1, 3, 56, 56},   {58, 8, 0, 2, 56, 58},
+                              {58, 8, 0, 3, 56, 58},     {58, 4, 1, 4, 56, 56},   {58, 4, 0, 4, 56, 58}};
         for (const auto& c : hc) {
+            const int H = c.H, W = c.W;
             CUtensorMap map;
             cuuint64_t dims[4] = {64, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)n};
             cuuint64_t strides[3] = {128, (cuuint64_t)W * 128, (cuuint64_t)H * W * 128};
@@ -160,7 +166,7 @@ int main() {
                 printf("4d encode failed\n");
                 continue;
             }
-            const int sx = c.bw - 2, sy = c.bh - 2;  // tile step (halo overlap of 2)
+            const int sx = (c.bw >= W) ? W : c.bw - 2, sy = c.bh - 2;  // tile step (halo overlap of 2)
             const int tx = W / sx, ty = H / sy;
             const int box_bytes = (c.bw * c.bh * 128 + 1023) / 1024 * 1024;
             const int smem = c.inflight * box_bytes + 1024 + 256;
