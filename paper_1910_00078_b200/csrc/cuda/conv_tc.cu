@@ -99,7 +99,7 @@ struct Smem {
     static constexpr int kStaging = 8 * kStgBufs * 32 * 128;  // 8 epilogue warps x bufs x 32 x 128 B
     static constexpr int kStagingOff = kResOff + kResB;
     static constexpr int kBarOff = kStagingOff + kStaging;
-    static constexpr int kBytes = kBarOff + (2 * STAGES + 5) * 8 + 16 + 1024;
+    static constexpr int kBytes = kBarOff + (2 * STAGES + 9) * 8 + 16 + 1024;
 };
 
 struct TileInfo {
@@ -163,13 +163,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
     uint64_t* empty = full + STAGES;
-    uint64_t* tmem_full = empty + STAGES;   // [2]
-    uint64_t* tmem_empty = tmem_full + 2;   // [2]
-    uint64_t* bfull = tmem_empty + 2;       // resident B loaded
+    // Narrow tiles (BN <= 64: one 64-column chunk per tile) would leave half the
+    // epilogue warps idle and make the per-tile epilogue latency the loop period
+    // (PK_TC_TRACE: ~2200 clk per tile on a K=64 1x1 layer); there the two
+    // epilogue halves take alternate TILES instead of alternate chunks, over
+    // four accumulator buffers.
+    constexpr bool kSplit = BN <= 64;
+    constexpr int kAccBufs = kSplit ? 4 : 2;
+    uint64_t* tmem_full = empty + STAGES;          // [kAccBufs]
+    uint64_t* tmem_empty = tmem_full + kAccBufs;   // [kAccBufs]
+    uint64_t* bfull = tmem_empty + kAccBufs;       // resident B loaded
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int kAccCols = 2 * BN;  // double-buffered accumulator
+    constexpr int kAccCols = kAccBufs * BN;  // multi-buffered accumulator
     constexpr uint32_t kTmemCols = kAccCols <= 32 ? 32 : kAccCols <= 64 ? 64 : kAccCols <= 128 ? 128
                                    : kAccCols <= 256 ? 256 : 512;
 
@@ -178,9 +185,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&full[i], kPlain ? 1 : 128 + 1);
             mbar_init(&empty[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kAccBufs; ++i) {
             mbar_init(&tmem_full[i], 1);
-            mbar_init(&tmem_empty[i], 8);
+            mbar_init(&tmem_empty[i], kSplit ? 4 : 8);  // the epilogue warps that read it
         }
         mbar_init(bfull, 1);
         fence_barrier_init();
@@ -346,8 +353,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
             const TileInfo ti = tile_info<MODE>(g, t);
             if (ti.nkb == 0) continue;
-            const int a = it & 1;
-            const uint32_t aphase = (it >> 1) & 1;
+            const int a = it % kAccBufs;
+            const uint32_t aphase = (it / kAccBufs) & 1;
             ++it;
             tcstamp(g, it - 1, 2);
             mbar_wait(&tmem_empty[a], aphase ^ 1);
@@ -395,15 +402,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         int it = 0;
         for (int t = blockIdx.x; t < g.total_tiles; t += gridDim.x) {
             const TileInfo ti = tile_info<MODE>(g, t);
+            const bool live = ti.nkb > 0;
+            // split mode: live tiles alternate between the halves (buffers a with
+            // a % 2 == half); tiles without taps (zero output, no TMEM) go to half 0
+            if (kSplit && (live ? (it & 1) != half : half != 0)) {
+                if (live) ++it;
+                continue;
+            }
             const int n0 = ti.n0 * BN;
             const int my_m = ti.m0 + q * 32 + lane;
             int my_n = 0, my_oy = 0, my_ox = 0;  // (n unused: epilogue indexes by oy, ox)
             if (my_m < ti.rows) row_coords<MODE>(g, ti.phase, my_m, my_n, my_oy, my_ox);
             int a = 0;
-            const bool live = ti.nkb > 0;
             if (live) {
-                a = it & 1;
-                const uint32_t aphase = (it >> 1) & 1;
+                a = it % kAccBufs;
+                const uint32_t aphase = (it / kAccBufs) & 1;
                 ++it;
                 if (warp == 5) tcstamp(g, it - 1, 5);
                 mbar_wait(&tmem_full[a], aphase);
@@ -414,7 +427,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int span = min(BN, g.out_pitch - n0);
             const int nchunks = (span + 63) / 64;
             int my_last = -1;
-            for (int ci = half; ci < nchunks; ci += 2) my_last = ci;
+            const int ci0 = kSplit ? 0 : half, cstep = kSplit ? 1 : 2;
+            for (int ci = ci0; ci < nchunks; ci += cstep) my_last = ci;
             if (live && my_last < 0) {
                 tc_fence_before();
                 __syncwarp();
@@ -422,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const int srow0 = lane >> 3, sj = lane & 7;
 #pragma unroll 1
-            for (int ci = half; ci < nchunks; ci += 2) {
+            for (int ci = ci0; ci < nchunks; ci += cstep) {
                 const int c0 = ci * 64;
                 uint32_t v[64];
                 if (live && (g.debug & 2)) {
