@@ -500,7 +500,10 @@ __global__ void __launch_bounds__(kFpropThreads, 1)
 
 // ---------------------------------------------------------------------------
 // wgrad: D[k][n], n = (r, s, c); reduction over 64-pixel rectangles.
-constexpr int kWgThreads = 192;  // producer, MMA, 4 epilogue warps
+// producer, MMA, 8 epilogue warps: the drain of the fp32 tile runs after the last
+// MMA (one tile per CTA), so two warps per TMEM lane quarter halve it
+// (PK_WG_TRACE: 15k clk for a 256 x 256 tile with one warp per quarter)
+constexpr int kWgThreads = 320;
 
 struct TmaWgArgs {
     int K, Nn;                 // GEMM M (out channels) and N (R*S*Cp)
@@ -700,13 +703,18 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         }
         // drain: 64 TMEM columns per round (one wait), staged through the now
         // idle pipeline smem so every global store writes two full 256-byte
-        // row segments of the partial (coalesced) instead of 32 scattered 16 B
+        // row segments of the partial (coalesced) instead of 32 scattered 16 B;
+        // the two warps of a lane quarter take alternate 64-column rounds
+        // (per-lane 256-byte bulk copies instead were no faster: all CTAs drain at
+        // once, so the drain runs at the aggregate write bandwidth either way)
+        static_assert(8 * 32 * 68 * 4 <= L::kBarOff, "drain staging fits the pipeline smem");
         float* stg = reinterpret_cast<float*>(smem) + (warp - 2) * 32 * 68;
         const uint32_t stg_u = smem_u32(stg);
+        const int half = (warp - 2) >> 2;
 #pragma unroll 1
         for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll 1
-            for (int c0 = 0; c0 < NB; c0 += 64) {
+            for (int c0 = 64 * half; c0 < NB; c0 += 128) {
                 uint32_t v[64];
                 if (live) {
                     const uint32_t ta = tmem_base + mt * NB + c0 + (static_cast<uint32_t>(q * 32) << 16);
