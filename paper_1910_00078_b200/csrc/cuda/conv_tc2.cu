@@ -48,6 +48,11 @@ struct Gemm2Args {
     int m_pairs, n_tiles, total;  // pair tiles: (M / 256) x (N / 256)
     int P, Q;       // output image extent (per-activation epilogues)
     int b_mn;       // B MN-major: two 64-wide atoms (8 KB apart) per CTA half
+    // Work items: the first full_items are 256 x 256 pair tiles; when the last
+    // round of tiles would leave pairs idle (R = total mod pairs, 2R <= pairs)
+    // those R tiles run as 2R half tiles of 256 x 128 (N=128 MMAs), so the tail
+    // takes half a tile time (ResNet conv5 1x1: 98 tiles on 74 pairs)
+    int items, full_items;
     unsigned long long* trace;  // PK_TC2_TRACE: summed wait clocks per role (profiling only)
 };
 
@@ -76,10 +81,24 @@ __device__ __forceinline__ void mma4_pair(uint32_t d, uint64_t a, uint64_t b, ui
         : "memory");
 }
 
+struct PairItem {
+    int mp, nt, h;  // pair tile (M, N) and half (-1: the whole 256-wide tile)
+};
+__device__ __forceinline__ PairItem pair_item(const Gemm2Args& g, int u) {
+    int t = u, h = -1;
+    if (u >= g.full_items) {
+        const int v = u - g.full_items;
+        t = g.full_items + (v >> 1);
+        h = v & 1;
+    }
+    const int mp = t / g.n_tiles;
+    return {mp, t - mp * g.n_tiles, h};
+}
+
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
     gemm_pair_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
-                     const __grid_constant__ CUtensorMap ymap, const __grid_constant__ Gemm2Args g,
-                     const pk_epilogue epi) {
+                     const __grid_constant__ CUtensorMap bmap_h, const __grid_constant__ CUtensorMap ymap,
+                     const __grid_constant__ Gemm2Args g, const pk_epilogue epi) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
@@ -104,6 +123,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         fence_barrier_init();
         tma_prefetch(&amap);
         tma_prefetch(&bmap);
+        if (g.items != g.full_items && !g.b_mn) tma_prefetch(&bmap_h);
         tma_prefetch(&ymap);
     }
     if (warp == 1) {
@@ -126,22 +146,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
             uint32_t phase = 0;
             long long tw = 0;
             const long long t0 = clock64();
-            for (int t = pair_id; t < g.total; t += num_pairs) {
-                const int mp = t / g.n_tiles, nt = t - mp * g.n_tiles;
-                const int arow = mp * 256 + (int)rank * 128, brow = nt * 256 + (int)rank * 128;
+            for (int u = pair_id; u < g.items; u += num_pairs) {
+                const PairItem pi = pair_item(g, u);
+                const int bh = pi.h < 0 ? 128 : 64;  // filter rows of B per CTA
+                const int arow = pi.mp * 256 + (int)rank * 128;
+                const int brow = pi.nt * 256 + (pi.h < 0 ? 0 : pi.h * 128) + (int)rank * bh;
                 for (int kb = 0; kb < g.num_kb; ++kb) {
                     const long long w0 = clock64();
                     mbar_wait(&empty[stage], phase ^ 1);
                     tw += clock64() - w0;
                     uint8_t* sa = smem + stage * kStage2;
                     const uint32_t fb = smem_u32(&full[stage]) & 0xFEFFFFFFu;  // leader's barrier
-                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * kStage2);
+                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (kHalfA + bh * 128));
                     tma_load_2d_pair(smem_u32(sa), &amap, fb, kb * 64, arow);
                     if (g.b_mn) {
                         tma_load_2d_pair(smem_u32(sa + kHalfA), &bmap, fb, brow, kb * 64);
-                        tma_load_2d_pair(smem_u32(sa + kHalfA + 8192), &bmap, fb, brow + 64, kb * 64);
+                        if (bh == 128)
+                            tma_load_2d_pair(smem_u32(sa + kHalfA + 8192), &bmap, fb, brow + 64, kb * 64);
                     } else {
-                        tma_load_2d_pair(smem_u32(sa + kHalfA), &bmap, fb, kb * 64, brow);
+                        tma_load_2d_pair(smem_u32(sa + kHalfA), bh == 128 ? &bmap : &bmap_h, fb, kb * 64,
+                                         brow);
                     }
                     if (++stage == kStages2) {
                         stage = 0;
@@ -156,13 +180,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
         }
     } else if (warp == 1) {
         if (rank == 0) {
-            const uint32_t idesc = idesc_bf16_f32(256, 256, false, g.b_mn != 0);
+            const uint32_t idesc_full = idesc_bf16_f32(256, 256, false, g.b_mn != 0);
+            const uint32_t idesc_half = idesc_bf16_f32(256, 128, false, g.b_mn != 0);
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
             long long tf = 0, te = 0;
             const long long t0 = clock64();
-            for (int t = pair_id; t < g.total; t += num_pairs, ++it) {
+            for (int u = pair_id; u < g.items; u += num_pairs, ++it) {
+                const uint32_t idesc = pair_item(g, u).h < 0 ? idesc_full : idesc_half;
                 const int a = it & 1;
                 long long w0 = clock64();
                 mbar_wait(&tmem_empty[a], ((it >> 1) & 1) ^ 1);
@@ -212,13 +238,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads2, 1)
                          : "=r"(leader_empty[i])
                          : "r"(smem_u32(&tmem_empty[i])));
         int it = 0;
-        for (int t = pair_id; t < g.total; t += num_pairs, ++it) {
-            const int mp = t / g.n_tiles, nt = t - mp * g.n_tiles;
-            const int m0 = mp * 256 + (int)rank * 128, n0 = nt * 256;
+        for (int u = pair_id; u < g.items; u += num_pairs, ++it) {
+            const PairItem pi = pair_item(g, u);
+            const int m0 = pi.mp * 256 + (int)rank * 128, n0 = pi.nt * 256 + (pi.h < 0 ? 0 : pi.h * 128);
             const int a = it & 1;
             mbar_wait(&tmem_full[a], (it >> 1) & 1);
             tc_fence_after();
-            const int span = min(256, g.out_pitch - n0);
+            const int span = min(pi.h < 0 ? 256 : 128, g.out_pitch - n0);
             const int nchunks = (span + 63) / 64;
             const int my_m = m0 + q * 32 + lane;
             int oy = 0, ox = 0;
@@ -292,9 +318,10 @@ int pk_gemm_pair_eligible(int M, int kdim, int n_out, int out_pitch) {
 cudaError_t pk_gemm_pair(const void* a, const void* b, void* y, int M, int kdim, int n_out,
                          int out_pitch, int P, int Q, const pk_epilogue* epi, cudaStream_t st,
                          int b_mn_pitch) {
-    CUtensorMap amap{}, bmap{}, ymap{};
+    CUtensorMap amap{}, bmap{}, bmap_h{}, ymap{};
     const bool bmap_ok = b_mn_pitch > 0 ? tc::make_map_2d(&bmap, b, kdim, b_mn_pitch, b_mn_pitch, 64)
-                                        : tc::make_map_2d(&bmap, b, n_out, kdim, kdim, 128);
+                                        : tc::make_map_2d(&bmap, b, n_out, kdim, kdim, 128) &&
+                                              tc::make_map_2d(&bmap_h, b, n_out, kdim, kdim, 64);
     if (!tc::make_map_2d(&amap, a, M, kdim, kdim, 128) || !bmap_ok ||
         !tc::make_map_2d(&ymap, y, M, out_pitch, out_pitch, 32))
         return cudaErrorInvalidValue;
@@ -330,8 +357,18 @@ cudaError_t pk_gemm_pair(const void* a, const void* b, void* y, int M, int kdim,
     }
     int grid = tc::num_sms_of_current_device() / 2 * 2;
     if (grid > 2 * g.total) grid = 2 * g.total;
+    static const bool no_split = [] {  // PK_TC2_TAIL=0: whole tiles only (A/B)
+        const char* v = std::getenv("PK_TC2_TAIL");
+        return v && v[0] == '0';
+    }();
+    const int pairs = grid / 2, rem = g.total % pairs;
+    g.full_items = g.items = g.total;
+    if (!no_split && rem > 0 && 2 * rem <= pairs) {
+        g.full_items = g.total - rem;
+        g.items = g.full_items + 2 * rem;
+    }
     const cudaError_t le = pk_launch(gemm_pair_kernel, dim3(grid), dim3(kThreads2), kBytes2, st, amap,
-                                     bmap, ymap, g, e);
+                                     bmap, bmap_h, ymap, g, e);
     count_launch();
     if (trace) {  // profiling only (PK_TC2_TRACE; not inside graph capture)
         unsigned long long h[8];
