@@ -1305,7 +1305,8 @@ cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, v
             if (le != cudaSuccess) return le;
             if (sync) return cudaSuccess;  // finished in-kernel
             const long long total = (long long)g->k * g->r * g->s * g->x_pitch;
-            long long blocks = (total + 255) / 256;
+            long long blocks = (total / 4 + 255) / 256;  // one float4 of output per thread
+            if (blocks < 1) blocks = 1;
             if (blocks > 148 * 16) blocks = 148 * 16;
             le = pk_launch(wgrad_sum_kernel, dim3((unsigned)blocks), dim3(256), 0, st,
                            (const float*)workspace, hs, total, (__nv_bfloat16*)dw);
@@ -1388,7 +1389,8 @@ cudaError_t pk_tma_wgrad(const pk_conv_geom* g, const void* dy, const void* x, v
         return cudaGetLastError();
     }
     const long long total = (long long)w.K * w.Nn;
-    long long blocks = (total + 255) / 256;
+    long long blocks = (total / 4 + 255) / 256;  // one float4 of output per thread
+    if (blocks < 1) blocks = 1;
     if (blocks > 148 * 16) blocks = 148 * 16;
     le = pk_launch(wgrad_sum_kernel, dim3((unsigned)blocks), dim3(256), 0, st, (const float*)workspace,
                    splits, total, (__nv_bfloat16*)dw);
