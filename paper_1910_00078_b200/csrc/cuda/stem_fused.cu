@@ -791,24 +791,32 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     }
 }
 
-// dw[k][r][s][c] = sum over CTAs (fixed order) of partial[cta][k][tap*4 + c]
+// dw[k][r][s][c] = sum over CTAs of partial[cta][k][tap*4 + c]: one WARP per
+// output element (lane l sums CTAs l, l + 32, ... in order, then a fixed xor
+// tree), so the ~148 partial loads of an element are in flight together
+// (one thread per element walked them serially: 28 us, latency-bound).
+// Deterministic: the order depends on nothing but the CTA count.
 __global__ void stem_wgrad_finish_kernel(const float* __restrict__ partial, int ctas, int K,
                                          int kcm, int taps, int f_pitch, int C,
                                          __nv_bfloat16* __restrict__ dw) {
     pdl_wait();
     pdl_trigger();
     const long long total = (long long)K * taps * f_pitch;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * blockDim.x / 32;
+    for (long long i = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 32; i < total; i += warps) {
         const int c = (int)(i % f_pitch);
         const long long kt = i / f_pitch;
         const int tap = (int)(kt % taps), k = (int)(kt / taps);
         float acc = 0.0f;
-        if (c < C) {
+        if (c < C) {  // warp-uniform
             const float* p = partial + (size_t)k * kcm + tap * 4 + c;
-            for (int s = 0; s < ctas; ++s) acc += p[(size_t)s * K * kcm];
+#pragma unroll 4
+            for (int s = lane; s < ctas; s += 32) acc += __ldcg(p + (size_t)s * K * kcm);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
         }
-        dw[i] = __float2bfloat16_rn(acc);
+        if (lane == 0) dw[i] = __float2bfloat16_rn(acc);
     }
 }
 
@@ -2206,7 +2214,7 @@ cudaError_t pk_cuda_stem_fused_wgrad(const pk_conv_geom* g, const void* dy, cons
     }
     if (err != cudaSuccess) return err;
     const long long total = (long long)g->k * a.taps * g->f_pitch;
-    const unsigned blocks = (unsigned)((total + 255) / 256);
+    const unsigned blocks = (unsigned)std::min<long long>((total * 32 + 255) / 256, 148LL * 16);
     err = pk_launch(stem_wgrad_finish_kernel, dim3(blocks), dim3(256), 0, st, (const float*)partial,
                     ctas, g->k, a.kcm, a.taps, g->f_pitch, g->c, (__nv_bfloat16*)dw);
     count_launch();
