@@ -30,7 +30,7 @@ namespace {
 
 using namespace pk::tc;
 
-constexpr int kHwThreads = 192;         // producer, MMA, 4 epilogue warps
+constexpr int kHwThreads = 320;         // producer, MMA, 8 epilogue warps (two per lane quarter)
 constexpr int kHwStages = 4;
 constexpr int kHaloRowsMax = 256;       // halo buffer rows (128 B each)
 constexpr int kHaloBytes = kHaloRowsMax * 128;
@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(kHwThreads, 1)
         }
     } else {
         // ---------------- epilogue: TMEM lane = (tap, c), column = k -------------
-        const int q = warp & 3;
+        const int q = warp & 3, half = (warp - 2) >> 2;  // the two warps of a quarter: alternate M tiles
         const bool live = kb_end > kb_begin;
         if (live) {
             mbar_wait(tmem_full, 0);
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kHwThreads, 1)
         const int row = q * 32 + lane;
         float* dst0 = partial + (size_t)blockIdx.x * g.K * g.Nn;
 #pragma unroll 1
-        for (int m = 0; m < g.mtiles; ++m) {
+        for (int m = half; m < g.mtiles; m += 2) {
             const int tap = 2 * m + (row >> 6), c = row & 63;
             const bool ok = tap < g.taps;
 #pragma unroll 1
