@@ -312,6 +312,71 @@ def step(lib, handle, net, directions=(0, 1, 2), dp=None, wside=None):
         main.wait_event(ev[len(net.items) + 1])
 
 
+def batchnorm_roofline(torch, lib, handle, layers, batch, hbm_peak):
+    """cfg4's batch-norm kernels against the HBM roofline (BASELINE north_star: "achieved
+    HBM GB/s against ... for batch-norm"): single-launch training forward and backward
+    (bn_coop.cu) on every distinct ResNet-50 BN input [N, K, P, P] (bf16, NHWC), L2
+    flushed by reading a 512 MB buffer before each call, median of 3, CUDA events on
+    the launching stream. Algorithmic bytes: forward 3|x| (statistics read, normalise
+    read, y write), backward 5|x| (x, dy for the sums; x, dy and the dx write)."""
+    import statistics
+    flush = torch.ones(128 << 20, dtype=torch.float32, device="cuda")
+    P = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    shapes = {}
+    for L in layers:
+        shapes[(L.k, L.out_h)] = shapes.get((L.k, L.out_h), 0) + 1
+
+    def timed(fn):
+        fn()
+        ts = []
+        for _ in range(3):
+            flush.max()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+    tot = {"fwd": [0.0, 0.0], "bwd": [0.0, 0.0]}
+    largest = None
+    for (k, p), count in sorted(shapes.items()):
+        x = (torch.rand((batch, p, p, k), device="cuda") * 2 - 1).to(torch.bfloat16)
+        y, dx = torch.empty_like(x), torch.empty_like(x)
+        dy = (torch.rand_like(x, dtype=torch.float32) * 2 - 1).to(torch.bfloat16)
+        g, b = torch.rand(k, device="cuda") + 0.5, torch.rand(k, device="cuda") - 0.5
+        rm, rv = torch.zeros(k, device="cuda"), torch.ones(k, device="cuda")
+        sm, si, dg, db = (torch.empty(k, device="cuda") for _ in range(4))
+        dims = (C.c_int64 * 4)(batch, k, p, p)
+        xb = x.numel() * 2
+
+        def fwd():
+            lib.check(lib.lib.primkit_batchnorm_forward_train_device(
+                handle.ptr, dims, 1, P(x), P(g), P(b), P(rm), P(rv), C.c_float(1e-5), C.c_float(0.1),
+                P(y), P(sm), P(si), 1))
+
+        def bwd():
+            lib.check(lib.lib.primkit_batchnorm_backward_device(
+                handle.ptr, dims, 1, P(x), P(y), P(dy), P(g), P(b), P(sm), P(si), P(dx), P(dg), P(db), 0))
+        fwd()
+        tf, tb = timed(fwd), timed(bwd)
+        for d, t, nb in (("fwd", tf, 3 * xb), ("bwd", tb, 5 * xb)):
+            tot[d][0] += count * nb
+            tot[d][1] += count * t
+        if largest is None or xb > largest[0]:
+            largest = (xb, k, p, 3 * xb / tf / 1e6, 5 * xb / tb / 1e6)
+        del x, y, dx, dy
+    out = {"unit": "GB/s", "peak": hbm_peak, "kernels": "bn_coop (single-launch training BN, bf16)",
+           "shapes": "every distinct ResNet-50 BN input at N=%d, weighted by its 53-layer count" % batch}
+    for d in ("fwd", "bwd"):
+        gbs = tot[d][0] / tot[d][1] / 1e6
+        out[d] = {"achieved": gbs, "frac": gbs / hbm_peak, "ms_all_layers": tot[d][1]}
+    out["largest"] = {"shape": [batch, largest[1], largest[2], largest[2]], "fwd_gbs": largest[3],
+                      "bwd_gbs": largest[4], "fwd_frac": largest[3] / hbm_peak,
+                      "bwd_frac": largest[4] / hbm_peak}
+    return out
+
+
 def time_region(torch, fn, iters):
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -761,6 +826,8 @@ def main():
         extras["roofline"]["step_frac_of_layer_roofline"] = 3 * roof_ms / ms_step
         if rank == 0:
             extras["fusion"] = fusion_speedup(torch, lib, handle, device)
+            extras["batchnorm"] = batchnorm_roofline(torch, lib, handle, layers, args.batch,
+                                                     peaks["hbm_gbs"])
             with mp.get_context("fork").Pool(os.cpu_count() or 1) as pool:
                 import oracle
                 if not oracle.reference_available():
